@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark: HE matmul/s of the column-ciphertext matmul (BASELINE.json config 2)
+on B200, plus NTT GB/s and the CPU baselines.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one HE matmul A(64x64)*B(64x64): matmul_outer over n = 64 resident
+column-ciphertext pairs (N = 2^14, 5 ciphertext primes + 60-bit special prime,
+scale 2^40, seed 1) = fused tensor-sum + one relinearisation + one rescale.
+Under torchrun every rank runs independent HE matmuls (weak scaling) and
+`value` is the whole-job throughput, timed on the device as the max over ranks.
+
+`e2e` is the same metric through the public API with host buffers: every step
+uploads A and B from pinned host memory, encrypts the 128 column ciphertexts
+(encode_left/encode_right), runs matmul_outer and downloads the decoded result.
+
+`--impl reference` times the CPU restatement of the same path (oracle/, real
+RNS-CKKS in C + OpenMP) on rank 0 only; the reference package itself is a
+float64 simulator with no cryptography and is reported as
+`reference_simulator` beside it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "HE matmul/s (column-ciphertext matmul_outer, BASELINE config 2: A,B 64x64, n=64 cts/operand, N=2^14)"
+UNIT = "HE matmul/s"
+CFG = 2
+DIM = 64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-extra", action="store_true", help="skip the NTT/config-1 side measurements")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def inputs(cfg=CFG, dim=DIM):
+    rng = np.random.default_rng(cfg - 1)  # BASELINE.json: config c uses seed c-1
+    a = rng.uniform(-1, 1, (dim, dim))
+    b = rng.uniform(-1, 1, (dim, dim))
+    return a, b
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled DURING the timed region
+class ClockSampler:
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                self.samples.append([x.strip() for x in out.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if len(s) > 2 and s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if len(s) > 2 and s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu --set full summary, if present."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    v = d.get("kernels", {}).get(kernel, {})
+    return v.get("dram_bytes_per_launch")
+
+
+# ---------------------------------------------------------------------------
+def cpu_port_matmul(cfg=CFG, dim=DIM, reps=1):
+    """Time the CPU residue oracle (C + OpenMP) on HE matmuls of the same workload."""
+    from oracle.engine import OracleEngine
+    from paper_2512_18646_b200.params import config_params
+
+    p = config_params(cfg)
+    e = OracleEngine.from_params(p)
+    a, b = inputs(cfg, dim)
+    L = [e.enc(np.repeat(a[:, k], dim)) for k in range(dim)]
+    R = [e.enc(np.tile(b[k, :], dim)) for k in range(dim)]
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = e.matmul_outer_blocks([L], R)[0]
+        times.append(time.perf_counter() - t0)
+    got = e.dec(out)[: dim * dim].reshape(dim, dim)
+    err = float(np.max(np.abs(got - a @ b)))
+    return times, err
+
+
+def simulator_matmul(cfg=CFG, dim=DIM, reps=20):
+    """Time the reference algorithm (float64 slot simulator, numpy restatement)."""
+    from oracle import sim
+
+    a, b = inputs(cfg, dim)
+    slots = {1: 4096, 2: 8192}[cfg]
+    eng = sim.SimEngine(slots)
+    L, R = sim.encode_left(eng, a, dim), sim.encode_right(eng, b, dim)
+    t = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        sim.matmul_outer(eng, L, R, dim, dim)
+        t.append(time.perf_counter() - t0)
+    return min(t)
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_port_matmul(reps=1)
+    times, err = cpu_port_matmul(reps=args.steps)
+    per = statistics.mean(times)
+    v = 1.0 / per
+    sim_t = simulator_matmul()
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seed 1, U[-1,1])",
+        "config": {"workload": "cfg2 HE matmul 64x64 (n=64 column ciphertexts), N=2^14, 5 primes + P"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} cfg-2 HE matmuls (matmul_outer on resident ciphertexts) in the C RNS-CKKS oracle, OpenMP over limbs",
+                         "max_abs_err": err},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_simulator": {"value": 1.0 / sim_t, "unit": UNIT, "cores": 1,
+                                "note": "reference algorithm as an exact float64 slot simulator (no cryptography)"},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, ws, rank, local):
+    import torch
+
+    from paper_2512_18646_b200 import _lib
+    from paper_2512_18646_b200 import CkksEngine, encode_left, encode_right, matmul_outer
+    from paper_2512_18646_b200.params import config_params
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    eng = CkksEngine(config_params(CFG), device=local)
+    lib = eng._lib
+    stream = eng._stream
+    a, b = inputs()
+    left = encode_left(eng, a, DIM)
+    right = encode_right(eng, b, DIM)
+    # correctness gate before timing
+    first = matmul_outer(eng, left, right)
+    err = float(np.max(np.abs(first.decode(eng) - a @ b)))
+    assert err < 1e-3, f"HE matmul error {err}"
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        matmul_outer(eng, left, right)
+    barrier()
+    torch.cuda.synchronize()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = lib.vr_launch_count()
+    with ClockSampler(local) as clk:
+        st.record(stream)
+        for _ in range(args.steps):
+            out = matmul_outer(eng, left, right)
+        en.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.vr_launch_count() - l0
+    barrier()
+    step_s = max_over_ranks(st.elapsed_time(en) / 1e3 / args.steps)
+    value = ws / step_s
+
+    # dominant kernel: the fused tensor-sum, timed alone on the same stream
+    nl = eng.L + 1
+    ptrsL = _lib.ptr_array([c.ptr() for c in left.cts])
+    ptrsR = _lib.ptr_array([c.ptr() for c in right.cts])
+    d3 = torch.empty((3, nl, eng.N), dtype=torch.int64, device="cuda")
+    po = _lib.ptr_array([d3.data_ptr()])
+    for _ in range(3):
+        _lib.check(lib.vr_tensor_sum(eng.handle, ptrsL, ptrsR, DIM, 1, eng.L, po))
+    reps = max(args.steps, 20)
+    torch.cuda.synchronize()
+    st.record(stream)
+    for _ in range(reps):
+        _lib.check(lib.vr_tensor_sum(eng.handle, ptrsL, ptrsR, DIM, 1, eng.L, po))
+    en.record(stream)
+    torch.cuda.synchronize()
+    ts_s = st.elapsed_time(en) / 1e3 / reps
+    alg_bytes = DIM * 4 * nl * eng.N * 8 + 3 * nl * eng.N * 8
+    peak, peak_src = peaks()
+    achieved = alg_bytes / ts_s / 1e9
+
+    # e2e through the public API with host buffers
+    pin_a = torch.from_numpy(a).pin_memory()
+    pin_b = torch.from_numpy(b).pin_memory()
+    e2e_steps = max(3, args.steps // 5)
+    for _ in range(2):
+        matmul_outer(eng, encode_left(eng, pin_a.numpy(), DIM), encode_right(eng, pin_b.numpy(), DIM)).decode(eng)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st.record(stream)
+    for _ in range(e2e_steps):
+        res = matmul_outer(eng, encode_left(eng, pin_a.numpy(), DIM), encode_right(eng, pin_b.numpy(), DIM)).decode(eng)
+    en.record(stream)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(max(st.elapsed_time(en) / 1e3, time.perf_counter() - t0) / e2e_steps)
+    h2d = 2 * DIM * (DIM * DIM) * 8  # two operands, n padded slot vectors of m*p doubles
+    d2h = eng.slots * 8
+
+    extra = {}
+    if not args.no_extra and rank == 0:
+        extra["ntt"] = bench_ntt(eng, peak)
+    line = None
+    if rank == 0:
+        cpu = None
+        try:
+            times, cerr = cpu_port_matmul(reps=2)
+            cv = 1.0 / statistics.median(times)
+            cpu = {"value": cv, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+                   "sample": "2 cfg-2 HE matmuls (matmul_outer on resident ciphertexts) in the C RNS-CKKS oracle, OpenMP",
+                   "max_abs_err": cerr}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port", "sample": f"failed: {exc}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic (seed 1, U[-1,1]); inputs larger than L2 (128 cts = 168 MB)",
+            "config": {"workload": "cfg2 HE matmul 64x64 (n=64 column ciphertexts/operand), N=2^14, q0 60b + 4x40b + P 60b, scale 2^40",
+                       "parallelism": f"replicas x{ws}", "l2": "inputs larger than L2"},
+            "max_abs_err": err,
+            "roofline": {"bound": "hbm", "kernel": "k_tensor_sum", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic("k_tensor_sum"),
+                         "alg_bytes_per_launch": alg_bytes, "launch_us": ts_s * 1e6, "step_share": ts_s / step_s,
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": {"value": ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "encode_left+encode_right (encrypt 128 cts) -> matmul_outer -> decode"},
+            "gpu_launches": int(launches),
+            "gpu_launches_per_step": launches / args.steps,
+            "clocks": clk.summary(),
+            **extra,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def bench_ntt(eng, peak):
+    """Forward NTT throughput on a batch larger than L2 (N=2^14 limbs, in place)."""
+    import torch
+
+    from paper_2512_18646_b200 import _lib
+
+    nl = eng.L + 1
+    polys = 256
+    data = torch.randint(0, 2 ** 39, (polys, nl, eng.N), dtype=torch.int64, device="cuda")
+    lib = eng._lib
+    for _ in range(3):
+        _lib.check(lib.vr_ntt(eng.handle, data.data_ptr(), polys, nl, 0, 0))
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    torch.cuda.synchronize()
+    st.record(eng._stream)
+    for _ in range(reps):
+        _lib.check(lib.vr_ntt(eng.handle, data.data_ptr(), polys, nl, 0, 0))
+    en.record(eng._stream)
+    torch.cuda.synchronize()
+    t = st.elapsed_time(en) / 1e3 / reps
+    nbytes = polys * nl * eng.N * 8
+    gbs = 2 * nbytes / t / 1e9  # read + write of every limb
+    butterflies = polys * nl * (eng.N // 2) * eng.params.log_n
+    return {"metric": "NTT HBM GB/s (forward, 2 passes, in place)", "N": eng.N, "limbs": polys * nl,
+            "gbs": gbs, "peak": peak, "frac": gbs / peak, "us_per_limb": t / (polys * nl) * 1e6,
+            "gbutterfly_s": butterflies / t / 1e9}
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

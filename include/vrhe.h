@@ -1,0 +1,127 @@
+/*
+ * vrhe.h -- C-ABI of libvrhe.so, the B200-native RNS-CKKS evaluator behind the
+ * packedhe SlotEngine surface (arXiv 2512.18646, Volley Revolver Inference++).
+ *
+ * The reference has no native code; its "FFI" for this path is the Python
+ * method surface of SlotEngine (/root/reference/pkg/src/packedhe/engine.py)
+ * and the multi-ciphertext drivers (multicipher.py, pipeline.py).  Each entry
+ * point below names the reference call it replaces.  INTEGRATION.md shows the
+ * ctypes binding a packedhe maintainer would add.
+ *
+ * Conventions
+ *   - All `uint64_t *` ciphertext/plaintext arguments are DEVICE pointers.
+ *     A ciphertext at level l with degree d is [d+1][l+1][N] uint64 residues in
+ *     NTT form (limb i is mod primes[i]); a plaintext is [l+1][N].
+ *   - Pointer-table arguments (`const uint64_t *const *`) are HOST arrays of
+ *     device pointers, one entry per ciphertext in the batch.
+ *   - Every call is stream-ordered on the stream given to vr_set_stream and
+ *     returns a status: VR_OK, or an error whose message vr_last_error()
+ *     returns.  The Python host layer maps codes to the reference exception
+ *     classes (CapacityError / LayoutError / EngineError, engine.py:32-41).
+ */
+#ifndef VRHE_H
+#define VRHE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VR_OK 0
+#define VR_ERR_CAPACITY 1 /* engine.py:36-37 CapacityError */
+#define VR_ERR_LAYOUT 2   /* engine.py:40-41 LayoutError */
+#define VR_ERR_ENGINE 3   /* engine.py:32-33 EngineError */
+#define VR_ERR_CUDA 4
+
+typedef struct vr_ctx vr_ctx;
+
+/* ---- context ------------------------------------------------------------- */
+/* EngineParams + SlotEngine.__init__ (engine.py:54-90, 175-178).  primes holds
+ * num_q ciphertext primes q0..q_{num_q-1} followed by the special prime P.
+ * Generates the secret and public key on the device from `seed`. */
+int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, int sym_enc, int device, vr_ctx **out);
+int vr_ctx_destroy(vr_ctx *ctx);
+const char *vr_last_error(void);
+/* total kernels this library has launched (instrumentation for bench.py) */
+unsigned long long vr_launch_count(void);
+int vr_set_stream(vr_ctx *ctx, void *cuda_stream);
+int vr_sync(vr_ctx *ctx);
+
+/* ---- keys ---------------------------------------------------------------- */
+int vr_gen_relin_key(vr_ctx *ctx);
+/* Galois element 5^(steps mod S) mod 2N for a LEFT rotation (engine.py:232-236) */
+int vr_galois_elt(vr_ctx *ctx, int64_t steps, uint32_t *g_out);
+int vr_gen_galois_key(vr_ctx *ctx, uint32_t g);
+/* host-buffer exports for parity tests: s in NTT form [np][N]; pk [2][L+1][N];
+ * switching keys [L+1][2][np][N] */
+int vr_export_secret(vr_ctx *ctx, uint64_t *host_out);
+int vr_export_public_key(vr_ctx *ctx, uint64_t *host_out);
+int vr_export_relin_key(vr_ctx *ctx, uint64_t *host_out);
+int vr_export_galois_key(vr_ctx *ctx, uint32_t g, uint64_t *host_out);
+
+/* ---- transforms ---------------------------------------------------------- */
+/* in-place NTT/INTT of [polys][limbs][N] (limb i uses prime index prime0 + i) */
+int vr_ntt(vr_ctx *ctx, uint64_t *data, int polys, int limbs, int prime0, int inverse);
+
+/* ---- encode / encrypt / decrypt -- SlotEngine.enc / dec / mask ----------- */
+/* SlotEngine.mask + plaintext encoding (engine.py:244-251): values [count][nvals]
+ * (device doubles, zero-padded to S slots) -> plaintexts [count][level+1][N] */
+int vr_encode(vr_ctx *ctx, const double *vals, int count, int nvals, int level, double scale, uint64_t *pt_out);
+/* integer coefficients of the encoding (test hook), m_out [count][N] int64 */
+int vr_encode_coeffs(vr_ctx *ctx, const double *vals, int count, int nvals, double scale, int64_t *m_out);
+/* SlotEngine.enc (engine.py:193-202): fresh encryption, ciphertext c uses nonce0+c */
+int vr_encrypt(vr_ctx *ctx, const double *vals, int count, int nvals, int level, double scale, uint64_t nonce0,
+               uint64_t *ct_out);
+/* SlotEngine.dec (engine.py:204-206): decrypt on q0 and decode to real slots.
+ * out: device [count][S] doubles (may be NULL); coeffs_out: device [count][N] int64 (may be NULL). */
+int vr_decrypt_decode(vr_ctx *ctx, const uint64_t *const *cts, const int *degs, const int *levels, const double *scales,
+                      int count, double *out, int64_t *coeffs_out);
+
+/* ---- primitive arithmetic (batched) ------------------------------------- */
+/* SlotEngine.add (engine.py:208-213); op 0 = add, 1 = sub */
+int vr_add(vr_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out, int count, int deg,
+           int level, int op);
+int vr_tensor(vr_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out, int count, int level);
+int vr_relin(vr_ctx *ctx, const uint64_t *const *d3, uint64_t *const *out, int count, int level);
+int vr_rescale(vr_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int deg, int level);
+/* SlotEngine.mul (engine.py:215-220): tensor -> relinearise -> rescale */
+int vr_mul(vr_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out, int count, int level);
+/* SlotEngine.cmul (engine.py:222-230) building blocks: plaintext / integer-scalar products */
+int vr_mul_plain(vr_ctx *ctx, const uint64_t *const *ct, const uint64_t *const *pt, uint64_t *const *out, int count, int deg,
+                 int level, int shared_pt);
+int vr_mul_scalar(vr_ctx *ctx, const uint64_t *const *ct, int64_t s, uint64_t *const *out, int count, int deg, int level);
+int vr_add_const(vr_ctx *ctx, uint64_t *const *ct, int64_t s, int count, int level);
+int vr_drop_level(vr_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int deg, int level_from,
+                  int level_to);
+/* SlotEngine.rot (engine.py:232-236), hoisted: out[c*nrot + r] = rot(in[c], steps[r]) */
+int vr_rotate(vr_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int level, int nrot,
+              const int64_t *steps);
+/* raw key switch of one polynomial [level+1][N] with the relin key (g == 0) or Galois key g; out [2][level+1][N] */
+int vr_keyswitch(vr_ctx *ctx, const uint64_t *poly, int level, uint32_t g, uint64_t *out);
+/* reduce residue sums (< 2^64) mod q_i in place: [polys][level+1][N] (after an NCCL uint64 sum) */
+int vr_mod_reduce(vr_ctx *ctx, uint64_t *data, long long polys, int level);
+
+/* ---- column-ciphertext drivers ------------------------------------------ */
+/* matmul_outer (multicipher.py:88-103): out[b] = rescale(relin(sum_k L[b*n+k] (x) R[k])), nb row
+ * blocks share R (nb in {1,2,4}) */
+int vr_matmul_outer(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
+                    uint64_t *const *out);
+/* the degree-2 partial sum only (multi-GPU: all-reduce, vr_mod_reduce, then vr_relin + vr_rescale) */
+int vr_tensor_sum(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
+                  uint64_t *const *out);
+/* conv_columns (multicipher.py:123-162) for C channels x F filters:
+ *   Y[f*nout+o] = rescale(mask * (sum_{c,q,p} w[f][c][p][q] * rot(X[c*W + cols[o]+q], p) + bias[f]))
+ * w: host int64 [F][C][k][k] (quantised weights), bias: host int64 [F], mask: device plaintext [level+1][N] */
+int vr_conv_columns(vr_ctx *ctx, const uint64_t *const *X, int C, int W, int k, const int64_t *w, const int64_t *bias, int F,
+                    const int *out_cols, int nout, const uint64_t *mask_pt, int level, uint64_t *const *Y);
+/* poly_activation (pipeline.py:180-197) on a batch; kc = integer constants {c3, c2, c1, c0} at their
+ * target scales */
+int vr_poly_activation(vr_ctx *ctx, const uint64_t *const *x, int count, int level, const int64_t *kc, int c3_zero,
+                       uint64_t *const *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VRHE_H */

@@ -1,0 +1,29 @@
+"""B200-native RNS-CKKS evaluator for the Volley Revolver column-ciphertext
+HE-matmul / HE-conv path (arXiv 2512.18646), a drop-in for packedhe's
+SlotEngine + multicipher + poly_activation API.
+
+Compute runs in hand-written sm_100a kernels (libvrhe.so, C-ABI in
+include/vrhe.h); this package is the host-side mirror of the reference
+interface.  There is no CPU fallback.
+"""
+
+from .errors import CapacityError, EngineError, LayoutError
+from .params import EngineParams, config_params, gen_primes, is_pow2, next_pow2
+from .engine import Ciphertext, CkksEngine, OpMeter, PlainMask, SlotEngine
+from .encoding import Encoding, Kernel, MatrixShape, PackedMatrix
+from .multicipher import (
+    ColumnEncodedImage,
+    ColumnEncodedMatrix,
+    conv_columns,
+    conv_columns_multi,
+    encode_image_columns,
+    encode_left,
+    encode_right,
+    matmul_outer,
+    matmul_outer_blocks,
+    pad_images,
+    reassemble_columns,
+)
+from .pipeline import activation_constants, poly_activation, poly_activation_batch
+
+__version__ = "0.1.0"

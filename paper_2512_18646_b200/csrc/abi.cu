@@ -1,0 +1,473 @@
+// abi.cu -- extern "C" entry points of libvrhe.so (declared in include/vrhe.h)
+// and context construction (prime tables, NTT twiddles, FFT tables, keys).
+#include <math.h>
+
+#include <cstring>
+
+#include "../../include/vrhe.h"
+#include "encode.cuh"
+
+struct vr_ctx {
+    vr::Ctx c;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+typedef unsigned __int128 u128h;
+
+uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)(((u128h)a * b) % q); }
+uint64_t h_pow(uint64_t b, uint64_t e, uint64_t q) {
+    uint64_t r = 1 % q;
+    b %= q;
+    while (e) {
+        if (e & 1) r = h_mulmod(r, b, q);
+        b = h_mulmod(b, b, q);
+        e >>= 1;
+    }
+    return r;
+}
+uint64_t h_inv(uint64_t a, uint64_t q) { return h_pow(a % q, q - 2, q); }
+uint64_t h_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((u128h)w << 64) / q); }
+uint32_t h_brev(uint32_t x, int bits) {
+    uint32_t r = 0;
+    for (int i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+
+// minimal primitive 2N-th root of unity (same rule as the oracle)
+uint64_t h_min_psi(uint64_t q, int n) {
+    const uint64_t two_n = 2ull * n;
+    uint64_t psi = 0;
+    for (uint64_t g = 2;; g++) {
+        uint64_t x = h_pow(g, (q - 1) / two_n, q);
+        if (h_pow(x, n, q) == q - 1) { psi = x; break; }
+    }
+    uint64_t best = psi, sq = h_mulmod(psi, psi, q), cur = psi;
+    for (int k = 1; k < n; k++) {
+        cur = h_mulmod(cur, sq, q);
+        if (cur < best) best = cur;
+    }
+    return best;
+}
+
+void build_cdt(uint64_t *cdt) {
+    double z = 1.0;
+    for (int k = 1; k < 64; k++) z += 2.0 * exp(-(double)(k * k) / (2.0 * 3.2 * 3.2));
+    double cum = 1.0 / z;
+    for (int m = 0; m < vr::CDT_LEN; m++) {
+        if (m > 0) cum += 2.0 * exp(-(double)(m * m) / (2.0 * 3.2 * 3.2)) / z;
+        double t = cum * 9223372036854775808.0;
+        cdt[m] = (t >= 9223372036854775808.0) ? 0x8000000000000000ull : (uint64_t)t;
+    }
+    cdt[vr::CDT_LEN - 1] = 0x8000000000000000ull;
+}
+
+template <class T>
+T *upload(vr::Ctx &c, const std::vector<T> &h) {
+    T *d = nullptr;
+    VR_CUDA(cudaMalloc((void **)&d, sizeof(T) * h.size()));
+    VR_CUDA(cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    return d;
+}
+
+template <class F>
+int guard(F &&f) {
+    try {
+        f();
+        return VR_OK;
+    } catch (const vr::VrError &e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return VR_ERR_ENGINE;
+    }
+}
+
+std::vector<const uint64_t *> vec(const uint64_t *const *p, size_t n) { return std::vector<const uint64_t *>(p, p + n); }
+std::vector<const uint64_t *> vecm(uint64_t *const *p, size_t n) { return std::vector<const uint64_t *>(p, p + n); }
+
+void check_level(const vr::Ctx &c, int level) {
+    if (level < 0 || level > c.L) throw vr::VrError(VR_ERR_ENGINE, "level out of range");
+}
+
+}  // namespace
+
+namespace vr {
+unsigned long long g_launches = 0;
+}
+
+extern "C" {
+
+const char *vr_last_error(void) { return g_err.c_str(); }
+unsigned long long vr_launch_count(void) { return __atomic_load_n(&vr::g_launches, __ATOMIC_RELAXED); }
+
+int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, int sym_enc, int device, vr_ctx **out) {
+    return guard([&] {
+        if (log_n < 2 || log_n > 17) throw vr::VrError(VR_ERR_ENGINE, "log_n must be in [2, 17]");
+        if (num_q < 1 || num_q + 1 > vr::MAXP) throw vr::VrError(VR_ERR_ENGINE, "unsupported number of primes");
+        VR_CUDA(cudaSetDevice(device));
+        auto *h = new vr_ctx();
+        vr::Ctx &c = h->c;
+        c.device = device;
+        c.log_n = log_n;
+        c.n = 1 << log_n;
+        c.slots = c.n / 2;
+        c.L = num_q - 1;
+        c.np = num_q + 1;
+        c.seed = seed;
+        c.sym_enc = sym_enc;
+        const int n = c.n, np = c.np;
+        for (int p = 0; p < np; p++) {
+            const uint64_t q = primes[p];
+            if (q >= (1ull << 61) || q % (2ull * n) != 1) {
+                delete h;
+                throw vr::VrError(VR_ERR_ENGINE, "primes must be < 2^61 and == 1 mod 2N");
+            }
+            c.q[p] = q;
+            u128h r = (~(u128h)0) / q;
+            c.primes.m[p] = vr::Modulus{q, (uint64_t)(r >> 64), (uint64_t)r};
+        }
+        std::vector<uint64_t> tw((size_t)np * n), tws((size_t)np * n), itw((size_t)np * n), itws((size_t)np * n);
+        c.h_ntt_const.resize(np);
+        for (int p = 0; p < np; p++) {
+            const uint64_t q = c.q[p];
+            const uint64_t psi = h_min_psi(q, n), ipsi = h_inv(psi, q);
+            std::vector<uint64_t> pw(n), ipw(n);
+            pw[0] = ipw[0] = 1;
+            for (int i = 1; i < n; i++) { pw[i] = h_mulmod(pw[i - 1], psi, q); ipw[i] = h_mulmod(ipw[i - 1], ipsi, q); }
+            for (int i = 0; i < n; i++) {
+                const uint32_t r = h_brev(i, log_n);
+                tw[(size_t)p * n + i] = pw[r];
+                tws[(size_t)p * n + i] = h_shoup(pw[r], q);
+                itw[(size_t)p * n + i] = ipw[r];
+                itws[(size_t)p * n + i] = h_shoup(ipw[r], q);
+            }
+            const uint64_t ninv = h_inv((uint64_t)n % q, q);
+            const uint64_t w0n = h_mulmod(itw[(size_t)p * n + 1], ninv, q);
+            c.h_ntt_const[p] = vr::NttConst{ninv, h_shoup(ninv, q), w0n, h_shoup(w0n, q)};
+        }
+        c.h_inv_tab.assign((size_t)np * np * 2, 0);
+        for (int a = 0; a < np; a++)
+            for (int b = 0; b < np; b++) {
+                if (a == b) continue;
+                const uint64_t v = h_inv(c.q[a] % c.q[b], c.q[b]);
+                c.h_inv_tab[((size_t)a * np + b) * 2] = v;
+                c.h_inv_tab[((size_t)a * np + b) * 2 + 1] = h_shoup(v, c.q[b]);
+            }
+        std::vector<double> zr(n), zi(n);
+        for (int k = 0; k < n; k++) {
+            const double ang = M_PI * (double)k / (double)n;
+            zr[k] = cos(ang);
+            zi[k] = sin(ang);
+        }
+        std::vector<int> sp(c.slots);
+        uint64_t g = 1;
+        for (int j = 0; j < c.slots; j++) { sp[j] = (int)((g - 1) / 4); g = (g * 5) % (2ull * n); }
+        std::vector<uint64_t> cdt(vr::CDT_LEN);
+        build_cdt(cdt.data());
+
+        c.tw = upload(c, tw);
+        c.tw_sh = upload(c, tws);
+        c.itw = upload(c, itw);
+        c.itw_sh = upload(c, itws);
+        c.ntt_const = upload(c, c.h_ntt_const);
+        c.inv_tab = upload(c, c.h_inv_tab);
+        c.zr = upload(c, zr);
+        c.zi = upload(c, zi);
+        c.slot_pos = upload(c, sp);
+        c.cdt = upload(c, cdt);
+        VR_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        vr::keygen(c);
+        VR_CUDA(cudaStreamSynchronize(c.stream));
+        // a user stream replaces the private one via vr_set_stream; keep the private one alive
+        *out = h;
+    });
+}
+
+int vr_ctx_destroy(vr_ctx *h) {
+    if (!h) return VR_OK;
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        cudaSetDevice(c.device);
+        cudaDeviceSynchronize();
+        void *ptrs[] = {c.tw, c.tw_sh, c.itw, c.itw_sh, c.ntt_const, c.inv_tab, c.zr, c.zi, c.slot_pos, c.cdt, c.rlk};
+        for (void *p : ptrs)
+            if (p) cudaFree(p);
+        if (c.s_ntt) cudaFree(c.s_ntt);
+        if (c.pk) cudaFree(c.pk);
+        for (auto &kv : c.gkeys) cudaFree(kv.second);
+        delete h;
+    });
+}
+
+int vr_set_stream(vr_ctx *h, void *stream) {
+    return guard([&] { h->c.stream = (cudaStream_t)stream; });
+}
+
+int vr_sync(vr_ctx *h) {
+    return guard([&] { VR_CUDA(cudaStreamSynchronize(h->c.stream)); });
+}
+
+int vr_gen_relin_key(vr_ctx *h) {
+    return guard([&] { vr::relin_key(h->c); });
+}
+
+int vr_galois_elt(vr_ctx *h, int64_t steps, uint32_t *g_out) {
+    return guard([&] {
+        const int64_t S = h->c.slots;
+        const int64_t r = ((steps % S) + S) % S;
+        uint64_t g = 1;
+        for (int64_t i = 0; i < r; i++) g = (g * 5) % (2ull * h->c.n);
+        *g_out = (uint32_t)g;
+    });
+}
+
+int vr_gen_galois_key(vr_ctx *h, uint32_t g) {
+    return guard([&] { vr::galois_key(h->c, g); });
+}
+
+static void export_dev(vr::Ctx &c, const uint64_t *d, size_t words, uint64_t *host) {
+    VR_CUDA(cudaMemcpyAsync(host, d, words * 8, cudaMemcpyDeviceToHost, c.stream));
+    VR_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+int vr_export_secret(vr_ctx *h, uint64_t *host_out) {
+    return guard([&] { export_dev(h->c, h->c.s_ntt, (size_t)h->c.np * h->c.n, host_out); });
+}
+int vr_export_public_key(vr_ctx *h, uint64_t *host_out) {
+    return guard([&] { export_dev(h->c, h->c.pk, (size_t)2 * (h->c.L + 1) * h->c.n, host_out); });
+}
+int vr_export_relin_key(vr_ctx *h, uint64_t *host_out) {
+    return guard([&] { export_dev(h->c, vr::relin_key(h->c), h->c.key_words(), host_out); });
+}
+int vr_export_galois_key(vr_ctx *h, uint32_t g, uint64_t *host_out) {
+    return guard([&] { export_dev(h->c, vr::galois_key(h->c, g), h->c.key_words(), host_out); });
+}
+
+int vr_ntt(vr_ctx *h, uint64_t *data, int polys, int limbs, int prime0, int inverse) {
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        if (prime0 < 0 || prime0 + limbs > c.np) throw vr::VrError(VR_ERR_ENGINE, "prime index out of range");
+        vr::NttBatch b{data, polys * limbs, limbs, (long long)limbs * c.n, limbs, prime0, 0, 0};
+        if (inverse) vr::ntt_inverse(c, b);
+        else vr::ntt_forward(c, b);
+    });
+}
+
+int vr_encode(vr_ctx *h, const double *vals, int count, int nvals, int level, double scale, uint64_t *pt_out) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (nvals > h->c.slots) throw vr::VrError(VR_ERR_CAPACITY, "payload exceeds slot count");
+        if (count > 0) vr::encode_plain(h->c, vals, count, nvals, level, scale, pt_out);
+    });
+}
+
+int vr_encode_coeffs(vr_ctx *h, const double *vals, int count, int nvals, double scale, int64_t *m_out) {
+    return guard([&] {
+        if (nvals > h->c.slots) throw vr::VrError(VR_ERR_CAPACITY, "payload exceeds slot count");
+        if (count > 0) vr::encode_coeffs(h->c, vals, count, nvals, scale, m_out);
+    });
+}
+
+int vr_encrypt(vr_ctx *h, const double *vals, int count, int nvals, int level, double scale, uint64_t nonce0, uint64_t *ct_out) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (nvals > h->c.slots) throw vr::VrError(VR_ERR_CAPACITY, "payload exceeds slot count");
+        if (count > 0) vr::encrypt(h->c, vals, count, nvals, level, scale, nonce0, ct_out);
+    });
+}
+
+int vr_decrypt_decode(vr_ctx *h, const uint64_t *const *cts, const int *degs, const int *levels, const double *scales,
+                      int count, double *out, int64_t *coeffs_out) {
+    return guard([&] {
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable t(c, vec(cts, count));
+        vr::DevArray<int> dd(c, degs, count), dl(c, levels, count);
+        vr::DevArray<double> ds(c, scales, count);
+        vr::decrypt_decode(c, t.c_(), dd.get(), dl.get(), ds.get(), count, out, coeffs_out);
+    });
+}
+
+int vr_add(vr_ctx *h, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out, int count, int deg, int level,
+           int op) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ta(c, vec(a, count)), tb(c, vec(b, count)), to(c, vecm(out, count));
+        vr::binop(c, ta.c_(), tb.c_(), to.m_(), count, deg + 1, level + 1, op);
+    });
+}
+
+int vr_tensor(vr_ctx *h, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out, int count, int level) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ta(c, vec(a, count)), tb(c, vec(b, count)), to(c, vecm(out, count));
+        vr::tensor(c, ta.c_(), tb.c_(), to.m_(), count, level + 1);
+    });
+}
+
+int vr_relin(vr_ctx *h, const uint64_t *const *d3, uint64_t *const *out, int count, int level) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ti(c, vec(d3, count)), to(c, vecm(out, count));
+        vr::relin_batch(c, ti.c_(), to.m_(), count, level);
+    });
+}
+
+int vr_rescale(vr_ctx *h, const uint64_t *const *in, uint64_t *const *out, int count, int deg, int level) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ti(c, vec(in, count)), to(c, vecm(out, count));
+        vr::rescale(c, ti.c_(), to.m_(), count, deg + 1, level);
+    });
+}
+
+int vr_mul(vr_ctx *h, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out, int count, int level) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ta(c, vec(a, count)), tb(c, vec(b, count)), to(c, vecm(out, count));
+        vr::mul_batch(c, ta.c_(), tb.c_(), to.m_(), count, level);
+    });
+}
+
+int vr_mul_plain(vr_ctx *h, const uint64_t *const *ct, const uint64_t *const *pt, uint64_t *const *out, int count, int deg,
+                 int level, int shared_pt) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ta(c, vec(ct, count)), tp(c, vec(pt, shared_pt ? 1 : count)), to(c, vecm(out, count));
+        vr::mul_plain(c, ta.c_(), tp.c_(), to.m_(), count, deg + 1, level + 1, shared_pt);
+    });
+}
+
+int vr_mul_scalar(vr_ctx *h, const uint64_t *const *ct, int64_t s, uint64_t *const *out, int count, int deg, int level) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ta(c, vec(ct, count)), to(c, vecm(out, count));
+        vr::mul_scalar(c, ta.c_(), to.m_(), count, deg + 1, level + 1, vr::limb_scalars(c, s, level + 1));
+    });
+}
+
+int vr_add_const(vr_ctx *h, uint64_t *const *ct, int64_t s, int count, int level) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ta(c, vecm(ct, count));
+        vr::add_const(c, ta.m_(), count, level + 1, vr::limb_scalars(c, s, level + 1));
+    });
+}
+
+int vr_drop_level(vr_ctx *h, const uint64_t *const *in, uint64_t *const *out, int count, int deg, int level_from, int level_to) {
+    return guard([&] {
+        check_level(h->c, level_from);
+        if (level_to < 0 || level_to > level_from) throw vr::VrError(VR_ERR_ENGINE, "bad target level");
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ta(c, vec(in, count)), to(c, vecm(out, count));
+        vr::copy_limbs(c, ta.c_(), to.m_(), count, deg + 1, level_from + 1, level_to + 1, 0);
+    });
+}
+
+int vr_rotate(vr_ctx *h, const uint64_t *const *in, uint64_t *const *out, int count, int level, int nrot, const int64_t *steps) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (count <= 0 || nrot <= 0) return;
+        vr::Ctx &c = h->c;
+        std::vector<uint32_t> gs(nrot);
+        for (int r = 0; r < nrot; r++) {
+            uint32_t g;
+            vr_galois_elt(h, steps[r], &g);
+            gs[r] = g;
+        }
+        vr::PtrTable ta(c, vec(in, count)), to(c, vecm(out, (size_t)count * nrot));
+        vr::rotate_batch(c, ta.c_(), to.m_(), count, level, nrot, gs.data());
+    });
+}
+
+int vr_keyswitch(vr_ctx *h, const uint64_t *poly, int level, uint32_t g, uint64_t *out) {
+    return guard([&] {
+        check_level(h->c, level);
+        vr::Ctx &c = h->c;
+        const uint64_t *key = g == 0 ? vr::relin_key(c) : vr::galois_key(c, g);
+        vr::Scratch d(c, sizeof(uint64_t) * (size_t)(level + 1) * (level + 2) * c.n);
+        std::vector<const uint64_t *> p{poly};
+        vr::PtrTable tp(c, p);
+        vr::modup(c, tp.c_(), 1, level, d.as<uint64_t>());
+        vr::ks_inner_moddown(c, d.as<uint64_t>(), 1, level, key, 1, out);
+    });
+}
+
+int vr_mod_reduce(vr_ctx *h, uint64_t *data, long long polys, int level) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (polys > 0) vr::mod_fixup(h->c, data, polys, level + 1);
+    });
+}
+
+int vr_matmul_outer(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *out) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
+        if (n <= 0) throw vr::VrError(VR_ERR_LAYOUT, "matmul_outer needs at least one column ciphertext");
+        vr::Ctx &c = h->c;
+        vr::PtrTable tl(c, vec(L, (size_t)n * nb)), tr(c, vec(R, n)), to(c, vecm(out, nb));
+        vr::matmul_outer(c, tl.c_(), tr.c_(), n, nb, level, to.m_());
+    });
+}
+
+int vr_tensor_sum(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *out) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (n <= 0) throw vr::VrError(VR_ERR_LAYOUT, "tensor_sum needs at least one column ciphertext");
+        vr::Ctx &c = h->c;
+        vr::PtrTable tl(c, vec(L, (size_t)n * nb)), tr(c, vec(R, n)), to(c, vecm(out, nb));
+        vr::tensor_sum(c, tl.c_(), tr.c_(), n, nb, level + 1, to.m_());
+    });
+}
+
+int vr_conv_columns(vr_ctx *h, const uint64_t *const *X, int C, int W, int k, const int64_t *w, const int64_t *bias, int F,
+                    const int *out_cols, int nout, const uint64_t *mask_pt, int level, uint64_t *const *Y) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
+        if (k < 1 || C < 1 || F < 1 || W < 1) throw vr::VrError(VR_ERR_ENGINE, "bad conv shape");
+        for (int o = 0; o < nout; o++)
+            if (out_cols[o] < 0 || out_cols[o] + k > W) throw vr::VrError(VR_ERR_ENGINE, "output column out of range");
+        std::vector<const uint64_t *> xs(X, X + (size_t)C * W);
+        std::vector<uint64_t *> ys(Y, Y + (size_t)F * nout);
+        vr::conv_columns(h->c, xs, C, W, k, w, bias, F, out_cols, nout, mask_pt, level, ys);
+    });
+}
+
+int vr_poly_activation(vr_ctx *h, const uint64_t *const *x, int count, int level, const int64_t *kc, int c3_zero,
+                       uint64_t *const *out) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (level < 2) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (poly_activation needs 2 levels)");
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable tx(c, vec(x, count)), to(c, vecm(out, count));
+        vr::poly_activation(c, tx.c_(), count, level, kc, c3_zero, to.m_());
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,219 @@
+// drivers.cu -- batched column-ciphertext drivers.
+//
+//   matmul_outer   multicipher.py:88-103   sum_k tensor(L_k, R_k) in one pass,
+//                                           then ONE relinearisation + ONE rescale
+//   conv_columns   multicipher.py:123-162  hoisted rotations shared by every
+//                                           filter/output column, one MAC kernel
+//                                           for all (filter, column, channel, tap)
+//   poly_activation pipeline.py:180-197    the same op sequence for a whole batch
+//
+// Each driver restates the op order of the matching oracle/ckks_oracle.c
+// function, so residues are bit-identical to the CPU oracle.
+#include <algorithm>
+#include <map>
+
+#include "encode.cuh"
+
+namespace vr {
+
+namespace {
+
+constexpr int TB = 256;
+
+std::vector<const uint64_t *> strided(const uint64_t *base, int count, size_t stride) {
+    std::vector<const uint64_t *> v(count);
+    for (int i = 0; i < count; i++) v[i] = base + (size_t)i * stride;
+    return v;
+}
+
+// Conv MAC: Yp[f][o] = mask * (sum_{c,q,p} w[f][c][p][q] * T[c][cols[o]+q][p] + bias[f])
+template <int FG>
+__global__ void __launch_bounds__(128) k_conv_mac(const uint64_t *const *T, const int *cols, int nout, int C, int W, int k,
+                                                  int F, const uint64_t *wq, const uint64_t *bq, const uint64_t *mask, int nl,
+                                                  int N, DevPrimes pr, uint64_t *Yp) {
+    const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (kk >= N) return;
+    const int poly = blockIdx.y / nl, i = blockIdx.y - poly * nl;
+    const int nfg = F / FG;
+    const int o = blockIdx.z / nfg, f0 = (blockIdx.z - o * nfg) * FG;
+    const Modulus m = pr.m[i];
+    u128 acc[FG];
+#pragma unroll
+    for (int f = 0; f < FG; f++) acc[f] = u128{0, 0};
+    int cnt = 0;
+    const size_t off = ((size_t)poly * nl + i) * N + kk;
+    const int kk2 = k * k;
+    for (int c = 0; c < C; c++)
+        for (int q = 0; q < k; q++) {
+            const int j = cols[o] + q;
+            for (int p = 0; p < k; p++) {
+                const uint64_t *src = T[((size_t)c * W + j) * k + p];
+                if (!src) continue;
+                const uint64_t v = src[off];
+                const uint64_t *wr = wq + (((size_t)i * F + f0) * C + c) * kk2 + p * k + q;
+#pragma unroll
+                for (int f = 0; f < FG; f++) mac_to(acc[f], v, __ldg(wr + (size_t)f * C * kk2));
+                if (++cnt == 16) {
+                    cnt = 0;
+#pragma unroll
+                    for (int f = 0; f < FG; f++) acc[f] = u128{reduce128(acc[f], m), 0};
+                }
+            }
+        }
+    const uint64_t mk = mask[(size_t)i * N + kk];
+#pragma unroll
+    for (int f = 0; f < FG; f++) {
+        uint64_t r = reduce128(acc[f], m);
+        if (poly == 0) r = add_mod(r, bq[(size_t)i * F + f0 + f], m.q);
+        r = mul_mod(r, mk, m);
+        Yp[((size_t)(f0 + f) * nout + o) * 2 * nl * N + off] = r;
+    }
+}
+
+}  // namespace
+
+void mul_batch(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *Out, int count, int level) {
+    const int N = c.n, nl = level + 1;
+    Scratch d3(c, sizeof(uint64_t) * count * 3 * nl * N), r(c, sizeof(uint64_t) * count * 2 * nl * N);
+    PtrTable td(c, strided(d3.as<uint64_t>(), count, (size_t)3 * nl * N));
+    PtrTable tr(c, strided(r.as<uint64_t>(), count, (size_t)2 * nl * N));
+    tensor(c, A, B, td.m_(), count, nl);
+    relin_batch(c, td.c_(), tr.m_(), count, level);
+    rescale(c, tr.c_(), Out, count, 2, level);
+}
+
+void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out) {
+    const int N = c.n, nl = level + 1;
+    Scratch d3(c, sizeof(uint64_t) * nb * 3 * nl * N), r(c, sizeof(uint64_t) * nb * 2 * nl * N);
+    PtrTable td(c, strided(d3.as<uint64_t>(), nb, (size_t)3 * nl * N));
+    PtrTable tr(c, strided(r.as<uint64_t>(), nb, (size_t)2 * nl * N));
+    tensor_sum(c, L, R, n, nb, nl, td.m_());
+    relin_batch(c, td.c_(), tr.m_(), nb, level);
+    rescale(c, tr.c_(), Out, nb, 2, level);
+}
+
+void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, int k, const int64_t *w, const int64_t *bias,
+                  int F, const int *out_cols, int nout, const uint64_t *mask_pt, int level, const std::vector<uint64_t *> &Y) {
+    const int N = c.n, nl = level + 1;
+    const size_t ctw = (size_t)2 * nl * N;
+    // 1. which rotations are needed: (ch, j, p) with p >= 1 and some nonzero tap reading it
+    std::vector<std::vector<int>> need((size_t)C * W);
+    for (int ch = 0; ch < C; ch++)
+        for (int j = 0; j < W; j++)
+            for (int p = 1; p < k; p++) {
+                bool nd = false;
+                for (int f = 0; f < F && !nd; f++)
+                    for (int q = 0; q < k && !nd; q++) {
+                        if (w[(((size_t)f * C + ch) * k + p) * k + q] == 0) continue;
+                        for (int o = 0; o < nout; o++)
+                            if (out_cols[o] + q == j) { nd = true; break; }
+                    }
+                if (nd) need[(size_t)ch * W + j].push_back(p);
+            }
+    // rotated copies, grouped by identical rotation set so each group is one hoisted batch
+    size_t nrot_total = 0;
+    for (auto &v : need) nrot_total += v.size();
+    Scratch rot(c, sizeof(uint64_t) * std::max<size_t>(nrot_total, 1) * ctw);
+    std::vector<const uint64_t *> table((size_t)C * W * k, nullptr);
+    std::map<std::vector<int>, std::vector<int>> groups;
+    for (int cj = 0; cj < C * W; cj++) {
+        table[(size_t)cj * k] = X[cj];
+        if (!need[cj].empty()) groups[need[cj]].push_back(cj);
+    }
+    size_t slot = 0;
+    const size_t d_bytes_per_ct = sizeof(uint64_t) * (size_t)nl * (nl + 1) * N;
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>(256, ((size_t)2 << 30) / d_bytes_per_ct));
+    for (auto &kv : groups) {
+        const std::vector<int> &ps = kv.first;
+        const std::vector<int> &cts = kv.second;
+        std::vector<uint32_t> gs(ps.size());
+        for (size_t r = 0; r < ps.size(); r++) {
+            const int64_t S = c.slots;
+            int64_t st = ((ps[r] % S) + S) % S;
+            uint64_t g = 1;
+            for (int64_t t = 0; t < st; t++) g = (g * 5) % (2ull * N);
+            gs[r] = (uint32_t)g;
+        }
+        for (size_t b0 = 0; b0 < cts.size(); b0 += chunk) {
+            const int cnt = (int)std::min<size_t>(chunk, cts.size() - b0);
+            std::vector<const uint64_t *> in(cnt), outs((size_t)cnt * ps.size());
+            for (int t = 0; t < cnt; t++) {
+                const int cj = cts[b0 + t];
+                in[t] = X[cj];
+                for (size_t r = 0; r < ps.size(); r++) {
+                    uint64_t *dst = rot.as<uint64_t>() + (slot++) * ctw;
+                    outs[(size_t)t * ps.size() + r] = dst;
+                    table[(size_t)cj * k + ps[r]] = dst;
+                }
+            }
+            PtrTable ti(c, in), to(c, outs);
+            rotate_batch(c, ti.c_(), to.m_(), cnt, level, (int)ps.size(), gs.data());
+        }
+    }
+    // 2. weights / bias reduced per limb
+    std::vector<uint64_t> wq((size_t)nl * F * C * k * k), bq((size_t)nl * F);
+    for (int i = 0; i < nl; i++) {
+        const Modulus &m = c.primes.m[i];
+        for (size_t t = 0; t < (size_t)F * C * k * k; t++) wq[(size_t)i * F * C * k * k + t] = from_i64(w[t], m);
+        for (int f = 0; f < F; f++) bq[(size_t)i * F + f] = from_i64(bias[f], m);
+    }
+    DevArray<uint64_t> dwq(c, wq.data(), wq.size()), dbq(c, bq.data(), bq.size());
+    DevArray<int> dcols(c, out_cols, nout);
+    PtrTable tt(c, table);
+    // 3. MAC + mask into pre-rescale buffer (chunked over output columns), then rescale
+    const int FG = (F % 8 == 0) ? 8 : (F % 4 == 0 ? 4 : (F % 2 == 0 ? 2 : 1));
+    const int ocols = std::max(1, std::min(nout, (int)(((size_t)2 << 30) / (ctw * 8 * F))));
+    Scratch yp(c, sizeof(uint64_t) * (size_t)F * ocols * ctw);
+    for (int o0 = 0; o0 < nout; o0 += ocols) {
+        const int no = std::min(ocols, nout - o0);
+        dim3 grid(nblocks(N, 128), 2 * nl, (unsigned)no * (F / FG));
+        const int *colp = dcols.get() + o0;
+        switch (FG) {
+            case 8: k_conv_mac<8><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+            case 4: k_conv_mac<4><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+            case 2: k_conv_mac<2><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+            default: k_conv_mac<1><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+        }
+        check_launch("k_conv_mac");
+        std::vector<const uint64_t *> ins((size_t)F * no);
+        std::vector<const uint64_t *> outs((size_t)F * no);
+        for (int f = 0; f < F; f++)
+            for (int o = 0; o < no; o++) {
+                ins[(size_t)f * no + o] = yp.as<uint64_t>() + ((size_t)f * no + o) * ctw;
+                outs[(size_t)f * no + o] = Y[(size_t)f * nout + o0 + o];
+            }
+        PtrTable ti(c, ins), to(c, outs);
+        rescale(c, ti.c_(), to.m_(), F * no, 2, level);
+    }
+}
+
+void poly_activation(Ctx &c, const uint64_t *const *X, int count, int level, const int64_t *kc, int c3_zero,
+                     uint64_t *const *Out) {
+    if (level < 2) throw VrError(3, "poly_activation needs two levels");
+    const int N = c.n;
+    const size_t w1 = (size_t)2 * level * N, w2 = (size_t)2 * (level - 1) * N;
+    Scratch x2(c, sizeof(uint64_t) * count * w1), tmp(c, sizeof(uint64_t) * count * w1), t(c, sizeof(uint64_t) * count * w2);
+    PtrTable tx2(c, strided(x2.as<uint64_t>(), count, w1)), ttmp(c, strided(tmp.as<uint64_t>(), count, w1)),
+        tt(c, strided(t.as<uint64_t>(), count, w2));
+    mul_batch(c, X, X, tx2.m_(), count, level);  // x^2 at level-1
+    if (c3_zero) {
+        mul_scalar(c, tx2.c_(), tx2.m_(), count, 2, level, limb_scalars(c, kc[1], level));
+        rescale(c, tx2.c_(), Out, count, 2, level - 1);
+    } else {
+        Scratch inner(c, sizeof(uint64_t) * count * w1), xs(c, sizeof(uint64_t) * count * 2 * (level + 1) * N);
+        PtrTable tin(c, strided(inner.as<uint64_t>(), count, w1)),
+            txs(c, strided(xs.as<uint64_t>(), count, (size_t)2 * (level + 1) * N));
+        mul_scalar(c, X, txs.m_(), count, 2, level + 1, limb_scalars(c, kc[0], level + 1));
+        rescale(c, txs.c_(), tin.m_(), count, 2, level);
+        add_const(c, tin.m_(), count, level, limb_scalars(c, kc[1], level));
+        mul_batch(c, tx2.c_(), tin.c_(), Out, count, level - 1);
+    }
+    // c1 * x at level-2: drop to level-1, scalar, rescale
+    copy_limbs(c, X, ttmp.m_(), count, 2, level + 1, level, 0);
+    mul_scalar(c, ttmp.c_(), ttmp.m_(), count, 2, level, limb_scalars(c, kc[2], level));
+    rescale(c, ttmp.c_(), tt.m_(), count, 2, level - 1);
+    binop(c, (const uint64_t *const *)Out, tt.c_(), Out, count, 2, level - 1, 0);
+    add_const(c, Out, count, level - 1, limb_scalars(c, kc[3], level - 1));
+}
+
+}  // namespace vr

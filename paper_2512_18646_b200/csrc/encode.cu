@@ -1,0 +1,375 @@
+// encode.cu -- CKKS encode (canonical embedding), public/secret-key
+// encryption, decryption + decode, and key generation, all on the device.
+//
+// Encode/decode is a length-S complex FFT (S = N/2) twisted by zeta^k
+// (zeta = exp(i*pi/N)); slot j sits at DFT bin r_j = (5^j mod 2N - 1)/4, so the
+// Galois map X -> X^(5^l) is a LEFT rotation by l, matching np.roll(-l) in
+// engine.py:232-236.  Every floating-point operation uses explicit _rn
+// intrinsics in the same order as oracle/ckks_oracle.c (compiled with
+// -ffp-contract=off), so encoded integers are bit-identical to the oracle's.
+//
+// Randomness comes from the counter-based generator in modarith.cuh keyed by
+// (seed, domain, nonce/digit, limb): identical integers on CPU and GPU, so
+// ciphertext residues are bit-identical too.
+#include "encode.cuh"
+
+namespace vr {
+
+namespace {
+
+constexpr int TB = 256;
+
+__device__ __forceinline__ int64_t gauss(uint64_t u, const uint64_t *cdt) {
+    const uint64_t r = u >> 1;
+    int mag = 0;
+    while (mag < CDT_LEN - 1 && r >= cdt[mag]) mag++;
+    return (u & 1) ? -(int64_t)mag : (int64_t)mag;
+}
+
+__device__ __forceinline__ unsigned brev_bits(unsigned x, int bits) { return bits ? __brev(x) >> (32 - bits) : 0; }
+
+// In-place radix-2 DIT FFT over re/im (bit-reversed input already in place).
+__device__ void fft_stages(double *re, double *im, int S, const double *zr, const double *zi, bool inverse) {
+    for (int len = 2; len <= S; len <<= 1) {
+        const int half = len >> 1, step = S / len;
+        for (int b = threadIdx.x; b < S / 2; b += blockDim.x) {
+            const int blk = b / half, j = b - blk * half;
+            const int i0 = blk * len + j, i1 = i0 + half;
+            const int idx = 4 * j * step;
+            const double wr = zr[idx], wi = inverse ? -zi[idx] : zi[idx];
+            const double ar = re[i0], ai = im[i0], br = re[i1], bi = im[i1];
+            const double tr = __dsub_rn(__dmul_rn(br, wr), __dmul_rn(bi, wi));
+            const double ti = __dadd_rn(__dmul_rn(br, wi), __dmul_rn(bi, wr));
+            re[i0] = __dadd_rn(ar, tr);
+            im[i0] = __dadd_rn(ai, ti);
+            re[i1] = __dsub_rn(ar, tr);
+            im[i1] = __dsub_rn(ai, ti);
+        }
+        __syncthreads();
+    }
+}
+
+// one CTA per ciphertext: values [count][nvals] -> m [count][N] (int64)
+__global__ void k_encode(const double *vals, int nvals, int S, int logS, double f, const double *zr, const double *zi,
+                         const int *slot_pos, double *wre, double *wim, int64_t *m) {
+    const int c = blockIdx.x;
+    double *re = wre + (size_t)c * S, *im = wim + (size_t)c * S;
+    const double *v = vals + (size_t)c * nvals;
+    for (int j = threadIdx.x; j < S; j += blockDim.x) {
+        const int pos = brev_bits((unsigned)slot_pos[j], logS);
+        re[pos] = j < nvals ? v[j] : 0.0;
+        im[pos] = 0.0;
+    }
+    __syncthreads();
+    fft_stages(re, im, S, zr, zi, true);
+    int64_t *out = m + (size_t)c * 2 * S;
+    for (int k = threadIdx.x; k < S; k += blockDim.x) {
+        const double yr = re[k], yi = im[k];
+        const double xr = __dadd_rn(__dmul_rn(yr, zr[k]), __dmul_rn(yi, zi[k]));
+        const double xi = __dsub_rn(__dmul_rn(yi, zr[k]), __dmul_rn(yr, zi[k]));
+        out[k] = __double2ll_rn(__dmul_rn(xr, f));
+        out[k + S] = __double2ll_rn(__dmul_rn(xi, f));
+    }
+}
+
+// one CTA per ciphertext: centred m [count][N], scales[count] -> real slots [count][S]
+__global__ void k_decode(const int64_t *m, const double *scales, int S, int logS, const double *zr, const double *zi,
+                         const int *slot_pos, double *wre, double *wim, double *out) {
+    const int c = blockIdx.x;
+    double *re = wre + (size_t)c * S, *im = wim + (size_t)c * S;
+    const int64_t *mc = m + (size_t)c * 2 * S;
+    const double scale = scales[c];
+    for (int k = threadIdx.x; k < S; k += blockDim.x) {
+        const double ur = __ddiv_rn(__ll2double_rn(mc[k]), scale), ui = __ddiv_rn(__ll2double_rn(mc[k + S]), scale);
+        const int pos = brev_bits((unsigned)k, logS);
+        re[pos] = __dsub_rn(__dmul_rn(ur, zr[k]), __dmul_rn(ui, zi[k]));
+        im[pos] = __dadd_rn(__dmul_rn(ur, zi[k]), __dmul_rn(ui, zr[k]));
+    }
+    __syncthreads();
+    fft_stages(re, im, S, zr, zi, false);
+    double *o = out + (size_t)c * S;
+    for (int j = threadIdx.x; j < S; j += blockDim.x) o[j] = re[slot_pos[j]];
+}
+
+// m [count][N] (int64) -> residues [count][nl][N] (coefficient domain)
+__global__ void k_reduce_coeffs(const int64_t *m, int count, int nl, int N, DevPrimes pr, uint64_t *out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)count * nl * N) return;
+    const int k = (int)(e % N);
+    const long long ci = e / N;
+    const int i = (int)(ci % nl);
+    const long long c = ci / nl;
+    out[e] = from_i64(m[c * N + k], pr.m[i]);
+}
+
+// public-key encryption samples: buf [count][3][nl][N] = (v, m + e0, e1) per limb
+// secret-key encryption:          buf [count][2][nl][N] = (m + e, a (already NTT))
+__global__ void k_enc_sample(const int64_t *m, int count, int nl, int N, uint64_t seed, uint64_t nonce0, int sym,
+                             const uint64_t *cdt, DevPrimes pr, uint64_t *buf) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)count * N) return;
+    const long long c = e / N;
+    const int k = (int)(e - c * N);
+    const uint64_t nonce = nonce0 + (uint64_t)c;
+    const int64_t e0 = gauss(rnd(stream_key(seed, DOM_ENC_E0, nonce, 0), k), cdt) + m[e];
+    if (sym) {
+        uint64_t *b = buf + (size_t)c * 2 * nl * N;
+        for (int i = 0; i < nl; i++) {
+            b[(size_t)i * N + k] = from_i64(e0, pr.m[i]);
+            b[(size_t)(nl + i) * N + k] = sample_uniform(rnd(stream_key(seed, DOM_ENC_A, nonce, i), k), pr.m[i].q);
+        }
+        return;
+    }
+    const int64_t v = sample_ternary(rnd(stream_key(seed, DOM_ENC_V, nonce, 0), k));
+    const int64_t e1 = gauss(rnd(stream_key(seed, DOM_ENC_E1, nonce, 0), k), cdt);
+    uint64_t *b = buf + (size_t)c * 3 * nl * N;
+    for (int i = 0; i < nl; i++) {
+        b[(size_t)i * N + k] = from_i64(v, pr.m[i]);
+        b[(size_t)(nl + i) * N + k] = from_i64(e0, pr.m[i]);
+        b[(size_t)(2 * nl + i) * N + k] = from_i64(e1, pr.m[i]);
+    }
+}
+
+// combine NTT'd samples into ciphertexts out [count][2][nl][N]
+__global__ void k_enc_combine(const uint64_t *buf, int count, int nl, int N, int Ltop, int sym, const uint64_t *pk,
+                              const uint64_t *s_ntt, DevPrimes pr, uint64_t *out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)count * nl * N) return;
+    const int k = (int)(e % N);
+    const long long ci = e / N;
+    const int i = (int)(ci % nl);
+    const long long c = ci / nl;
+    const Modulus m = pr.m[i];
+    uint64_t *o = out + (size_t)c * 2 * nl * N;
+    if (sym) {
+        const uint64_t *b = buf + (size_t)c * 2 * nl * N;
+        const uint64_t me = b[(size_t)i * N + k], a = b[(size_t)(nl + i) * N + k];
+        o[(size_t)i * N + k] = sub_mod(me, mul_mod(a, s_ntt[(size_t)i * N + k], m), m.q);
+        o[(size_t)(nl + i) * N + k] = a;
+        return;
+    }
+    const uint64_t *b = buf + (size_t)c * 3 * nl * N;
+    const uint64_t v = b[(size_t)i * N + k], me0 = b[(size_t)(nl + i) * N + k], e1 = b[(size_t)(2 * nl + i) * N + k];
+    const uint64_t p0 = pk[(size_t)i * N + k], p1 = pk[(size_t)(Ltop + 1 + i) * N + k];
+    o[(size_t)i * N + k] = add_mod(mul_mod(v, p0, m), me0, m.q);
+    o[(size_t)(nl + i) * N + k] = add_mod(mul_mod(v, p1, m), e1, m.q);
+}
+
+// x[c][k] = c0 + c1 s (+ c2 s^2) on limb q0 (NTT domain)
+__global__ void k_dec_limb0(const uint64_t *const *C, const int *degs, const int *levels, int count, int N,
+                            const uint64_t *s_ntt, DevPrimes pr, uint64_t *x) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)count * N) return;
+    const long long c = e / N;
+    const int k = (int)(e - c * N);
+    const Modulus m = pr.m[0];
+    const uint64_t *ct = C[c];
+    const size_t nl = (size_t)levels[c] + 1;
+    const uint64_t s = s_ntt[k];
+    uint64_t v = add_mod(ct[k], mul_mod(ct[nl * N + k], s, m), m.q);
+    if (degs[c] == 2) v = add_mod(v, mul_mod(ct[2 * nl * N + k], mul_mod(s, s, m), m), m.q);
+    x[e] = v;
+}
+
+__global__ void k_center(const uint64_t *x, long long total, uint64_t q, int64_t *m) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const uint64_t v = x[e];
+    m[e] = v > (q >> 1) ? -(int64_t)(q - v) : (int64_t)v;
+}
+
+// ---- key generation ----
+__global__ void k_sample_secret(int n, int np, uint64_t seed, DevPrimes pr, uint64_t *s) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)np * n) return;
+    const int p = (int)(e / n), k = (int)(e - (long long)p * n);
+    const int64_t v = sample_ternary(rnd(stream_key(seed, DOM_SK, 0, 0), k));
+    s[e] = from_i64(v, pr.m[p]);
+}
+
+// pk: a_i uniform (NTT domain), e gaussian (coeff) -> buf_e [nl][N]
+__global__ void k_pk_sample(int n, int nl, uint64_t seed, const uint64_t *cdt, DevPrimes pr, uint64_t *pk_a, uint64_t *e_buf) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)nl * n) return;
+    const int i = (int)(e / n), k = (int)(e - (long long)i * n);
+    pk_a[e] = sample_uniform(rnd(stream_key(seed, DOM_PK_A, 0, i), k), pr.m[i].q);
+    e_buf[e] = from_i64(gauss(rnd(stream_key(seed, DOM_PK_E, 0, 0), k), cdt), pr.m[i]);
+}
+
+__global__ void k_pk_combine(int n, int nl, const uint64_t *s_ntt, const uint64_t *e_ntt, DevPrimes pr, uint64_t *pk) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)nl * n) return;
+    const int i = (int)(e / n);
+    const Modulus m = pr.m[i];
+    const uint64_t a = pk[(size_t)nl * n + e];
+    pk[e] = add_mod(neg_mod(mul_mod(a, s_ntt[e], m), m.q), e_ntt[e], m.q);
+}
+
+// switching key for s' (NTT, [np][N]): key [L+1][2][np][N]; e_buf [L+1][np][N]
+__global__ void k_gkey_sample(int n, int nd, int np, uint64_t seed, uint64_t dom_a, uint64_t dom_e, uint64_t id,
+                              const uint64_t *cdt, DevPrimes pr, uint64_t *key, uint64_t *e_buf) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)nd * np * n) return;
+    const int k = (int)(e % n);
+    const long long jp = e / n;
+    const int p = (int)(jp % np), j = (int)(jp / np);
+    key[(((size_t)j * 2 + 1) * np + p) * n + k] =
+        sample_uniform(rnd(stream_key(seed, dom_a, id, (uint64_t)j * 256 + p), k), pr.m[p].q);
+    e_buf[e] = from_i64(gauss(rnd(stream_key(seed, dom_e, id, j), k), cdt), pr.m[p]);
+}
+
+__global__ void k_gkey_combine(int n, int nd, int np, const uint64_t *s_ntt, const uint64_t *sp_ntt, const uint64_t *e_ntt,
+                               DevPrimes pr, uint64_t *key) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)nd * np * n) return;
+    const int k = (int)(e % n);
+    const long long jp = e / n;
+    const int p = (int)(jp % np), j = (int)(jp / np);
+    const Modulus m = pr.m[p];
+    const size_t pk_ = (size_t)p * n + k;
+    const uint64_t a = key[(((size_t)j * 2 + 1) * np + p) * n + k];
+    uint64_t v = add_mod(neg_mod(mul_mod(a, s_ntt[pk_], m), m.q), e_ntt[e], m.q);
+    if (p == j) {
+        const uint64_t pm = reduce64(pr.m[np - 1].q, m);
+        v = add_mod(v, mul_mod(pm, sp_ntt[pk_], m), m.q);
+    }
+    key[(((size_t)j * 2 + 0) * np + p) * n + k] = v;
+}
+
+__global__ void k_square(const uint64_t *s, int np, int n, DevPrimes pr, uint64_t *out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)np * n) return;
+    const int p = (int)(e / n);
+    out[e] = mul_mod(s[e], s[e], pr.m[p]);
+}
+
+__global__ void k_perm_rows(const uint64_t *in, int rows, int logN, uint32_t g, uint64_t *out) {
+    const int N = 1 << logN;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)rows * N) return;
+    const int k = (int)(e & (N - 1));
+    const uint32_t brk = __brev((uint32_t)k) >> (32 - logN);
+    const uint32_t ex = ((2u * brk + 1u) * g) & ((2u << logN) - 1u);
+    const int src = (int)(__brev((ex - 1u) >> 1) >> (32 - logN));
+    out[e] = in[(e - k) + src];
+}
+
+int log2i(int x) {
+    int l = 0;
+    while ((1 << l) < x) l++;
+    return l;
+}
+
+int fft_threads(int S) { return S >= 1024 ? 512 : (S >= 64 ? S / 2 : 32); }
+
+}  // namespace
+
+void encode_coeffs(Ctx &c, const double *d_vals, int count, int nvals, double scale, int64_t *d_m) {
+    const int S = c.slots;
+    Scratch wr(c, sizeof(double) * count * S), wi(c, sizeof(double) * count * S);
+    const double f = scale / (double)S;
+    k_encode<<<count, fft_threads(S), 0, c.stream>>>(d_vals, nvals, S, log2i(S), f, c.zr, c.zi, c.slot_pos, wr.as<double>(),
+                                                      wi.as<double>(), d_m);
+    check_launch("k_encode");
+}
+
+void encode_plain(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t *d_pt) {
+    const int N = c.n, nl = level + 1;
+    Scratch m(c, sizeof(int64_t) * count * N);
+    encode_coeffs(c, d_vals, count, nvals, scale, m.as<int64_t>());
+    k_reduce_coeffs<<<nblocks((long long)count * nl * N, TB), TB, 0, c.stream>>>(m.as<int64_t>(), count, nl, N, c.primes, d_pt);
+    check_launch("k_reduce_coeffs");
+    ntt_forward(c, batch_limbs(d_pt, count, nl, N));
+}
+
+void encrypt(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t nonce0, uint64_t *d_ct) {
+    const int N = c.n, nl = level + 1;
+    Scratch m(c, sizeof(int64_t) * count * N);
+    encode_coeffs(c, d_vals, count, nvals, scale, m.as<int64_t>());
+    const int rows = c.sym_enc ? 2 : 3;
+    Scratch buf(c, sizeof(uint64_t) * count * rows * nl * N);
+    k_enc_sample<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(m.as<int64_t>(), count, nl, N, c.seed, nonce0,
+                                                                         c.sym_enc, c.cdt, c.primes, buf.as<uint64_t>());
+    check_launch("k_enc_sample");
+    if (c.sym_enc) {
+        // only the (m + e) rows need a forward NTT: rows at [c][0][*]
+        ntt_forward(c, NttBatch{buf.as<uint64_t>(), count * nl, nl, (long long)2 * nl * N, nl, 0, 0, 0});
+    } else {
+        ntt_forward(c, batch_limbs(buf.as<uint64_t>(), count * 3, nl, N));
+    }
+    k_enc_combine<<<nblocks((long long)count * nl * N, TB), TB, 0, c.stream>>>(buf.as<uint64_t>(), count, nl, N, c.L,
+                                                                               c.sym_enc, c.pk, c.s_ntt, c.primes, d_ct);
+    check_launch("k_enc_combine");
+}
+
+void decrypt_decode(Ctx &c, const uint64_t *const *d_cts, const int *d_degs, const int *d_levels, const double *d_scales,
+                    int count, double *d_out, int64_t *d_coeffs_out) {
+    const int N = c.n, S = c.slots;
+    Scratch x(c, sizeof(uint64_t) * count * N), m(c, sizeof(int64_t) * count * N);
+    k_dec_limb0<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(d_cts, d_degs, d_levels, count, N, c.s_ntt, c.primes,
+                                                                        x.as<uint64_t>());
+    check_launch("k_dec_limb0");
+    ntt_inverse(c, NttBatch{x.as<uint64_t>(), count, 1, (long long)N, 1, 0, 0, 0});
+    int64_t *mp = d_coeffs_out ? d_coeffs_out : m.as<int64_t>();
+    k_center<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(x.as<uint64_t>(), (long long)count * N, c.q[0], mp);
+    check_launch("k_center");
+    if (!d_out) return;
+    Scratch wr(c, sizeof(double) * count * S), wi(c, sizeof(double) * count * S);
+    k_decode<<<count, fft_threads(S), 0, c.stream>>>(mp, d_scales, S, log2i(S), c.zr, c.zi, c.slot_pos, wr.as<double>(),
+                                                      wi.as<double>(), d_out);
+    check_launch("k_decode");
+}
+
+void keygen(Ctx &c) {
+    const int n = c.n, np = c.np, nl = c.L + 1;
+    VR_CUDA(cudaMallocAsync((void **)&c.s_ntt, sizeof(uint64_t) * np * n, c.stream));
+    k_sample_secret<<<nblocks((long long)np * n, TB), TB, 0, c.stream>>>(n, np, c.seed, c.primes, c.s_ntt);
+    check_launch("k_sample_secret");
+    ntt_forward(c, batch_limbs(c.s_ntt, 1, np, n));
+    VR_CUDA(cudaMallocAsync((void **)&c.pk, sizeof(uint64_t) * 2 * nl * n, c.stream));
+    Scratch e(c, sizeof(uint64_t) * nl * n);
+    k_pk_sample<<<nblocks((long long)nl * n, TB), TB, 0, c.stream>>>(n, nl, c.seed, c.cdt, c.primes, c.pk + (size_t)nl * n,
+                                                                     e.as<uint64_t>());
+    check_launch("k_pk_sample");
+    ntt_forward(c, batch_limbs(e.as<uint64_t>(), 1, nl, n));
+    k_pk_combine<<<nblocks((long long)nl * n, TB), TB, 0, c.stream>>>(n, nl, c.s_ntt, e.as<uint64_t>(), c.primes, c.pk);
+    check_launch("k_pk_combine");
+}
+
+static uint64_t *gen_switch_key(Ctx &c, const uint64_t *sp_ntt, uint64_t dom_a, uint64_t dom_e, uint64_t id) {
+    const int n = c.n, np = c.np, nd = c.L + 1;
+    uint64_t *key = nullptr;
+    VR_CUDA(cudaMalloc((void **)&key, sizeof(uint64_t) * c.key_words()));
+    Scratch e(c, sizeof(uint64_t) * nd * np * n);
+    const long long tot = (long long)nd * np * n;
+    k_gkey_sample<<<nblocks(tot, TB), TB, 0, c.stream>>>(n, nd, np, c.seed, dom_a, dom_e, id, c.cdt, c.primes, key,
+                                                         e.as<uint64_t>());
+    check_launch("k_gkey_sample");
+    ntt_forward(c, batch_limbs(e.as<uint64_t>(), nd, np, n));
+    k_gkey_combine<<<nblocks(tot, TB), TB, 0, c.stream>>>(n, nd, np, c.s_ntt, sp_ntt, e.as<uint64_t>(), c.primes, key);
+    check_launch("k_gkey_combine");
+    return key;
+}
+
+uint64_t *relin_key(Ctx &c) {
+    if (!c.rlk) {
+        Scratch s2(c, sizeof(uint64_t) * c.np * c.n);
+        k_square<<<nblocks((long long)c.np * c.n, TB), TB, 0, c.stream>>>(c.s_ntt, c.np, c.n, c.primes, s2.as<uint64_t>());
+        check_launch("k_square");
+        c.rlk = gen_switch_key(c, s2.as<uint64_t>(), DOM_RLK_A, DOM_RLK_E, 0);
+    }
+    return c.rlk;
+}
+
+uint64_t *galois_key(Ctx &c, uint32_t g) {
+    auto it = c.gkeys.find(g);
+    if (it != c.gkeys.end()) return it->second;
+    Scratch sg(c, sizeof(uint64_t) * c.np * c.n);
+    k_perm_rows<<<nblocks((long long)c.np * c.n, TB), TB, 0, c.stream>>>(c.s_ntt, c.np, c.log_n, g, sg.as<uint64_t>());
+    check_launch("k_perm_rows");
+    uint64_t *key = gen_switch_key(c, sg.as<uint64_t>(), DOM_GAL_A, DOM_GAL_E, g);
+    c.gkeys[g] = key;
+    return key;
+}
+
+}  // namespace vr

@@ -1,0 +1,22 @@
+// encode.cuh -- encode / encrypt / decrypt / keygen entry points (device level).
+#pragma once
+#include "ring.cuh"
+
+namespace vr {
+
+void encode_coeffs(Ctx &c, const double *d_vals, int count, int nvals, double scale, int64_t *d_m);
+void encode_plain(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t *d_pt);
+void encrypt(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t nonce0, uint64_t *d_ct);
+void decrypt_decode(Ctx &c, const uint64_t *const *d_cts, const int *d_degs, const int *d_levels, const double *d_scales,
+                    int count, double *d_out, int64_t *d_coeffs_out);
+void keygen(Ctx &c);
+
+// drivers (drivers.cu)
+void mul_batch(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *Out, int count, int level);
+void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out);
+void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, int k, const int64_t *w, const int64_t *bias,
+                  int F, const int *out_cols, int nout, const uint64_t *mask_pt, int level, const std::vector<uint64_t *> &Y);
+void poly_activation(Ctx &c, const uint64_t *const *X, int count, int level, const int64_t *kc, int c3_zero,
+                     uint64_t *const *Out);
+
+}  // namespace vr

@@ -1,0 +1,56 @@
+// ring.cuh -- device-level building blocks shared by abi.cu and the drivers.
+// All pointer-table arguments are DEVICE arrays of device pointers; each entry
+// addresses one ciphertext laid out [poly][limb][N] (limb i uses prime i).
+#pragma once
+#include "vrhe_internal.cuh"
+
+namespace vr {
+
+struct LimbScalars {
+    uint64_t v[MAXP], sh[MAXP];
+};
+LimbScalars limb_scalars(const Ctx &c, int64_t s, int nl);
+
+// elementwise (op 0 = add, 1 = sub)
+void binop(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *O, int count, int polys, int nl, int op);
+void tensor(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *O, int count, int nl);
+void mul_plain(Ctx &c, const uint64_t *const *C, const uint64_t *const *P, uint64_t *const *O, int count, int polys, int nl,
+               int shared_pt);
+void mul_scalar(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, const LimbScalars &s);
+void add_const(Ctx &c, uint64_t *const *C, int count, int nl, const LimbScalars &s);
+void permute(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, uint32_t g);
+void copy_limbs(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl_in, int nl_out, int limb0);
+void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl);
+void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O);
+
+// rescale: in [polys][l+1][N] -> out [polys][l][N] for each ciphertext
+void rescale(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int count, int polys, int level);
+
+// Key switching.  ModUp of `count` polys (each [l+1][N], NTT) into
+// D [count][l+1][l+2][N] (NTT form; target l+1 is the special prime).
+void modup(Ctx &c, const uint64_t *const *Polys, int count, int level, uint64_t *D);
+// Inner product with a key ([L+1][2][np][N]) followed by ModDown; the
+// Galois element g (1 = identity) permutes D on read (hoisted rotations).
+// Out: [count][2][l+1][N] contiguous; if Add0 != nullptr, Out[.][0] += perm_g(Add0[.]) and
+// Out[.][1] += perm_g(Add1[.]) (Add1 may be nullptr).
+void ks_inner_moddown(Ctx &c, const uint64_t *D, int count, int level, const uint64_t *key, uint32_t g, uint64_t *Out);
+
+// Convenience wrappers operating on pointer tables (device) of ciphertexts.
+void relin_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level);  // deg2 -> deg1, same level
+void rotate_batch(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int count, int level, int nrot, const uint32_t *gs);
+
+uint64_t *galois_key(Ctx &c, uint32_t g);
+uint64_t *relin_key(Ctx &c);
+
+// host helper: build a device pointer table
+struct PtrTable {
+    Scratch s;
+    PtrTable(Ctx &c, const std::vector<const uint64_t *> &v)
+        : s(c, sizeof(void *) * (v.empty() ? 1 : v.size())) {
+        if (!v.empty()) VR_CUDA(cudaMemcpyAsync(s.p, v.data(), sizeof(void *) * v.size(), cudaMemcpyHostToDevice, c.stream));
+    }
+    const uint64_t *const *c_() const { return (const uint64_t *const *)s.p; }
+    uint64_t *const *m_() const { return (uint64_t *const *)s.p; }
+};
+
+}  // namespace vr

@@ -1,0 +1,134 @@
+// vrhe_internal.cuh -- context, device tables and launch helpers shared by the
+// CUDA translation units of libvrhe.so.  Nothing here is exported; the C-ABI
+// lives in abi.cu and is declared in include/vrhe.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "modarith.cuh"
+
+namespace vr {
+
+constexpr int MAXP = 40;
+
+struct DevPrimes {
+    Modulus m[MAXP];
+};
+
+// Per-prime NTT scalars: n^-1 and (psi^-1_br[1] * n^-1), each with Shoup companion.
+struct NttConst {
+    uint64_t ninv, ninv_sh, w0n, w0n_sh;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = 0;
+    int log_n = 0, n = 0, slots = 0, L = 0, np = 0;  // np = L + 2 (ciphertext chain + special prime)
+    uint64_t q[MAXP] = {0};
+    DevPrimes primes;
+    uint64_t seed = 0;
+    int sym_enc = 0;
+
+    // device tables
+    uint64_t *tw = nullptr, *tw_sh = nullptr, *itw = nullptr, *itw_sh = nullptr;  // [np][N]
+    NttConst *ntt_const = nullptr;                                                 // [np]
+    uint64_t *inv_tab = nullptr;  // [np][np][2]: (q_a^-1 mod q_b, shoup)
+    double *zr = nullptr, *zi = nullptr;  // zeta^k, k < N
+    int *slot_pos = nullptr;              // [S]
+    uint64_t *cdt = nullptr;              // [CDT_LEN]
+
+    // keys (device)
+    uint64_t *s_ntt = nullptr;  // [np][N]
+    uint64_t *pk = nullptr;     // [2][L+1][N]
+    uint64_t *rlk = nullptr;    // [L+1][2][np][N]
+    std::map<uint32_t, uint64_t *> gkeys;
+
+    // host copies of small constants
+    std::vector<NttConst> h_ntt_const;
+    std::vector<uint64_t> h_inv_tab;
+
+    // pinned staging for pointer tables
+    void *pin = nullptr;
+    size_t pin_bytes = 0;
+
+    size_t key_words() const { return (size_t)(L + 1) * 2 * np * n; }
+};
+
+struct VrError : std::runtime_error {
+    int code;
+    VrError(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define VR_CUDA(call)                                                                              \
+    do {                                                                                           \
+        cudaError_t _e = (call);                                                                   \
+        if (_e != cudaSuccess)                                                                     \
+            throw ::vr::VrError(4, std::string(#call) + ": " + cudaGetErrorString(_e));            \
+    } while (0)
+
+// number of kernels launched by this library (bench.py reports it as gpu_launches)
+extern unsigned long long g_launches;
+
+inline void check_launch(const char *what) {
+    __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw VrError(4, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// stream-ordered scratch buffer
+struct Scratch {
+    Ctx &c;
+    void *p = nullptr;
+    Scratch(Ctx &cx, size_t bytes) : c(cx) {
+        if (bytes) VR_CUDA(cudaMallocAsync(&p, bytes, c.stream));
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, c.stream);
+    }
+    template <class T>
+    T *as() const { return (T *)p; }
+    Scratch(const Scratch &) = delete;
+};
+
+// Upload a small host array (pointer table etc.) to a stream-ordered device buffer.
+template <class T>
+struct DevArray {
+    Scratch s;
+    DevArray(Ctx &c, const T *host, size_t count) : s(c, sizeof(T) * (count ? count : 1)) {
+        if (count) VR_CUDA(cudaMemcpyAsync(s.p, host, sizeof(T) * count, cudaMemcpyHostToDevice, c.stream));
+    }
+    T *get() const { return s.as<T>(); }
+};
+
+// ---------------------------------------------------------------------------
+// NTT batch descriptor: transform t lives at
+//   data + (t / group) * gstride + (t % group) * N
+// and uses prime index  r < nq ? poff + r : pspecial   (r = t % group).
+// skip_diag > 0 skips transforms with r == (t / group) % skip_diag (ModUp digit's own prime).
+struct NttBatch {
+    uint64_t *data;
+    int count;
+    int group;
+    long long gstride;
+    int nq;
+    int poff;
+    int pspecial;
+    int skip_diag;
+};
+
+inline NttBatch batch_limbs(uint64_t *data, int polys, int limbs, int n) {
+    return NttBatch{data, polys * limbs, limbs, (long long)limbs * n, limbs, 0, 0, 0};
+}
+
+void ntt_forward(Ctx &c, const NttBatch &b);
+void ntt_inverse(Ctx &c, const NttBatch &b);
+
+// grid helper
+inline unsigned nblocks(long long work, int per_block) { return (unsigned)((work + per_block - 1) / per_block); }
+
+}  // namespace vr

@@ -1,0 +1,393 @@
+"""CkksEngine: the reference SlotEngine surface (engine.py:167-251) backed by
+RNS-CKKS on the B200 through libvrhe.so.
+
+Same methods, signatures, meter semantics and exceptions as the simulator:
+``enc, dec, add, mul, cmul, rot, mask, meter_snapshot, slots, params``.  A
+ciphertext carries (device residues, level, scale, depth, layout); depth keeps
+the reference's bookkeeping (add: max, mul/cmul: +1) and always equals
+``L - level`` because every multiplication consumes exactly one prime.
+
+Scale management: every level l has one canonical scale
+s[l] (s[L] = 2^delta, s[l-1] = s[l]^2 / q[l]).  Products are rescaled
+immediately, plaintext/constant operands are encoded at s[l], and an ``add``
+of operands at different levels brings the higher one down with one integer
+scalar multiplication + rescale, so results are always at the canonical scale
+of their level.  All of this runs on the GPU; the host only does bookkeeping.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import CapacityError, EngineError, LayoutError
+from .params import EngineParams, is_pow2, next_pow2
+
+__all__ = [
+    "EngineError",
+    "CapacityError",
+    "LayoutError",
+    "EngineParams",
+    "OpMeter",
+    "Ciphertext",
+    "PlainMask",
+    "CkksEngine",
+    "SlotEngine",
+    "is_pow2",
+    "next_pow2",
+]
+
+
+@dataclass
+class OpMeter:
+    """Operation counters, identical to engine.py:93-131."""
+
+    add_count: int = 0
+    mul_count: int = 0
+    cmul_count: int = 0
+    rot_count: int = 0
+    enc_count: int = 0
+    max_depth: int = 0
+
+    def copy(self) -> "OpMeter":
+        return replace(self)
+
+    def merged(self, other: "OpMeter") -> "OpMeter":
+        return OpMeter(
+            add_count=self.add_count + other.add_count,
+            mul_count=self.mul_count + other.mul_count,
+            cmul_count=self.cmul_count + other.cmul_count,
+            rot_count=self.rot_count + other.rot_count,
+            enc_count=self.enc_count + other.enc_count,
+            max_depth=max(self.max_depth, other.max_depth),
+        )
+
+    def delta_since(self, earlier: "OpMeter") -> "OpMeter":
+        return OpMeter(
+            add_count=self.add_count - earlier.add_count,
+            mul_count=self.mul_count - earlier.mul_count,
+            cmul_count=self.cmul_count - earlier.cmul_count,
+            rot_count=self.rot_count - earlier.rot_count,
+            enc_count=self.enc_count - earlier.enc_count,
+            max_depth=self.max_depth,
+        )
+
+
+def _frozen(values) -> np.ndarray:
+    out = np.array(values, dtype=np.float64)
+    out.flags.writeable = False
+    return out
+
+
+@dataclass(frozen=True, eq=False)
+class Ciphertext:
+    """Immutable RNS-CKKS ciphertext: residues [degree+1][level+1][N] on the GPU."""
+
+    data: torch.Tensor
+    level: int
+    scale: float
+    depth: int = 0
+    layout: tuple | None = None
+    engine_id: int = 0
+
+    @property
+    def degree(self) -> int:
+        return self.data.shape[0] - 1
+
+    def ptr(self) -> int:
+        return self.data.data_ptr()
+
+    def residues(self) -> np.ndarray:
+        """Copy of the residues as uint64 numpy (for parity checks)."""
+        return self.data.cpu().numpy().view(np.uint64)
+
+
+@dataclass(frozen=True, eq=False)
+class PlainMask:
+    """Plaintext constant vector for cmul (engine.py:153-164).  Filter masks are 0/1."""
+
+    values: np.ndarray
+    role: str = "constant"
+
+    def __post_init__(self):
+        if self.role == "filter":
+            vals = self.values
+            if not np.all((vals == 0.0) | (vals == 1.0)):
+                raise EngineError("filter masks may contain only 0.0 and 1.0")
+
+
+class CkksEngine:
+    """Metered RNS-CKKS engine over ``params.slots`` slots on one CUDA device."""
+
+    def __init__(self, params: EngineParams | None = None, device: int | None = None):
+        self.params = params if params is not None else EngineParams()
+        if not torch.cuda.is_available():
+            raise EngineError("CkksEngine needs a CUDA device (libvrhe has no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self._lib = _lib.load()
+        p = self.params
+        primes = (ctypes.c_uint64 * len(p.primes))(*p.primes)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.vr_ctx_create(p.log_n, len(p.prime_bits), primes, p.seed,
+                                               1 if p.encryption == "secret" else 0, self.device.index,
+                                               ctypes.byref(h)))
+            self._stream = torch.cuda.current_stream(self.device)
+        self._h = h
+        _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(self._stream.cuda_stream)))
+        self._meter = OpMeter()
+        self._nonce = 0
+        self._pin = None
+        self._pin_evt = None
+        self.h2d_bytes = 0
+        self.L = p.levels
+        self.N = p.n
+        self.q = list(p.primes)
+        self.scales = p.scale_chain()
+        self._id = id(self)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                self._lib.vr_ctx_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # -- basics -----------------------------------------------------------
+    @property
+    def slots(self) -> int:
+        return self.params.slots
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _observe(self, depth: int) -> None:
+        if depth > self._meter.max_depth:
+            self._meter.max_depth = depth
+
+    def meter_snapshot(self) -> OpMeter:
+        return self._meter.copy()
+
+    def _empty(self, degree: int, level: int, count: int | None = None) -> torch.Tensor:
+        shape = (degree + 1, level + 1, self.N) if count is None else (count, degree + 1, level + 1, self.N)
+        return torch.empty(shape, dtype=torch.int64, device=self.device)
+
+    def _wrap(self, data, level, depth, layout) -> Ciphertext:
+        return Ciphertext(data, level, self.scales[level], depth, layout, self._id)
+
+    def _check(self, ct: Ciphertext) -> None:
+        if not isinstance(ct, Ciphertext) or ct.engine_id != self._id:
+            raise EngineError("operands come from engines with different slot counts")
+
+    def _check_pair(self, a: Ciphertext, b: Ciphertext) -> None:
+        self._check(a)
+        self._check(b)
+
+    def _h2d(self, vals: np.ndarray) -> torch.Tensor:
+        """Host float64 array -> device, staged through a reusable pinned buffer."""
+        nbytes = vals.nbytes
+        if self._pin is None or self._pin.numel() < vals.size:
+            self._pin = torch.empty(max(vals.size, 1 << 16), dtype=torch.float64, pin_memory=True)
+            self._pin_evt = None
+        if self._pin_evt is not None:
+            self._pin_evt.synchronize()
+        stage = self._pin[: vals.size].view(vals.shape)
+        stage.numpy()[...] = vals
+        out = torch.empty(vals.shape, dtype=torch.float64, device=self.device)
+        out.copy_(stage, non_blocking=True)
+        self._pin_evt = torch.cuda.Event()
+        self._pin_evt.record(self._stream)
+        self.h2d_bytes += nbytes
+        return out
+
+    def _pad(self, rows) -> np.ndarray:
+        """List of value vectors -> zero-padded [count][width] float64 (width <= slots)."""
+        vecs = [np.asarray(v, dtype=np.float64).reshape(-1) for v in rows]
+        width = max([v.size for v in vecs] + [1])
+        if width > self.slots:
+            raise CapacityError(f"{width} values exceed {self.slots} slots")
+        out = np.zeros((len(vecs), width), dtype=np.float64)
+        for i, v in enumerate(vecs):
+            out[i, : v.size] = v
+        return out
+
+    # -- primitive API (engine.py:193-251) ---------------------------------
+    def enc(self, values, layout: tuple | None = None) -> Ciphertext:
+        """Encode into the leading slots (zeros elsewhere) and encrypt at the top level."""
+        return self.enc_batch([values], layout)[0]
+
+    def enc_batch(self, rows, layout: tuple | None = None) -> list[Ciphertext]:
+        """``enc`` of many vectors in one launch (one enc_count each)."""
+        vals = self._pad(rows)
+        count = vals.shape[0]
+        d_vals = self._h2d(vals)
+        out = self._empty(1, self.L, count)
+        _lib.check(self._lib.vr_encrypt(self._h, d_vals.data_ptr(), count, vals.shape[1], self.L,
+                                        self.scales[self.L], self._nonce, out.data_ptr()))
+        self._nonce += count
+        self._meter.enc_count += count
+        self._observe(0)
+        return [self._wrap(out[i], self.L, 0, layout) for i in range(count)]
+
+    def dec(self, ct: Ciphertext) -> np.ndarray:
+        """Full slot vector (real parts), like engine.py:204-206."""
+        return self.dec_batch([ct])[0]
+
+    def dec_batch(self, cts) -> np.ndarray:
+        cts = list(cts)
+        for ct in cts:
+            self._check(ct)
+        count = len(cts)
+        out = torch.empty((count, self.slots), dtype=torch.float64, device=self.device)
+        degs = (ctypes.c_int * count)(*[ct.degree for ct in cts])
+        lvls = (ctypes.c_int * count)(*[ct.level for ct in cts])
+        scl = (ctypes.c_double * count)(*[ct.scale for ct in cts])
+        _lib.check(self._lib.vr_decrypt_decode(self._h, _lib.ptr_array([ct.ptr() for ct in cts]), degs, lvls, scl,
+                                               count, out.data_ptr(), None))
+        return out.cpu().numpy()
+
+    def add(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+        self._check_pair(a, b)
+        a2, b2 = self._align(a, b)
+        depth = max(a.depth, b.depth)
+        out = self._binop(a2, b2, 0)
+        self._meter.add_count += 1
+        self._observe(depth)
+        return self._wrap(out, a2.level, depth, a.layout)
+
+    def sub(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+        """Not in the reference surface; metered as an add."""
+        self._check_pair(a, b)
+        a2, b2 = self._align(a, b)
+        depth = max(a.depth, b.depth)
+        out = self._binop(a2, b2, 1)
+        self._meter.add_count += 1
+        self._observe(depth)
+        return self._wrap(out, a2.level, depth, a.layout)
+
+    def mul(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+        self._check_pair(a, b)
+        a2, b2 = self._align(a, b)
+        lv = a2.level
+        if lv < 1:
+            raise EngineError("multiplicative depth exhausted: operands are at level 0")
+        out = self._empty(1, lv - 1)
+        _lib.check(self._lib.vr_mul(self._h, _lib.ptr_array([a2.ptr()]), _lib.ptr_array([b2.ptr()]),
+                                    _lib.ptr_array([out.data_ptr()]), 1, lv))
+        depth = max(a.depth, b.depth) + 1
+        self._meter.mul_count += 1
+        self._observe(depth)
+        return self._wrap(out, lv - 1, depth, a.layout)
+
+    def cmul(self, mask: PlainMask, ct: Ciphertext) -> Ciphertext:
+        if mask.values.size != self.slots:
+            raise EngineError(f"mask length {mask.values.size} != slot count {self.slots}")
+        self._check(ct)
+        lv = ct.level
+        if lv < 1:
+            raise EngineError("multiplicative depth exhausted: operand is at level 0")
+        vals = mask.values
+        tmp = self._empty(ct.degree, lv)
+        if np.all(vals == vals[0]):
+            k = int(round(float(vals[0]) * ct.scale))
+            _lib.check(self._lib.vr_mul_scalar(self._h, _lib.ptr_array([ct.ptr()]), k,
+                                               _lib.ptr_array([tmp.data_ptr()]), 1, ct.degree, lv))
+        else:
+            pt = self.encode_plain(vals, lv, ct.scale)
+            _lib.check(self._lib.vr_mul_plain(self._h, _lib.ptr_array([ct.ptr()]), _lib.ptr_array([pt.data_ptr()]),
+                                              _lib.ptr_array([tmp.data_ptr()]), 1, ct.degree, lv, 1))
+        out = self._empty(ct.degree, lv - 1)
+        _lib.check(self._lib.vr_rescale(self._h, _lib.ptr_array([tmp.data_ptr()]), _lib.ptr_array([out.data_ptr()]),
+                                        1, ct.degree, lv))
+        depth = ct.depth + 1
+        self._meter.cmul_count += 1
+        self._observe(depth)
+        return self._wrap(out, lv - 1, depth, ct.layout)
+
+    def rot(self, ct: Ciphertext, l: int) -> Ciphertext:
+        """Cyclic left rotation by ``l`` slots; negative ``l`` rotates right."""
+        self._check(ct)
+        self._meter.rot_count += 1
+        self._observe(ct.depth)
+        if int(l) % self.slots == 0:
+            return self._wrap(ct.data, ct.level, ct.depth, ct.layout)
+        return self._wrap(self.rotate_many(ct, [int(l)])[0], ct.level, ct.depth, ct.layout)
+
+    def mask(self, values, role: str = "constant") -> PlainMask:
+        vec = np.asarray(values, dtype=np.float64).reshape(-1)
+        if vec.size > self.slots:
+            raise CapacityError(f"mask payload {vec.size} exceeds {self.slots} slots")
+        full = np.zeros(self.slots, dtype=np.float64)
+        full[: vec.size] = vec
+        return PlainMask(_frozen(full), role=role)
+
+    # -- device-level helpers (no metering) --------------------------------
+    def encode_plain(self, values, level: int, scale: float) -> torch.Tensor:
+        vals = self._pad([values])
+        d_vals = self._h2d(vals)
+        pt = torch.empty((level + 1, self.N), dtype=torch.int64, device=self.device)
+        _lib.check(self._lib.vr_encode(self._h, d_vals.data_ptr(), 1, vals.shape[1], level, scale, pt.data_ptr()))
+        return pt
+
+    def _binop(self, a: Ciphertext, b: Ciphertext, op: int) -> torch.Tensor:
+        if a.degree != b.degree:
+            raise EngineError("operand degrees differ")
+        out = self._empty(a.degree, a.level)
+        _lib.check(self._lib.vr_add(self._h, _lib.ptr_array([a.ptr()]), _lib.ptr_array([b.ptr()]),
+                                    _lib.ptr_array([out.data_ptr()]), 1, a.degree, a.level, op))
+        return out
+
+    def rotate_many(self, ct: Ciphertext, steps) -> list[torch.Tensor]:
+        """Hoisted rotations of one ciphertext (one ModUp shared by all amounts)."""
+        steps = [int(s) for s in steps]
+        outs = [self._empty(1, ct.level) for _ in steps]
+        st = (ctypes.c_int64 * len(steps))(*steps)
+        _lib.check(self._lib.vr_rotate(self._h, _lib.ptr_array([ct.ptr()]), _lib.ptr_array([o.data_ptr() for o in outs]),
+                                       1, ct.level, len(steps), st))
+        return outs
+
+    def adjust(self, ct: Ciphertext, level: int) -> Ciphertext:
+        """Bring ``ct`` down to ``level`` at that level's canonical scale (no metering).
+
+        Drop to level+1, multiply by round(s[level] * q[level+1] / scale), rescale.
+        """
+        if level == ct.level:
+            return ct
+        if level > ct.level:
+            raise EngineError("cannot raise a ciphertext's level")
+        cur, lv = ct, ct.level
+        if lv > level + 1:
+            dropped = self._empty(cur.degree, level + 1)
+            _lib.check(self._lib.vr_drop_level(self._h, _lib.ptr_array([cur.ptr()]), _lib.ptr_array([dropped.data_ptr()]),
+                                               1, cur.degree, lv, level + 1))
+            cur = Ciphertext(dropped, level + 1, ct.scale, ct.depth, ct.layout, self._id)
+        k = int(round(self.scales[level] * float(self.q[level + 1]) / cur.scale))
+        tmp = self._empty(cur.degree, level + 1)
+        _lib.check(self._lib.vr_mul_scalar(self._h, _lib.ptr_array([cur.ptr()]), k, _lib.ptr_array([tmp.data_ptr()]),
+                                           1, cur.degree, level + 1))
+        out = self._empty(cur.degree, level)
+        _lib.check(self._lib.vr_rescale(self._h, _lib.ptr_array([tmp.data_ptr()]), _lib.ptr_array([out.data_ptr()]),
+                                        1, cur.degree, level + 1))
+        return Ciphertext(out, level, self.scales[level], ct.depth, ct.layout, self._id)
+
+    def _align(self, a: Ciphertext, b: Ciphertext):
+        if a.level == b.level:
+            if a.scale != b.scale:
+                raise EngineError("operands at the same level carry different scales")
+            return a, b
+        lv = min(a.level, b.level)
+        return self.adjust(a, lv), self.adjust(b, lv)
+
+    def sync(self) -> None:
+        _lib.check(self._lib.vr_sync(self._h))
+
+
+# The reference name: algorithm modules construct ``SlotEngine(EngineParams(...))``.
+SlotEngine = CkksEngine

@@ -1,0 +1,273 @@
+"""Multi-ciphertext encodings and their batched GPU evaluation.
+
+Same public names, signatures, validation and meter accounting as the
+reference (multicipher.py:23-172):
+
+* ``encode_left`` / ``encode_right``   n column ciphertexts per operand, all
+  encrypted in ONE launch (multicipher.py:62-85);
+* ``matmul_outer``   sum_k L_k * R_k as one fused tensor-sum kernel, then a
+  single relinearisation and rescale (multicipher.py:88-103);
+* ``encode_image_columns`` / ``conv_columns`` / ``reassemble_columns``
+  (multicipher.py:106-172): hoisted rotations shared by every tap, one MAC
+  kernel for all output columns.
+
+Extensions the BASELINE configs need and the reference lacks (SURVEY.md
+section 8d): ``conv_columns_multi`` (C input channels x F filters, the
+paper's channel sum, with an explicit output-column list so a
+stride-2 layer computes only even columns), ``matmul_outer_blocks`` (row-tiled
+left operand sharing one right operand) and ``pad_images``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .encoding import Encoding, Kernel, MatrixShape, PackedMatrix
+from .engine import CapacityError, Ciphertext, CkksEngine, EngineError, LayoutError
+
+__all__ = [
+    "ColumnEncodedMatrix",
+    "ColumnEncodedImage",
+    "encode_left",
+    "encode_right",
+    "matmul_outer",
+    "matmul_outer_blocks",
+    "encode_image_columns",
+    "conv_columns",
+    "conv_columns_multi",
+    "reassemble_columns",
+    "pad_images",
+    "conv_constants",
+]
+
+
+@dataclass(frozen=True, eq=False)
+class ColumnEncodedMatrix:
+    """n ciphertexts holding one matmul operand in broadcast form."""
+
+    cts: list
+    role: str  # "left" or "right"
+    m: int
+    n: int
+    p: int
+
+
+@dataclass(frozen=True, eq=False)
+class ColumnEncodedImage:
+    """w ciphertexts, one image column each; batched images stack at ``stride``."""
+
+    cts: list
+    h: int
+    w: int
+    m: int
+    stride: int
+
+
+def encode_left(engine: CkksEngine, a, p: int) -> ColumnEncodedMatrix:
+    """Ciphertext k = column k of A broadcast across an m x p grid (slot i*p+j = A[i,k])."""
+    a = np.atleast_2d(np.asarray(a, dtype=np.float64))
+    m, n = a.shape
+    if m * p > engine.slots:
+        raise CapacityError(f"{m}x{p} broadcast needs {m * p} slots, engine has {engine.slots}")
+    grids = np.repeat(a.T, p, axis=1)  # [n][m*p]
+    cts = engine.enc_batch(list(grids), layout=("grid", m, p))
+    return ColumnEncodedMatrix(cts, "left", m, n, p)
+
+
+def encode_right(engine: CkksEngine, b, m: int) -> ColumnEncodedMatrix:
+    """Ciphertext k = row k of B tiled down m grid rows (slot i*p+j = B[k,j])."""
+    b = np.atleast_2d(np.asarray(b, dtype=np.float64))
+    n, p = b.shape
+    if m * p > engine.slots:
+        raise CapacityError(f"{m}x{p} tiling needs {m * p} slots, engine has {engine.slots}")
+    grids = np.tile(b, (1, m))  # [n][m*p]
+    cts = engine.enc_batch(list(grids), layout=("grid", m, p))
+    return ColumnEncodedMatrix(cts, "right", m, n, p)
+
+
+def _common_level(engine: CkksEngine, cts):
+    lv = min(ct.level for ct in cts)
+    return [engine.adjust(ct, lv) for ct in cts], lv
+
+
+def matmul_outer(engine: CkksEngine, left: ColumnEncodedMatrix, right: ColumnEncodedMatrix) -> PackedMatrix:
+    """Sum of the n slot-wise products; no rotations, depth + 1 (multicipher.py:88-103)."""
+    if left.role != "left" or right.role != "right":
+        raise LayoutError("operands must be a (left, right) column-encoded pair")
+    if (left.n, left.m, left.p) != (right.n, right.m, right.p):
+        raise LayoutError(
+            f"operand dims differ: left {(left.m, left.n, left.p)}, right {(right.m, right.n, right.p)}"
+        )
+    ct = matmul_outer_blocks(engine, [left], right)[0]
+    return PackedMatrix(ct, MatrixShape(left.m, left.p), Encoding.ROW_MAJOR)
+
+
+def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -> list[Ciphertext]:
+    """Row-tiled matmul_outer: block b = sum_k L_b,k * R_k for 1, 2 or 4 blocks sharing R.
+
+    Meter: per block exactly the reference's n muls and n-1 adds.
+    """
+    nb = len(lefts)
+    if nb not in (1, 2, 4):
+        raise EngineError("matmul_outer_blocks supports 1, 2 or 4 row blocks")
+    n = right.n
+    for lf in lefts:
+        if lf.role != "left" or right.role != "right":
+            raise LayoutError("operands must be a (left, right) column-encoded pair")
+        if lf.n != n or lf.p != right.p:
+            raise LayoutError("row blocks must share n and p with the right operand")
+    allc = [c for lf in lefts for c in lf.cts] + list(right.cts)
+    for c in allc:
+        engine._check(c)
+    allc, lv = _common_level(engine, allc)
+    if lv < 1:
+        raise EngineError("multiplicative depth exhausted: operands are at level 0")
+    Ls, Rs = allc[: nb * n], allc[nb * n:]
+    outs = torch.empty((nb, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
+    _lib.check(engine._lib.vr_matmul_outer(
+        engine.handle, _lib.ptr_array([c.ptr() for c in Ls]), _lib.ptr_array([c.ptr() for c in Rs]), n, nb, lv,
+        _lib.ptr_array([outs[b].data_ptr() for b in range(nb)])))
+    res = []
+    for b, lf in enumerate(lefts):
+        depth = max(c.depth for c in list(lf.cts) + list(right.cts)) + 1
+        engine._meter.mul_count += n
+        engine._meter.add_count += n - 1
+        engine._observe(depth)
+        res.append(Ciphertext(outs[b], lv - 1, engine.scales[lv - 1], depth, lf.cts[0].layout, engine._id))
+    return res
+
+
+def encode_image_columns(engine: CkksEngine, images) -> ColumnEncodedImage:
+    """Split images into per-column ciphertexts (batch at stride h), multicipher.py:106-120."""
+    arr = np.asarray(images, dtype=np.float64)
+    if arr.ndim == 2:
+        arr = arr[None, :, :]
+    if arr.ndim != 3:
+        raise EngineError(f"expected one image or a batch, got ndim={arr.ndim}")
+    m, h, w = arr.shape
+    if m * h > engine.slots:
+        raise CapacityError(f"{m} columns of {h} pixels need {m * h} slots")
+    cols = np.transpose(arr, (2, 0, 1)).reshape(w, m * h)  # column j: slot b*h+i = img[b,i,j]
+    cts = engine.enc_batch(list(cols), layout=("column", h, m))
+    return ColumnEncodedImage(cts, h, w, m, stride=h)
+
+
+def pad_images(images, pad: int) -> np.ndarray:
+    """Zero padding on the host (the reference conv is valid-only, multicipher.py:132-134)."""
+    arr = np.asarray(images, dtype=np.float64)
+    widths = [(0, 0)] * (arr.ndim - 2) + [(pad, pad), (pad, pad)]
+    return np.pad(arr, widths)
+
+
+def conv_constants(engine: CkksEngine, level: int, scale: float, weights, biases):
+    """Integer tap weights, biases and the mask scale for the fused conv.
+
+    acc = sum w_int * x has scale ``scale * 2^delta_c``; the valid mask is encoded at
+    s_m = s[level] / 2^delta_c so that mask * acc, rescaled by q[level], lands exactly
+    on the canonical s[level-1].
+    """
+    dc = float(2 ** engine.params.delta_c)
+    w = np.asarray(weights, dtype=np.float64)
+    w_int = np.array([int(round(float(x) * dc)) for x in w.reshape(-1)], dtype=np.int64).reshape(w.shape)
+    b_int = np.array([int(round(float(b) * scale * dc)) for b in np.asarray(biases, dtype=np.float64).reshape(-1)],
+                     dtype=np.int64)
+    mask_scale = engine.scales[level] / dc
+    return w_int, b_int, mask_scale
+
+
+def _valid_mask(m: int, stride: int, out_h: int) -> np.ndarray:
+    valid = np.zeros((m, stride), dtype=np.float64)
+    valid[:, :out_h] = 1.0
+    return valid.reshape(-1)
+
+
+def conv_columns(engine: CkksEngine, img: ColumnEncodedImage, kernel: Kernel) -> ColumnEncodedImage:
+    """Valid convolution in the column domain (multicipher.py:123-162)."""
+    k = kernel.k
+    if k > img.h or k > img.w:
+        raise EngineError(f"{k}x{k} kernel larger than {img.h}x{img.w} image")
+    w4 = kernel.weights[None, None, :, :]
+    return conv_columns_multi(engine, [img], w4, [kernel.bias])[0]
+
+
+def _meter_conv_call(engine: CkksEngine, weights2d: np.ndarray, out_cols, depth_in: int) -> None:
+    """Meter exactly what one reference conv_columns call records (multicipher.py:139-161)."""
+    k = weights2d.shape[0]
+    nz = [(p, q) for q in range(k) for p in range(k) if weights2d[p, q] != 0.0]
+    rots = {(jp + q, p) for jp in out_cols for (p, q) in nz if p != 0}
+    m = engine._meter
+    m.rot_count += len(rots)
+    m.enc_count += len(out_cols)
+    m.cmul_count += len(nz) * len(out_cols)
+    m.add_count += len(nz) * len(out_cols)
+    engine._observe(depth_in + (1 if nz else 0))
+
+
+def conv_columns_multi(engine: CkksEngine, imgs, weights, biases, out_cols=None) -> list[ColumnEncodedImage]:
+    """F-filter, C-channel column convolution in one driver call.
+
+    ``weights`` is [F][C][k][k]; output filter f = sum_c conv_columns(imgs[c], K[f][c]) + bias[f],
+    restricted to ``out_cols`` (default: every valid column).  Rotations are computed once per
+    (channel, column, shift) and shared by all filters; the meter records the reference
+    composition (one conv_columns per (f, c) plus C-1 channel adds per filter).
+    """
+    imgs = list(imgs)
+    w = np.asarray(weights, dtype=np.float64)
+    if w.ndim != 4 or w.shape[2] != w.shape[3]:
+        raise EngineError(f"weights must be [F][C][k][k], got {w.shape}")
+    F, C, k, _ = w.shape
+    if len(imgs) != C:
+        raise LayoutError(f"{C} weight channels but {len(imgs)} images")
+    base = imgs[0]
+    for im in imgs:
+        if (im.h, im.w, im.m, im.stride) != (base.h, base.w, base.m, base.stride):
+            raise LayoutError("channel images must share h, w, m and stride")
+    if k > base.h or k > base.w:
+        raise EngineError(f"{k}x{k} kernel larger than {base.h}x{base.w} image")
+    out_h, out_w = base.h - k + 1, base.w - k + 1
+    cols = list(range(out_w)) if out_cols is None else [int(c) for c in out_cols]
+    if any(c < 0 or c >= out_w for c in cols):
+        raise EngineError("output column out of range")
+    biases = np.broadcast_to(np.asarray(biases, dtype=np.float64).reshape(-1), (F,))
+    X = [ct for im in imgs for ct in im.cts]
+    for ct in X:
+        engine._check(ct)
+    X, lv = _common_level(engine, X)
+    if lv < 1:
+        raise EngineError("multiplicative depth exhausted: operands are at level 0")
+    w_int, b_int, mask_scale = conv_constants(engine, lv, X[0].scale, w, biases)
+    mask_pt = engine.encode_plain(_valid_mask(base.m, base.stride, out_h), lv, mask_scale)
+    nout = len(cols)
+    Y = torch.empty((F, nout, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
+    yptrs = [Y[f, o].data_ptr() for f in range(F) for o in range(nout)]
+    w_c = np.ascontiguousarray(w_int, dtype=np.int64)
+    b_c = np.ascontiguousarray(b_int, dtype=np.int64)
+    cols_c = (ctypes.c_int * max(1, nout))(*cols)
+    _lib.check(engine._lib.vr_conv_columns(
+        engine.handle, _lib.ptr_array([c.ptr() for c in X]), C, base.w, k,
+        w_c.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), b_c.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), F,
+        cols_c, nout, mask_pt.data_ptr(), lv, _lib.ptr_array(yptrs)))
+    depth_in = max(ct.depth for ct in X)
+    out = []
+    for f in range(F):
+        for c in range(C):
+            _meter_conv_call(engine, w[f, c], cols, depth_in)
+        engine._meter.add_count += C - 1
+        cts = [Ciphertext(Y[f, o], lv - 1, engine.scales[lv - 1], depth_in + 1, ("column", out_h, base.m), engine._id)
+               for o in range(nout)]
+        out.append(ColumnEncodedImage(cts, out_h, nout, base.m, base.stride))
+    return out
+
+
+def reassemble_columns(engine: CkksEngine, img: ColumnEncodedImage) -> np.ndarray:
+    """Decode to an (m, h, w) array (multicipher.py:165-172); one batched decrypt."""
+    vecs = engine.dec_batch(img.cts)  # [w][slots]
+    out = np.empty((img.m, img.h, img.w), dtype=np.float64)
+    for b in range(img.m):
+        out[b, :, :] = vecs[:, b * img.stride: b * img.stride + img.h].T
+    return out

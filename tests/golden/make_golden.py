@@ -1,0 +1,94 @@
+"""Generate decoded-value fixtures by running the REFERENCE package itself.
+
+Run in the build container (needs /root/reference):
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+Writes tests/golden/reference_golden.npz.  Each case stores the seeded inputs,
+the reference outputs and the reference meter deltas, so tests can pin
+oracle/sim.py (and, on the GPU, the CKKS engine's decoded values) against the
+reference without /root/reference being present.
+"""
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+from packedhe.conv import Kernel  # noqa: E402
+from packedhe.engine import EngineParams, SlotEngine  # noqa: E402
+from packedhe.multicipher import (  # noqa: E402
+    conv_columns, encode_image_columns, encode_left, encode_right, matmul_outer, reassemble_columns)
+from packedhe.pipeline import poly_activation  # noqa: E402
+
+OUT = Path(__file__).resolve().parent / "reference_golden.npz"
+
+
+def meter_tuple(d):
+    return np.array([d.add_count, d.mul_count, d.cmul_count, d.rot_count, d.enc_count, d.max_depth])
+
+
+def main():
+    rng = np.random.default_rng(0xC0FFEE)
+    data = {}
+    # matmul_outer grid (acceptance criterion 2 shapes) + BASELINE cfg1/cfg2 shapes
+    mm = [(1, 1, 1), (2, 2, 2), (2, 4, 2), (4, 8, 4), (8, 2, 2), (8, 16, 4), (3, 5, 7)]
+    for idx, (m, n, p) in enumerate(mm):
+        a = rng.integers(-4, 5, size=(m, n)).astype(float)
+        b = rng.integers(-4, 5, size=(n, p)).astype(float)
+        eng = SlotEngine(EngineParams(slots=max(2, 1 << (m * p - 1).bit_length())))
+        left, right = encode_left(eng, a, p), encode_right(eng, b, m)
+        before = eng.meter_snapshot()
+        out = matmul_outer(eng, left, right)
+        d = eng.meter_snapshot().delta_since(before)
+        data[f"mm{idx}_a"], data[f"mm{idx}_b"] = a, b
+        data[f"mm{idx}_c"] = out.decode(eng)
+        data[f"mm{idx}_meter"] = meter_tuple(d)
+        data[f"mm{idx}_depth"] = np.array([out.ct.depth])
+    for cfg, (seed, dim, slots) in {1: (0, 8, 4096), 2: (1, 64, 8192)}.items():
+        r = np.random.default_rng(seed)
+        a = r.uniform(-1, 1, (dim, dim))
+        b = r.uniform(-1, 1, (dim, dim))
+        eng = SlotEngine(EngineParams(slots=slots))
+        out = matmul_outer(eng, encode_left(eng, a, dim), encode_right(eng, b, dim))
+        data[f"cfg{cfg}_a"], data[f"cfg{cfg}_b"], data[f"cfg{cfg}_c"] = a, b, out.decode(eng)
+    # conv_columns cases
+    cc = [(2, 6, 6, 3, 0.5), (1, 5, 7, 2, -1.0), (3, 8, 5, 3, 0.0), (2, 16, 16, 3, 0.5), (1, 9, 9, 5, 2.0)]
+    for idx, (m, h, w, k, bias) in enumerate(cc):
+        imgs = rng.integers(-2, 5, size=(m, h, w)).astype(float)
+        kw = rng.integers(-4, 5, size=(k, k)).astype(float)
+        kw[0, k - 1] = 0.0  # exercise the zero-tap skip
+        eng = SlotEngine(EngineParams(slots=max(2, 1 << (m * h - 1).bit_length())))
+        cei = encode_image_columns(eng, imgs)
+        before = eng.meter_snapshot()
+        out = conv_columns(eng, cei, Kernel(kw, bias=bias))
+        d = eng.meter_snapshot().delta_since(before)
+        data[f"cv{idx}_img"], data[f"cv{idx}_w"], data[f"cv{idx}_bias"] = imgs, kw, np.array([bias])
+        data[f"cv{idx}_out"] = reassemble_columns(eng, out)
+        data[f"cv{idx}_meter"] = meter_tuple(d)
+    # poly_activation cases
+    pc = [(0.25, 0.5, 0.125, 0.0), (-0.00015120704, 0.4610149, 2.0225089, -1.4511951),
+          (-1.5650465, -0.9943767, 1.6794522, 0.5350255), (0.0, 1.0, 0.0, 0.0)]
+    for idx, coeffs in enumerate(pc):
+        x = rng.uniform(-1, 1, size=16)
+        eng = SlotEngine(EngineParams(slots=16))
+        ct = eng.enc(x)
+        before = eng.meter_snapshot()
+        out = poly_activation(eng, ct, coeffs)
+        d = eng.meter_snapshot().delta_since(before)
+        data[f"pa{idx}_x"], data[f"pa{idx}_coeffs"] = x, np.array(coeffs)
+        data[f"pa{idx}_out"] = eng.dec(out)
+        data[f"pa{idx}_meter"] = meter_tuple(d)
+        data[f"pa{idx}_depth"] = np.array([out.depth])
+    # rotation golden (test_engine.py:87-106)
+    eng = SlotEngine(EngineParams(slots=8))
+    x = np.arange(1, 9, dtype=float)
+    ct = eng.enc(x)
+    data["rot_x"] = x
+    data["rot_steps"] = np.array([1, -1, 3, 8, -9])
+    data["rot_out"] = np.stack([eng.dec(eng.rot(ct, s)) for s in data["rot_steps"]])
+    np.savez_compressed(OUT, **data)
+    print(f"wrote {OUT} ({len(data)} arrays)")
+
+
+if __name__ == "__main__":
+    main()
