@@ -112,8 +112,9 @@ int vr_tensor_sum(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *
                   uint64_t *const *out);
 /* conv_columns (multicipher.py:123-162) for C channels x F filters:
  *   Y[f*nout+o] = rescale(mask * (sum_{c,q,p} w[f][c][p][q] * rot(X[c*W + cols[o]+q], p) + bias[f]))
- * w: host int64 [F][C][k][k] (quantised weights), bias: host int64 [F], mask: device plaintext [level+1][N] */
-int vr_conv_columns(vr_ctx *ctx, const uint64_t *const *X, int C, int W, int k, const int64_t *w, const int64_t *bias, int F,
+ * w: host int64 [F][C][k][k] (quantised weights), bias_res: host [F][level+1] residues of the bias
+ * integer (it may exceed 64 bits), mask: device plaintext [level+1][N] */
+int vr_conv_columns(vr_ctx *ctx, const uint64_t *const *X, int C, int W, int k, const int64_t *w, const uint64_t *bias_res, int F,
                     const int *out_cols, int nout, const uint64_t *mask_pt, int level, uint64_t *const *Y);
 /* poly_activation (pipeline.py:180-197) on a batch; kc = integer constants {c3, c2, c1, c0} at their
  * target scales */

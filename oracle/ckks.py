@@ -73,7 +73,7 @@ def lib():
         L.orc_mul.argtypes = [vp, u64p, u64p, ctypes.c_int, u64p]
         L.orc_matmul_outer.argtypes = [vp, ctypes.POINTER(u64p), ctypes.POINTER(u64p), ctypes.c_int, ctypes.c_int, u64p]
         L.orc_conv_columns.argtypes = [
-            vp, ctypes.POINTER(u64p), ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, i64p, ctypes.c_int,
+            vp, ctypes.POINTER(u64p), ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, u64p, ctypes.c_int,
             ctypes.POINTER(ctypes.c_int), ctypes.c_int, u64p, ctypes.c_int, ctypes.POINTER(u64p),
         ]
         L.orc_poly_activation.argtypes = [vp, u64p, ctypes.c_int, i64p, ctypes.c_int, u64p]
@@ -296,17 +296,17 @@ class OracleCkks:
         lib().orc_matmul_outer(self._c, la, ra, n, lvl, _p(out))
         return out
 
-    def conv_columns(self, X, C, W, k, w_int, bias_int, F, out_cols, mask_pt):
-        """X: list of C*W cts; w_int: int64 [F][C][k][k]; bias_int: int64 [F]."""
+    def conv_columns(self, X, C, W, k, w_int, bias_res, F, out_cols, mask_pt):
+        """X: list of C*W cts; w_int: int64 [F][C][k][k]; bias_res: uint64 [F][l+1] residues."""
         lvl = X[0].shape[1] - 1
         xa = (u64p * len(X))(*[_p(x) for x in X])
         w_int = np.ascontiguousarray(w_int, dtype=np.int64)
-        bias_int = np.ascontiguousarray(bias_int, dtype=np.int64)
+        bias_res = np.ascontiguousarray(bias_res, dtype=np.uint64)
         cols = (ctypes.c_int * len(out_cols))(*[int(c) for c in out_cols])
         Y = [self._ct(1, lvl - 1) for _ in range(F * len(out_cols))]
         ya = (u64p * len(Y))(*[_p(y) for y in Y])
         lib().orc_conv_columns(
-            self._c, xa, C, W, k, _p(w_int, i64p), _p(bias_int, i64p), F, cols, len(out_cols),
+            self._c, xa, C, W, k, _p(w_int, i64p), _p(bias_res), F, cols, len(out_cols),
             _p(np.ascontiguousarray(mask_pt)), lvl, ya,
         )
         return Y

@@ -777,11 +777,12 @@ void orc_matmul_outer(orc_ctx *c, const uint64_t *const *Ls, const uint64_t *con
  * channels and F filters (the paper's channel sum):
  *   Y[f][o] = rescale( mask * ( sum_{c,p,q} w[f][c][p][q] * rot(X[c][out_cols[o]+q], p)
  *                               + bias[f] ) )
- * w: int64 [F][C][k][k] (already quantised), bias: int64 [F] (at the
- * accumulator scale), mask: plaintext [l+1][N] NTT.  X: C*W pointers,
+ * w: int64 [F][C][k][k] (already quantised), bias_res: [F][l+1] residues of
+ * the bias integer at the accumulator scale (it can exceed 64 bits),
+ * mask: plaintext [l+1][N] NTT.  X: C*W pointers,
  * Y: F*nout pointers, each [2][l][N]. */
 void orc_conv_columns(orc_ctx *c, const uint64_t *const *X, int C, int W, int k, const int64_t *w,
-                      const int64_t *bias, int F, const int *out_cols, int nout, const uint64_t *mask,
+                      const uint64_t *bias_res, int F, const int *out_cols, int nout, const uint64_t *mask,
                       int level, uint64_t *const *Y) {
     const int n = c->n, nl = level + 1;
     const size_t ctw = (size_t)2 * nl * n;
@@ -819,7 +820,10 @@ void orc_conv_columns(orc_ctx *c, const uint64_t *const *X, int C, int W, int k,
                                 for (int kk = 0; kk < n; kk++) acc[off + kk] = addmod(acc[off + kk], mulmod(src[off + kk], wv, q), q);
                             }
                     }
-            orc_add_const(c, acc, bias[f], level);
+            for (int i = 0; i < nl; i++) {
+                const uint64_t q = c->q[i], bv = bias_res[(size_t)f * nl + i] % q;
+                for (int kk = 0; kk < n; kk++) acc[(size_t)i * n + kk] = addmod(acc[(size_t)i * n + kk], bv, q);
+            }
             orc_mul_plain(c, acc, mask, 1, level, acc);
             orc_rescale(c, acc, 1, level, Y[f * nout + o]);
             free(acc);

@@ -122,12 +122,12 @@ class OracleEngine:
         dc = float(2 ** self.delta_c)
         w_int = np.array([int(round(float(x) * dc)) for x in w.reshape(-1)], dtype=np.int64).reshape(w.shape)
         scale = X[0].scale
-        b_int = np.array([int(round(float(b) * scale * dc)) for b in np.broadcast_to(np.asarray(biases, dtype=np.float64).reshape(-1), (F,))],
-                         dtype=np.int64)
+        b_ints = [int(round(float(b) * scale * dc)) for b in np.broadcast_to(np.asarray(biases, dtype=np.float64).reshape(-1), (F,))]
+        b_res = np.array([[bi % self.q[i] for i in range(lv + 1)] for bi in b_ints], dtype=np.uint64)
         valid = np.zeros((m, stride))
         valid[:, :out_h] = 1.0
         mask_pt = self.c.encode(valid.reshape(-1), lv, self.scales[lv] / dc)
-        Y = self.c.conv_columns([x.data for x in X], C, W, k, w_int, b_int, F, list(out_cols), mask_pt)
+        Y = self.c.conv_columns([x.data for x in X], C, W, k, w_int, b_res, F, list(out_cols), mask_pt)
         return [OCt(y, lv - 1, self.scales[lv - 1]) for y in Y]
 
     def poly_activation(self, ct: OCt, coeffs) -> OCt:

@@ -97,6 +97,24 @@ void check_level(const vr::Ctx &c, int level) {
 
 namespace vr {
 unsigned long long g_launches = 0;
+
+void upload_async(Ctx &c, void *dst, const void *src, size_t bytes) {
+    const char *p = (const char *)src;
+    char *d = (char *)dst;
+    while (bytes) {
+        const size_t chunk = bytes < Ctx::kStageBytes ? bytes : Ctx::kStageBytes;
+        const int slot = c.stage_next;
+        c.stage_next = (c.stage_next + 1) % Ctx::kStageSlots;
+        VR_CUDA(cudaEventSynchronize(c.stage_evt[slot]));  // previous copy out of this slot is done
+        char *h = c.stage + (size_t)slot * Ctx::kStageBytes;
+        std::memcpy(h, p, chunk);
+        VR_CUDA(cudaMemcpyAsync(d, h, chunk, cudaMemcpyHostToDevice, c.stream));
+        VR_CUDA(cudaEventRecord(c.stage_evt[slot], c.stream));
+        p += chunk;
+        d += chunk;
+        bytes -= chunk;
+    }
+}
 }
 
 extern "C" {
@@ -130,7 +148,7 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
             u128h r = (~(u128h)0) / q;
             c.primes.m[p] = vr::Modulus{q, (uint64_t)(r >> 64), (uint64_t)r};
         }
-        std::vector<uint64_t> tw((size_t)np * n), tws((size_t)np * n), itw((size_t)np * n), itws((size_t)np * n);
+        std::vector<ulonglong2> tw((size_t)np * n), itw((size_t)np * n);
         c.h_ntt_const.resize(np);
         for (int p = 0; p < np; p++) {
             const uint64_t q = c.q[p];
@@ -140,13 +158,11 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
             for (int i = 1; i < n; i++) { pw[i] = h_mulmod(pw[i - 1], psi, q); ipw[i] = h_mulmod(ipw[i - 1], ipsi, q); }
             for (int i = 0; i < n; i++) {
                 const uint32_t r = h_brev(i, log_n);
-                tw[(size_t)p * n + i] = pw[r];
-                tws[(size_t)p * n + i] = h_shoup(pw[r], q);
-                itw[(size_t)p * n + i] = ipw[r];
-                itws[(size_t)p * n + i] = h_shoup(ipw[r], q);
+                tw[(size_t)p * n + i] = make_ulonglong2(pw[r], h_shoup(pw[r], q));
+                itw[(size_t)p * n + i] = make_ulonglong2(ipw[r], h_shoup(ipw[r], q));
             }
             const uint64_t ninv = h_inv((uint64_t)n % q, q);
-            const uint64_t w0n = h_mulmod(itw[(size_t)p * n + 1], ninv, q);
+            const uint64_t w0n = h_mulmod(itw[(size_t)p * n + 1].x, ninv, q);
             c.h_ntt_const[p] = vr::NttConst{ninv, h_shoup(ninv, q), w0n, h_shoup(w0n, q)};
         }
         c.h_inv_tab.assign((size_t)np * np * 2, 0);
@@ -169,10 +185,8 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         std::vector<uint64_t> cdt(vr::CDT_LEN);
         build_cdt(cdt.data());
 
-        c.tw = upload(c, tw);
-        c.tw_sh = upload(c, tws);
-        c.itw = upload(c, itw);
-        c.itw_sh = upload(c, itws);
+        c.tw2 = upload(c, tw);
+        c.itw2 = upload(c, itw);
         c.ntt_const = upload(c, c.h_ntt_const);
         c.inv_tab = upload(c, c.h_inv_tab);
         c.zr = upload(c, zr);
@@ -180,6 +194,16 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         c.slot_pos = upload(c, sp);
         c.cdt = upload(c, cdt);
         VR_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        VR_CUDA(cudaMallocHost((void **)&c.stage, (size_t)vr::Ctx::kStageSlots * vr::Ctx::kStageBytes));
+        for (int i = 0; i < vr::Ctx::kStageSlots; i++)
+            VR_CUDA(cudaEventCreateWithFlags(&c.stage_evt[i], cudaEventDisableTiming));
+        {
+            // keep freed scratch in the stream-ordered pool instead of returning it at every sync
+            cudaMemPool_t pool;
+            VR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t thr = ~0ull;
+            VR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
         vr::keygen(c);
         VR_CUDA(cudaStreamSynchronize(c.stream));
         // a user stream replaces the private one via vr_set_stream; keep the private one alive
@@ -193,12 +217,15 @@ int vr_ctx_destroy(vr_ctx *h) {
         vr::Ctx &c = h->c;
         cudaSetDevice(c.device);
         cudaDeviceSynchronize();
-        void *ptrs[] = {c.tw, c.tw_sh, c.itw, c.itw_sh, c.ntt_const, c.inv_tab, c.zr, c.zi, c.slot_pos, c.cdt, c.rlk};
+        void *ptrs[] = {c.tw2, c.itw2, c.ntt_const, c.inv_tab, c.zr, c.zi, c.slot_pos, c.cdt, c.rlk};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (c.s_ntt) cudaFree(c.s_ntt);
         if (c.pk) cudaFree(c.pk);
         for (auto &kv : c.gkeys) cudaFree(kv.second);
+        for (int i = 0; i < vr::Ctx::kStageSlots; i++)
+            if (c.stage_evt[i]) cudaEventDestroy(c.stage_evt[i]);
+        if (c.stage) cudaFreeHost(c.stage);
         delete h;
     });
 }
@@ -408,11 +435,8 @@ int vr_keyswitch(vr_ctx *h, const uint64_t *poly, int level, uint32_t g, uint64_
         check_level(h->c, level);
         vr::Ctx &c = h->c;
         const uint64_t *key = g == 0 ? vr::relin_key(c) : vr::galois_key(c, g);
-        vr::Scratch d(c, sizeof(uint64_t) * (size_t)(level + 1) * (level + 2) * c.n);
-        std::vector<const uint64_t *> p{poly};
-        vr::PtrTable tp(c, p);
-        vr::modup(c, tp.c_(), 1, level, d.as<uint64_t>());
-        vr::ks_inner_moddown(c, d.as<uint64_t>(), 1, level, key, 1, out);
+        vr::PtrTable tp(c, std::vector<const uint64_t *>{poly}), to(c, std::vector<const uint64_t *>{out});
+        vr::keyswitch_poly(c, tp.c_(), 1, level, key, to.m_());
     });
 }
 
@@ -444,7 +468,7 @@ int vr_tensor_sum(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *R,
     });
 }
 
-int vr_conv_columns(vr_ctx *h, const uint64_t *const *X, int C, int W, int k, const int64_t *w, const int64_t *bias, int F,
+int vr_conv_columns(vr_ctx *h, const uint64_t *const *X, int C, int W, int k, const int64_t *w, const uint64_t *bias, int F,
                     const int *out_cols, int nout, const uint64_t *mask_pt, int level, uint64_t *const *Y) {
     return guard([&] {
         check_level(h->c, level);

@@ -92,7 +92,7 @@ void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, in
     rescale(c, tr.c_(), Out, nb, 2, level);
 }
 
-void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, int k, const int64_t *w, const int64_t *bias,
+void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, int k, const int64_t *w, const uint64_t *bias,
                   int F, const int *out_cols, int nout, const uint64_t *mask_pt, int level, const std::vector<uint64_t *> &Y) {
     const int N = c.n, nl = level + 1;
     const size_t ctw = (size_t)2 * nl * N;
@@ -155,7 +155,7 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
     for (int i = 0; i < nl; i++) {
         const Modulus &m = c.primes.m[i];
         for (size_t t = 0; t < (size_t)F * C * k * k; t++) wq[(size_t)i * F * C * k * k + t] = from_i64(w[t], m);
-        for (int f = 0; f < F; f++) bq[(size_t)i * F + f] = from_i64(bias[f], m);
+        for (int f = 0; f < F; f++) bq[(size_t)i * F + f] = reduce64(bias[(size_t)f * nl + i], m);
     }
     DevArray<uint64_t> dwq(c, wq.data(), wq.size()), dbq(c, bq.data(), bq.size());
     DevArray<int> dcols(c, out_cols, nout);

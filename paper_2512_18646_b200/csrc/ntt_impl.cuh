@@ -1,0 +1,363 @@
+// ntt_impl.cuh -- batched negacyclic NTT / INTT kernels with fused prologues
+// and epilogues (included by ntt.cu and keyswitch.cu).
+//
+// Transform definition (identical to oracle/ckks_oracle.c orc_ntt/orc_intt):
+//   forward  = Cooley-Tukey, natural in -> bit-reversed out; stage g pairs
+//              elements at distance N >> (g+1) with twiddle
+//              psi_br[2^g + (E >> (logN - g))]  (E = index of the upper element);
+//   inverse  = Gentleman-Sande with psi^-1 in the same indexing, times N^-1.
+//
+// Structure.  N = N1 * N2.  Pass 1 runs stages g < log N1 on "columns"
+// {c + r*N2}; a CTA stages TPC adjacent columns (coalesced rows).  Pass 2 runs
+// the remaining stages inside contiguous N2-element rows.  Each thread owns 8
+// elements and performs up to three stages per radix-8 group in registers;
+// groups exchange through (swizzled) shared memory.  The group schedule is a
+// compile-time function of the tile size, so every index is constant-folded.
+// Butterflies are Harvey-lazy (forward values in [0,4q), inverse [0,2q)) with
+// Shoup twiddle products; twiddles and their Shoup companions are stored
+// interleaved so each butterfly issues one 16-byte load.  The inverse folds
+// N^-1 into its last stage.
+//
+// Fusion.  The first pass reads its input through a Load functor and the last
+// pass writes through a Store functor, so base conversions (centred lift from
+// another prime), pointer-table gathers and the ModDown / rescale combine
+// "(a - z) * q^-1" run inside the transform instead of as separate kernels.
+#pragma once
+#include "vrhe_internal.cuh"
+
+namespace vr {
+namespace nttk {
+
+__device__ __forceinline__ bool locate(const NttBatch &b, int t, int N, uint64_t *&ptr, int &pidx) {
+    const int g = t / b.group, r = t - g * b.group;
+    if (b.skip_diag > 0 && r == g % b.skip_diag) return false;
+    ptr = b.data + (long long)g * b.gstride + (long long)r * N;
+    pidx = r < b.nq ? b.poff + r : b.pspecial;
+    return true;
+}
+
+template <bool COLS>
+__device__ __forceinline__ int sidx(int j, int L, int T, int TPC) {
+    if (COLS) return L * TPC + j;
+    return j * T + (L ^ ((L >> 4) & 15));
+}
+
+__device__ __forceinline__ void bf_fwd(uint64_t &X, uint64_t &Y, ulonglong2 w, uint64_t q, uint64_t q2) {
+    const uint64_t x = X >= q2 ? X - q2 : X;
+    const uint64_t t = mul_shoup_lazy(Y, w.x, w.y, q);
+    X = x + t;
+    Y = x - t + q2;
+}
+
+__device__ __forceinline__ void bf_inv(uint64_t &X, uint64_t &Y, ulonglong2 w, uint64_t q, uint64_t q2) {
+    uint64_t t = X + Y;
+    t = t >= q2 ? t - q2 : t;
+    const uint64_t u = X - Y + q2;
+    Y = mul_shoup_lazy(u, w.x, w.y, q);
+    X = t;
+}
+
+// ---- load functors (first pass of a transform) -----------------------------
+struct LdPlain {
+    __device__ __forceinline__ uint64_t operator()(const uint64_t *ptr, int, long long E, const DevPrimes &, int) const {
+        return ptr[E];
+    }
+};
+// centred lift of src[(t / div) * N + E] from prime (from_fixed >= 0 ? from_fixed : (t/div) % mod) into the target prime
+struct LdLift {
+    const uint64_t *src;
+    int div, mod, from_fixed, N;
+    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int pidx) const {
+        const int row = t / div;
+        const int fp = from_fixed >= 0 ? from_fixed : row % mod;
+        return lift_centered(src[(long long)row * N + E], pr.m[fp].q, pr.m[pidx]);
+    }
+};
+// ptrs[t / div] + (t % div) * stride + off + E
+struct LdGather {
+    const uint64_t *const *ptrs;
+    int div;
+    long long stride, off;
+    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &, int) const {
+        const int a = t / div;
+        return ptrs[a][(long long)(t - a * div) * stride + off + E];
+    }
+};
+
+// ---- store functors (last pass) ------------------------------------------------
+struct StPlain {
+    __device__ __forceinline__ void operator()(uint64_t *ptr, int, long long E, uint64_t v, const DevPrimes &, int) const {
+        ptr[E] = v;
+    }
+};
+// t = row * nout + i;  row = r0 * rdiv + r1:
+//   out = (A[r0][(r1 * a_limbs + i) * N + E] - v) * inv_i  (+ add[r0][(r1 * nout + i) * N + perm_g(E)] if r1 < add_polys)
+//   written to O[r0][(r1 * nout + i) * N + E]
+struct StCombine {
+    const uint64_t *const *A;
+    uint64_t *const *O;
+    const uint64_t *const *add;
+    const uint64_t *inv;  // inv_tab row: (inv, shoup) pairs per target prime
+    int nout, rdiv, a_limbs, add_polys, logN;
+    uint32_t g;
+    __device__ __forceinline__ void operator()(uint64_t *, int t, long long E, uint64_t v, const DevPrimes &pr, int pidx) const {
+        const int N = 1 << logN;
+        const int row = t / nout, i = t - row * nout;
+        const int r0 = row / rdiv, r1 = row - r0 * rdiv;
+        const uint64_t q = pr.m[pidx].q;
+        const uint64_t a = A[r0][((long long)r1 * a_limbs + i) * N + E];
+        uint64_t r = mul_shoup(sub_mod(a, v, q), inv[2 * i], inv[2 * i + 1], q);
+        if (add && r1 < add_polys) {
+            long long src = E;
+            if (g != 1) {
+                const uint32_t brk = __brev((uint32_t)E) >> (32 - logN);
+                const uint32_t e = ((2u * brk + 1u) * g) & ((2u << logN) - 1u);
+                src = (long long)(__brev((e - 1u) >> 1) >> (32 - logN));
+            }
+            r = add_mod(r, add[r0][((long long)r1 * nout + i) * N + src], q);
+        }
+        O[r0][((long long)r1 * nout + i) * N + E] = r;
+    }
+};
+
+struct PassArgs {
+    int logN, s0, TPC;
+    int last;  // this pass writes the final (fully reduced) output through the store functor
+};
+
+template <bool INV, int R>
+__device__ __forceinline__ void group_compute(uint64_t (&x)[8], const int (&base)[8], int d, int s, int logT, int s0, int hi,
+                                              uint64_t q, const ulonglong2 *__restrict__ W, const NttConst &nc) {
+    constexpr int E2 = 1 << R, U = 8 >> R;
+    const uint64_t q2 = 2 * q;
+#pragma unroll
+    for (int v = 0; v < U; v++) {
+        // all twiddles of this unit first (independent loads in flight)
+        ulonglong2 tw[E2 - 1];
+#pragma unroll
+        for (int r = 0, n = 0; r < R; r++) {
+            const int g = s0 + s + r, half = E2 >> (r + 1), shift = logT - (s + r);
+#pragma unroll
+            for (int w = 0; w < E2; w += 2 * half, n++) {
+                if (INV && g == 0) continue;
+                tw[n] = __ldg(W + (1 << g) + (hi << (g - s0)) + ((base[v] + w * d) >> shift));
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; rr++) {
+            const int r = INV ? R - 1 - rr : rr;
+            const int g = s0 + s + r, half = E2 >> (r + 1);
+            const int n0 = (1 << r) - 1;  // twiddle slots used by stage r start here
+#pragma unroll
+            for (int w = 0; w < E2; w++) {
+                if (w & half) continue;
+                uint64_t &X = x[v * E2 + w], &Y = x[v * E2 + w + half];
+                if (INV && g == 0) {
+                    const uint64_t a = X, b = Y;
+                    X = mul_shoup_lazy(a + b, nc.ninv, nc.ninv_sh, q);
+                    Y = mul_shoup_lazy(a - b + q2, nc.w0n, nc.w0n_sh, q);
+                } else {
+                    const ulonglong2 t = tw[n0 + w / (2 * half)];
+                    if (INV) bf_inv(X, Y, t, q, q2);
+                    else bf_fwd(X, Y, t, q, q2);
+                }
+            }
+        }
+    }
+}
+
+template <bool INV, bool COLS, int LOGT, class LD, class ST>
+__global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrimes pr, const ulonglong2 *__restrict__ tw,
+                                                const NttConst *__restrict__ ncs, LD ld, ST st) {
+    extern __shared__ uint64_t sm[];
+    constexpr int T = 1 << LOGT, NG = (LOGT + 2) / 3;
+    const int logN = a.logN, N = 1 << logN, s0 = a.s0;
+    const int lo_bits = logN - s0 - LOGT, TPC = a.TPC;
+    const int chunks = (N >> LOGT) / TPC;
+    const int t = blockIdx.x / chunks, chunk = blockIdx.x - t * chunks;
+    uint64_t *ptr;
+    int pidx;
+    if (!locate(b, t, N, ptr, pidx)) return;
+    const uint64_t q = pr.m[pidx].q;
+    const ulonglong2 *W = tw + (size_t)pidx * N;
+    const NttConst nc = ncs[pidx];
+    const int tile0 = chunk * TPC, lomask = (1 << lo_bits) - 1;
+    constexpr int tpt = T >> 3;
+    int j, sub;
+    if (COLS) { j = threadIdx.x % TPC; sub = threadIdx.x / TPC; }
+    else { j = threadIdx.x / tpt; sub = threadIdx.x - j * tpt; }
+    const int tile = tile0 + j, hi = tile >> lo_bits, lo = tile & lomask;
+    const long long ebase = ((long long)hi << (logN - s0)) | lo;
+
+    uint64_t x[8];
+    int base[8];
+#pragma unroll
+    for (int step = 0; step < NG; step++) {
+        const int gi = INV ? NG - 1 - step : step;
+        const int s = 3 * gi, R = (LOGT - s) < 3 ? (LOGT - s) : 3;
+        const int logd = LOGT - s - R, d = 1 << logd, E2 = 1 << R;
+#pragma unroll
+        for (int v = 0; v < 8; v++) {
+            const int uid = sub * (8 >> R) + v;
+            base[v] = v < (8 >> R) ? (((uid >> logd) << (logd + R)) | (uid & (d - 1))) : 0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            const int L = base[e >> R] + (e & (E2 - 1)) * d;
+            if (step == 0) x[e] = ld(ptr, t, ebase | ((long long)L << lo_bits), pr, pidx);
+            else x[e] = sm[sidx<COLS>(j, L, T, TPC)];
+        }
+        if (R == 3) group_compute<INV, 3>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+        else if (R == 2) group_compute<INV, 2>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+        else group_compute<INV, 1>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+        const bool last_group = step == NG - 1;
+        if (last_group && a.last) {
+            const uint64_t q2 = 2 * q;
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                uint64_t v = x[e];
+                if (!INV) v = v >= q2 ? v - q2 : v;
+                x[e] = v >= q ? v - q : v;
+            }
+        }
+        if (last_group && COLS) {
+            // consecutive threads own consecutive columns -> coalesced direct stores
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int L = base[e >> R] + (e & (E2 - 1)) * d;
+                st(ptr, t, ebase | ((long long)L << lo_bits), x[e], pr, pidx);
+            }
+            return;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; e++) sm[sidx<COLS>(j, base[e >> R] + (e & (E2 - 1)) * d, T, TPC)] = x[e];
+        __syncthreads();  // one owner per element within a group: a single barrier per group boundary
+    }
+    // rows: coalesced cooperative store out of shared memory
+#pragma unroll
+    for (int r = 0; r < 8; r++) {  // blockDim.x * 8 == TPC * T
+        const int idx = threadIdx.x + r * blockDim.x;
+        const int jj = idx >> LOGT, mid = idx & (T - 1);
+        const int tl = tile0 + jj, h2 = tl >> lo_bits, lo2 = tl & lomask;
+        st(ptr, t, ((long long)h2 << (logN - s0)) | ((long long)mid << lo_bits) | lo2, sm[sidx<COLS>(jj, mid, T, TPC)], pr,
+           pidx);
+    }
+}
+
+// one thread per transform for N <= 4 (slots = 2, test-only parameter sets)
+template <bool INV, class LD, class ST>
+__global__ void ntt_tiny(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *__restrict__ tw, const NttConst *__restrict__ ncs,
+                         LD ld, ST st) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= b.count) return;
+    const int N = 1 << logN;
+    uint64_t *ptr;
+    int pidx;
+    if (!locate(b, t, N, ptr, pidx)) return;
+    const uint64_t q = pr.m[pidx].q;
+    const ulonglong2 *w = tw + (size_t)pidx * N;
+    uint64_t a[4];
+    for (int k = 0; k < N; k++) a[k] = ld(ptr, t, k, pr, pidx);
+    if (!INV) {
+        int tt = N;
+        for (int m = 1; m < N; m <<= 1) {
+            tt >>= 1;
+            for (int i = 0; i < m; i++)
+                for (int jx = 2 * i * tt; jx < 2 * i * tt + tt; jx++) {
+                    const uint64_t u = a[jx], v = mul_shoup(a[jx + tt], w[m + i].x, w[m + i].y, q);
+                    a[jx] = add_mod(u, v, q);
+                    a[jx + tt] = sub_mod(u, v, q);
+                }
+        }
+    } else {
+        int tt = 1;
+        for (int m = N; m > 1; m >>= 1) {
+            const int h = m >> 1;
+            for (int i = 0, j1 = 0; i < h; i++, j1 += 2 * tt)
+                for (int jx = j1; jx < j1 + tt; jx++) {
+                    const uint64_t u = a[jx], v = a[jx + tt];
+                    a[jx] = add_mod(u, v, q);
+                    a[jx + tt] = mul_shoup(sub_mod(u, v, q), w[h + i].x, w[h + i].y, q);
+                }
+            tt <<= 1;
+        }
+        const NttConst nc = ncs[pidx];
+        for (int k = 0; k < N; k++) a[k] = mul_shoup(a[k], nc.ninv, nc.ninv_sh, q);
+    }
+    for (int k = 0; k < N; k++) st(ptr, t, k, a[k], pr, pidx);
+}
+
+template <bool INV, bool COLS, int LOGT, class LD, class ST>
+void launch_pass(Ctx &c, const NttBatch &b, const PassArgs &a, const LD &ld, const ST &st) {
+    constexpr int T = 1 << LOGT;
+    const int chunks = (c.n >> LOGT) / a.TPC;
+    const int threads = a.TPC * (T >> 3);
+    const size_t smem = (size_t)a.TPC * T * sizeof(uint64_t);
+    const unsigned blocks = (unsigned)b.count * chunks;
+    ntt_pass<INV, COLS, LOGT, LD, ST><<<blocks, threads, smem, c.stream>>>(b, a, c.primes, INV ? c.itw2 : c.tw2, c.ntt_const,
+                                                                           ld, st);
+    check_launch("ntt_pass");
+}
+
+template <bool INV, bool COLS, class LD, class ST>
+void dispatch_pass(Ctx &c, const NttBatch &b, const PassArgs &a, int logT, const LD &ld, const ST &st) {
+    switch (logT) {
+        case 3: launch_pass<INV, COLS, 3>(c, b, a, ld, st); break;
+        case 4: launch_pass<INV, COLS, 4>(c, b, a, ld, st); break;
+        case 5: launch_pass<INV, COLS, 5>(c, b, a, ld, st); break;
+        case 6: launch_pass<INV, COLS, 6>(c, b, a, ld, st); break;
+        case 7: launch_pass<INV, COLS, 7>(c, b, a, ld, st); break;
+        case 8: launch_pass<INV, COLS, 8>(c, b, a, ld, st); break;
+        case 9: launch_pass<INV, COLS, 9>(c, b, a, ld, st); break;
+        case 10: launch_pass<INV, COLS, 10>(c, b, a, ld, st); break;
+        default: throw VrError(3, "unsupported NTT tile size");
+    }
+}
+
+// Tiles per CTA: as many as fit a 512-thread CTA, reduced for small batches so
+// the launch still spreads over every SM.
+inline int pick_tpc(int count, int tiles_per_tf, int T, int max_tpc, int min_tpc) {
+    int tpc = max_tpc;
+    while (tpc > min_tpc && (long long)count * (tiles_per_tf / tpc) < 2 * 148) tpc >>= 1;
+    while (tpc > 1 && tpc * (T >> 3) > 512) tpc >>= 1;
+    if (tpc > tiles_per_tf) tpc = tiles_per_tf;
+    return tpc;
+}
+
+template <bool INV, class LD, class ST>
+void run_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
+    if (b.count <= 0) return;
+    const int logN = c.log_n;
+    if (c.n <= 4) {
+        ntt_tiny<INV><<<nblocks(b.count, 64), 64, 0, c.stream>>>(b, logN, c.primes, INV ? c.itw2 : c.tw2, c.ntt_const, ld, st);
+        check_launch("ntt_tiny");
+        return;
+    }
+    if (c.n < 2048) {
+        PassArgs a{logN, 0, 1, 1};
+        dispatch_pass<INV, false>(c, b, a, logN, ld, st);
+        return;
+    }
+    const int la = logN / 2, lb = logN - la;
+    const int T1 = 1 << la, T2 = 1 << lb;
+    PassArgs p1{logN, 0, pick_tpc(b.count, 1 << lb, T1, 16, 4), 0};
+    PassArgs p2{logN, la, pick_tpc(b.count, 1 << la, T2, 2048 / T2, 1), 0};
+    if (!INV) {
+        p2.last = 1;
+        dispatch_pass<false, true>(c, b, p1, la, ld, StPlain{});
+        dispatch_pass<false, false>(c, b, p2, lb, LdPlain{}, st);
+    } else {
+        p1.last = 1;
+        dispatch_pass<true, false>(c, b, p2, lb, ld, StPlain{});
+        dispatch_pass<true, true>(c, b, p1, la, LdPlain{}, st);
+    }
+}
+
+}  // namespace nttk
+
+template <class LD, class ST>
+void ntt_forward_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) { nttk::run_fused<false>(c, b, ld, st); }
+template <class LD, class ST>
+void ntt_inverse_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) { nttk::run_fused<true>(c, b, ld, st); }
+
+}  // namespace vr

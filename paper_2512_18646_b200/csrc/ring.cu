@@ -5,6 +5,8 @@
 // All kernels are HBM-bound streaming passes over [poly][limb][N] uint64
 // arrays; each thread handles two adjacent coefficients with 128-bit loads so
 // a warp moves 512 contiguous bytes per access.
+#include <cooperative_groups.h>
+
 #include "ring.cuh"
 
 namespace vr {
@@ -142,16 +144,27 @@ __global__ void k_mod_fixup(uint64_t *data, long long count_polys, int nl, int N
 }
 
 // Fused sum_k tensor(L[b][k], R[k]) for NB row blocks sharing the right operand.
-// One thread = (limb, 2 coefficients); R is read once per block group, every
-// product is accumulated in 128 bits and folded mod q every 8 terms.
+// Grid (coefficient tiles, limbs, SPLIT): the SPLIT CTAs of a thread-block
+// cluster walk disjoint quarters of the k range for the same 256 coefficients,
+// accumulate 64x64->128-bit products (folded mod q every 8 terms), reduce
+// their partials mod q and combine them through distributed shared memory;
+// cluster rank 0 writes the degree-2 result.  R is read once per block group.
+constexpr int TS_THREADS = 128, TS_SPLIT = 4;
+
 template <int NB>
-__global__ void __launch_bounds__(256) k_tensor_sum(const uint64_t *const *L, const uint64_t *const *R, int n, int nl,
-                                                    int N, DevPrimes pr, uint64_t *const *O) {
+__global__ void __cluster_dims__(1, 1, TS_SPLIT) __launch_bounds__(TS_THREADS)
+    k_tensor_sum(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O) {
+    __shared__ ulonglong2 part[NB * 3][TS_THREADS];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
     const int k = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
     const int i = blockIdx.y;
-    if (k >= N) return;
+    const int z = (int)cluster.block_rank();
+    const bool live = k < N;
     const Modulus m = pr.m[i];
     const size_t o0 = (size_t)i * N + k, o1 = (size_t)(nl + i) * N + k;
+    const int per = (n + TS_SPLIT - 1) / TS_SPLIT;
+    const int tb = z * per, te = min(n, tb + per);
     u128 acc[NB][3][2];
 #pragma unroll
     for (int b = 0; b < NB; b++)
@@ -159,42 +172,61 @@ __global__ void __launch_bounds__(256) k_tensor_sum(const uint64_t *const *L, co
         for (int p = 0; p < 3; p++)
 #pragma unroll
             for (int e = 0; e < 2; e++) acc[b][p][e] = u128{0, 0};
-    for (int t0 = 0; t0 < n; t0 += 8) {
-        const int tend = min(n, t0 + 8);
-#pragma unroll 2
-        for (int t = t0; t < tend; t++) {
-            const uint64_t *r = R[t];
-            const ulonglong2 r0 = ld2(r + o0), r1 = ld2(r + o1);
+    if (live) {
+        for (int t0 = tb; t0 < te; t0 += 8) {
+            const int tend = min(te, t0 + 8);
+#pragma unroll 4
+            for (int t = t0; t < tend; t++) {
+                const uint64_t *r = R[t];
+                const ulonglong2 r0 = ld2(r + o0), r1 = ld2(r + o1);
 #pragma unroll
-            for (int b = 0; b < NB; b++) {
-                const uint64_t *l = L[b * n + t];
-                const ulonglong2 l0 = ld2(l + o0), l1 = ld2(l + o1);
-                mac_to(acc[b][0][0], l0.x, r0.x);
-                mac_to(acc[b][0][1], l0.y, r0.y);
-                mac_to(acc[b][1][0], l0.x, r1.x);
-                mac_to(acc[b][1][1], l0.y, r1.y);
-                mac_to(acc[b][1][0], l1.x, r0.x);
-                mac_to(acc[b][1][1], l1.y, r0.y);
-                mac_to(acc[b][2][0], l1.x, r1.x);
-                mac_to(acc[b][2][1], l1.y, r1.y);
+                for (int b = 0; b < NB; b++) {
+                    const uint64_t *l = L[b * n + t];
+                    const ulonglong2 l0 = ld2(l + o0), l1 = ld2(l + o1);
+                    mac_to(acc[b][0][0], l0.x, r0.x);
+                    mac_to(acc[b][0][1], l0.y, r0.y);
+                    mac_to(acc[b][1][0], l0.x, r1.x);
+                    mac_to(acc[b][1][1], l0.y, r1.y);
+                    mac_to(acc[b][1][0], l1.x, r0.x);
+                    mac_to(acc[b][1][1], l1.y, r0.y);
+                    mac_to(acc[b][2][0], l1.x, r1.x);
+                    mac_to(acc[b][2][1], l1.y, r1.y);
+                }
+            }
+            if (tend < te) {
+#pragma unroll
+                for (int b = 0; b < NB; b++)
+#pragma unroll
+                    for (int p = 0; p < 3; p++)
+#pragma unroll
+                        for (int e = 0; e < 2; e++) acc[b][p][e] = u128{reduce128(acc[b][p][e], m), 0};
             }
         }
-        if (tend < n) {
-#pragma unroll
-            for (int b = 0; b < NB; b++)
-#pragma unroll
-                for (int p = 0; p < 3; p++)
-#pragma unroll
-                    for (int e = 0; e < 2; e++) acc[b][p][e] = u128{reduce128(acc[b][p][e], m), 0};
-        }
     }
 #pragma unroll
-    for (int b = 0; b < NB; b++) {
-        uint64_t *o = O[b];
+    for (int b = 0; b < NB; b++)
 #pragma unroll
         for (int p = 0; p < 3; p++)
-            st2(o + (size_t)(p * nl + i) * N + k, reduce128(acc[b][p][0], m), reduce128(acc[b][p][1], m));
+            part[b * 3 + p][threadIdx.x] = make_ulonglong2(reduce128(acc[b][p][0], m), reduce128(acc[b][p][1], m));
+    cluster.sync();
+    if (z == 0 && live) {
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+            uint64_t *o = O[b];
+#pragma unroll
+            for (int p = 0; p < 3; p++) {
+                ulonglong2 v = part[b * 3 + p][threadIdx.x];
+#pragma unroll
+                for (int r = 1; r < TS_SPLIT; r++) {
+                    const ulonglong2 w = cluster.map_shared_rank(&part[b * 3 + p][0], r)[threadIdx.x];
+                    v.x = add_mod(v.x, w.x, m.q);
+                    v.y = add_mod(v.y, w.y, m.q);
+                }
+                st2(o + (size_t)(p * nl + i) * N + k, v.x, v.y);
+            }
+        }
     }
+    cluster.sync();  // peers keep their shared memory alive until rank 0 has read it
 }
 
 constexpr int TB = 256;
@@ -264,11 +296,11 @@ void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl) {
 }
 
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O) {
-    dim3 grid(nblocks(c.n / 2, 128), nl);
+    dim3 grid(nblocks(c.n / 2, TS_THREADS), nl, TS_SPLIT);
     switch (nb) {
-        case 1: k_tensor_sum<1><<<grid, 128, 0, c.stream>>>(L, R, n, nl, c.n, c.primes, O); break;
-        case 2: k_tensor_sum<2><<<grid, 128, 0, c.stream>>>(L, R, n, nl, c.n, c.primes, O); break;
-        case 4: k_tensor_sum<4><<<grid, 128, 0, c.stream>>>(L, R, n, nl, c.n, c.primes, O); break;
+        case 1: k_tensor_sum<1><<<grid, TS_THREADS, 0, c.stream>>>(L, R, n, nl, c.n, c.primes, O); break;
+        case 2: k_tensor_sum<2><<<grid, TS_THREADS, 0, c.stream>>>(L, R, n, nl, c.n, c.primes, O); break;
+        case 4: k_tensor_sum<4><<<grid, TS_THREADS, 0, c.stream>>>(L, R, n, nl, c.n, c.primes, O); break;
         default: throw VrError(3, "tensor_sum: nblocks must be 1, 2 or 4");
     }
     check_launch("k_tensor_sum");

@@ -27,13 +27,12 @@ void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int 
 void rescale(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int count, int polys, int level);
 
 // Key switching.  ModUp of `count` polys (each [l+1][N], NTT) into
-// D [count][l+1][l+2][N] (NTT form; target l+1 is the special prime).
+// D [count][l+1][l+2][N] (NTT form; target l+1 is the special prime; the
+// digit's own prime is not materialised -- the inner product reads it from
+// the input polynomial).
 void modup(Ctx &c, const uint64_t *const *Polys, int count, int level, uint64_t *D);
-// Inner product with a key ([L+1][2][np][N]) followed by ModDown; the
-// Galois element g (1 = identity) permutes D on read (hoisted rotations).
-// Out: [count][2][l+1][N] contiguous; if Add0 != nullptr, Out[.][0] += perm_g(Add0[.]) and
-// Out[.][1] += perm_g(Add1[.]) (Add1 may be nullptr).
-void ks_inner_moddown(Ctx &c, const uint64_t *D, int count, int level, const uint64_t *key, uint32_t g, uint64_t *Out);
+// Full key switch of `count` polys with `key` ([L+1][2][np][N]) into Out[c] = [2][l+1][N].
+void keyswitch_poly(Ctx &c, const uint64_t *const *Polys, int count, int level, const uint64_t *key, uint64_t *const *Out);
 
 // Convenience wrappers operating on pointer tables (device) of ciphertexts.
 void relin_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level);  // deg2 -> deg1, same level
@@ -47,7 +46,7 @@ struct PtrTable {
     Scratch s;
     PtrTable(Ctx &c, const std::vector<const uint64_t *> &v)
         : s(c, sizeof(void *) * (v.empty() ? 1 : v.size())) {
-        if (!v.empty()) VR_CUDA(cudaMemcpyAsync(s.p, v.data(), sizeof(void *) * v.size(), cudaMemcpyHostToDevice, c.stream));
+        if (!v.empty()) upload_async(c, s.p, v.data(), sizeof(void *) * v.size());
     }
     const uint64_t *const *c_() const { return (const uint64_t *const *)s.p; }
     uint64_t *const *m_() const { return (uint64_t *const *)s.p; }

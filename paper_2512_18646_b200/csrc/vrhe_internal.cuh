@@ -35,7 +35,7 @@ struct Ctx {
     int sym_enc = 0;
 
     // device tables
-    uint64_t *tw = nullptr, *tw_sh = nullptr, *itw = nullptr, *itw_sh = nullptr;  // [np][N]
+    ulonglong2 *tw2 = nullptr, *itw2 = nullptr;  // [np][N] (twiddle, Shoup companion) psi^(br i), psi^-(br i)
     NttConst *ntt_const = nullptr;                                                 // [np]
     uint64_t *inv_tab = nullptr;  // [np][np][2]: (q_a^-1 mod q_b, shoup)
     double *zr = nullptr, *zi = nullptr;  // zeta^k, k < N
@@ -52,9 +52,13 @@ struct Ctx {
     std::vector<NttConst> h_ntt_const;
     std::vector<uint64_t> h_inv_tab;
 
-    // pinned staging for pointer tables
-    void *pin = nullptr;
-    size_t pin_bytes = 0;
+    // pinned staging ring for small host->device uploads (pointer tables, weights):
+    // pageable cudaMemcpyAsync would block the host until the stream drains.
+    static constexpr int kStageSlots = 64;
+    static constexpr size_t kStageBytes = 64 << 10;
+    char *stage = nullptr;
+    cudaEvent_t stage_evt[kStageSlots] = {};
+    int stage_next = 0;
 
     size_t key_words() const { return (size_t)(L + 1) * 2 * np * n; }
 };
@@ -95,12 +99,15 @@ struct Scratch {
     Scratch(const Scratch &) = delete;
 };
 
+// stream-ordered host->device copy through the pinned staging ring
+void upload_async(Ctx &c, void *dst, const void *src, size_t bytes);
+
 // Upload a small host array (pointer table etc.) to a stream-ordered device buffer.
 template <class T>
 struct DevArray {
     Scratch s;
     DevArray(Ctx &c, const T *host, size_t count) : s(c, sizeof(T) * (count ? count : 1)) {
-        if (count) VR_CUDA(cudaMemcpyAsync(s.p, host, sizeof(T) * count, cudaMemcpyHostToDevice, c.stream));
+        if (count) upload_async(c, s.p, host, sizeof(T) * count);
     }
     T *get() const { return s.as<T>(); }
 };

@@ -165,7 +165,7 @@ def pad_images(images, pad: int) -> np.ndarray:
 
 
 def conv_constants(engine: CkksEngine, level: int, scale: float, weights, biases):
-    """Integer tap weights, biases and the mask scale for the fused conv.
+    """Integer tap weights, bias residues and the mask scale for the fused conv.
 
     acc = sum w_int * x has scale ``scale * 2^delta_c``; the valid mask is encoded at
     s_m = s[level] / 2^delta_c so that mask * acc, rescaled by q[level], lands exactly
@@ -174,10 +174,11 @@ def conv_constants(engine: CkksEngine, level: int, scale: float, weights, biases
     dc = float(2 ** engine.params.delta_c)
     w = np.asarray(weights, dtype=np.float64)
     w_int = np.array([int(round(float(x) * dc)) for x in w.reshape(-1)], dtype=np.int64).reshape(w.shape)
-    b_int = np.array([int(round(float(b) * scale * dc)) for b in np.asarray(biases, dtype=np.float64).reshape(-1)],
-                     dtype=np.int64)
+    # the bias integer lives at scale * 2^delta_c and can exceed 64 bits: pass exact residues
+    b_ints = [int(round(float(b) * scale * dc)) for b in np.asarray(biases, dtype=np.float64).reshape(-1)]
+    b_res = np.array([[bi % engine.q[i] for i in range(level + 1)] for bi in b_ints], dtype=np.uint64)
     mask_scale = engine.scales[level] / dc
-    return w_int, b_int, mask_scale
+    return w_int, b_res, mask_scale
 
 
 def _valid_mask(m: int, stride: int, out_h: int) -> np.ndarray:
@@ -246,11 +247,11 @@ def conv_columns_multi(engine: CkksEngine, imgs, weights, biases, out_cols=None)
     Y = torch.empty((F, nout, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
     yptrs = [Y[f, o].data_ptr() for f in range(F) for o in range(nout)]
     w_c = np.ascontiguousarray(w_int, dtype=np.int64)
-    b_c = np.ascontiguousarray(b_int, dtype=np.int64)
+    b_c = np.ascontiguousarray(b_int, dtype=np.uint64)
     cols_c = (ctypes.c_int * max(1, nout))(*cols)
     _lib.check(engine._lib.vr_conv_columns(
         engine.handle, _lib.ptr_array([c.ptr() for c in X]), C, base.w, k,
-        w_c.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), b_c.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), F,
+        w_c.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), b_c.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), F,
         cols_c, nout, mask_pt.data_ptr(), lv, _lib.ptr_array(yptrs)))
     depth_in = max(ct.depth for ct in X)
     out = []
