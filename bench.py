@@ -288,6 +288,7 @@ def run_ours(args, ws, rank, local):
     extra = {}
     if not args.no_extra and rank == 0:
         extra["ntt"] = bench_ntt(eng, peak)
+        extra["configs"] = {"cfg1": bench_cfg1(), "cfg4": bench_cfg4(steps=2)}
     line = None
     if rank == 0:
         cpu = None
@@ -321,6 +322,68 @@ def run_ours(args, ws, rank, local):
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def bench_cfg1(steps=50):
+    """Config 1: HE matmul 8x8 (n = 8 column ciphertexts, N = 2^13), device time per matmul."""
+    import torch
+
+    from paper_2512_18646_b200 import CkksEngine, config_params, encode_left, encode_right, matmul_outer
+    from tools.workloads import cfg_matmul
+
+    a, b = cfg_matmul(1)
+    eng = CkksEngine(config_params(1))
+    left, right = encode_left(eng, a, 8), encode_right(eng, b, 8)
+    err = float(np.max(np.abs(matmul_outer(eng, left, right).decode(eng) - a @ b)))
+    for _ in range(3):
+        matmul_outer(eng, left, right)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    st.record(eng._stream)
+    for _ in range(steps):
+        matmul_outer(eng, left, right)
+    en.record(eng._stream)
+    torch.cuda.synchronize()
+    t = st.elapsed_time(en) / 1e3 / steps
+    return {"metric": "HE matmul/s (cfg1 8x8, N=2^13)", "value": 1.0 / t, "ms_per_matmul": t * 1e3, "max_abs_err": err}
+
+
+def bench_cfg4(steps=2):
+    """Config 4: 16 images 3x224x224, 16-filter 3x3 conv (padding 1) + 0.125x^2+0.5x+0.25, N = 2^15."""
+    import torch
+
+    from paper_2512_18646_b200 import CkksEngine, config_params
+    from paper_2512_18646_b200.cnn import conv_layer, decode_layer, encode_images
+    from tools.workloads import ACT4, cfg4, conv_plain, poly_plain
+
+    imgs, w, b = cfg4(16)
+    eng = CkksEngine(config_params(4))
+    chans = encode_images(eng, imgs, padding=1)
+    ys = conv_layer(eng, chans, w, b, activation=ACT4)  # warm-up + correctness
+    got = decode_layer(eng, ys)
+    err = float(np.max(np.abs(got - poly_plain(conv_plain(imgs, w, b, padding=1), ACT4))))
+    del ys
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    l0 = eng._lib.vr_launch_count()
+    st.record(eng._stream)
+    for _ in range(steps):
+        ys = conv_layer(eng, chans, w, b, activation=ACT4)
+        del ys
+    en.record(eng._stream)
+    torch.cuda.synchronize()
+    t = st.elapsed_time(en) / 1e3 / steps
+    launches = (eng._lib.vr_launch_count() - l0) / steps
+    # e2e: encrypt from host, layer, decrypt to host
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ys = conv_layer(eng, encode_images(eng, imgs, padding=1), w, b, activation=ACT4)
+    decode_layer(eng, ys)
+    torch.cuda.synchronize()
+    te = time.perf_counter() - t0
+    return {"metric": "encrypted-CNN images/s (cfg4 conv 16x3x3x3 + degree-2 activation, 16 images/batch, N=2^15)",
+            "value": 16 / t, "s_per_batch": t, "max_abs_err": err, "launches_per_batch": launches,
+            "e2e_images_per_s": 16 / te, "e2e_h2d_bytes": 3 * 226 * 16 * 226 * 8, "e2e_d2h_bytes": 16 * 224 * eng.slots * 8}
 
 
 def bench_ntt(eng, peak):

@@ -832,32 +832,37 @@ void orc_conv_columns(orc_ctx *c, const uint64_t *const *X, int C, int W, int k,
     free(R);
 }
 
-/* poly_activation (pipeline.py:180-197) fused, see DESIGN.md §4.3.
- * k = {k_c3, k_c2, k_c1, k_c0} integer constants computed by the host;
- * c3_zero selects the x^2 * c2 scalar path.  x: [2][l+1][N] -> out [2][l-1][N] */
+/* poly_activation (pipeline.py:180-197) fused, see DESIGN.md section 4.3.
+ * x at level l (scale s_l), x' = x with limbs 0..l-1 (same scale):
+ *   x2  = rescale(relin(x (x) x))                                   level l-1, s_{l-1}
+ *   c3 == 0:  pre = x2 * kc[1] + x' * kc[2]                         level l-1, s_{l-1}^2
+ *   c3 != 0:  inner = rescale(x * kc[0]) + kc[1]                    level l-1, s_{l-1}
+ *             pre = relin(x2 (x) inner) + x' * kc[2]                level l-1, s_{l-1}^2
+ *   out = rescale(pre) + kc[3]                                      level l-2, s_{l-2}
+ * kc = {round(c3 s_l), round(c2 s_{l-1}), round(c1 s_{l-1}^2 / s_l), round(c0 s_{l-2})}.
+ * x: [2][l+1][N] -> out [2][l-1][N] */
 void orc_poly_activation(orc_ctx *c, const uint64_t *x, int level, const int64_t *kc, int c3_zero, uint64_t *out) {
     const int n = c->n, nl = level + 1;
-    const size_t w1 = (size_t)2 * level * n, w2 = (size_t)2 * (level - 1) * n;
-    uint64_t *x2 = malloc(8 * w1), *t = malloc(8 * w2), *tmp = malloc(8 * 2 * nl * n);
+    const size_t w1 = (size_t)2 * level * n;
+    uint64_t *x2 = malloc(8 * w1), *pre = malloc(8 * w1), *xd = malloc(8 * w1), *tmp = malloc(8 * 2 * nl * n);
     orc_mul(c, x, x, level, x2);
     if (c3_zero) {
-        orc_mul_scalar(c, x2, kc[1], 1, level - 1, x2);
-        orc_rescale(c, x2, 1, level - 1, out);
+        orc_mul_scalar(c, x2, kc[1], 1, level - 1, pre);
     } else {
-        uint64_t *inner = malloc(8 * w1);
+        uint64_t *inner = malloc(8 * w1), *d3 = malloc(8 * 3 * (size_t)level * n);
         orc_mul_scalar(c, x, kc[0], 1, level, tmp);
         orc_rescale(c, tmp, 1, level, inner);
         orc_add_const(c, inner, kc[1], level - 1);
-        orc_mul(c, x2, inner, level - 1, out);
-        free(inner);
+        orc_tensor(c, x2, inner, level - 1, d3);
+        orc_relin(c, d3, level - 1, pre);
+        free(inner); free(d3);
     }
-    /* c1 * x brought to level l-2 */
-    orc_drop_level(c, x, 1, level, level - 1, tmp);
-    orc_mul_scalar(c, tmp, kc[2], 1, level - 1, tmp);
-    orc_rescale(c, tmp, 1, level - 1, t);
-    orc_add(c, out, t, 1, level - 2, out);
+    orc_drop_level(c, x, 1, level, level - 1, xd);
+    orc_mul_scalar(c, xd, kc[2], 1, level - 1, xd);
+    orc_add(c, pre, xd, 1, level - 1, pre);
+    orc_rescale(c, pre, 1, level - 1, out);
     orc_add_const(c, out, kc[3], level - 2);
-    free(x2); free(t); free(tmp);
+    free(x2); free(pre); free(xd); free(tmp);
 }
 
 /* single-limb helpers for unit tests */

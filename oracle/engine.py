@@ -135,6 +135,6 @@ class OracleEngine:
         c0, c1, c2, c3 = (float(c) for c in coeffs)
         s, q = self.scales, self.q
         kc = (int(round(c3 * s[lv])), int(round(c2 * s[lv - 1])),
-              int(round(c1 * s[lv - 2] * float(q[lv - 1]) / s[lv])), int(round(c0 * s[lv - 2])))
+              int(round(c1 * s[lv - 1] * s[lv - 1] / s[lv])), int(round(c0 * s[lv - 2])))
         out = self.c.poly_activation(ct.data, kc, c3 == 0.0)
         return OCt(out, lv - 2, s[lv - 2], ct.depth + 2, ct.layout)

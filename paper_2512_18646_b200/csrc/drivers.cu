@@ -70,6 +70,88 @@ __global__ void __launch_bounds__(128) k_conv_mac(const uint64_t *const *T, cons
     }
 }
 
+// Small-weight conv MAC.  Quantised weights satisfy |w| < B = 2^bb, so w' = w + B
+// is a u32.  Splitting each residue v = vh * 2^32 + vl, every product w' * v is
+// accumulated as two 32x32+64 multiply-adds (IMAD.WIDE.U32) into 64-bit partial
+// sums that cannot overflow within `flush` taps; the bias B * sum(v) is shared by
+// all filters and removed once at the end.  Pointers and weights for the CTA's
+// output column live in shared memory.
+template <int FG>
+__global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T, const int *cols, int nout, int C, int W,
+                                                        int k, int F, const uint32_t *wb, uint64_t bb_pow, int flush,
+                                                        const uint64_t *bq, const uint64_t *mask, int nl, int N, DevPrimes pr,
+                                                        uint64_t *Yp) {
+    extern __shared__ uint64_t smc[];
+    const int taps = C * k * k;
+    const uint64_t **sptr = (const uint64_t **)smc;
+    uint32_t *sw = (uint32_t *)(smc + taps);  // [taps][FG]
+    const int nfg = F / FG;
+    const int o = blockIdx.z / nfg, f0 = (blockIdx.z - o * nfg) * FG;
+    for (int t = threadIdx.x; t < taps; t += blockDim.x) {
+        const int c = t / (k * k), r = t - c * k * k, q = r / k, p = r - q * k;  // tap order (c, q, p)
+        sptr[t] = T[((size_t)c * W + cols[o] + q) * k + p];
+        for (int f = 0; f < FG; f++) sw[t * FG + f] = wb[((size_t)(f0 + f) * C + c) * k * k + p * k + q];
+    }
+    __syncthreads();
+    const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (kk >= N) return;
+    const int poly = blockIdx.y / nl, i = blockIdx.y - poly * nl;
+    const Modulus m = pr.m[i];
+    const size_t off = ((size_t)poly * nl + i) * N + kk;
+    uint64_t alo[FG], ahi[FG];
+    u128 acc[FG];
+#pragma unroll
+    for (int f = 0; f < FG; f++) { alo[f] = 0; ahi[f] = 0; acc[f] = u128{0, 0}; }
+    u128 sv{0, 0};
+    int cnt = 0;
+    for (int t0 = 0; t0 < taps; t0 += 8) {
+        // issue the next (up to) 8 tap loads before any multiply-accumulate
+        uint64_t vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const uint64_t *src = (t0 + u < taps) ? sptr[t0 + u] : nullptr;
+            vv[u] = src ? src[off] : 0;  // null: every filter's weight on this tap is zero
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            if (t0 + u >= taps) break;
+            const uint64_t v = vv[u];
+            const uint32_t vl = (uint32_t)v, vh = (uint32_t)(v >> 32);
+            sv.lo += v;
+            sv.hi += sv.lo < v;
+            const uint32_t *wt = sw + (t0 + u) * FG;
+#pragma unroll
+            for (int f = 0; f < FG; f++) {
+                const uint64_t w = wt[f];
+                alo[f] += (uint64_t)vl * w;
+                ahi[f] += (uint64_t)vh * w;
+            }
+            if (++cnt == flush) {
+                cnt = 0;
+#pragma unroll
+                for (int f = 0; f < FG; f++) {
+                    add_to(acc[f], u128{alo[f], 0});
+                    add_to(acc[f], u128{ahi[f] << 32, ahi[f] >> 32});
+                    alo[f] = ahi[f] = 0;
+                }
+            }
+        }
+    }
+    const uint64_t svq = reduce128(sv, m);
+    const uint64_t bq_pow = reduce64(bb_pow, m);
+    const uint64_t bias_sum = mul_mod(svq, bq_pow, m);  // B * sum(v) mod q
+    const uint64_t mk = mask[(size_t)i * N + kk];
+#pragma unroll
+    for (int f = 0; f < FG; f++) {
+        add_to(acc[f], u128{alo[f], 0});
+        add_to(acc[f], u128{ahi[f] << 32, ahi[f] >> 32});
+        uint64_t r = sub_mod(reduce128(acc[f], m), bias_sum, m.q);
+        if (poly == 0) r = add_mod(r, bq[(size_t)i * F + f0 + f], m.q);
+        r = mul_mod(r, mk, m);
+        Yp[((size_t)(f0 + f) * nout + o) * 2 * nl * N + off] = r;
+    }
+}
+
 }  // namespace
 
 void mul_batch(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *Out, int count, int level) {
@@ -161,13 +243,42 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
     DevArray<int> dcols(c, out_cols, nout);
     PtrTable tt(c, table);
     // 3. MAC + mask into pre-rescale buffer (chunked over output columns), then rescale
-    const int FG = (F % 8 == 0) ? 8 : (F % 4 == 0 ? 4 : (F % 2 == 0 ? 2 : 1));
+    // small-weight fast path: |w| < 2^bb with bb <= 30
+    int64_t wmax = 0;
+    for (size_t t = 0; t < (size_t)F * C * k * k; t++) wmax = std::max<int64_t>(wmax, w[t] < 0 ? -w[t] : w[t]);
+    int bb = 1;
+    while ((int64_t(1) << bb) <= wmax) bb++;
+    const bool small = bb <= 30;
+    std::vector<uint32_t> wbias;
+    int flush = 1;
+    if (small) {
+        wbias.resize((size_t)F * C * k * k);
+        for (size_t t = 0; t < wbias.size(); t++) wbias[t] = (uint32_t)(w[t] + (int64_t(1) << bb));
+        // 2^32 * 2^(bb+1) * flush < 2^64
+        flush = (int)std::max<int64_t>(1, std::min<int64_t>(1 << 20, (int64_t(1) << (31 - bb))));
+    }
+    DevArray<uint32_t> dwb(c, small ? wbias.data() : nullptr, small ? wbias.size() : 0);
+    const int taps = C * k * k;
+    const int FG = small ? ((F % 16 == 0) ? 16 : (F % 8 == 0) ? 8 : (F % 4 == 0 ? 4 : (F % 2 == 0 ? 2 : 1)))
+                         : ((F % 8 == 0) ? 8 : (F % 4 == 0 ? 4 : (F % 2 == 0 ? 2 : 1)));
     const int ocols = std::max(1, std::min(nout, (int)(((size_t)2 << 30) / (ctw * 8 * F))));
     Scratch yp(c, sizeof(uint64_t) * (size_t)F * ocols * ctw);
     for (int o0 = 0; o0 < nout; o0 += ocols) {
         const int no = std::min(ocols, nout - o0);
         dim3 grid(nblocks(N, 128), 2 * nl, (unsigned)no * (F / FG));
         const int *colp = dcols.get() + o0;
+        if (small) {
+            const size_t sm = (size_t)taps * 8 + (size_t)taps * FG * 4;
+            const uint64_t bpow = uint64_t(1) << bb;
+            switch (FG) {
+                case 16: k_conv_mac_small<16><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                case 8: k_conv_mac_small<8><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                case 4: k_conv_mac_small<4><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                case 2: k_conv_mac_small<2><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                default: k_conv_mac_small<1><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+            }
+            check_launch("k_conv_mac_small");
+        } else {
         switch (FG) {
             case 8: k_conv_mac<8><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
             case 4: k_conv_mac<4><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
@@ -175,6 +286,7 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
             default: k_conv_mac<1><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
         }
         check_launch("k_conv_mac");
+        }
         std::vector<const uint64_t *> ins((size_t)F * no);
         std::vector<const uint64_t *> outs((size_t)F * no);
         for (int f = 0; f < F; f++)
@@ -187,33 +299,44 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
     }
 }
 
-void poly_activation(Ctx &c, const uint64_t *const *X, int count, int level, const int64_t *kc, int c3_zero,
-                     uint64_t *const *Out) {
-    if (level < 2) throw VrError(3, "poly_activation needs two levels");
+// oracle/ckks_oracle.c:orc_poly_activation -- one relinearisation (two if c3 != 0) and the
+// c1*x term folded into the final rescale.
+static void poly_activation_chunk(Ctx &c, const uint64_t *const *X, int count, int level, const int64_t *kc, int c3_zero,
+                                  uint64_t *const *Out) {
     const int N = c.n;
-    const size_t w1 = (size_t)2 * level * N, w2 = (size_t)2 * (level - 1) * N;
-    Scratch x2(c, sizeof(uint64_t) * count * w1), tmp(c, sizeof(uint64_t) * count * w1), t(c, sizeof(uint64_t) * count * w2);
-    PtrTable tx2(c, strided(x2.as<uint64_t>(), count, w1)), ttmp(c, strided(tmp.as<uint64_t>(), count, w1)),
-        tt(c, strided(t.as<uint64_t>(), count, w2));
+    const size_t w1 = (size_t)2 * level * N;
+    Scratch x2(c, sizeof(uint64_t) * count * w1), pre(c, sizeof(uint64_t) * count * w1);
+    PtrTable tx2(c, strided(x2.as<uint64_t>(), count, w1)), tpre(c, strided(pre.as<uint64_t>(), count, w1));
     mul_batch(c, X, X, tx2.m_(), count, level);  // x^2 at level-1
     if (c3_zero) {
-        mul_scalar(c, tx2.c_(), tx2.m_(), count, 2, level, limb_scalars(c, kc[1], level));
-        rescale(c, tx2.c_(), Out, count, 2, level - 1);
+        mul_scalar(c, tx2.c_(), tpre.m_(), count, 2, level, limb_scalars(c, kc[1], level));
     } else {
-        Scratch inner(c, sizeof(uint64_t) * count * w1), xs(c, sizeof(uint64_t) * count * 2 * (level + 1) * N);
+        Scratch inner(c, sizeof(uint64_t) * count * w1), xs(c, sizeof(uint64_t) * count * 2 * (level + 1) * N),
+            d3(c, sizeof(uint64_t) * count * 3 * level * N);
         PtrTable tin(c, strided(inner.as<uint64_t>(), count, w1)),
-            txs(c, strided(xs.as<uint64_t>(), count, (size_t)2 * (level + 1) * N));
+            txs(c, strided(xs.as<uint64_t>(), count, (size_t)2 * (level + 1) * N)),
+            td3(c, strided(d3.as<uint64_t>(), count, (size_t)3 * level * N));
         mul_scalar(c, X, txs.m_(), count, 2, level + 1, limb_scalars(c, kc[0], level + 1));
         rescale(c, txs.c_(), tin.m_(), count, 2, level);
         add_const(c, tin.m_(), count, level, limb_scalars(c, kc[1], level));
-        mul_batch(c, tx2.c_(), tin.c_(), Out, count, level - 1);
+        tensor(c, tx2.c_(), tin.c_(), td3.m_(), count, level);
+        relin_batch(c, td3.c_(), tpre.m_(), count, level - 1);
     }
-    // c1 * x at level-2: drop to level-1, scalar, rescale
-    copy_limbs(c, X, ttmp.m_(), count, 2, level + 1, level, 0);
-    mul_scalar(c, ttmp.c_(), ttmp.m_(), count, 2, level, limb_scalars(c, kc[2], level));
-    rescale(c, ttmp.c_(), tt.m_(), count, 2, level - 1);
-    binop(c, (const uint64_t *const *)Out, tt.c_(), Out, count, 2, level - 1, 0);
+    axpy(c, tpre.m_(), X, count, 2, level, level + 1, limb_scalars(c, kc[2], level));
+    rescale(c, tpre.c_(), Out, count, 2, level - 1);
     add_const(c, Out, count, level - 1, limb_scalars(c, kc[3], level - 1));
+}
+
+void poly_activation(Ctx &c, const uint64_t *const *X, int count, int level, const int64_t *kc, int c3_zero,
+                     uint64_t *const *Out) {
+    if (level < 2) throw VrError(3, "poly_activation needs two levels");
+    // scratch per ciphertext is dominated by the relinearisation ModUp (nl * (nl+1) * N words)
+    const size_t per_ct = sizeof(uint64_t) * (size_t)c.n * ((size_t)(level + 1) * (level + 2) + 12 * (level + 1));
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, ((size_t)4 << 30) / per_ct));
+    for (int c0 = 0; c0 < count; c0 += chunk) {
+        const int n = std::min(chunk, count - c0);
+        poly_activation_chunk(c, X + c0, n, level, kc, c3_zero, Out + c0);
+    }
 }
 
 }  // namespace vr

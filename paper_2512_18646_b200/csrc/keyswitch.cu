@@ -39,29 +39,57 @@ struct LdStrided {
 
 // A[c][x][t][k] = sum_j D[c][j][t][src(k)] * key[j][x][pidx(t)][k]; the digit's own
 // prime (t == j) is read from the input polynomial (ModUp never materialises it).
-__global__ void k_ks_inner(const uint64_t *D, const uint64_t *const *P, long long poly_off, int count, int level, int N,
-                           int logN, int np, const uint64_t *key, uint32_t g, DevPrimes pr, uint64_t *A) {
+// Grid (t*N + k, ciphertext groups of CG): a thread keeps its key column
+// (2 x (l+1) words) in registers and issues all CG x (l+1) digit loads before
+// the multiply-accumulates, so the key is read count/CG times per launch and
+// every thread has CG*(l+1) independent loads in flight.
+constexpr int KS_CG = 4;
+template <int KS_MAXD>
+__global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint64_t *const *P, long long poly_off, int count,
+                                                  int level, int N, int logN, int np, const uint64_t *key, uint32_t g,
+                                                  DevPrimes pr, uint64_t *A) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int nl = level + 1, nt = level + 2;
-    if (e >= (long long)count * nt * N) return;
-    const int k = (int)(e % N);
-    long long rest = e / N;
-    const int t = (int)(rest % nt);
-    const long long c = rest / nt;
+    if (e >= (long long)nt * N) return;
+    const int k = (int)(e % N), t = (int)(e / N);
+    const int c0 = blockIdx.y * KS_CG;
     const int pidx = t < nl ? t : np - 1;
     const Modulus m = pr.m[pidx];
     const int src = galois_src(k, g, logN);
-    u128 a0{0, 0}, a1{0, 0};
-    for (int j = 0; j < nl; j++) {
-        const uint64_t d = (t == j) ? P[c][poly_off + (long long)j * N + src] : D[((c * nl + j) * nt + t) * N + src];
-        const uint64_t k0 = key[(((size_t)j * 2 + 0) * np + pidx) * N + k];
-        const uint64_t k1 = key[(((size_t)j * 2 + 1) * np + pidx) * N + k];
-        mac_to(a0, d, k0);
-        mac_to(a1, d, k1);
-        if ((j & 7) == 7) { a0 = u128{reduce128(a0, m), 0}; a1 = u128{reduce128(a1, m), 0}; }
+    uint64_t k0[KS_MAXD], k1[KS_MAXD];
+#pragma unroll
+    for (int j = 0; j < KS_MAXD; j++) {
+        if (j < nl) {
+            k0[j] = __ldg(key + (((size_t)j * 2 + 0) * np + pidx) * N + k);
+            k1[j] = __ldg(key + (((size_t)j * 2 + 1) * np + pidx) * N + k);
+        }
     }
-    A[((c * 2 + 0) * nt + t) * N + k] = reduce128(a0, m);
-    A[((c * 2 + 1) * nt + t) * N + k] = reduce128(a1, m);
+    uint64_t dv[KS_CG][KS_MAXD];
+#pragma unroll
+    for (int cc = 0; cc < KS_CG; cc++) {
+        const int c = c0 + cc;
+        if (c >= count) break;
+#pragma unroll
+        for (int j = 0; j < KS_MAXD; j++)
+            if (j < nl)
+                dv[cc][j] = (t == j) ? P[c][poly_off + (long long)j * N + src] : D[(((long long)c * nl + j) * nt + t) * N + src];
+    }
+#pragma unroll
+    for (int cc = 0; cc < KS_CG; cc++) {
+        const int c = c0 + cc;
+        if (c >= count) break;
+        u128 a0{0, 0}, a1{0, 0};
+#pragma unroll
+        for (int j = 0; j < KS_MAXD; j++) {
+            if (j < nl) {
+                mac_to(a0, dv[cc][j], k0[j]);
+                mac_to(a1, dv[cc][j], k1[j]);
+                if ((j & 7) == 7) { a0 = u128{reduce128(a0, m), 0}; a1 = u128{reduce128(a1, m), 0}; }
+            }
+        }
+        A[(((long long)c * 2 + 0) * nt + t) * N + k] = reduce128(a0, m);
+        A[(((long long)c * 2 + 1) * nt + t) * N + k] = reduce128(a1, m);
+    }
 }
 
 std::vector<const uint64_t *> strided_ptrs(const uint64_t *base, int count, size_t stride) {
@@ -101,8 +129,13 @@ static void inner_moddown(Ctx &c, const uint64_t *D, const uint64_t *const *Poly
                           const uint64_t *key, uint32_t g, uint64_t *const *Out, const uint64_t *const *Add, int add_polys) {
     const int N = c.n, nl = level + 1, nt = level + 2, P = c.np - 1;
     Scratch a(c, sizeof(uint64_t) * count * 2 * nt * N);
-    k_ks_inner<<<nblocks((long long)count * nt * N, TB), TB, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np,
-                                                                           key, g, c.primes, a.as<uint64_t>());
+    const dim3 blocks(nblocks((long long)nt * N, 128), (count + KS_CG - 1) / KS_CG);
+    if (nl <= 8)
+        k_ks_inner<8><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, a.as<uint64_t>());
+    else if (nl <= 16)
+        k_ks_inner<16><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, a.as<uint64_t>());
+    else
+        k_ks_inner<40><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, a.as<uint64_t>());
     check_launch("k_ks_inner");
     const int rows = count * 2;
     Scratch y(c, sizeof(uint64_t) * rows * N), z(c, sizeof(uint64_t) * rows * nl * N);

@@ -93,6 +93,20 @@ __global__ void k_mul_scalar(const uint64_t *const *C, uint64_t *const *O, int c
     st2(O[x.ct] + off, mul_shoup(a.x, w, wsh, q), mul_shoup(a.y, w, wsh, q));
 }
 
+// O[c][p][i] += B[c][p][i] * s_i  where B has nlb >= nl limbs per poly (level-dropped read)
+__global__ void k_axpy(uint64_t *const *O, const uint64_t *const *B, int count, int polys, int nl, int nlb, int N,
+                       LimbScalars s, DevPrimes pr) {
+    const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pair >= (long long)count * polys * nl * (N / 2)) return;
+    Idx x;
+    decompose(pair, polys, nl, N, x);
+    const uint64_t q = pr.m[x.limb].q, w = s.v[x.limb], wsh = s.sh[x.limb];
+    uint64_t *o = O[x.ct] + ((size_t)x.poly * nl + x.limb) * N + x.k;
+    const ulonglong2 b = ld2(B[x.ct] + ((size_t)x.poly * nlb + x.limb) * N + x.k);
+    const ulonglong2 a = ld2(o);
+    st2(o, add_mod(a.x, mul_shoup(b.x, w, wsh, q), q), add_mod(a.y, mul_shoup(b.y, w, wsh, q), q));
+}
+
 __global__ void k_add_const(uint64_t *const *C, int count, int nl, int N, LimbScalars s, DevPrimes pr) {
     const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= (long long)count * nl * (N / 2)) return;
@@ -268,6 +282,12 @@ void mul_scalar(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count,
     const long long pairs = (long long)count * polys * nl * (c.n / 2);
     k_mul_scalar<<<nblocks(pairs, TB), TB, 0, c.stream>>>(C, O, count, polys, nl, c.n, s, c.primes);
     check_launch("k_mul_scalar");
+}
+
+void axpy(Ctx &c, uint64_t *const *O, const uint64_t *const *B, int count, int polys, int nl, int nlb, const LimbScalars &s) {
+    const long long pairs = (long long)count * polys * nl * (c.n / 2);
+    k_axpy<<<nblocks(pairs, TB), TB, 0, c.stream>>>(O, B, count, polys, nl, nlb, c.n, s, c.primes);
+    check_launch("k_axpy");
 }
 
 void add_const(Ctx &c, uint64_t *const *C, int count, int nl, const LimbScalars &s) {

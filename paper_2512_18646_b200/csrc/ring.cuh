@@ -18,6 +18,8 @@ void mul_plain(Ctx &c, const uint64_t *const *C, const uint64_t *const *P, uint6
                int shared_pt);
 void mul_scalar(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, const LimbScalars &s);
 void add_const(Ctx &c, uint64_t *const *C, int count, int nl, const LimbScalars &s);
+// O[c][p][i] += B[c][p][i] * s_i for i < nl (B has nlb >= nl limbs per poly)
+void axpy(Ctx &c, uint64_t *const *O, const uint64_t *const *B, int count, int polys, int nl, int nlb, const LimbScalars &s);
 void permute(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, uint32_t g);
 void copy_limbs(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl_in, int nl_out, int limb0);
 void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl);
