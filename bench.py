@@ -286,9 +286,14 @@ def run_ours(args, ws, rank, local):
     d2h = eng.slots * 8
 
     extra = {}
+    cfg5 = {}
+    if not args.no_extra:
+        del left, right, first, out
+        cfg5["cfg5a"] = bench_cfg5a(ws, rank, local, max_over_ranks, barrier)
+        cfg5["cfg5b"] = bench_cfg5b(ws, rank, local, max_over_ranks, barrier)
     if not args.no_extra and rank == 0:
         extra["ntt"] = bench_ntt(eng, peak)
-        extra["configs"] = {"cfg1": bench_cfg1(), "cfg4": bench_cfg4(steps=2)}
+        extra["configs"] = {"cfg1": bench_cfg1(), "cfg4": bench_cfg4(steps=3), **cfg5}
     line = None
     if rank == 0:
         cpu = None
@@ -384,6 +389,72 @@ def bench_cfg4(steps=2):
     return {"metric": "encrypted-CNN images/s (cfg4 conv 16x3x3x3 + degree-2 activation, 16 images/batch, N=2^15)",
             "value": 16 / t, "s_per_batch": t, "max_abs_err": err, "launches_per_batch": launches,
             "e2e_images_per_s": 16 / te, "e2e_h2d_bytes": 3 * 226 * 16 * 226 * 8, "e2e_d2h_bytes": 16 * 224 * eng.slots * 8}
+
+
+def bench_cfg5a(ws, rank, local, max_over_ranks, barrier, steps=5):
+    """Config 5a: HE matmul 256x256 (4 row blocks of 64 x 256 column cts), k sharded over ranks,
+    degree-2 partials summed with one NCCL int64 all-reduce (strong scaling)."""
+    import torch
+
+    from paper_2512_18646_b200 import CkksEngine, config_params
+    from paper_2512_18646_b200.dist import encode_operands_sharded, matmul_outer_sharded, shard_range
+    from tools.workloads import cfg_matmul
+
+    a, b = cfg_matmul(5)
+    blocks = [a[64 * i: 64 * (i + 1)] for i in range(4)]
+    eng = CkksEngine(config_params(5), device=local)
+    lo, hi = shard_range(256, rank, ws)
+    lefts, right = encode_operands_sharded(eng, blocks, b, lo, hi)
+    outs = matmul_outer_sharded(eng, lefts, right)
+    got = np.concatenate([eng.dec(o)[: 64 * 256].reshape(64, 256) for o in outs])
+    err = max_over_ranks(float(np.max(np.abs(got - a @ b))))
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    st.record(eng._stream)
+    for _ in range(steps):
+        outs = matmul_outer_sharded(eng, lefts, right)
+    en.record(eng._stream)
+    torch.cuda.synchronize()
+    t = max_over_ranks(st.elapsed_time(en) / 1e3 / steps)
+    return {"metric": "HE matmul/s (cfg5a 256x256, 4 row blocks x 256 column cts, k sharded, NCCL int64 sum)",
+            "value": 1.0 / t, "ms_per_matmul": t * 1e3, "n_gpus": ws, "scaling": "strong", "max_abs_err": err,
+            "k_per_rank": hi - lo}
+
+
+def bench_cfg5b(ws, rank, local, max_over_ranks, barrier, images=512, group=64):
+    """Config 5b: the config-4 layer on 512 images, 64 images per column ciphertext (8 groups),
+    groups sharded over ranks, no collective (strong scaling)."""
+    import torch
+
+    from paper_2512_18646_b200 import CkksEngine, config_params
+    from paper_2512_18646_b200.cnn import conv_layer, decode_layer, encode_images
+    from paper_2512_18646_b200.dist import image_groups
+    from tools.workloads import ACT4, cfg5b, conv_plain, poly_plain
+
+    imgs, w, b = cfg5b(images)
+    eng = CkksEngine(config_params(5), device=local)
+    mine = image_groups(images, group, rank, ws)
+    chans = [encode_images(eng, imgs[lo:hi], padding=1) for lo, hi in mine]
+    err = 0.0
+    if mine:  # correctness on the first local group
+        lo, hi = mine[0]
+        got = decode_layer(eng, conv_layer(eng, chans[0], w, b, activation=ACT4))
+        err = float(np.max(np.abs(got - poly_plain(conv_plain(imgs[lo:hi], w, b, padding=1), ACT4))))
+    err = max_over_ranks(err)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    st.record(eng._stream)
+    for ch in chans:
+        ys = conv_layer(eng, ch, w, b, activation=ACT4)
+        del ys
+    en.record(eng._stream)
+    torch.cuda.synchronize()
+    t = max_over_ranks(st.elapsed_time(en) / 1e3)
+    return {"metric": "encrypted-CNN images/s (cfg5b: cfg4 layer on 512 images, 64 images/ct, groups sharded)",
+            "value": images / t, "s_per_512_images": t, "n_gpus": ws, "scaling": "strong", "max_abs_err": err,
+            "groups_per_rank": len(mine)}
 
 
 def bench_ntt(eng, peak):

@@ -223,15 +223,22 @@ class CkksEngine:
         """Encode into the leading slots (zeros elsewhere) and encrypt at the top level."""
         return self.enc_batch([values], layout)[0]
 
-    def enc_batch(self, rows, layout: tuple | None = None) -> list[Ciphertext]:
-        """``enc`` of many vectors in one launch (one enc_count each)."""
+    def enc_batch(self, rows, layout: tuple | None = None, nonce0: int | None = None) -> list[Ciphertext]:
+        """``enc`` of many vectors in one launch (one enc_count each).
+
+        Ciphertext i uses encryption nonce ``nonce0 + i`` (default: the engine's running
+        counter).  An explicit ``nonce0`` lets sharded ranks reproduce exactly the
+        ciphertexts a single-GPU run would have produced.
+        """
         vals = self._pad(rows)
         count = vals.shape[0]
         d_vals = self._h2d(vals)
         out = self._empty(1, self.L, count)
+        n0 = self._nonce if nonce0 is None else int(nonce0)
         _lib.check(self._lib.vr_encrypt(self._h, d_vals.data_ptr(), count, vals.shape[1], self.L,
-                                        self.scales[self.L], self._nonce, out.data_ptr()))
-        self._nonce += count
+                                        self.scales[self.L], n0, out.data_ptr()))
+        if nonce0 is None:
+            self._nonce += count
         self._meter.enc_count += count
         self._observe(0)
         return [self._wrap(out[i], self.L, 0, layout) for i in range(count)]
