@@ -293,7 +293,7 @@ def run_ours(args, ws, rank, local):
         cfg5["cfg5b"] = bench_cfg5b(ws, rank, local, max_over_ranks, barrier)
     if not args.no_extra and rank == 0:
         extra["ntt"] = bench_ntt(eng, peak)
-        extra["configs"] = {"cfg1": bench_cfg1(), "cfg4": bench_cfg4(steps=3), **cfg5}
+        extra["configs"] = {"cfg1": bench_cfg1(), "cfg3": bench_cfg3(), "cfg4": bench_cfg4(steps=3), **cfg5}
     line = None
     if rank == 0:
         cpu = None
@@ -389,6 +389,32 @@ def bench_cfg4(steps=2):
     return {"metric": "encrypted-CNN images/s (cfg4 conv 16x3x3x3 + degree-2 activation, 16 images/batch, N=2^15)",
             "value": 16 / t, "s_per_batch": t, "max_abs_err": err, "launches_per_batch": launches,
             "e2e_images_per_s": 16 / te, "e2e_h2d_bytes": 3 * 226 * 16 * 226 * 8, "e2e_d2h_bytes": 16 * 224 * eng.slots * 8}
+
+
+def bench_cfg3(steps=3):
+    """Config 3: 64 images 28x28 -> conv 5x4x4 stride 2 -> square -> dense 845->64 -> square -> dense 64->10
+    (N = 2^14, depth 5), images/s of the encrypted inference (inputs resident, dense plaintexts included)."""
+    import torch
+
+    from paper_2512_18646_b200 import CkksEngine, config_params
+    from paper_2512_18646_b200.cnn import cnn_cfg3, decode_logits
+    from tools.workloads import cfg3, cfg3_plain
+
+    imgs, w, w1, w2 = cfg3()
+    eng = CkksEngine(config_params(3))
+    logits = cnn_cfg3(eng, imgs, w, w1, w2)
+    err = float(np.max(np.abs(decode_logits(eng, logits, 64, 28) - cfg3_plain(imgs, w, w1, w2))))
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    st.record(eng._stream)
+    for _ in range(steps):
+        logits = cnn_cfg3(eng, imgs, w, w1, w2)
+    en.record(eng._stream)
+    torch.cuda.synchronize()
+    t = st.elapsed_time(en) / 1e3 / steps
+    return {"metric": "encrypted-CNN images/s (cfg3 small CNN, 64 images per pass, N=2^14, depth 5)",
+            "value": 64 / t, "s_per_pass": t, "max_abs_err": err,
+            "note": "each pass encrypts the 28 image columns and encodes the 4160+640 dense-layer plaintexts"}
 
 
 def bench_cfg5a(ws, rank, local, max_over_ranks, barrier, steps=5):

@@ -116,6 +116,10 @@ int vr_tensor_sum(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *
  * integer (it may exceed 64 bits), mask: device plaintext [level+1][N] */
 int vr_conv_columns(vr_ctx *ctx, const uint64_t *const *X, int C, int W, int k, const int64_t *w, const uint64_t *bias_res, int F,
                     const int *out_cols, int nout, const uint64_t *mask_pt, int level, uint64_t *const *Y);
+/* plaintext-weight dense layer on column ciphertexts (config 3; built from SlotEngine.cmul + add,
+ * engine.py:208-230): Y[u] = rescale(sum_j PT[u*nx + j] (.) X[j]), PT are encoded plaintexts [level+1][N] */
+int vr_pt_matvec(vr_ctx *ctx, const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int level,
+                 uint64_t *const *Y);
 /* poly_activation (pipeline.py:180-197) on a batch; kc = integer constants {c3, c2, c1, c0} at their
  * target scales */
 int vr_poly_activation(vr_ctx *ctx, const uint64_t *const *x, int count, int level, const int64_t *kc, int c3_zero,

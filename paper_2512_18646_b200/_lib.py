@@ -58,6 +58,7 @@ _SIGS = {
     "vr_conv_columns": [c_vp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
                         c_u64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, c_vp,
                         ctypes.c_int, c_vpp],
+    "vr_pt_matvec": [c_vp, c_vpp, ctypes.c_int, c_vpp, ctypes.c_int, ctypes.c_int, c_vpp],
     "vr_poly_activation": [c_vp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, c_vpp],
 }
 

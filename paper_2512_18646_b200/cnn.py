@@ -87,3 +87,155 @@ def decode_layer(engine: CkksEngine, ys, stride: int = 1) -> np.ndarray:
         img = np.stack([vecs[:, b * y.stride: b * y.stride + y.h].T for b in range(y.m)])  # (m, h, w)
         outs.append(img[:, ::stride, :])
     return np.stack(outs, axis=1)
+
+
+# ---------------------------------------------------------------------------
+# Config 3: conv 5x4x4 stride 2 -> square -> dense 845->64 -> square -> dense 64->10
+# entirely in the column layout (the reference has no column-layout dense layer,
+# SURVEY.md section 8d).  Depth 1 + 1 + 1 + 1 + 1 = 5.
+
+def encode_plain_batch(engine: CkksEngine, rows, level: int, scale: float):
+    """Encode many slot vectors as plaintexts [count][level+1][N] (one launch)."""
+    import torch
+
+    from . import _lib
+
+    vals = engine._pad(rows)
+    d_vals = engine._h2d(vals)
+    pts = torch.empty((vals.shape[0], level + 1, engine.N), dtype=torch.int64, device=engine.device)
+    _lib.check(engine._lib.vr_encode(engine.handle, d_vals.data_ptr(), vals.shape[0], vals.shape[1], level, scale,
+                                     pts.data_ptr()))
+    return pts
+
+
+def dense_columns(engine: CkksEngine, cts, pts, ny: int):
+    """Y[u] = sum_j pts[u*nx + j] (.) cts[j], rescaled: a plaintext-weight dense layer.
+
+    Metered like the reference composition: nx cmuls and nx-1 adds per output.
+    """
+    import torch
+
+    from . import _lib
+    from .engine import Ciphertext
+
+    cts = list(cts)
+    nx = len(cts)
+    lv = cts[0].level
+    if any(c.level != lv for c in cts):
+        raise EngineError("dense_columns inputs must share a level")
+    out = torch.empty((ny, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
+    _lib.check(engine._lib.vr_pt_matvec(engine.handle, _lib.ptr_array([c.ptr() for c in cts]), nx,
+                                        _lib.ptr_array([pts[i].data_ptr() for i in range(ny * nx)]), ny, lv,
+                                        _lib.ptr_array([out[u].data_ptr() for u in range(ny)])))
+    depth = max(c.depth for c in cts) + 1
+    engine._meter.cmul_count += ny * nx
+    engine._meter.add_count += ny * (nx - 1)
+    engine._observe(depth)
+    return [Ciphertext(out[u], lv - 1, engine.scales[lv - 1], depth, cts[0].layout, engine._id) for u in range(ny)]
+
+
+def rotate_batch(engine: CkksEngine, cts, steps):
+    """Hoisted rotations of many ciphertexts: result[c][r] = rot(cts[c], steps[r])."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .engine import Ciphertext
+
+    cts = list(cts)
+    lv = cts[0].level
+    steps = [int(s) for s in steps]
+    out = torch.empty((len(cts), len(steps), 2, lv + 1, engine.N), dtype=torch.int64, device=engine.device)
+    st = (ctypes.c_int64 * len(steps))(*steps)
+    _lib.check(engine._lib.vr_rotate(engine.handle, _lib.ptr_array([c.ptr() for c in cts]),
+                                     _lib.ptr_array([out[i, r].data_ptr() for i in range(len(cts)) for r in range(len(steps))]),
+                                     len(cts), lv, len(steps), st))
+    engine._meter.rot_count += len(cts) * len(steps)
+    return [[Ciphertext(out[i, r], lv, c.scale, c.depth, c.layout, engine._id) for r in range(len(steps))]
+            for i, c in enumerate(cts)]
+
+
+def add_batch(engine: CkksEngine, xs, ys):
+    import torch
+
+    from . import _lib
+    from .engine import Ciphertext
+
+    xs, ys = list(xs), list(ys)
+    lv = xs[0].level
+    out = torch.empty((len(xs), 2, lv + 1, engine.N), dtype=torch.int64, device=engine.device)
+    _lib.check(engine._lib.vr_add(engine.handle, _lib.ptr_array([x.ptr() for x in xs]), _lib.ptr_array([y.ptr() for y in ys]),
+                                  _lib.ptr_array([out[i].data_ptr() for i in range(len(xs))]), len(xs), 1, lv, 0))
+    engine._meter.add_count += len(xs)
+    return [Ciphertext(out[i], lv, x.scale, max(x.depth, y.depth), x.layout, engine._id) for i, (x, y) in enumerate(zip(xs, ys))]
+
+
+def block_sum(engine: CkksEngine, cts, terms: int, stride: int):
+    """slot p <- sum_{r < terms} slot(p + stride * r), by rotate-and-add doubling (hoisted per level).
+
+    For terms = 13, stride = 2 this uses 5 rotations: T2 = T1 + rot(T1, 2), T4 = T2 + rot(T2, 4),
+    T8 = T4 + rot(T4, 8), total = T8 + rot(T4, 16) + rot(T1, 24).
+    """
+    bits = [b for b in range(terms.bit_length()) if terms >> b & 1]
+    top = terms.bit_length() - 1
+    T = {0: list(cts)}
+    # extra rotations each power needs for the final combination (offset = stride * higher bits)
+    offsets = {}
+    acc_off = 1 << top
+    for b in sorted(bits, reverse=True)[1:]:
+        offsets[b] = stride * acc_off
+        acc_off += 1 << b
+    for lvl in range(top + 1):
+        steps = []
+        if lvl < top:
+            steps.append(stride << lvl)
+        if lvl in offsets:
+            steps.append(offsets[lvl])
+        rot = rotate_batch(engine, T[lvl], steps) if steps else [[] for _ in T[lvl]]
+        if lvl < top:
+            T[lvl + 1] = add_batch(engine, T[lvl], [r[0] for r in rot])
+        if lvl in offsets:
+            offsets[lvl] = [r[-1] for r in rot]
+    total = T[top]
+    for b in sorted(offsets):
+        total = add_batch(engine, total, offsets[b])
+    return total
+
+
+def cnn_cfg3(engine: CkksEngine, imgs, w, w1, w2):
+    """Config 3 on a batch of (m, 28, 28) images: returns the 10 logit ciphertexts (logit v of image b
+    at slot b*28) and the plaintexts built for the dense layers."""
+    imgs = np.asarray(imgs, dtype=np.float64)
+    m, h, wd = imgs.shape
+    F, _, k, _ = w.shape
+    out_w = wd - k + 1
+    cols = list(range(0, out_w, 2))                      # stride-2 columns: 13
+    rows = list(range(0, h - k + 1, 2))                  # stride-2 rows (slot offsets): 13
+    x = encode_image_columns(engine, imgs)
+    conv = conv_columns_multi(engine, [x], w, np.zeros(F), out_cols=cols)
+    feats = square_batch(engine, [ct for y in conv for ct in y.cts])          # F*13 cts, order (f, o)
+    lv = feats[0].level
+    S = engine.slots
+    nr, no = len(rows), len(cols)
+    # dense 1: neuron u, input ct (f, o): value W1[u, f*169 + r*13 + o] at slots b*h + 2r
+    ny = w1.shape[0]
+    masks = np.zeros((ny, F * no, S))
+    slot_idx = (np.arange(m)[:, None] * h + np.asarray(rows)[None, :]).reshape(-1)  # (b, r) -> slot
+    for f in range(F):
+        for o in range(no):
+            wv = w1[:, f * nr * no + np.arange(nr) * no + o]                        # (ny, nr)
+            masks[:, f * no + o, slot_idx] = np.tile(wv, (1, m))
+    pts1 = encode_plain_batch(engine, masks.reshape(ny * F * no, S), lv, engine.scales[lv])
+    hid = dense_columns(engine, feats, pts1, ny)
+    hid = block_sum(engine, hid, nr, 2)
+    hid = square_batch(engine, hid)
+    lv2 = hid[0].level
+    nz = w2.shape[0]
+    pts2 = encode_plain_batch(engine, np.repeat(w2.reshape(-1, 1), S, axis=1), lv2, engine.scales[lv2])
+    return dense_columns(engine, hid, pts2, nz)
+
+
+def decode_logits(engine: CkksEngine, logits, m: int, stride: int) -> np.ndarray:
+    vecs = engine.dec_batch(logits)  # [10][S]
+    return vecs[:, np.arange(m) * stride].T

@@ -482,6 +482,18 @@ int vr_conv_columns(vr_ctx *h, const uint64_t *const *X, int C, int W, int k, co
     });
 }
 
+int vr_pt_matvec(vr_ctx *h, const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int level,
+                 uint64_t *const *Y) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
+        if (nx <= 0 || ny <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable tx(c, vec(X, nx)), tp(c, vec(PT, (size_t)nx * ny)), ty(c, vecm(Y, ny));
+        vr::pt_matvec(c, tx.c_(), nx, tp.c_(), ny, level, ty.m_());
+    });
+}
+
 int vr_poly_activation(vr_ctx *h, const uint64_t *const *x, int count, int level, const int64_t *kc, int c3_zero,
                        uint64_t *const *out) {
     return guard([&] {

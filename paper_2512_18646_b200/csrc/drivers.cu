@@ -152,6 +152,47 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
     }
 }
 
+// Plaintext mat-vec: Yp[u] = sum_j PT[u*nx + j] (.) X[j] (both polys), 128-bit accumulation.
+// One thread = (limb, coefficient) x UG outputs; each plaintext word feeds two MACs.
+template <int UG>
+__global__ void __launch_bounds__(128) k_pt_matvec(const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int nl,
+                                                   int N, DevPrimes pr, uint64_t *Yp) {
+    const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (kk >= N) return;
+    const int i = blockIdx.y;
+    const int u0 = blockIdx.z * UG;
+    const Modulus m = pr.m[i];
+    const size_t o0 = (size_t)i * N + kk, o1 = (size_t)(nl + i) * N + kk;
+    u128 acc[UG][2];
+#pragma unroll
+    for (int u = 0; u < UG; u++) acc[u][0] = acc[u][1] = u128{0, 0};
+    for (int j = 0; j < nx; j++) {
+        const uint64_t x0 = X[j][o0], x1 = X[j][o1];
+#pragma unroll
+        for (int u = 0; u < UG; u++) {
+            if (u0 + u < ny) {
+                const uint64_t pt = PT[(size_t)(u0 + u) * nx + j][o0];
+                mac_to(acc[u][0], pt, x0);
+                mac_to(acc[u][1], pt, x1);
+            }
+        }
+        if ((j & 7) == 7) {
+#pragma unroll
+            for (int u = 0; u < UG; u++) {
+                acc[u][0] = u128{reduce128(acc[u][0], m), 0};
+                acc[u][1] = u128{reduce128(acc[u][1], m), 0};
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < UG; u++) {
+        if (u0 + u >= ny) break;
+        uint64_t *y = Yp + (size_t)(u0 + u) * 2 * nl * N;
+        y[o0] = reduce128(acc[u][0], m);
+        y[o1] = reduce128(acc[u][1], m);
+    }
+}
+
 }  // namespace
 
 void mul_batch(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *Out, int count, int level) {
@@ -336,6 +377,24 @@ void poly_activation(Ctx &c, const uint64_t *const *X, int count, int level, con
     for (int c0 = 0; c0 < count; c0 += chunk) {
         const int n = std::min(chunk, count - c0);
         poly_activation_chunk(c, X + c0, n, level, kc, c3_zero, Out + c0);
+    }
+}
+
+void pt_matvec(Ctx &c, const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int level, uint64_t *const *Y) {
+    const int N = c.n, nl = level + 1;
+    const size_t ctw = (size_t)2 * nl * N;
+    constexpr int UG = 8;
+    const int chunk = (int)std::max<size_t>(UG, std::min<size_t>((size_t)ny, ((size_t)2 << 30) / (ctw * 8)));
+    Scratch yp(c, sizeof(uint64_t) * (size_t)std::min(chunk, ny) * ctw);
+    for (int u0 = 0; u0 < ny; u0 += chunk) {
+        const int nu = std::min(chunk, ny - u0);
+        dim3 grid(nblocks(N, 128), nl, (nu + UG - 1) / UG);
+        k_pt_matvec<UG><<<grid, 128, 0, c.stream>>>(X, nx, PT + (size_t)u0 * nx, nu, nl, N, c.primes, yp.as<uint64_t>());
+        check_launch("k_pt_matvec");
+        std::vector<const uint64_t *> ins(nu);
+        for (int u = 0; u < nu; u++) ins[u] = yp.as<uint64_t>() + (size_t)u * ctw;
+        PtrTable ti(c, ins);
+        rescale(c, ti.c_(), Y + u0, nu, 2, level);
     }
 }
 

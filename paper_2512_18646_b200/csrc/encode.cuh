@@ -16,6 +16,7 @@ void mul_batch(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint6
 void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out);
 void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, int k, const int64_t *w, const uint64_t *bias,
                   int F, const int *out_cols, int nout, const uint64_t *mask_pt, int level, const std::vector<uint64_t *> &Y);
+void pt_matvec(Ctx &c, const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int level, uint64_t *const *Y);
 void poly_activation(Ctx &c, const uint64_t *const *X, int count, int level, const int64_t *kc, int c3_zero,
                      uint64_t *const *Out);
 

@@ -64,3 +64,70 @@ def test_cfg4_full_size_decoded():
     assert got.shape == (16, 16, 224, 224)
     assert float(np.max(np.abs(got - want))) < TOL
     assert all(ct.depth == 3 for y in ys for ct in y.cts)
+
+
+def _oracle_cfg3(o, imgs, w, w1, w2):
+    """Oracle restatement of paper_2512_18646_b200.cnn.cnn_cfg3 (same ciphertexts, same op order)."""
+    m, h, wd = imgs.shape
+    F, _, k, _ = w.shape
+    cols = list(range(0, wd - k + 1, 2))
+    rows = list(range(0, h - k + 1, 2))
+    X = [o.enc(imgs[:, :, j].reshape(-1)) for j in range(wd)]
+    conv = o.conv_columns_multi(X, 1, wd, w, np.zeros(F), cols, m, h, h - k + 1)
+    feats = [o.mul(c, c) for c in conv]
+    lv = feats[0].level
+    S, nr, no, ny = o.slots, len(rows), len(cols), w1.shape[0]
+    slot_idx = (np.arange(m)[:, None] * h + np.asarray(rows)[None, :]).reshape(-1)
+
+    def dense(xs, mask_rows, ny_):
+        lvx = xs[0].level
+        outs = []
+        for u in range(ny_):
+            acc = None
+            for j, x in enumerate(xs):
+                term = o.c.mul_plain(x.data, o.c.encode(mask_rows[u * len(xs) + j], lvx, o.scales[lvx]))
+                acc = term if acc is None else o.c.add(acc, term)
+            outs.append(type(xs[0])(o.c.rescale(acc), lvx - 1, o.scales[lvx - 1]))
+        return outs
+
+    masks = np.zeros((ny, F * no, S))
+    for f in range(F):
+        for oc in range(no):
+            masks[:, f * no + oc, slot_idx] = np.tile(w1[:, f * nr * no + np.arange(nr) * no + oc], (1, m))
+    hid = dense(feats, masks.reshape(-1, S), ny)
+    T1 = hid
+    T2 = [o.add(t, o.rot(t, 2)) for t in T1]
+    T4 = [o.add(t, o.rot(t, 4)) for t in T2]
+    T8 = [o.add(t, o.rot(t, 8)) for t in T4]
+    tot = [o.add(o.add(a, o.rot(t1, 24)), o.rot(t4, 16)) for a, t1, t4 in zip(T8, T1, T4)]
+    sq = [o.mul(t, t) for t in tot]
+    return dense(sq, np.repeat(w2.reshape(-1, 1), S, axis=1), w2.shape[0])
+
+
+def test_cfg3_reduced_bit_exact():
+    from paper_2512_18646_b200.cnn import cnn_cfg3
+    from tools.workloads import cfg3
+
+    imgs, w, w1, w2 = cfg3()
+    imgs, w1, w2 = imgs[:3], w1[:4], w2[:, :4]
+    p = config_params(3)
+    g, o = CkksEngine(p), OracleEngine.from_params(p)
+    logits = cnn_cfg3(g, imgs, w, w1, w2)
+    want = _oracle_cfg3(o, imgs, w, w1, w2)
+    for gl, ol in zip(logits, want):
+        assert gl.level == 0
+        np.testing.assert_array_equal(gl.residues(), ol.data)
+
+
+def test_cfg3_full_size_decoded():
+    from paper_2512_18646_b200.cnn import cnn_cfg3, decode_logits
+    from tools.workloads import cfg3, cfg3_plain
+
+    imgs, w, w1, w2 = cfg3()
+    g = CkksEngine(config_params(3))
+    logits = cnn_cfg3(g, imgs, w, w1, w2)
+    got = decode_logits(g, logits, 64, 28)
+    want = cfg3_plain(imgs, w, w1, w2)
+    assert got.shape == (64, 10)
+    assert float(np.max(np.abs(got - want))) < TOL
+    assert all(c.level == 0 and c.depth == 5 for c in logits)
