@@ -98,6 +98,34 @@ void check_level(const vr::Ctx &c, int level) {
 namespace vr {
 unsigned long long g_launches = 0;
 
+const void *const *cached_table(Ctx &c, const void *const *ptrs, size_t n) {
+    static const void *empty_slot = nullptr;
+    if (n == 0) n = 1, ptrs = &empty_slot;
+    c.table_clock++;
+    for (auto &e : c.tables)
+        if (e.key.size() == n && std::memcmp(e.key.data(), ptrs, n * sizeof(void *)) == 0) {
+            e.last_use = c.table_clock;
+            return (const void *const *)e.dev;
+        }
+    constexpr size_t kMaxTables = 512;
+    Ctx::TableEntry *slot = nullptr;
+    if (c.tables.size() < kMaxTables) {
+        c.tables.emplace_back();
+        slot = &c.tables.back();
+    } else {
+        slot = &c.tables[0];
+        for (auto &e : c.tables)
+            if (e.last_use < slot->last_use) slot = &e;
+        VR_CUDA(cudaFreeAsync(slot->dev, c.stream));  // stream-ordered: earlier users finish first
+        slot->dev = nullptr;
+    }
+    slot->key.assign(ptrs, ptrs + n);
+    slot->last_use = c.table_clock;
+    VR_CUDA(cudaMallocAsync(&slot->dev, n * sizeof(void *), c.stream));
+    upload_async(c, slot->dev, ptrs, n * sizeof(void *));
+    return (const void *const *)slot->dev;
+}
+
 void upload_async(Ctx &c, void *dst, const void *src, size_t bytes) {
     const char *p = (const char *)src;
     char *d = (char *)dst;
@@ -223,6 +251,8 @@ int vr_ctx_destroy(vr_ctx *h) {
         if (c.s_ntt) cudaFree(c.s_ntt);
         if (c.pk) cudaFree(c.pk);
         for (auto &kv : c.gkeys) cudaFree(kv.second);
+        for (auto &e : c.tables)
+            if (e.dev) cudaFree(e.dev);
         for (int i = 0; i < vr::Ctx::kStageSlots; i++)
             if (c.stage_evt[i]) cudaEventDestroy(c.stage_evt[i]);
         if (c.stage) cudaFreeHost(c.stage);

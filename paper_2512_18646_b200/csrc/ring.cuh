@@ -43,15 +43,13 @@ void rotate_batch(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int c
 uint64_t *galois_key(Ctx &c, uint32_t g);
 uint64_t *relin_key(Ctx &c);
 
-// host helper: build a device pointer table
+// host helper: device pointer table (cached by value in the context)
 struct PtrTable {
-    Scratch s;
+    const void *const *p;
     PtrTable(Ctx &c, const std::vector<const uint64_t *> &v)
-        : s(c, sizeof(void *) * (v.empty() ? 1 : v.size())) {
-        if (!v.empty()) upload_async(c, s.p, v.data(), sizeof(void *) * v.size());
-    }
-    const uint64_t *const *c_() const { return (const uint64_t *const *)s.p; }
-    uint64_t *const *m_() const { return (uint64_t *const *)s.p; }
+        : p(cached_table(c, (const void *const *)v.data(), v.size())) {}
+    const uint64_t *const *c_() const { return (const uint64_t *const *)p; }
+    uint64_t *const *m_() const { return (uint64_t *const *)p; }
 };
 
 }  // namespace vr

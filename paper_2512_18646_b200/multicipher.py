@@ -92,7 +92,24 @@ def encode_right(engine: CkksEngine, b, m: int) -> ColumnEncodedMatrix:
 
 def _common_level(engine: CkksEngine, cts):
     lv = min(ct.level for ct in cts)
+    if all(ct.level == lv for ct in cts):
+        return cts, lv
     return [engine.adjust(ct, lv) for ct in cts], lv
+
+
+def _checked_ptrs(engine: CkksEngine, cem: ColumnEncodedMatrix):
+    """(level, [device pointers]) of a column-encoded operand, validated and cached on the object."""
+    cached = getattr(cem, "_vr_ptrs", None)
+    if cached is not None and cached[0] == engine._id:
+        return cached[1], cached[2]
+    for c in cem.cts:
+        engine._check(c)
+    lv = min(c.level for c in cem.cts)
+    ptrs = None
+    if all(c.level == lv for c in cem.cts):
+        ptrs = [c.ptr() for c in cem.cts]
+        object.__setattr__(cem, "_vr_ptrs", (engine._id, lv, ptrs))
+    return lv, ptrs
 
 
 def matmul_outer(engine: CkksEngine, left: ColumnEncodedMatrix, right: ColumnEncodedMatrix) -> PackedMatrix:
@@ -121,20 +138,26 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
             raise LayoutError("operands must be a (left, right) column-encoded pair")
         if lf.n != n or lf.p != right.p:
             raise LayoutError("row blocks must share n and p with the right operand")
-    allc = [c for lf in lefts for c in lf.cts] + list(right.cts)
-    for c in allc:
-        engine._check(c)
-    allc, lv = _common_level(engine, allc)
+    infos = [_checked_ptrs(engine, lf) for lf in lefts] + [_checked_ptrs(engine, right)]
+    lvs = {lv for lv, _ in infos}
+    if len(lvs) == 1 and all(p is not None for _, p in infos):
+        lv = lvs.pop()
+        lptrs = [p for _, ps in infos[:-1] for p in ps]
+        rptrs = infos[-1][1]
+    else:
+        allc, lv = _common_level(engine, [c for lf in lefts for c in lf.cts] + list(right.cts))
+        lptrs = [c.ptr() for c in allc[: nb * n]]
+        rptrs = [c.ptr() for c in allc[nb * n:]]
     if lv < 1:
         raise EngineError("multiplicative depth exhausted: operands are at level 0")
-    Ls, Rs = allc[: nb * n], allc[nb * n:]
     outs = torch.empty((nb, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
     _lib.check(engine._lib.vr_matmul_outer(
-        engine.handle, _lib.ptr_array([c.ptr() for c in Ls]), _lib.ptr_array([c.ptr() for c in Rs]), n, nb, lv,
+        engine.handle, _lib.ptr_array(lptrs), _lib.ptr_array(rptrs), n, nb, lv,
         _lib.ptr_array([outs[b].data_ptr() for b in range(nb)])))
+    rdepth = max(c.depth for c in right.cts)
     res = []
     for b, lf in enumerate(lefts):
-        depth = max(c.depth for c in list(lf.cts) + list(right.cts)) + 1
+        depth = max(rdepth, max(c.depth for c in lf.cts)) + 1
         engine._meter.mul_count += n
         engine._meter.add_count += n - 1
         engine._observe(depth)
