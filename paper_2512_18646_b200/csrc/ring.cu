@@ -6,6 +6,8 @@
 // arrays; each thread handles two adjacent coefficients with 128-bit loads so
 // a warp moves 512 contiguous bytes per access.
 #include <cooperative_groups.h>
+#include <algorithm>
+#include <cstdlib>
 
 #include "ring.cuh"
 
@@ -157,57 +159,134 @@ __global__ void k_mod_fixup(uint64_t *data, long long count_polys, int nl, int N
     st2(p, reduce64(a.x, m), reduce64(a.y, m));
 }
 
-// Fused sum_k tensor(L[b][k], R[k]) for NB row blocks sharing the right operand.
-// Grid (coefficient tiles, limbs, SPLIT): the SPLIT CTAs of a thread-block
-// cluster walk disjoint quarters of the k range for the same 256 coefficients,
-// accumulate 64x64->128-bit products (folded mod q every 8 terms), reduce
-// their partials mod q and combine them through distributed shared memory;
-// cluster rank 0 writes the degree-2 result.  R is read once per block group.
-constexpr int TS_THREADS = 128, TS_SPLIT = 4;
+// ---- TMA bulk-copy + mbarrier helpers (sm_90+/sm_100a PTX) ----------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done)
+                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "memory");
+    } while (!done);
+}
+// global -> shared bulk copy (TMA engine, no tensor map), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 
-template <int NB>
-__global__ void __cluster_dims__(1, 1, TS_SPLIT) __launch_bounds__(TS_THREADS)
+// Fused sum_k tensor(L[b][k], R[k]) for NB row blocks sharing the right operand.
+// Grid (coefficient tiles of TS_TILE, limbs, TS_SPLIT): the TS_SPLIT CTAs of a
+// thread-block cluster take disjoint parts of the k range.  Inside a CTA one
+// producer warp streams the 2*NB + 2 limb tiles of every k into an
+// TS_STAGES-deep shared-memory ring with TMA bulk copies (cp.async.bulk +
+// mbarrier expect_tx), so ~64 KB per CTA are always in flight; the consumer
+// warps accumulate the 64x64 -> 128-bit products (folded mod q every 8 terms).
+// Partials are reduced mod q and combined through distributed shared memory;
+// cluster rank 0 writes the degree-2 result.  R is streamed once per group.
+template <int NB, int TILE, int MAXST = 8>
+__host__ __device__ constexpr int ts_stages() {
+    // ring of (2 NB + 2) limb tiles per stage, <= ~200 KB of shared memory, 2..8 stages
+    return (200 * 1024) / ((2 * NB + 2) * TILE * 8) > MAXST ? MAXST
+           : ((200 * 1024) / ((2 * NB + 2) * TILE * 8) < 2 ? 2 : (200 * 1024) / ((2 * NB + 2) * TILE * 8));
+}
+
+template <int NB, int TS_TILE, int TS_SPLIT, int MAXST>
+__global__ void __launch_bounds__(TS_TILE / 2 + 32)
     k_tensor_sum(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O) {
-    __shared__ ulonglong2 part[NB * 3][TS_THREADS];
+    constexpr int TS_CONSUMERS = TS_TILE / 2;  // 2 coefficients per consumer thread
+    constexpr int TS_STAGES = ts_stages<NB, TS_TILE, MAXST>();
+    constexpr int ARR = 2 * NB + 2;  // limb tiles per stage: L[b] poly0/poly1 ..., R poly0/poly1
+    extern __shared__ __align__(128) uint64_t ts_smem[];
+    uint64_t *ring = ts_smem;                                        // [STAGES][ARR][tile]
+    __shared__ __align__(8) uint64_t full[TS_STAGES], empty[TS_STAGES];
+    // partials reuse the ring after the stream is drained: [NB*3][TS_CONSUMERS]
+    ulonglong2(*part)[TS_CONSUMERS] = reinterpret_cast<ulonglong2(*)[TS_CONSUMERS]>(ts_smem);
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
-    const int k = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
-    const int i = blockIdx.y;
+    const int tile = N < TS_TILE ? N : TS_TILE;
+    const int cons = tile / 2;
+    const int k0 = blockIdx.x * tile, i = blockIdx.y;
     const int z = (int)cluster.block_rank();
-    const bool live = k < N;
-    const Modulus m = pr.m[i];
-    const size_t o0 = (size_t)i * N + k, o1 = (size_t)(nl + i) * N + k;
     const int per = (n + TS_SPLIT - 1) / TS_SPLIT;
-    const int tb = z * per, te = min(n, tb + per);
-    u128 acc[NB][3][2];
-#pragma unroll
-    for (int b = 0; b < NB; b++)
-#pragma unroll
-        for (int p = 0; p < 3; p++)
-#pragma unroll
-            for (int e = 0; e < 2; e++) acc[b][p][e] = u128{0, 0};
-    if (live) {
-        for (int t0 = tb; t0 < te; t0 += 8) {
-            const int tend = min(te, t0 + 8);
-#pragma unroll 4
-            for (int t = t0; t < tend; t++) {
-                const uint64_t *r = R[t];
-                const ulonglong2 r0 = ld2(r + o0), r1 = ld2(r + o1);
+    const int tb = min(n, z * per), te = min(n, tb + per);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int producer_warp = TS_CONSUMERS / 32;  // the last warp
+    const int nwarps_cons = (cons + 31) / 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TS_STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], nwarps_cons);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const Modulus m = pr.m[i];
+    if (warp == producer_warp) {
+        if (lane == 0) {
+            const uint32_t bytes = (uint32_t)tile * 8;
+            const size_t o0 = (size_t)i * N + k0, o1 = (size_t)(nl + i) * N + k0;
+            for (int t = tb, it = 0; t < te; t++, it++) {
+                const int s = it % TS_STAGES;
+                if (it >= TS_STAGES) mbar_wait(&empty[s], ((it / TS_STAGES) - 1) & 1);
+                uint64_t *st = ring + (size_t)s * ARR * tile;
+                mbar_expect_tx(&full[s], bytes * ARR);
 #pragma unroll
                 for (int b = 0; b < NB; b++) {
                     const uint64_t *l = L[b * n + t];
-                    const ulonglong2 l0 = ld2(l + o0), l1 = ld2(l + o1);
-                    mac_to(acc[b][0][0], l0.x, r0.x);
-                    mac_to(acc[b][0][1], l0.y, r0.y);
-                    mac_to(acc[b][1][0], l0.x, r1.x);
-                    mac_to(acc[b][1][1], l0.y, r1.y);
-                    mac_to(acc[b][1][0], l1.x, r0.x);
-                    mac_to(acc[b][1][1], l1.y, r0.y);
-                    mac_to(acc[b][2][0], l1.x, r1.x);
-                    mac_to(acc[b][2][1], l1.y, r1.y);
+                    bulk_g2s(st + (2 * b) * tile, l + o0, bytes, &full[s]);
+                    bulk_g2s(st + (2 * b + 1) * tile, l + o1, bytes, &full[s]);
                 }
+                const uint64_t *r = R[t];
+                bulk_g2s(st + (2 * NB) * tile, r + o0, bytes, &full[s]);
+                bulk_g2s(st + (2 * NB + 1) * tile, r + o1, bytes, &full[s]);
             }
-            if (tend < te) {
+        }
+    }
+    u128 acc[NB][3][2];
+    if (warp != producer_warp && threadIdx.x < cons) {
+#pragma unroll
+        for (int b = 0; b < NB; b++)
+#pragma unroll
+            for (int p = 0; p < 3; p++)
+#pragma unroll
+                for (int e = 0; e < 2; e++) acc[b][p][e] = u128{0, 0};
+        const int c2 = threadIdx.x * 2;
+        const int live = cons - warp * 32;  // consumer lanes in this warp (small N: partial warp)
+        const unsigned wmask = live >= 32 ? 0xffffffffu : ((1u << live) - 1u);
+        for (int t = tb, it = 0; t < te; t++, it++) {
+            const int s = it % TS_STAGES;
+            mbar_wait(&full[s], (it / TS_STAGES) & 1);
+            const uint64_t *st = ring + (size_t)s * ARR * tile;
+            const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB) * tile + c2);
+            const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB + 1) * tile + c2);
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                const ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(st + (2 * b) * tile + c2);
+                const ulonglong2 l1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * b + 1) * tile + c2);
+                mac_to(acc[b][0][0], l0.x, r0.x);
+                mac_to(acc[b][0][1], l0.y, r0.y);
+                mac_to(acc[b][1][0], l0.x, r1.x);
+                mac_to(acc[b][1][1], l0.y, r1.y);
+                mac_to(acc[b][1][0], l1.x, r0.x);
+                mac_to(acc[b][1][1], l1.y, r0.y);
+                mac_to(acc[b][2][0], l1.x, r1.x);
+                mac_to(acc[b][2][1], l1.y, r1.y);
+            }
+            __syncwarp(wmask);
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if ((it & 7) == 7) {
 #pragma unroll
                 for (int b = 0; b < NB; b++)
 #pragma unroll
@@ -217,13 +296,17 @@ __global__ void __cluster_dims__(1, 1, TS_SPLIT) __launch_bounds__(TS_THREADS)
             }
         }
     }
+    __syncthreads();  // ring drained: reuse it for the partials
+    if (warp != producer_warp && threadIdx.x < cons) {
 #pragma unroll
-    for (int b = 0; b < NB; b++)
+        for (int b = 0; b < NB; b++)
 #pragma unroll
-        for (int p = 0; p < 3; p++)
-            part[b * 3 + p][threadIdx.x] = make_ulonglong2(reduce128(acc[b][p][0], m), reduce128(acc[b][p][1], m));
+            for (int p = 0; p < 3; p++)
+                part[b * 3 + p][threadIdx.x] = make_ulonglong2(reduce128(acc[b][p][0], m), reduce128(acc[b][p][1], m));
+    }
     cluster.sync();
-    if (z == 0 && live) {
+    if (z == 0 && threadIdx.x < cons) {
+        const int k = k0 + threadIdx.x * 2;
 #pragma unroll
         for (int b = 0; b < NB; b++) {
             uint64_t *o = O[b];
@@ -315,12 +398,48 @@ void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl) {
     check_launch("k_mod_fixup");
 }
 
+// Launch shape (tile, split-K) -- tuned on B200 with tools/bw_probe.py; VR_TS_VARIANT overrides.
+template <int NB, int TILE, int SPLIT, int MAXST = 8>
+static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O) {
+    constexpr int ARR = 2 * NB + 2;
+    const int tile = c.n < TILE ? c.n : TILE;
+    size_t smem = (size_t)ts_stages<NB, TILE, MAXST>() * ARR * tile * sizeof(uint64_t);
+    smem = std::max<size_t>(smem, (size_t)NB * 3 * (TILE / 2) * 16);
+    auto kern = k_tensor_sum<NB, TILE, SPLIT, MAXST>;
+    VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c.n / tile, nl, SPLIT);
+    cfg.blockDim = dim3(TILE / 2 + 32, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = SPLIT;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VR_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, n, nl, c.n, c.primes, O));
+}
+
+template <int NB>
+static void ts_variant(Ctx &c, int v, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O) {
+    switch (v) {
+        case 1: launch_ts<NB, 256, 1, 8>(c, L, R, n, nl, O); break;
+        case 2: launch_ts<NB, 128, 2, 8>(c, L, R, n, nl, O); break;
+        default: launch_ts<NB, 256, 2, 4>(c, L, R, n, nl, O); break;  // best on B200 (tools/bw_probe.py)
+    }
+}
+
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O) {
-    dim3 grid(nblocks(c.n / 2, TS_THREADS), nl, TS_SPLIT);
+    static int variant = [] {
+        const char *e = getenv("VR_TS_VARIANT");
+        return e ? atoi(e) : 0;  // 0 = tuned default
+    }();
     switch (nb) {
-        case 1: k_tensor_sum<1><<<grid, TS_THREADS, 0, c.stream>>>(L, R, n, nl, c.n, c.primes, O); break;
-        case 2: k_tensor_sum<2><<<grid, TS_THREADS, 0, c.stream>>>(L, R, n, nl, c.n, c.primes, O); break;
-        case 4: k_tensor_sum<4><<<grid, TS_THREADS, 0, c.stream>>>(L, R, n, nl, c.n, c.primes, O); break;
+        case 1: ts_variant<1>(c, variant, L, R, n, nl, O); break;
+        case 2: ts_variant<2>(c, variant, L, R, n, nl, O); break;
+        case 4: ts_variant<4>(c, variant, L, R, n, nl, O); break;
         default: throw VrError(3, "tensor_sum: nblocks must be 1, 2 or 4");
     }
     check_launch("k_tensor_sum");
