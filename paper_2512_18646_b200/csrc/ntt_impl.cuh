@@ -85,8 +85,14 @@ struct LdGather {
 };
 
 // ---- store functors (last pass) ------------------------------------------------
+// Store functors expose prefetch(t, E) -> Pre (all global loads the store needs) and
+// finish(ptr, t, E, v, Pre): the kernel prefetches the 8 elements a thread owns before
+// any store, so the loads are not serialised behind possibly-aliasing stores.
 struct StPlain {
-    __device__ __forceinline__ void operator()(uint64_t *ptr, int, long long E, uint64_t v, const DevPrimes &, int) const {
+    struct Pre {};
+    __device__ __forceinline__ Pre prefetch(int, long long, const DevPrimes &, int) const { return Pre{}; }
+    __device__ __forceinline__ void finish(uint64_t *ptr, int, long long E, uint64_t v, const Pre &, const DevPrimes &,
+                                           int) const {
         ptr[E] = v;
     }
 };
@@ -100,13 +106,16 @@ struct StCombine {
     const uint64_t *inv;  // inv_tab row: (inv, shoup) pairs per target prime
     int nout, rdiv, a_limbs, add_polys, logN;
     uint32_t g;
-    __device__ __forceinline__ void operator()(uint64_t *, int t, long long E, uint64_t v, const DevPrimes &pr, int pidx) const {
+    struct Pre {
+        uint64_t a, b;
+    };
+    __device__ __forceinline__ Pre prefetch(int t, long long E, const DevPrimes &, int) const {
         const int N = 1 << logN;
         const int row = t / nout, i = t - row * nout;
         const int r0 = row / rdiv, r1 = row - r0 * rdiv;
-        const uint64_t q = pr.m[pidx].q;
-        const uint64_t a = A[r0][((long long)r1 * a_limbs + i) * N + E];
-        uint64_t r = mul_shoup(sub_mod(a, v, q), inv[2 * i], inv[2 * i + 1], q);
+        Pre p;
+        p.a = A[r0][((long long)r1 * a_limbs + i) * N + E];
+        p.b = 0;
         if (add && r1 < add_polys) {
             long long src = E;
             if (g != 1) {
@@ -114,8 +123,18 @@ struct StCombine {
                 const uint32_t e = ((2u * brk + 1u) * g) & ((2u << logN) - 1u);
                 src = (long long)(__brev((e - 1u) >> 1) >> (32 - logN));
             }
-            r = add_mod(r, add[r0][((long long)r1 * nout + i) * N + src], q);
+            p.b = add[r0][((long long)r1 * nout + i) * N + src];
         }
+        return p;
+    }
+    __device__ __forceinline__ void finish(uint64_t *, int t, long long E, uint64_t v, const Pre &p, const DevPrimes &pr,
+                                           int pidx) const {
+        const int N = 1 << logN;
+        const int row = t / nout, i = t - row * nout;
+        const int r0 = row / rdiv, r1 = row - r0 * rdiv;
+        const uint64_t q = pr.m[pidx].q;
+        uint64_t r = mul_shoup(sub_mod(p.a, v, q), inv[2 * i], inv[2 * i + 1], q);
+        if (add && r1 < add_polys) r = add_mod(r, p.b, q);
         O[r0][((long long)r1 * nout + i) * N + E] = r;
     }
 };
@@ -222,10 +241,16 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
         }
         if (last_group && COLS) {
             // consecutive threads own consecutive columns -> coalesced direct stores
+            typename ST::Pre pre[8];
 #pragma unroll
             for (int e = 0; e < 8; e++) {
                 const int L = base[e >> R] + (e & (E2 - 1)) * d;
-                st(ptr, t, ebase | ((long long)L << lo_bits), x[e], pr, pidx);
+                pre[e] = st.prefetch(t, ebase | ((long long)L << lo_bits), pr, pidx);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int L = base[e >> R] + (e & (E2 - 1)) * d;
+                st.finish(ptr, t, ebase | ((long long)L << lo_bits), x[e], pre[e], pr, pidx);
             }
             return;
         }
@@ -233,14 +258,22 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
         for (int e = 0; e < 8; e++) sm[sidx<COLS>(j, base[e >> R] + (e & (E2 - 1)) * d, T, TPC)] = x[e];
         __syncthreads();  // one owner per element within a group: a single barrier per group boundary
     }
-    // rows: coalesced cooperative store out of shared memory
+    // rows: coalesced cooperative store out of shared memory (prefetch the epilogue's loads first)
+    long long Es[8];
+    typename ST::Pre pre[8];
 #pragma unroll
     for (int r = 0; r < 8; r++) {  // blockDim.x * 8 == TPC * T
         const int idx = threadIdx.x + r * blockDim.x;
         const int jj = idx >> LOGT, mid = idx & (T - 1);
         const int tl = tile0 + jj, h2 = tl >> lo_bits, lo2 = tl & lomask;
-        st(ptr, t, ((long long)h2 << (logN - s0)) | ((long long)mid << lo_bits) | lo2, sm[sidx<COLS>(jj, mid, T, TPC)], pr,
-           pidx);
+        Es[r] = ((long long)h2 << (logN - s0)) | ((long long)mid << lo_bits) | lo2;
+        pre[r] = st.prefetch(t, Es[r], pr, pidx);
+    }
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        const int idx = threadIdx.x + r * blockDim.x;
+        const int jj = idx >> LOGT, mid = idx & (T - 1);
+        st.finish(ptr, t, Es[r], sm[sidx<COLS>(jj, mid, T, TPC)], pre[r], pr, pidx);
     }
 }
 
@@ -284,7 +317,7 @@ __global__ void ntt_tiny(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *_
         const NttConst nc = ncs[pidx];
         for (int k = 0; k < N; k++) a[k] = mul_shoup(a[k], nc.ninv, nc.ninv_sh, q);
     }
-    for (int k = 0; k < N; k++) st(ptr, t, k, a[k], pr, pidx);
+    for (int k = 0; k < N; k++) st.finish(ptr, t, k, a[k], st.prefetch(t, k, pr, pidx), pr, pidx);
 }
 
 template <bool INV, bool COLS, int LOGT, class LD, class ST>
