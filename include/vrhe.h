@@ -85,6 +85,8 @@ int vr_add(vr_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint
 int vr_tensor(vr_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out, int count, int level);
 int vr_relin(vr_ctx *ctx, const uint64_t *const *d3, uint64_t *const *out, int count, int level);
 int vr_rescale(vr_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int count, int deg, int level);
+/* relinearise + rescale as one rounding step, (P d + KS) / (P q_l): degree 2 at level -> degree 1 at level-1 */
+int vr_relin_rescale(vr_ctx *ctx, const uint64_t *const *d3, uint64_t *const *out, int count, int level);
 /* SlotEngine.mul (engine.py:215-220): tensor -> relinearise -> rescale */
 int vr_mul(vr_ctx *ctx, const uint64_t *const *a, const uint64_t *const *b, uint64_t *const *out, int count, int level);
 /* SlotEngine.cmul (engine.py:222-230) building blocks: plaintext / integer-scalar products */

@@ -67,6 +67,7 @@ def lib():
         L.orc_rescale.argtypes = [vp, u64p, ctypes.c_int, ctypes.c_int, u64p]
         L.orc_keyswitch.argtypes = [vp, u64p, ctypes.c_int, u64p, u64p]
         L.orc_relin.argtypes = [vp, u64p, ctypes.c_int, u64p]
+        L.orc_relin_rescale.argtypes = [vp, u64p, ctypes.c_int, u64p]
         L.orc_galois_elt.restype = ctypes.c_uint32
         L.orc_galois_elt.argtypes = [vp, ctypes.c_int64]
         L.orc_rotate.argtypes = [vp, u64p, ctypes.c_int, ctypes.c_int64, u64p]
@@ -273,6 +274,12 @@ class OracleCkks:
         lvl = d3.shape[1] - 1
         out = self._ct(1, lvl)
         lib().orc_relin(self._c, _p(d3), lvl, _p(out))
+        return out
+
+    def relin_rescale(self, d3):
+        lvl = d3.shape[1] - 1
+        out = self._ct(1, lvl - 1)
+        lib().orc_relin_rescale(self._c, _p(np.ascontiguousarray(d3)), lvl, _p(out))
         return out
 
     def rotate(self, ct, steps: int):

@@ -646,10 +646,11 @@ void orc_rescale(const orc_ctx *c, const uint64_t *ct, int deg, int level, uint6
 
 /* hybrid key switch, dnum = l+1 single-prime digits, one special prime P.
  * cpoly: [l+1][N] NTT; key: [L+1][2][np][N]; out: [2][l+1][N] */
-void orc_keyswitch(const orc_ctx *c, const uint64_t *cpoly, int level, const uint64_t *key, uint64_t *out) {
+/* inner product accumulators acc[2][l+2][N] (targets q0..ql, P) of the hybrid key switch */
+static void keyswitch_acc(orc_ctx *c, const uint64_t *cpoly, int level, const uint64_t *key, uint64_t *acc) {
     const int n = c->n, nl = level + 1, np = c->np, P = np - 1;
     const int nt = nl + 1; /* target primes q0..ql, P */
-    uint64_t *acc = calloc((size_t)2 * nt * n, 8);
+    memset(acc, 0, 16ull * nt * n);
     uint64_t *x = malloc(8ull * n), *d = malloc(8ull * n);
     for (int j = 0; j < nl; j++) {
         memcpy(x, cpoly + (size_t)j * n, 8ull * n);
@@ -669,6 +670,17 @@ void orc_keyswitch(const orc_ctx *c, const uint64_t *cpoly, int level, const uin
             }
         }
     }
+    free(x); free(d);
+}
+
+/* hybrid key switch, dnum = l+1 single-prime digits, one special prime P.
+ * cpoly: [l+1][N] NTT; key: [L+1][2][np][N]; out: [2][l+1][N] */
+void orc_keyswitch(const orc_ctx *c, const uint64_t *cpoly, int level, const uint64_t *key, uint64_t *out) {
+    const int n = c->n, nl = level + 1, np = c->np, P = np - 1;
+    const int nt = nl + 1;
+    uint64_t *acc = malloc(16ull * nt * n);
+    keyswitch_acc((orc_ctx *)c, cpoly, level, key, acc);
+    uint64_t *x = malloc(8ull * n), *d = malloc(8ull * n);
     const uint64_t Pq = c->q[P];
     for (int b = 0; b < 2; b++) {
         memcpy(x, acc + ((size_t)b * nt + nl) * n, 8ull * n);
@@ -697,6 +709,49 @@ void orc_relin(orc_ctx *c, const uint64_t *d3, int level, uint64_t *out) {
             for (int k = 0; k < n; k++) out[o + k] = addmod(d3[o + k], ks[o + k], q);
         }
     free(ks);
+}
+
+/* Fused relinearisation + rescale: with acc = ModUp/inner(d2)
+ * over {q_0..q_l, P}, X = P*d_{0,1} + acc_{0,1} is divided by P*q_l with rounding:
+ *   out_i = (X_i - lift([X]_{P q_l})) * (P q_l)^-1 mod q_i,   i < l
+ * where [X]_{P q_l} is the centred CRT combination of X mod P and X mod q_l.
+ * d3: [3][l+1][N] -> out [2][l][N] */
+static void keyswitch_acc(orc_ctx *c, const uint64_t *cpoly, int level, const uint64_t *key, uint64_t *acc);
+void orc_relin_rescale(orc_ctx *c, const uint64_t *d3, int level, uint64_t *out) {
+    const int n = c->n, nl = level + 1, nt = nl + 1, np = c->np, P = np - 1;
+    const uint64_t Pq = c->q[P], ql = c->q[level];
+    uint64_t *acc = malloc(16ull * nt * n);
+    keyswitch_acc(c, d3 + (size_t)2 * nl * n, level, get_rlk(c), acc);
+    uint64_t *yq = malloc(8ull * n), *yp = malloc(8ull * n), *z = malloc(8ull * n);
+    const uint64_t pinv_ql = invmod(Pq % ql, ql), p_ql = Pq % ql;
+    for (int b = 0; b < 2; b++) {
+        const uint64_t *ab = acc + (size_t)b * nt * n, *db = d3 + (size_t)b * nl * n;
+        for (int k = 0; k < n; k++) {
+            yq[k] = addmod(mulmod(p_ql, db[(size_t)level * n + k], ql), ab[(size_t)level * n + k], ql);
+            yp[k] = ab[(size_t)nl * n + k];
+        }
+        orc_intt(c, level, yq);
+        orc_intt(c, P, yp);
+        for (int i = 0; i < level; i++) {
+            const uint64_t q = c->q[i], pm = Pq % q, pqm = mulmod(pm, ql % q, q);
+            const uint64_t inv = invmod(pqm, q);
+            for (int k = 0; k < n; k++) {
+                /* x = yp + P * t, t = (yq - yp) * P^-1 mod ql, x in [0, P ql) */
+                const uint64_t t = mulmod(submod(yq[k], yp[k] % ql, ql), pinv_ql, ql);
+                uint64_t v = addmod(yp[k] % q, mulmod(pm, t % q, q), q);
+                const int neg = (t > (ql - 1) / 2) || (t == (ql - 1) / 2 && yp[k] > Pq / 2);
+                if (neg) v = submod(v, pqm, q);
+                z[k] = v;
+            }
+            orc_ntt(c, i, z);
+            uint64_t *o = out + ((size_t)b * level + i) * n;
+            for (int k = 0; k < n; k++) {
+                const uint64_t x = addmod(mulmod(pm, db[(size_t)i * n + k], q), ab[(size_t)i * n + k], q);
+                o[k] = mulmod(submod(x, z[k], q), inv, q);
+            }
+        }
+    }
+    free(acc); free(yq); free(yp); free(z);
 }
 
 uint32_t orc_galois_elt(const orc_ctx *c, int64_t steps) {
@@ -736,11 +791,10 @@ void orc_rotate(orc_ctx *c, const uint64_t *ct, int level, int64_t steps, uint64
 /* mul = tensor -> relin -> rescale (level l -> l-1) */
 void orc_mul(orc_ctx *c, const uint64_t *a, const uint64_t *b, int level, uint64_t *out) {
     const int n = c->n, nl = level + 1;
-    uint64_t *d = malloc(24ull * nl * n), *r = malloc(16ull * nl * n);
+    uint64_t *d = malloc(24ull * nl * n);
     orc_tensor(c, a, b, level, d);
-    orc_relin(c, d, level, r);
-    orc_rescale(c, r, 1, level, out);
-    free(d); free(r);
+    orc_relin_rescale(c, d, level, out);
+    free(d);
 }
 
 /* ------------------------------------------------------------------ */
@@ -767,10 +821,8 @@ void orc_matmul_outer(orc_ctx *c, const uint64_t *const *Ls, const uint64_t *con
             }
         }
     }
-    uint64_t *r = malloc(16ull * nl * n);
-    orc_relin(c, d, level, r);
-    orc_rescale(c, r, 1, level, out);
-    free(d); free(r);
+    orc_relin_rescale(c, d, level, out);
+    free(d);
 }
 
 /* Column-domain convolution (multicipher.py:123-162), generalised to C input
@@ -844,25 +896,28 @@ void orc_conv_columns(orc_ctx *c, const uint64_t *const *X, int C, int W, int k,
 void orc_poly_activation(orc_ctx *c, const uint64_t *x, int level, const int64_t *kc, int c3_zero, uint64_t *out) {
     const int n = c->n, nl = level + 1;
     const size_t w1 = (size_t)2 * level * n;
-    uint64_t *x2 = malloc(8 * w1), *pre = malloc(8 * w1), *xd = malloc(8 * w1), *tmp = malloc(8 * 2 * nl * n);
+    uint64_t *x2 = malloc(8 * w1), *xd = malloc(8 * w1), *tmp = malloc(8 * 2 * nl * n);
     orc_mul(c, x, x, level, x2);
+    orc_drop_level(c, x, 1, level, level - 1, xd);
+    orc_mul_scalar(c, xd, kc[2], 1, level - 1, xd);
     if (c3_zero) {
+        uint64_t *pre = malloc(8 * w1);
         orc_mul_scalar(c, x2, kc[1], 1, level - 1, pre);
+        orc_add(c, pre, xd, 1, level - 1, pre);
+        orc_rescale(c, pre, 1, level - 1, out);
+        free(pre);
     } else {
         uint64_t *inner = malloc(8 * w1), *d3 = malloc(8 * 3 * (size_t)level * n);
         orc_mul_scalar(c, x, kc[0], 1, level, tmp);
         orc_rescale(c, tmp, 1, level, inner);
         orc_add_const(c, inner, kc[1], level - 1);
         orc_tensor(c, x2, inner, level - 1, d3);
-        orc_relin(c, d3, level - 1, pre);
+        orc_add(c, d3, xd, 1, level - 1, d3); /* x' k1 joins (d0, d1) before the fused relin+rescale */
+        orc_relin_rescale(c, d3, level - 1, out);
         free(inner); free(d3);
     }
-    orc_drop_level(c, x, 1, level, level - 1, xd);
-    orc_mul_scalar(c, xd, kc[2], 1, level - 1, xd);
-    orc_add(c, pre, xd, 1, level - 1, pre);
-    orc_rescale(c, pre, 1, level - 1, out);
     orc_add_const(c, out, kc[3], level - 2);
-    free(x2); free(pre); free(xd); free(tmp);
+    free(x2); free(xd); free(tmp);
 }
 
 /* single-limb helpers for unit tests */

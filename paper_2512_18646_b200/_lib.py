@@ -45,6 +45,7 @@ _SIGS = {
     "vr_tensor": [c_vp, c_vpp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int],
     "vr_relin": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int],
     "vr_rescale": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int],
+    "vr_relin_rescale": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int],
     "vr_mul": [c_vp, c_vpp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int],
     "vr_mul_plain": [c_vp, c_vpp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int],
     "vr_mul_scalar": [c_vp, c_vpp, ctypes.c_int64, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int],

@@ -201,6 +201,28 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
                 c.h_inv_tab[((size_t)a * np + b) * 2] = v;
                 c.h_inv_tab[((size_t)a * np + b) * 2 + 1] = h_shoup(v, c.q[b]);
             }
+        std::vector<uint64_t> rr((size_t)(c.L + 1) * vr::RR_STRIDE, 0);
+        {
+            const uint64_t P = c.q[np - 1];
+            for (int l = 1; l <= c.L; l++) {
+                uint64_t *row = rr.data() + (size_t)l * vr::RR_STRIDE;
+                const uint64_t ql = c.q[l];
+                for (int i = 0; i < l; i++) {
+                    const uint64_t q = c.q[i], pm = P % q, pqm = h_mulmod(pm, ql % q, q), inv = h_inv(pqm, q);
+                    row[i * 8 + 0] = pm;
+                    row[i * 8 + 1] = h_shoup(pm, q);
+                    row[i * 8 + 2] = pqm;
+                    row[i * 8 + 3] = inv;
+                    row[i * 8 + 4] = h_shoup(inv, q);
+                }
+                const uint64_t pq = P % ql, pinv = h_inv(pq, ql);
+                row[vr::MAXP * 8 + 0] = pq;
+                row[vr::MAXP * 8 + 1] = h_shoup(pq, ql);
+                row[vr::MAXP * 8 + 2] = pinv;
+                row[vr::MAXP * 8 + 3] = h_shoup(pinv, ql);
+                row[vr::MAXP * 8 + 4] = P;
+            }
+        }
         std::vector<double> zr(n), zi(n);
         for (int k = 0; k < n; k++) {
             const double ang = M_PI * (double)k / (double)n;
@@ -217,6 +239,7 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         c.itw2 = upload(c, itw);
         c.ntt_const = upload(c, c.h_ntt_const);
         c.inv_tab = upload(c, c.h_inv_tab);
+        c.rr_tab = upload(c, rr);
         c.zr = upload(c, zr);
         c.zi = upload(c, zi);
         c.slot_pos = upload(c, sp);
@@ -245,7 +268,7 @@ int vr_ctx_destroy(vr_ctx *h) {
         vr::Ctx &c = h->c;
         cudaSetDevice(c.device);
         cudaDeviceSynchronize();
-        void *ptrs[] = {c.tw2, c.itw2, c.ntt_const, c.inv_tab, c.zr, c.zi, c.slot_pos, c.cdt, c.rlk};
+        void *ptrs[] = {c.tw2, c.itw2, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.slot_pos, c.cdt, c.rlk};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (c.s_ntt) cudaFree(c.s_ntt);
@@ -253,6 +276,7 @@ int vr_ctx_destroy(vr_ctx *h) {
         for (auto &kv : c.gkeys) cudaFree(kv.second);
         for (auto &e : c.tables)
             if (e.dev) cudaFree(e.dev);
+        if (c.arena) cudaFree(c.arena);
         for (int i = 0; i < vr::Ctx::kStageSlots; i++)
             if (c.stage_evt[i]) cudaEventDestroy(c.stage_evt[i]);
         if (c.stage) cudaFreeHost(c.stage);
@@ -388,6 +412,17 @@ int vr_rescale(vr_ctx *h, const uint64_t *const *in, uint64_t *const *out, int c
         vr::Ctx &c = h->c;
         vr::PtrTable ti(c, vec(in, count)), to(c, vecm(out, count));
         vr::rescale(c, ti.c_(), to.m_(), count, deg + 1, level);
+    });
+}
+
+int vr_relin_rescale(vr_ctx *h, const uint64_t *const *d3, uint64_t *const *out, int count, int level) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
+        if (count <= 0) return;
+        vr::Ctx &c = h->c;
+        vr::PtrTable ti(c, vec(d3, count)), to(c, vecm(out, count));
+        vr::relin_rescale_batch(c, ti.c_(), to.m_(), count, level);
     });
 }
 

@@ -197,22 +197,18 @@ __global__ void __launch_bounds__(128) k_pt_matvec(const uint64_t *const *X, int
 
 void mul_batch(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *Out, int count, int level) {
     const int N = c.n, nl = level + 1;
-    Scratch d3(c, sizeof(uint64_t) * count * 3 * nl * N), r(c, sizeof(uint64_t) * count * 2 * nl * N);
+    Scratch d3(c, sizeof(uint64_t) * count * 3 * nl * N);
     PtrTable td(c, strided(d3.as<uint64_t>(), count, (size_t)3 * nl * N));
-    PtrTable tr(c, strided(r.as<uint64_t>(), count, (size_t)2 * nl * N));
     tensor(c, A, B, td.m_(), count, nl);
-    relin_batch(c, td.c_(), tr.m_(), count, level);
-    rescale(c, tr.c_(), Out, count, 2, level);
+    relin_rescale_batch(c, td.c_(), Out, count, level);
 }
 
 void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out) {
     const int N = c.n, nl = level + 1;
-    Scratch d3(c, sizeof(uint64_t) * nb * 3 * nl * N), r(c, sizeof(uint64_t) * nb * 2 * nl * N);
+    Scratch d3(c, sizeof(uint64_t) * nb * 3 * nl * N);
     PtrTable td(c, strided(d3.as<uint64_t>(), nb, (size_t)3 * nl * N));
-    PtrTable tr(c, strided(r.as<uint64_t>(), nb, (size_t)2 * nl * N));
     tensor_sum(c, L, R, n, nb, nl, td.m_());
-    relin_batch(c, td.c_(), tr.m_(), nb, level);
-    rescale(c, tr.c_(), Out, nb, 2, level);
+    relin_rescale_batch(c, td.c_(), Out, nb, level);
 }
 
 void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, int k, const int64_t *w, const uint64_t *bias,
@@ -351,6 +347,8 @@ static void poly_activation_chunk(Ctx &c, const uint64_t *const *X, int count, i
     mul_batch(c, X, X, tx2.m_(), count, level);  // x^2 at level-1
     if (c3_zero) {
         mul_scalar(c, tx2.c_(), tpre.m_(), count, 2, level, limb_scalars(c, kc[1], level));
+        axpy(c, tpre.m_(), X, count, 2, level, level + 1, limb_scalars(c, kc[2], level));
+        rescale(c, tpre.c_(), Out, count, 2, level - 1);
     } else {
         Scratch inner(c, sizeof(uint64_t) * count * w1), xs(c, sizeof(uint64_t) * count * 2 * (level + 1) * N),
             d3(c, sizeof(uint64_t) * count * 3 * level * N);
@@ -361,10 +359,10 @@ static void poly_activation_chunk(Ctx &c, const uint64_t *const *X, int count, i
         rescale(c, txs.c_(), tin.m_(), count, 2, level);
         add_const(c, tin.m_(), count, level, limb_scalars(c, kc[1], level));
         tensor(c, tx2.c_(), tin.c_(), td3.m_(), count, level);
-        relin_batch(c, td3.c_(), tpre.m_(), count, level - 1);
+        // x' k1 joins (d0, d1) before the fused relinearise + rescale
+        axpy(c, td3.m_(), X, count, 2, level, level + 1, limb_scalars(c, kc[2], level));
+        relin_rescale_batch(c, td3.c_(), Out, count, level - 1);
     }
-    axpy(c, tpre.m_(), X, count, 2, level, level + 1, limb_scalars(c, kc[2], level));
-    rescale(c, tpre.c_(), Out, count, 2, level - 1);
     add_const(c, Out, count, level - 1, limb_scalars(c, kc[3], level - 1));
 }
 

@@ -92,6 +92,67 @@ __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint6
     }
 }
 
+// ---- fused relinearise + rescale (oracle/ckks_oracle.c:orc_relin_rescale) ----------
+// X_b = P * d_b + acc_b; rows of Y: 0 = X_b mod q_l, 1 = acc_b mod P (= X_b mod P)
+struct LdXrow {
+    const uint64_t *A;              // [count][2][nt][N] accumulators
+    const uint64_t *const *D3;      // relin inputs [3][l+1][N]
+    const uint64_t *rr;             // rr_tab row for this level
+    int level, nt, N;
+    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int) const {
+        const int cb = t >> 1, w = t & 1, c = cb >> 1, b = cb & 1;
+        const uint64_t *a = A + ((long long)cb * nt) * N;
+        if (w) return a[(long long)(nt - 1) * N + E];
+        const uint64_t q = pr.m[level].q;
+        const uint64_t d = D3[c][((long long)b * (level + 1) + level) * N + E];
+        return add_mod(mul_shoup(d, rr[MAXP * 8 + 0], rr[MAXP * 8 + 1], q), a[(long long)level * N + E], q);
+    }
+};
+// centred CRT lift of (Y[cb][0] mod q_l, Y[cb][1] mod P) into q_i; t = cb * level + i
+struct LdCrt {
+    const uint64_t *Y;
+    const uint64_t *rr;
+    int level, N;
+    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int pidx) const {
+        const int cb = t / level, i = t - cb * level;
+        const Modulus &mq = pr.m[level];
+        const uint64_t yq = Y[((long long)cb * 2) * N + E], yp = Y[((long long)cb * 2 + 1) * N + E];
+        const uint64_t ql = mq.q;
+        const uint64_t tq = mul_shoup(sub_mod(yq, reduce64(yp, mq), ql), rr[MAXP * 8 + 2], rr[MAXP * 8 + 3], ql);
+        const Modulus &m = pr.m[pidx];
+        uint64_t v = add_mod(reduce64(yp, m), mul_shoup(reduce64(tq, m), rr[i * 8 + 0], rr[i * 8 + 1], m.q), m.q);
+        const uint64_t half_q = (ql - 1) >> 1;
+        const bool neg = tq > half_q || (tq == half_q && yp > (rr[MAXP * 8 + 4] >> 1));
+        if (neg) v = sub_mod(v, rr[i * 8 + 2], m.q);
+        return v;
+    }
+};
+// out[c][b][i] = (P d_b[i] + acc_b[i] - z) * (P q_l)^-1 mod q_i   (t = (c*2+b) * level + i)
+struct StRelinRescale {
+    const uint64_t *A;
+    const uint64_t *const *D3;
+    uint64_t *const *O;
+    const uint64_t *rr;
+    int level, nt, N;
+    struct Pre {
+        uint64_t a, d;
+    };
+    __device__ __forceinline__ Pre prefetch(int t, long long E, const DevPrimes &, int) const {
+        const int cb = t / level, i = t - cb * level, c = cb >> 1, b = cb & 1;
+        Pre p;
+        p.a = A[((long long)cb * nt + i) * N + E];
+        p.d = D3[c][((long long)b * (level + 1) + i) * N + E];
+        return p;
+    }
+    __device__ __forceinline__ void finish(uint64_t *, int t, long long E, uint64_t z, const Pre &p, const DevPrimes &pr,
+                                           int pidx) const {
+        const int cb = t / level, i = t - cb * level, c = cb >> 1, b = cb & 1;
+        const uint64_t q = pr.m[pidx].q;
+        const uint64_t x = add_mod(mul_shoup(p.d, rr[i * 8 + 0], rr[i * 8 + 1], q), p.a, q);
+        O[c][((long long)b * level + i) * N + E] = mul_shoup(sub_mod(x, z, q), rr[i * 8 + 3], rr[i * 8 + 4], q);
+    }
+};
+
 std::vector<const uint64_t *> strided_ptrs(const uint64_t *base, int count, size_t stride) {
     std::vector<const uint64_t *> v(count);
     for (int i = 0; i < count; i++) v[i] = base + (size_t)i * stride;
@@ -124,6 +185,19 @@ static void modup_impl(Ctx &c, const uint64_t *const *Polys, long long poly_off,
 
 void modup(Ctx &c, const uint64_t *const *Polys, int count, int level, uint64_t *D) { modup_impl(c, Polys, 0, count, level, D); }
 
+static void launch_ks_inner(Ctx &c, const uint64_t *D, const uint64_t *const *Polys, long long poly_off, int count, int level,
+                            const uint64_t *key, uint32_t g, uint64_t *A) {
+    const int N = c.n, nl = level + 1, nt = level + 2;
+    const dim3 blocks(nblocks((long long)nt * N, 128), (count + KS_CG - 1) / KS_CG);
+    if (nl <= 8)
+        k_ks_inner<8><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
+    else if (nl <= 16)
+        k_ks_inner<16><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
+    else
+        k_ks_inner<40><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
+    check_launch("k_ks_inner");
+}
+
 // Out (pointer table, count entries of [2][l+1][N]) = ModDown(inner(D, key)) (+ add)
 static void inner_moddown(Ctx &c, const uint64_t *D, const uint64_t *const *Polys, long long poly_off, int count, int level,
                           const uint64_t *key, uint32_t g, uint64_t *const *Out, const uint64_t *const *Add, int add_polys) {
@@ -151,6 +225,23 @@ void keyswitch_poly(Ctx &c, const uint64_t *const *Polys, int count, int level, 
     Scratch d(c, sizeof(uint64_t) * count * nl * nt * N);
     modup_impl(c, Polys, 0, count, level, d.as<uint64_t>());
     inner_moddown(c, d.as<uint64_t>(), Polys, 0, count, level, key, 1, Out, nullptr, 0);
+}
+
+// relinearise and rescale in one rounding step: (P d + acc) / (P q_l)
+void relin_rescale_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level) {
+    if (level < 1) throw VrError(3, "relin_rescale: no level left to drop");
+    const int N = c.n, nl = level + 1, nt = level + 2, P = c.np - 1;
+    const uint64_t *key = relin_key(c);
+    const long long off = (long long)2 * nl * N;
+    Scratch d(c, sizeof(uint64_t) * count * nl * nt * N), a(c, sizeof(uint64_t) * count * 2 * nt * N);
+    modup_impl(c, D3, off, count, level, d.as<uint64_t>());
+    launch_ks_inner(c, d.as<uint64_t>(), D3, off, count, level, key, 1, a.as<uint64_t>());
+    const uint64_t *rr = c.rr_tab + (size_t)level * RR_STRIDE;
+    Scratch y(c, sizeof(uint64_t) * count * 4 * N), z(c, sizeof(uint64_t) * count * 2 * level * N);
+    ntt_inverse_fused(c, NttBatch{y.as<uint64_t>(), count * 4, 2, (long long)2 * N, 1, level, P, 0},
+                      LdXrow{a.as<uint64_t>(), D3, rr, level, nt, N}, nttk::StPlain{});
+    ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), count * 2, level, N), LdCrt{y.as<uint64_t>(), rr, level, N},
+                      StRelinRescale{a.as<uint64_t>(), D3, Out, rr, level, nt, N});
 }
 
 void relin_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level) {

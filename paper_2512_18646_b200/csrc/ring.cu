@@ -406,7 +406,11 @@ static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
     size_t smem = (size_t)ts_stages<NB, TILE, MAXST>() * ARR * tile * sizeof(uint64_t);
     smem = std::max<size_t>(smem, (size_t)NB * 3 * (TILE / 2) * 16);
     auto kern = k_tensor_sum<NB, TILE, SPLIT, MAXST>;
-    VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static size_t configured = 0;  // per instantiation: raise the dynamic smem limit once
+    if (smem > configured) {
+        VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c.n / tile, nl, SPLIT);
     cfg.blockDim = dim3(TILE / 2 + 32, 1, 1);

@@ -38,6 +38,8 @@ void keyswitch_poly(Ctx &c, const uint64_t *const *Polys, int count, int level, 
 
 // Convenience wrappers operating on pointer tables (device) of ciphertexts.
 void relin_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level);  // deg2 -> deg1, same level
+// deg2 at level l -> deg1 at level l-1: (P d + KS-acc) / (P q_l) in one rounding step
+void relin_rescale_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level);
 void rotate_batch(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int count, int level, int nrot, const uint32_t *gs);
 
 uint64_t *galois_key(Ctx &c, uint32_t g);

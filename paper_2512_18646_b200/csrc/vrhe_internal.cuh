@@ -15,6 +15,7 @@
 namespace vr {
 
 constexpr int MAXP = 40;
+constexpr int RR_STRIDE = MAXP * 8 + 8;
 
 struct DevPrimes {
     Modulus m[MAXP];
@@ -38,6 +39,10 @@ struct Ctx {
     ulonglong2 *tw2 = nullptr, *itw2 = nullptr;  // [np][N] (twiddle, Shoup companion) psi^(br i), psi^-(br i)
     NttConst *ntt_const = nullptr;                                                 // [np]
     uint64_t *inv_tab = nullptr;  // [np][np][2]: (q_a^-1 mod q_b, shoup)
+    // fused relinearise+rescale constants per level l >= 1: rr_tab + l * RR_STRIDE
+    //   [i*8 + 0..5] = P mod q_i (+shoup), (P q_l) mod q_i, (P q_l)^-1 mod q_i (+shoup), 0
+    //   [MAXP*8 + 0..3] = P mod q_l (+shoup), P^-1 mod q_l (+shoup)
+    uint64_t *rr_tab = nullptr;
     double *zr = nullptr, *zi = nullptr;  // zeta^k, k < N
     int *slot_pos = nullptr;              // [S]
     uint64_t *cdt = nullptr;              // [CDT_LEN]
@@ -70,6 +75,10 @@ struct Ctx {
     std::vector<TableEntry> tables;
     unsigned long long table_clock = 0;
 
+    // stack arena for per-call scratch (LIFO, stream-ordered reuse is safe on one stream)
+    char *arena = nullptr;
+    size_t arena_cap = 0, arena_top = 0, arena_peak = 0;
+
     size_t key_words() const { return (size_t)(L + 1) * 2 * np * n; }
 };
 
@@ -94,15 +103,44 @@ inline void check_launch(const char *what) {
     if (e != cudaSuccess) throw VrError(4, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// stream-ordered scratch buffer
+// Per-call scratch.  Carved LIFO out of the context's arena (kernels on the one stream
+// run in order, so the next call may reuse the bytes immediately); when the arena is
+// too small the request falls back to cudaMallocAsync and the arena is regrown, to the
+// high-water mark, the next time it is empty.
 struct Scratch {
     Ctx &c;
     void *p = nullptr;
-    Scratch(Ctx &cx, size_t bytes) : c(cx) {
-        if (bytes) VR_CUDA(cudaMallocAsync(&p, bytes, c.stream));
+    size_t bytes = 0;
+    bool pooled = false;
+    static constexpr size_t kArenaMaxBuffer = size_t(64) << 20, kArenaMaxCap = size_t(512) << 20;
+    Scratch(Ctx &cx, size_t b) : c(cx) {
+        bytes = (b + 255) & ~size_t(255);
+        if (!bytes) return;
+        if (bytes > kArenaMaxBuffer) {  // big buffers: the pool's own reuse is cheap relative to their work
+            VR_CUDA(cudaMallocAsync(&p, bytes, c.stream));
+            return;
+        }
+        if (c.arena_top == 0 && c.arena_cap < c.arena_peak) {
+            if (c.arena) cudaFreeAsync(c.arena, c.stream);
+            c.arena = nullptr;
+            c.arena_cap = 0;
+            if (cudaMallocAsync((void **)&c.arena, c.arena_peak, c.stream) == cudaSuccess) c.arena_cap = c.arena_peak;
+            else cudaGetLastError();
+        }
+        if (c.arena && c.arena_top + bytes <= c.arena_cap) {
+            p = c.arena + c.arena_top;
+            c.arena_top += bytes;
+            pooled = true;
+        } else {
+            VR_CUDA(cudaMallocAsync(&p, bytes, c.stream));
+        }
+        const size_t want = c.arena_top + (pooled ? 0 : bytes);
+        if (want > c.arena_peak && want <= kArenaMaxCap) c.arena_peak = want;
     }
     ~Scratch() {
-        if (p) cudaFreeAsync(p, c.stream);
+        if (!p) return;
+        if (pooled) c.arena_top -= bytes;
+        else cudaFreeAsync(p, c.stream);
     }
     template <class T>
     T *as() const { return (T *)p; }

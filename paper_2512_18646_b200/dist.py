@@ -104,16 +104,13 @@ def matmul_partials(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -> tu
 
 
 def matmul_finish(engine: CkksEngine, part: torch.Tensor, level: int, m: int, p: int) -> list[Ciphertext]:
-    """Summed partials -> mod q -> one relinearisation + one rescale per row block."""
+    """Summed partials -> mod q -> one fused relinearisation + rescale per row block."""
     nb = part.shape[0]
     lib = engine._lib
     _lib.check(lib.vr_mod_reduce(engine.handle, part.data_ptr(), nb * 3, level))
-    relin = torch.empty((nb, 2, level + 1, engine.N), dtype=torch.int64, device=engine.device)
     out = torch.empty((nb, 2, level, engine.N), dtype=torch.int64, device=engine.device)
-    _lib.check(lib.vr_relin(engine.handle, _lib.ptr_array([part[b].data_ptr() for b in range(nb)]),
-                            _lib.ptr_array([relin[b].data_ptr() for b in range(nb)]), nb, level))
-    _lib.check(lib.vr_rescale(engine.handle, _lib.ptr_array([relin[b].data_ptr() for b in range(nb)]),
-                              _lib.ptr_array([out[b].data_ptr() for b in range(nb)]), nb, 1, level))
+    _lib.check(lib.vr_relin_rescale(engine.handle, _lib.ptr_array([part[b].data_ptr() for b in range(nb)]),
+                                    _lib.ptr_array([out[b].data_ptr() for b in range(nb)]), nb, level))
     engine._observe(engine.L - level + 1)
     return [Ciphertext(out[b], level - 1, engine.scales[level - 1], engine.L - level + 1, ("grid", m, p), engine._id)
             for b in range(nb)]

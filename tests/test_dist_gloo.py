@@ -68,7 +68,7 @@ def _finish(o, summed):
     res = []
     for bi in range(NB):
         d3 = (summed[bi].astype(np.uint64) % q[None, :, None]).astype(np.uint64)
-        res.append(o.c.rescale(o.c.relin(np.ascontiguousarray(d3))))
+        res.append(o.c.relin_rescale(np.ascontiguousarray(d3)))
     return res
 
 
