@@ -520,9 +520,23 @@ def bench_ntt(eng, peak):
     nbytes = polys * nl * eng.N * 8
     gbs = 2 * nbytes / t / 1e9  # read + write of every limb
     butterflies = polys * nl * (eng.N // 2) * eng.params.log_n
+    # integer-pipe peak: the same butterfly on registers only (k_bfly_peak)
+    sink = torch.zeros(1, dtype=torch.int64, device="cuda")
+    blocks, iters = 148 * 16, 256
+    _lib.check(lib.vr_bench_butterflies(eng.handle, blocks, 16, sink.data_ptr()))
+    torch.cuda.synchronize()
+    st.record(eng._stream)
+    _lib.check(lib.vr_bench_butterflies(eng.handle, blocks, iters, sink.data_ptr()))
+    en.record(eng._stream)
+    torch.cuda.synchronize()
+    tp = st.elapsed_time(en) / 1e3
+    peak_bf = blocks * 256 * iters * 8 / tp / 1e9
     return {"metric": "NTT HBM GB/s (forward, 2 passes, in place)", "N": eng.N, "limbs": polys * nl,
             "gbs": gbs, "peak": peak, "frac": gbs / peak, "us_per_limb": t / (polys * nl) * 1e6,
-            "gbutterfly_s": butterflies / t / 1e9}
+            "gbutterfly_s": butterflies / t / 1e9,
+            "int_roofline": {"bound": "int (IMAD pipe)", "achieved_gbutterfly_s": butterflies / t / 1e9,
+                             "peak_gbutterfly_s": peak_bf, "frac": (butterflies / t / 1e9) / peak_bf,
+                             "peak_source": "measured live: k_bfly_peak, register-only Harvey/Shoup butterflies"}}
 
 
 def main():

@@ -328,7 +328,40 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
 
 constexpr int TB = 256;
 
+// Integer-pipe roofline probe: the NTT's Harvey/Shoup forward butterfly on registers only,
+// 8 independent chains per thread (no memory traffic).  bench.py divides the NTT's achieved
+// butterflies/s by this peak.
+__global__ void __launch_bounds__(256) k_bfly_peak(uint64_t q, uint64_t w, uint64_t wsh, int iters, uint64_t *sink) {
+    uint64_t x[8], y[8];
+    const uint64_t q2 = 2 * q;
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+        x[e] = (threadIdx.x * 977u + e * 131u) % q;
+        y[e] = (blockIdx.x * 613u + e * 71u) % q;
+    }
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            const uint64_t xx = x[e] >= q2 ? x[e] - q2 : x[e];
+            const uint64_t t = mul_shoup_lazy(y[e], w, wsh, q);
+            x[e] = xx + t;
+            y[e] = xx - t + q2;
+        }
+    }
+    uint64_t acc = 0;
+#pragma unroll
+    for (int e = 0; e < 8; e++) acc ^= x[e] ^ y[e];
+    if (acc == 0x12345) sink[0] = acc;  // keep the chains alive
+}
+
 }  // namespace
+
+void bfly_peak(Ctx &c, int blocks, int iters, uint64_t *sink) {
+    const uint64_t q = c.q[1 < c.np ? 1 : 0];
+    const uint64_t w = 1234567 % q, wsh = (uint64_t)(((unsigned __int128)w << 64) / q);
+    k_bfly_peak<<<blocks, 256, 0, c.stream>>>(q, w, wsh, iters, sink);
+    check_launch("k_bfly_peak");
+}
 
 LimbScalars limb_scalars(const Ctx &c, int64_t s, int nl) {
     LimbScalars r;

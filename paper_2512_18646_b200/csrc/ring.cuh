@@ -23,6 +23,7 @@ void axpy(Ctx &c, uint64_t *const *O, const uint64_t *const *B, int count, int p
 void permute(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, uint32_t g);
 void copy_limbs(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl_in, int nl_out, int limb0);
 void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl);
+void bfly_peak(Ctx &c, int blocks, int iters, uint64_t *sink);
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O);
 
 // rescale: in [polys][l+1][N] -> out [polys][l][N] for each ciphertext
