@@ -295,7 +295,7 @@ def run_ours(args, ws, rank, local):
     en.record(stream)
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(max(st.elapsed_time(en) / 1e3, time.perf_counter() - t0) / e2e_steps)
-    h2d = 2 * DIM * (DIM * DIM) * 8  # two operands, n padded slot vectors of m*p doubles
+    h2d = 2 * DIM * DIM * 8  # the raw A and B (broadcast/tiling happens in the encode kernel)
     d2h = eng.slots * 8
 
     extra = {}

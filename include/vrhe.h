@@ -73,6 +73,11 @@ int vr_encode_coeffs(vr_ctx *ctx, const double *vals, int count, int nvals, doub
 /* SlotEngine.enc (engine.py:193-202): fresh encryption, ciphertext c uses nonce0+c */
 int vr_encrypt(vr_ctx *ctx, const double *vals, int count, int nvals, int level, double scale, uint64_t nonce0,
                uint64_t *ct_out);
+/* encode_left / encode_right / encode_image_columns (multicipher.py:62-120) without host-side
+ * broadcasting: ciphertext c encrypts slot values src[c*sc + (j/p)*s1 + (j%p)*s2] for j < nvals
+ * (zeros beyond), src = the raw device matrix/images */
+int vr_encrypt_strided(vr_ctx *ctx, const double *src, long long sc, long long s1, long long s2, int p, int nvals, int count,
+                       int level, double scale, uint64_t nonce0, uint64_t *ct_out);
 /* SlotEngine.dec (engine.py:204-206): decrypt on q0 and decode to real slots.
  * out: device [count][S] doubles (may be NULL); coeffs_out: device [count][N] int64 (may be NULL). */
 int vr_decrypt_decode(vr_ctx *ctx, const uint64_t *const *cts, const int *degs, const int *levels, const double *scales,

@@ -361,6 +361,15 @@ int vr_encrypt(vr_ctx *h, const double *vals, int count, int nvals, int level, d
     });
 }
 
+int vr_encrypt_strided(vr_ctx *h, const double *src, long long sc, long long s1, long long s2, int p, int nvals, int count,
+                       int level, double scale, uint64_t nonce0, uint64_t *ct_out) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (nvals > h->c.slots) throw vr::VrError(VR_ERR_CAPACITY, "payload exceeds slot count");
+        if (count > 0) vr::encrypt_src(h->c, src, sc, s1, s2, p, nvals, count, level, scale, nonce0, ct_out);
+    });
+}
+
 int vr_decrypt_decode(vr_ctx *h, const uint64_t *const *cts, const int *degs, const int *levels, const double *scales,
                       int count, double *out, int64_t *coeffs_out) {
     return guard([&] {

@@ -49,15 +49,31 @@ __device__ void fft_stages(double *re, double *im, int S, const double *zr, cons
     }
 }
 
-// one CTA per ciphertext: values [count][nvals] -> m [count][N] (int64)
-__global__ void k_encode(const double *vals, int nvals, int S, int logS, double f, const double *zr, const double *zi,
-                         const int *slot_pos, double *wre, double *wim, int64_t *m) {
+// Slot-value source of ciphertext c: value(c, j) = src[c*sc + (j / p)*s1 + (j % p)*s2] for j < nvals.
+// Dense rows: p = nvals, s1 = 0, s2 = 1, sc = nvals.  encode_left (slot i*p+j = A[i][c]): sc = 1,
+// s1 = n, s2 = 0.  encode_right (slot i*p+j = B[c][j]): sc = p, s1 = 0, s2 = 1.  Image columns
+// (slot b*h+i = img[b][i][c]): p = h, sc = 1, s1 = h*w, s2 = w.  Only the raw source crosses PCIe.
+struct SlotSrc {
+    const double *src;
+    long long sc, s1, s2;
+    int p, nvals;
+    __device__ __forceinline__ double at(int c, int j) const {
+        if (j >= nvals) return 0.0;
+        const int a = j / p, b = j - a * p;
+        return src[(long long)c * sc + (long long)a * s1 + (long long)b * s2];
+    }
+};
+
+// one CTA per ciphertext: slot values -> m [count][N] (int64); FFT in shared memory when it fits
+__global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr, const double *zi, const int *slot_pos,
+                         double *wre, double *wim, int64_t *m) {
+    extern __shared__ double fft_sm[];
     const int c = blockIdx.x;
-    double *re = wre + (size_t)c * S, *im = wim + (size_t)c * S;
-    const double *v = vals + (size_t)c * nvals;
+    const bool in_smem = wre == nullptr;
+    double *re = in_smem ? fft_sm : wre + (size_t)c * S, *im = in_smem ? fft_sm + S : wim + (size_t)c * S;
     for (int j = threadIdx.x; j < S; j += blockDim.x) {
         const int pos = brev_bits((unsigned)slot_pos[j], logS);
-        re[pos] = j < nvals ? v[j] : 0.0;
+        re[pos] = vs.at(c, j);
         im[pos] = 0.0;
     }
     __syncthreads();
@@ -75,8 +91,10 @@ __global__ void k_encode(const double *vals, int nvals, int S, int logS, double 
 // one CTA per ciphertext: centred m [count][N], scales[count] -> real slots [count][S]
 __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS, const double *zr, const double *zi,
                          const int *slot_pos, double *wre, double *wim, double *out) {
+    extern __shared__ double fft_sm[];
     const int c = blockIdx.x;
-    double *re = wre + (size_t)c * S, *im = wim + (size_t)c * S;
+    const bool in_smem = wre == nullptr;
+    double *re = in_smem ? fft_sm : wre + (size_t)c * S, *im = in_smem ? fft_sm + S : wim + (size_t)c * S;
     const int64_t *mc = m + (size_t)c * 2 * S;
     const double scale = scales[c];
     for (int k = threadIdx.x; k < S; k += blockDim.x) {
@@ -260,17 +278,36 @@ int log2i(int x) {
     return l;
 }
 
-int fft_threads(int S) { return S >= 1024 ? 512 : (S >= 64 ? S / 2 : 32); }
+int fft_threads(int S) { return S >= 2048 ? 1024 : (S >= 64 ? S / 2 : 32); }
+
+// shared-memory FFT when re+im fit (S <= 8192 at 227 KB per CTA)
+bool fft_in_smem(int S) { return (size_t)S * 16 <= (size_t)200 * 1024; }
+void fft_smem_attr(const void *kern, int S) {
+    static int done_enc = 0;
+    (void)done_enc;
+    VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((size_t)S * 16)));
+}
 
 }  // namespace
 
-void encode_coeffs(Ctx &c, const double *d_vals, int count, int nvals, double scale, int64_t *d_m) {
+static void encode_src(Ctx &c, const SlotSrc &vs, int count, double scale, int64_t *d_m) {
     const int S = c.slots;
-    Scratch wr(c, sizeof(double) * count * S), wi(c, sizeof(double) * count * S);
     const double f = scale / (double)S;
-    k_encode<<<count, fft_threads(S), 0, c.stream>>>(d_vals, nvals, S, log2i(S), f, c.zr, c.zi, c.slot_pos, wr.as<double>(),
-                                                      wi.as<double>(), d_m);
+    if (fft_in_smem(S)) {
+        static int attr_S = 0;
+        if (attr_S < S) { fft_smem_attr((const void *)k_encode, S); attr_S = S; }
+        k_encode<<<count, fft_threads(S), (size_t)S * 16, c.stream>>>(vs, S, log2i(S), f, c.zr, c.zi, c.slot_pos, nullptr,
+                                                                      nullptr, d_m);
+    } else {
+        Scratch wr(c, sizeof(double) * count * S), wi(c, sizeof(double) * count * S);
+        k_encode<<<count, fft_threads(S), 0, c.stream>>>(vs, S, log2i(S), f, c.zr, c.zi, c.slot_pos, wr.as<double>(),
+                                                          wi.as<double>(), d_m);
+    }
     check_launch("k_encode");
+}
+
+void encode_coeffs(Ctx &c, const double *d_vals, int count, int nvals, double scale, int64_t *d_m) {
+    encode_src(c, SlotSrc{d_vals, nvals, 0, 1, nvals > 0 ? nvals : 1, nvals}, count, scale, d_m);
 }
 
 void encode_plain(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t *d_pt) {
@@ -282,10 +319,18 @@ void encode_plain(Ctx &c, const double *d_vals, int count, int nvals, int level,
     ntt_forward(c, batch_limbs(d_pt, count, nl, N));
 }
 
+void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long long s2, int p, int nvals, int count, int level,
+                 double scale, uint64_t nonce0, uint64_t *d_ct);
+
 void encrypt(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t nonce0, uint64_t *d_ct) {
+    encrypt_src(c, d_vals, nvals, 0, 1, nvals > 0 ? nvals : 1, nvals, count, level, scale, nonce0, d_ct);
+}
+
+void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long long s2, int p, int nvals, int count, int level,
+                 double scale, uint64_t nonce0, uint64_t *d_ct) {
     const int N = c.n, nl = level + 1;
     Scratch m(c, sizeof(int64_t) * count * N);
-    encode_coeffs(c, d_vals, count, nvals, scale, m.as<int64_t>());
+    encode_src(c, SlotSrc{src, sc, s1, s2, p > 0 ? p : 1, nvals}, count, scale, m.as<int64_t>());
     const int rows = c.sym_enc ? 2 : 3;
     Scratch buf(c, sizeof(uint64_t) * count * rows * nl * N);
     k_enc_sample<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(m.as<int64_t>(), count, nl, N, c.seed, nonce0,
@@ -314,9 +359,16 @@ void decrypt_decode(Ctx &c, const uint64_t *const *d_cts, const int *d_degs, con
     k_center<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(x.as<uint64_t>(), (long long)count * N, c.q[0], mp);
     check_launch("k_center");
     if (!d_out) return;
-    Scratch wr(c, sizeof(double) * count * S), wi(c, sizeof(double) * count * S);
-    k_decode<<<count, fft_threads(S), 0, c.stream>>>(mp, d_scales, S, log2i(S), c.zr, c.zi, c.slot_pos, wr.as<double>(),
-                                                      wi.as<double>(), d_out);
+    if (fft_in_smem(S)) {
+        static int attr_S = 0;
+        if (attr_S < S) { fft_smem_attr((const void *)k_decode, S); attr_S = S; }
+        k_decode<<<count, fft_threads(S), (size_t)S * 16, c.stream>>>(mp, d_scales, S, log2i(S), c.zr, c.zi, c.slot_pos,
+                                                                      nullptr, nullptr, d_out);
+    } else {
+        Scratch wr(c, sizeof(double) * count * S), wi(c, sizeof(double) * count * S);
+        k_decode<<<count, fft_threads(S), 0, c.stream>>>(mp, d_scales, S, log2i(S), c.zr, c.zi, c.slot_pos, wr.as<double>(),
+                                                          wi.as<double>(), d_out);
+    }
     check_launch("k_decode");
 }
 

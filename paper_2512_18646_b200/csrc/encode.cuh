@@ -7,6 +7,9 @@ namespace vr {
 void encode_coeffs(Ctx &c, const double *d_vals, int count, int nvals, double scale, int64_t *d_m);
 void encode_plain(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t *d_pt);
 void encrypt(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t nonce0, uint64_t *d_ct);
+// ciphertext c encrypts slot values src[c*sc + (j/p)*s1 + (j%p)*s2], j < nvals (zeros beyond)
+void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long long s2, int p, int nvals, int count, int level,
+                 double scale, uint64_t nonce0, uint64_t *d_ct);
 void decrypt_decode(Ctx &c, const uint64_t *const *d_cts, const int *d_degs, const int *d_levels, const double *d_scales,
                     int count, double *d_out, int64_t *d_coeffs_out);
 void keygen(Ctx &c);

@@ -55,11 +55,11 @@ def encode_operands_sharded(engine: CkksEngine, a_blocks, b, lo: int, hi: int, n
     p = b.shape[1]
     lefts = []
     for bi, a in enumerate(a_blocks):
-        grids = np.repeat(a[:, lo:hi].T, p, axis=1)
-        cts = engine.enc_batch(list(grids), layout=("grid", m, p), nonce0=nonce_base + bi * n + lo)
+        cts = engine.enc_strided(a, count=hi - lo, nvals=m * p, p=p, sc=1, s1=n, s2=0, offset=lo,
+                                 layout=("grid", m, p), nonce0=nonce_base + bi * n + lo)
         lefts.append(ColumnEncodedMatrix(cts, "left", m, hi - lo, p))
-    grids = np.tile(b[lo:hi], (1, m))
-    rcts = engine.enc_batch(list(grids), layout=("grid", m, p), nonce0=nonce_base + nb * n + lo)
+    rcts = engine.enc_strided(b, count=hi - lo, nvals=m * p, p=p, sc=p, s1=0, s2=1, offset=lo * p,
+                              layout=("grid", m, p), nonce0=nonce_base + nb * n + lo)
     return lefts, ColumnEncodedMatrix(rcts, "right", m, hi - lo, p)
 
 

@@ -243,6 +243,28 @@ class CkksEngine:
         self._observe(0)
         return [self._wrap(out[i], self.L, 0, layout) for i in range(count)]
 
+    def enc_strided(self, src, count: int, nvals: int, p: int, sc: int, s1: int, s2: int, offset: int = 0,
+                    layout: tuple | None = None, nonce0: int | None = None) -> list[Ciphertext]:
+        """Encrypt ``count`` slot vectors gathered on the device from one raw host array.
+
+        Ciphertext c holds slot j = src.flat[offset + c*sc + (j // p)*s1 + (j % p)*s2] for j < nvals
+        (zeros beyond): the broadcast/tiling of encode_left/encode_right/encode_image_columns is done by
+        the encode kernel, so only the raw matrix or images cross PCIe.
+        """
+        if nvals > self.slots:
+            raise CapacityError(f"{nvals} values exceed {self.slots} slots")
+        arr = np.ascontiguousarray(np.asarray(src, dtype=np.float64)).reshape(-1)
+        d_src = self._h2d(arr) if arr.size else torch.zeros(1, dtype=torch.float64, device=self.device)
+        out = self._empty(1, self.L, count)
+        n0 = self._nonce if nonce0 is None else int(nonce0)
+        _lib.check(self._lib.vr_encrypt_strided(self._h, d_src.data_ptr() + 8 * int(offset), sc, s1, s2, max(1, p), nvals,
+                                                count, self.L, self.scales[self.L], n0, out.data_ptr()))
+        if nonce0 is None:
+            self._nonce += count
+        self._meter.enc_count += count
+        self._observe(0)
+        return [self._wrap(out[i], self.L, 0, layout) for i in range(count)]
+
     def dec(self, ct: Ciphertext) -> np.ndarray:
         """Full slot vector (real parts), like engine.py:204-206."""
         return self.dec_batch([ct])[0]

@@ -74,8 +74,8 @@ def encode_left(engine: CkksEngine, a, p: int) -> ColumnEncodedMatrix:
     m, n = a.shape
     if m * p > engine.slots:
         raise CapacityError(f"{m}x{p} broadcast needs {m * p} slots, engine has {engine.slots}")
-    grids = np.repeat(a.T, p, axis=1)  # [n][m*p]
-    cts = engine.enc_batch(list(grids), layout=("grid", m, p))
+    # ct k, slot i*p + j = A[i, k]: broadcast done on the device from the raw m x n matrix
+    cts = engine.enc_strided(a, count=n, nvals=m * p, p=p, sc=1, s1=n, s2=0, layout=("grid", m, p))
     return ColumnEncodedMatrix(cts, "left", m, n, p)
 
 
@@ -85,8 +85,8 @@ def encode_right(engine: CkksEngine, b, m: int) -> ColumnEncodedMatrix:
     n, p = b.shape
     if m * p > engine.slots:
         raise CapacityError(f"{m}x{p} tiling needs {m * p} slots, engine has {engine.slots}")
-    grids = np.tile(b, (1, m))  # [n][m*p]
-    cts = engine.enc_batch(list(grids), layout=("grid", m, p))
+    # ct k, slot i*p + j = B[k, j]: tiling done on the device from the raw n x p matrix
+    cts = engine.enc_strided(b, count=n, nvals=m * p, p=p, sc=p, s1=0, s2=1, layout=("grid", m, p))
     return ColumnEncodedMatrix(cts, "right", m, n, p)
 
 
@@ -175,8 +175,8 @@ def encode_image_columns(engine: CkksEngine, images) -> ColumnEncodedImage:
     m, h, w = arr.shape
     if m * h > engine.slots:
         raise CapacityError(f"{m} columns of {h} pixels need {m * h} slots")
-    cols = np.transpose(arr, (2, 0, 1)).reshape(w, m * h)  # column j: slot b*h+i = img[b,i,j]
-    cts = engine.enc_batch(list(cols), layout=("column", h, m))
+    # column j: slot b*h + i = img[b, i, j], gathered on the device from the raw images
+    cts = engine.enc_strided(arr, count=w, nvals=m * h, p=h, sc=1, s1=h * w, s2=w, layout=("column", h, m))
     return ColumnEncodedImage(cts, h, w, m, stride=h)
 
 
