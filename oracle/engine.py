@@ -29,7 +29,7 @@ class OCt:
 
 class OracleEngine:
     def __init__(self, slots: int, prime_bits, special_bits: int = 60, delta: int = 45, delta_c: int = 20,
-                 seed: int = 0, encryption: str = "public"):
+                 seed: int = 0, encryption: str = "secret"):
         self.slots = slots
         self.log_n = int(math.log2(2 * slots))
         self.N = 2 * slots

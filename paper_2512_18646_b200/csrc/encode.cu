@@ -12,6 +12,7 @@
 // (seed, domain, nonce/digit, limb): identical integers on CPU and GPU, so
 // ciphertext residues are bit-identical too.
 #include "encode.cuh"
+#include "ntt_impl.cuh"
 
 namespace vr {
 
@@ -272,6 +273,40 @@ __global__ void k_perm_rows(const uint64_t *in, int rows, int logN, uint32_t g, 
     out[e] = in[(e - k) + src];
 }
 
+// Fused secret-key encryption: the NTT of (m + e) mod q_i reads its input straight from the
+// sampler, and its store writes c0 = NTT(m + e) - a s and c1 = a (a sampled in the NTT domain).
+struct LdSymEnc {
+    const int64_t *m;
+    const uint64_t *cdt;
+    uint64_t seed, nonce0;
+    int nl, N;
+    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int pidx) const {
+        const int c = t / nl;
+        const int64_t v = gauss(rnd(stream_key(seed, DOM_ENC_E0, nonce0 + (uint64_t)c, 0), (uint64_t)E), cdt) +
+                          m[(long long)c * N + E];
+        return from_i64(v, pr.m[pidx]);
+    }
+};
+struct StSymEnc {
+    const uint64_t *s_ntt;
+    uint64_t seed, nonce0;
+    int nl, N;
+    struct Pre {
+        uint64_t s;
+    };
+    __device__ __forceinline__ Pre prefetch(int t, long long E, const DevPrimes &, int) const {
+        return Pre{s_ntt[(long long)(t % nl) * N + E]};
+    }
+    __device__ __forceinline__ void finish(uint64_t *ptr, int t, long long E, uint64_t v, const Pre &p, const DevPrimes &pr,
+                                           int pidx) const {
+        const int c = t / nl, i = t - c * nl;
+        const Modulus &m = pr.m[pidx];
+        const uint64_t a = sample_uniform(rnd(stream_key(seed, DOM_ENC_A, nonce0 + (uint64_t)c, i), (uint64_t)E), m.q);
+        ptr[E] = sub_mod(v, mul_mod(a, p.s, m), m.q);
+        ptr[(long long)nl * N + E] = a;
+    }
+};
+
 int log2i(int x) {
     int l = 0;
     while ((1 << l) < x) l++;
@@ -331,6 +366,12 @@ void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long lon
     const int N = c.n, nl = level + 1;
     Scratch m(c, sizeof(int64_t) * count * N);
     encode_src(c, SlotSrc{src, sc, s1, s2, p > 0 ? p : 1, nvals}, count, scale, m.as<int64_t>());
+    if (c.sym_enc) {
+        // one fused NTT (2 passes): sample -> NTT -> (c0, c1), in place in the output ciphertexts
+        ntt_forward_fused(c, NttBatch{d_ct, count * nl, nl, (long long)2 * nl * N, nl, 0, 0, 0},
+                          LdSymEnc{m.as<int64_t>(), c.cdt, c.seed, nonce0, nl, N}, StSymEnc{c.s_ntt, c.seed, nonce0, nl, N});
+        return;
+    }
     const int rows = c.sym_enc ? 2 : 3;
     Scratch buf(c, sizeof(uint64_t) * count * rows * nl * N);
     k_enc_sample<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(m.as<int64_t>(), count, nl, N, c.seed, nonce0,

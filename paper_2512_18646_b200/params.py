@@ -10,7 +10,7 @@ from them so ``EngineParams(slots=...)`` behaves like the reference factory
                    filling ``log_q`` minus the q0 and special-prime budget)
 * ``special_bits`` bit size of the key-switching prime P (default 60)
 * ``seed``         seed of every key and encryption sample
-* ``encryption``   "public" (pk encryption, default) or "secret"
+* ``encryption``   "secret" (key-owner encryption, 1 NTT per limb, default) or "public" (pk)
 """
 
 from __future__ import annotations
@@ -91,7 +91,7 @@ class EngineParams:
     prime_bits: tuple | None = None
     special_bits: int = 60
     seed: int = 0
-    encryption: str = "public"
+    encryption: str = "secret"
     primes: tuple = field(init=False, repr=False, compare=False, default=())
 
     def __post_init__(self):
@@ -154,7 +154,7 @@ class EngineParams:
             prime_bits=tuple(raw["prime_bits"]) if "prime_bits" in raw else None,
             special_bits=int(raw.get("special_bits", 60)),
             seed=int(raw.get("seed", 0)),
-            encryption=str(raw.get("encryption", "public")),
+            encryption=str(raw.get("encryption", "secret")),
         )
 
 
