@@ -73,18 +73,18 @@ __global__ void __launch_bounds__(128) k_conv_mac(const uint64_t *const *T, cons
 // Small-weight conv MAC.  Quantised weights satisfy |w| < B = 2^bb, so w' = w + B
 // is a u32.  Splitting each residue v = vh * 2^32 + vl, every product w' * v is
 // accumulated as two 32x32+64 multiply-adds (IMAD.WIDE.U32) into 64-bit partial
-// sums that cannot overflow within `flush` taps; the bias B * sum(v) is shared by
-// all filters and removed once at the end.  Pointers and weights for the CTA's
-// output column live in shared memory.
+// sums, which the host guarantees cannot overflow for this tap count; the bias
+// B * sum(v) is shared by all filters and removed once at the end.  A thread owns
+// two adjacent coefficients (16-byte loads) and FG filters; pointers and weights
+// of the CTA's output column are staged in shared memory (weights read as 16 B).
 template <int FG>
 __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T, const int *cols, int nout, int C, int W,
-                                                        int k, int F, const uint32_t *wb, uint64_t bb_pow, int flush,
-                                                        const uint64_t *bq, const uint64_t *mask, int nl, int N, DevPrimes pr,
-                                                        uint64_t *Yp) {
-    extern __shared__ uint64_t smc[];
+                                                        int k, int F, const uint32_t *wb, uint64_t bb_pow, const uint64_t *bq,
+                                                        const uint64_t *mask, int nl, int N, DevPrimes pr, uint64_t *Yp) {
+    extern __shared__ __align__(16) uint64_t smc[];
     const int taps = C * k * k;
     const uint64_t **sptr = (const uint64_t **)smc;
-    uint32_t *sw = (uint32_t *)(smc + taps);  // [taps][FG]
+    uint32_t *sw = (uint32_t *)(smc + ((taps + 1) & ~1));  // [taps][FG], 16-byte aligned rows for FG % 4 == 0
     const int nfg = F / FG;
     const int o = blockIdx.z / nfg, f0 = (blockIdx.z - o * nfg) * FG;
     for (int t = threadIdx.x; t < taps; t += blockDim.x) {
@@ -93,63 +93,70 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
         for (int f = 0; f < FG; f++) sw[t * FG + f] = wb[((size_t)(f0 + f) * C + c) * k * k + p * k + q];
     }
     __syncthreads();
-    const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+    const int kk = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
     if (kk >= N) return;
     const int poly = blockIdx.y / nl, i = blockIdx.y - poly * nl;
     const Modulus m = pr.m[i];
     const size_t off = ((size_t)poly * nl + i) * N + kk;
-    uint64_t alo[FG], ahi[FG];
-    u128 acc[FG];
+    uint64_t alo[2][FG], ahi[2][FG];
 #pragma unroll
-    for (int f = 0; f < FG; f++) { alo[f] = 0; ahi[f] = 0; acc[f] = u128{0, 0}; }
-    u128 sv{0, 0};
-    int cnt = 0;
-    for (int t0 = 0; t0 < taps; t0 += 8) {
-        // issue the next (up to) 8 tap loads before any multiply-accumulate
-        uint64_t vv[8];
+    for (int f = 0; f < FG; f++) alo[0][f] = ahi[0][f] = alo[1][f] = ahi[1][f] = 0;
+    uint64_t svl[2] = {0, 0}, svh[2] = {0, 0};
+    for (int t0 = 0; t0 < taps; t0 += 4) {
+        ulonglong2 vv[4];
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
+        for (int u = 0; u < 4; u++) {
             const uint64_t *src = (t0 + u < taps) ? sptr[t0 + u] : nullptr;
-            vv[u] = src ? src[off] : 0;  // null: every filter's weight on this tap is zero
+            vv[u] = src ? *reinterpret_cast<const ulonglong2 *>(src + off) : make_ulonglong2(0, 0);  // null: all weights zero
         }
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
+        for (int u = 0; u < 4; u++) {
             if (t0 + u >= taps) break;
-            const uint64_t v = vv[u];
-            const uint32_t vl = (uint32_t)v, vh = (uint32_t)(v >> 32);
-            sv.lo += v;
-            sv.hi += sv.lo < v;
-            const uint32_t *wt = sw + (t0 + u) * FG;
+            const uint64_t v2[2] = {vv[u].x, vv[u].y};
+            uint32_t wv[FG];
 #pragma unroll
-            for (int f = 0; f < FG; f++) {
-                const uint64_t w = wt[f];
-                alo[f] += (uint64_t)vl * w;
-                ahi[f] += (uint64_t)vh * w;
+            for (int f = 0; f < FG; f += (FG >= 4 ? 4 : 1)) {
+                if (FG >= 4) {
+                    const uint4 w4 = *reinterpret_cast<const uint4 *>(sw + (t0 + u) * FG + f);
+                    wv[f] = w4.x; wv[f + 1] = w4.y; wv[f + 2] = w4.z; wv[f + 3] = w4.w;
+                } else {
+                    wv[f] = sw[(t0 + u) * FG + f];
+                }
             }
-            if (++cnt == flush) {
-                cnt = 0;
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const uint32_t vl = (uint32_t)v2[e], vh = (uint32_t)(v2[e] >> 32);
+                svl[e] += vl;
+                svh[e] += vh;
 #pragma unroll
                 for (int f = 0; f < FG; f++) {
-                    add_to(acc[f], u128{alo[f], 0});
-                    add_to(acc[f], u128{ahi[f] << 32, ahi[f] >> 32});
-                    alo[f] = ahi[f] = 0;
+                    alo[e][f] += (uint64_t)vl * wv[f];
+                    ahi[e][f] += (uint64_t)vh * wv[f];
                 }
             }
         }
     }
-    const uint64_t svq = reduce128(sv, m);
     const uint64_t bq_pow = reduce64(bb_pow, m);
-    const uint64_t bias_sum = mul_mod(svq, bq_pow, m);  // B * sum(v) mod q
-    const uint64_t mk = mask[(size_t)i * N + kk];
+    const ulonglong2 mk2 = *reinterpret_cast<const ulonglong2 *>(mask + (size_t)i * N + kk);
+    const uint64_t mk[2] = {mk2.x, mk2.y};
+    uint64_t outv[FG][2];
 #pragma unroll
-    for (int f = 0; f < FG; f++) {
-        add_to(acc[f], u128{alo[f], 0});
-        add_to(acc[f], u128{ahi[f] << 32, ahi[f] >> 32});
-        uint64_t r = sub_mod(reduce128(acc[f], m), bias_sum, m.q);
-        if (poly == 0) r = add_mod(r, bq[(size_t)i * F + f0 + f], m.q);
-        r = mul_mod(r, mk, m);
-        Yp[((size_t)(f0 + f) * nout + o) * 2 * nl * N + off] = r;
+    for (int e = 0; e < 2; e++) {
+        // sum(v) = svh * 2^32 + svl
+        const u128 sv{svl[e] + (svh[e] << 32), (svh[e] >> 32) + ((svl[e] + (svh[e] << 32)) < svl[e] ? 1u : 0u)};
+        const uint64_t bias_sum = mul_mod(reduce128(sv, m), bq_pow, m);  // B * sum(v) mod q
+#pragma unroll
+        for (int f = 0; f < FG; f++) {
+            u128 acc{alo[e][f], 0};
+            add_to(acc, u128{ahi[e][f] << 32, ahi[e][f] >> 32});
+            uint64_t r = sub_mod(reduce128(acc, m), bias_sum, m.q);
+            if (poly == 0) r = add_mod(r, bq[(size_t)i * F + f0 + f], m.q);
+            outv[f][e] = mul_mod(r, mk[e], m);
+        }
     }
+#pragma unroll
+    for (int f = 0; f < FG; f++)
+        *reinterpret_cast<ulonglong2 *>(Yp + ((size_t)(f0 + f) * nout + o) * 2 * nl * N + off) = make_ulonglong2(outv[f][0], outv[f][1]);
 }
 
 // Plaintext mat-vec: Yp[u] = sum_j PT[u*nx + j] (.) X[j] (both polys), 128-bit accumulation.
@@ -285,19 +292,19 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
     for (size_t t = 0; t < (size_t)F * C * k * k; t++) wmax = std::max<int64_t>(wmax, w[t] < 0 ? -w[t] : w[t]);
     int bb = 1;
     while ((int64_t(1) << bb) <= wmax) bb++;
-    const bool small = bb <= 30;
+    const int taps_total = C * k * k;
+    // 64-bit partials: 2^32 * 2^(bb+1) * taps < 2^64  (and sum(v) halves: taps < 2^31)
+    const bool small = bb <= 30 && (int64_t)taps_total <= (int64_t(1) << (31 - bb)) && N >= 2;
     std::vector<uint32_t> wbias;
     int flush = 1;
     if (small) {
         wbias.resize((size_t)F * C * k * k);
         for (size_t t = 0; t < wbias.size(); t++) wbias[t] = (uint32_t)(w[t] + (int64_t(1) << bb));
-        // 2^32 * 2^(bb+1) * flush < 2^64
-        flush = (int)std::max<int64_t>(1, std::min<int64_t>(1 << 20, (int64_t(1) << (31 - bb))));
+        flush = taps_total;
     }
     DevArray<uint32_t> dwb(c, small ? wbias.data() : nullptr, small ? wbias.size() : 0);
     const int taps = C * k * k;
-    const int FG = small ? ((F % 16 == 0) ? 16 : (F % 8 == 0) ? 8 : (F % 4 == 0 ? 4 : (F % 2 == 0 ? 2 : 1)))
-                         : ((F % 8 == 0) ? 8 : (F % 4 == 0 ? 4 : (F % 2 == 0 ? 2 : 1)));
+    const int FG = (F % 8 == 0) ? 8 : (F % 4 == 0 ? 4 : (F % 2 == 0 ? 2 : 1));
     const int ocols = std::max(1, std::min(nout, (int)(((size_t)2 << 30) / (ctw * 8 * F))));
     Scratch yp(c, sizeof(uint64_t) * (size_t)F * ocols * ctw);
     for (int o0 = 0; o0 < nout; o0 += ocols) {
@@ -305,14 +312,14 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
         dim3 grid(nblocks(N, 128), 2 * nl, (unsigned)no * (F / FG));
         const int *colp = dcols.get() + o0;
         if (small) {
-            const size_t sm = (size_t)taps * 8 + (size_t)taps * FG * 4;
+            const size_t sm = (size_t)((taps + 1) & ~1) * 8 + (size_t)taps * FG * 4 + 16;
             const uint64_t bpow = uint64_t(1) << bb;
+            dim3 gs(nblocks(N / 2, 128), 2 * nl, (unsigned)no * (F / FG));
             switch (FG) {
-                case 16: k_conv_mac_small<16><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-                case 8: k_conv_mac_small<8><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-                case 4: k_conv_mac_small<4><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-                case 2: k_conv_mac_small<2><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-                default: k_conv_mac_small<1><<<grid, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, flush, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                case 8: k_conv_mac_small<8><<<gs, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                case 4: k_conv_mac_small<4><<<gs, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                case 2: k_conv_mac_small<2><<<gs, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                default: k_conv_mac_small<1><<<gs, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
             }
             check_launch("k_conv_mac_small");
         } else {
