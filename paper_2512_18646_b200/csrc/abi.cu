@@ -245,6 +245,9 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         c.slot_pos = upload(c, sp);
         c.cdt = upload(c, cdt);
         VR_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        VR_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
+        VR_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+        VR_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
         VR_CUDA(cudaMallocHost((void **)&c.stage, (size_t)vr::Ctx::kStageSlots * vr::Ctx::kStageBytes));
         for (int i = 0; i < vr::Ctx::kStageSlots; i++)
             VR_CUDA(cudaEventCreateWithFlags(&c.stage_evt[i], cudaEventDisableTiming));
@@ -277,6 +280,9 @@ int vr_ctx_destroy(vr_ctx *h) {
         for (auto &e : c.tables)
             if (e.dev) cudaFree(e.dev);
         if (c.arena) cudaFree(c.arena);
+        if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+        if (c.ev_join) cudaEventDestroy(c.ev_join);
+        for (auto &b : c.big_free) cudaFree(b.second);
         for (int i = 0; i < vr::Ctx::kStageSlots; i++)
             if (c.stage_evt[i]) cudaEventDestroy(c.stage_evt[i]);
         if (c.stage) cudaFreeHost(c.stage);

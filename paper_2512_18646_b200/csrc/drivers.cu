@@ -214,6 +214,20 @@ void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, in
     const int N = c.n, nl = level + 1;
     Scratch d3(c, sizeof(uint64_t) * nb * 3 * nl * N);
     PtrTable td(c, strided(d3.as<uint64_t>(), nb, (size_t)3 * nl * N));
+    if (nb == 1 && n >= 8) {
+        // overlap: d2 = sum L1 R1 first (half the operand bytes) so the key switch starts early,
+        // while (d0, d1) accumulate on the auxiliary stream; the final combine waits for them.
+        VR_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        VR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
+        cudaStream_t main = c.stream;
+        c.stream = c.aux;
+        tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 2);
+        VR_CUDA(cudaEventRecord(c.ev_join, c.aux));
+        c.stream = main;
+        tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
+        relin_rescale_batch(c, td.c_(), Out, nb, level, c.ev_join);
+        return;
+    }
     tensor_sum(c, L, R, n, nb, nl, td.m_());
     relin_rescale_batch(c, td.c_(), Out, nb, level);
 }

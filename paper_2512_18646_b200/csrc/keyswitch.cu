@@ -12,6 +12,8 @@
 // Kernel count per key switch: ModUp = INTT (gather prologue) + NTT (lift
 // prologue); inner product; ModDown = INTT (strided prologue) + NTT (lift
 // prologue, "(a - z) * P^-1 (+ add)" epilogue).  Each NTT is two passes.
+#include <cstdlib>
+
 #include "ntt_impl.cuh"
 #include "ring.cuh"
 
@@ -43,8 +45,7 @@ struct LdStrided {
 // (2 x (l+1) words) in registers and issues all CG x (l+1) digit loads before
 // the multiply-accumulates, so the key is read count/CG times per launch and
 // every thread has CG*(l+1) independent loads in flight.
-constexpr int KS_CG = 4;
-template <int KS_MAXD>
+template <int KS_MAXD, int KS_CG>
 __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint64_t *const *P, long long poly_off, int count,
                                                   int level, int N, int logN, int np, const uint64_t *key, uint32_t g,
                                                   DevPrimes pr, uint64_t *A) {
@@ -185,17 +186,33 @@ static void modup_impl(Ctx &c, const uint64_t *const *Polys, long long poly_off,
 
 void modup(Ctx &c, const uint64_t *const *Polys, int count, int level, uint64_t *D) { modup_impl(c, Polys, 0, count, level, D); }
 
+template <int CG>
+static void launch_ks_inner_cg(Ctx &c, const uint64_t *D, const uint64_t *const *Polys, long long poly_off, int count, int level,
+                               const uint64_t *key, uint32_t g, uint64_t *A) {
+    const int N = c.n, nl = level + 1, nt = level + 2;
+    const dim3 blocks(nblocks((long long)nt * N, 128), (count + CG - 1) / CG);
+    if (nl <= 8)
+        k_ks_inner<8, CG><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
+    else if (nl <= 16)
+        k_ks_inner<16, CG><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
+    else
+        k_ks_inner<40, 1><<<dim3(blocks.x, count), 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g,
+                                                                         c.primes, A);
+    check_launch("k_ks_inner");
+}
+
 static void launch_ks_inner(Ctx &c, const uint64_t *D, const uint64_t *const *Polys, long long poly_off, int count, int level,
                             const uint64_t *key, uint32_t g, uint64_t *A) {
-    const int N = c.n, nl = level + 1, nt = level + 2;
-    const dim3 blocks(nblocks((long long)nt * N, 128), (count + KS_CG - 1) / KS_CG);
-    if (nl <= 8)
-        k_ks_inner<8><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
-    else if (nl <= 16)
-        k_ks_inner<16><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
-    else
-        k_ks_inner<40><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
-    check_launch("k_ks_inner");
+    static int cg = [] {
+        const char *e = getenv("VR_KS_CG");
+        return e ? atoi(e) : 2;  // swept on B200: 1/2/4/8 within 2%
+    }();
+    switch (cg) {
+        case 1: launch_ks_inner_cg<1>(c, D, Polys, poly_off, count, level, key, g, A); break;
+        case 2: launch_ks_inner_cg<2>(c, D, Polys, poly_off, count, level, key, g, A); break;
+        case 8: launch_ks_inner_cg<8>(c, D, Polys, poly_off, count, level, key, g, A); break;
+        default: launch_ks_inner_cg<4>(c, D, Polys, poly_off, count, level, key, g, A); break;
+    }
 }
 
 // Out (pointer table, count entries of [2][l+1][N]) = ModDown(inner(D, key)) (+ add)
@@ -203,14 +220,7 @@ static void inner_moddown(Ctx &c, const uint64_t *D, const uint64_t *const *Poly
                           const uint64_t *key, uint32_t g, uint64_t *const *Out, const uint64_t *const *Add, int add_polys) {
     const int N = c.n, nl = level + 1, nt = level + 2, P = c.np - 1;
     Scratch a(c, sizeof(uint64_t) * count * 2 * nt * N);
-    const dim3 blocks(nblocks((long long)nt * N, 128), (count + KS_CG - 1) / KS_CG);
-    if (nl <= 8)
-        k_ks_inner<8><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, a.as<uint64_t>());
-    else if (nl <= 16)
-        k_ks_inner<16><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, a.as<uint64_t>());
-    else
-        k_ks_inner<40><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, a.as<uint64_t>());
-    check_launch("k_ks_inner");
+    launch_ks_inner(c, D, Polys, poly_off, count, level, key, g, a.as<uint64_t>());
     const int rows = count * 2;
     Scratch y(c, sizeof(uint64_t) * rows * N), z(c, sizeof(uint64_t) * rows * nl * N);
     ntt_inverse_fused(c, NttBatch{y.as<uint64_t>(), rows, 1, (long long)N, 1, P, 0, 0},
@@ -228,7 +238,7 @@ void keyswitch_poly(Ctx &c, const uint64_t *const *Polys, int count, int level, 
 }
 
 // relinearise and rescale in one rounding step: (P d + acc) / (P q_l)
-void relin_rescale_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level) {
+void relin_rescale_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level, cudaEvent_t d01_ready) {
     if (level < 1) throw VrError(3, "relin_rescale: no level left to drop");
     const int N = c.n, nl = level + 1, nt = level + 2, P = c.np - 1;
     const uint64_t *key = relin_key(c);
@@ -238,6 +248,7 @@ void relin_rescale_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out
     launch_ks_inner(c, d.as<uint64_t>(), D3, off, count, level, key, 1, a.as<uint64_t>());
     const uint64_t *rr = c.rr_tab + (size_t)level * RR_STRIDE;
     Scratch y(c, sizeof(uint64_t) * count * 4 * N), z(c, sizeof(uint64_t) * count * 2 * level * N);
+    if (d01_ready) VR_CUDA(cudaStreamWaitEvent(c.stream, d01_ready, 0));  // (d0, d1) produced on another stream
     ntt_inverse_fused(c, NttBatch{y.as<uint64_t>(), count * 4, 2, (long long)2 * N, 1, level, P, 0},
                       LdXrow{a.as<uint64_t>(), D3, rr, level, nt, N}, nttk::StPlain{});
     ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), count * 2, level, N), LdCrt{y.as<uint64_t>(), rr, level, N},

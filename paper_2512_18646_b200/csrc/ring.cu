@@ -202,12 +202,15 @@ __host__ __device__ constexpr int ts_stages() {
            : ((200 * 1024) / ((2 * NB + 2) * TILE * 8) < 2 ? 2 : (200 * 1024) / ((2 * NB + 2) * TILE * 8));
 }
 
-template <int NB, int TS_TILE, int TS_SPLIT, int MAXST>
+// MODE 0: (d0, d1, d2); MODE 1: d2 = sum L1 R1 only (reads half the operands); MODE 2: (d0, d1) only.
+template <int NB, int TS_TILE, int TS_SPLIT, int MAXST, int MODE>
 __global__ void __launch_bounds__(TS_TILE / 2 + 32)
     k_tensor_sum(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O) {
     constexpr int TS_CONSUMERS = TS_TILE / 2;  // 2 coefficients per consumer thread
     constexpr int TS_STAGES = ts_stages<NB, TS_TILE, MAXST>();
-    constexpr int ARR = 2 * NB + 2;  // limb tiles per stage: L[b] poly0/poly1 ..., R poly0/poly1
+    // limb tiles per stage: L[b] poly0/poly1 ..., R poly0/poly1 (MODE 1: L[b] poly1 ..., R poly1)
+    constexpr int ARR = MODE == 1 ? NB + 1 : 2 * NB + 2;
+    constexpr int P0 = MODE == 1 ? 2 : 0, P1 = MODE == 2 ? 2 : 3;  // output polys [P0, P1)
     extern __shared__ __align__(128) uint64_t ts_smem[];
     uint64_t *ring = ts_smem;                                        // [STAGES][ARR][tile]
     __shared__ __align__(8) uint64_t full[TS_STAGES], empty[TS_STAGES];
@@ -242,15 +245,21 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
                 if (it >= TS_STAGES) mbar_wait(&empty[s], ((it / TS_STAGES) - 1) & 1);
                 uint64_t *st = ring + (size_t)s * ARR * tile;
                 mbar_expect_tx(&full[s], bytes * ARR);
+                if constexpr (MODE == 1) {
 #pragma unroll
-                for (int b = 0; b < NB; b++) {
-                    const uint64_t *l = L[b * n + t];
-                    bulk_g2s(st + (2 * b) * tile, l + o0, bytes, &full[s]);
-                    bulk_g2s(st + (2 * b + 1) * tile, l + o1, bytes, &full[s]);
+                    for (int b = 0; b < NB; b++) bulk_g2s(st + b * tile, L[b * n + t] + o1, bytes, &full[s]);
+                    bulk_g2s(st + NB * tile, R[t] + o1, bytes, &full[s]);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < NB; b++) {
+                        const uint64_t *l = L[b * n + t];
+                        bulk_g2s(st + (2 * b) * tile, l + o0, bytes, &full[s]);
+                        bulk_g2s(st + (2 * b + 1) * tile, l + o1, bytes, &full[s]);
+                    }
+                    const uint64_t *r = R[t];
+                    bulk_g2s(st + (2 * NB) * tile, r + o0, bytes, &full[s]);
+                    bulk_g2s(st + (2 * NB + 1) * tile, r + o1, bytes, &full[s]);
                 }
-                const uint64_t *r = R[t];
-                bulk_g2s(st + (2 * NB) * tile, r + o0, bytes, &full[s]);
-                bulk_g2s(st + (2 * NB + 1) * tile, r + o1, bytes, &full[s]);
             }
         }
     }
@@ -269,20 +278,32 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
             const int s = it % TS_STAGES;
             mbar_wait(&full[s], (it / TS_STAGES) & 1);
             const uint64_t *st = ring + (size_t)s * ARR * tile;
-            const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB) * tile + c2);
-            const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB + 1) * tile + c2);
+            if constexpr (MODE == 1) {
+                const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + NB * tile + c2);
 #pragma unroll
-            for (int b = 0; b < NB; b++) {
-                const ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(st + (2 * b) * tile + c2);
-                const ulonglong2 l1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * b + 1) * tile + c2);
-                mac_to(acc[b][0][0], l0.x, r0.x);
-                mac_to(acc[b][0][1], l0.y, r0.y);
-                mac_to(acc[b][1][0], l0.x, r1.x);
-                mac_to(acc[b][1][1], l0.y, r1.y);
-                mac_to(acc[b][1][0], l1.x, r0.x);
-                mac_to(acc[b][1][1], l1.y, r0.y);
-                mac_to(acc[b][2][0], l1.x, r1.x);
-                mac_to(acc[b][2][1], l1.y, r1.y);
+                for (int b = 0; b < NB; b++) {
+                    const ulonglong2 l1 = *reinterpret_cast<const ulonglong2 *>(st + b * tile + c2);
+                    mac_to(acc[b][2][0], l1.x, r1.x);
+                    mac_to(acc[b][2][1], l1.y, r1.y);
+                }
+            } else {
+                const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB) * tile + c2);
+                const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB + 1) * tile + c2);
+#pragma unroll
+                for (int b = 0; b < NB; b++) {
+                    const ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(st + (2 * b) * tile + c2);
+                    const ulonglong2 l1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * b + 1) * tile + c2);
+                    mac_to(acc[b][0][0], l0.x, r0.x);
+                    mac_to(acc[b][0][1], l0.y, r0.y);
+                    mac_to(acc[b][1][0], l0.x, r1.x);
+                    mac_to(acc[b][1][1], l0.y, r1.y);
+                    mac_to(acc[b][1][0], l1.x, r0.x);
+                    mac_to(acc[b][1][1], l1.y, r0.y);
+                    if constexpr (MODE == 0) {
+                        mac_to(acc[b][2][0], l1.x, r1.x);
+                        mac_to(acc[b][2][1], l1.y, r1.y);
+                    }
+                }
             }
             __syncwarp(wmask);
             if (lane == 0) mbar_arrive(&empty[s]);
@@ -290,7 +311,7 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
 #pragma unroll
                 for (int b = 0; b < NB; b++)
 #pragma unroll
-                    for (int p = 0; p < 3; p++)
+                    for (int p = P0; p < P1; p++)
 #pragma unroll
                         for (int e = 0; e < 2; e++) acc[b][p][e] = u128{reduce128(acc[b][p][e], m), 0};
             }
@@ -301,7 +322,7 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
 #pragma unroll
         for (int b = 0; b < NB; b++)
 #pragma unroll
-            for (int p = 0; p < 3; p++)
+            for (int p = P0; p < P1; p++)
                 part[b * 3 + p][threadIdx.x] = make_ulonglong2(reduce128(acc[b][p][0], m), reduce128(acc[b][p][1], m));
     }
     cluster.sync();
@@ -311,7 +332,7 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
         for (int b = 0; b < NB; b++) {
             uint64_t *o = O[b];
 #pragma unroll
-            for (int p = 0; p < 3; p++) {
+            for (int p = P0; p < P1; p++) {
                 ulonglong2 v = part[b * 3 + p][threadIdx.x];
 #pragma unroll
                 for (int r = 1; r < TS_SPLIT; r++) {
@@ -432,13 +453,13 @@ void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl) {
 }
 
 // Launch shape (tile, split-K) -- tuned on B200 with tools/bw_probe.py; VR_TS_VARIANT overrides.
-template <int NB, int TILE, int SPLIT, int MAXST = 8>
+template <int NB, int TILE, int SPLIT, int MAXST = 8, int MODE = 0>
 static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O) {
-    constexpr int ARR = 2 * NB + 2;
+    constexpr int ARR = MODE == 1 ? NB + 1 : 2 * NB + 2;
     const int tile = c.n < TILE ? c.n : TILE;
     size_t smem = (size_t)ts_stages<NB, TILE, MAXST>() * ARR * tile * sizeof(uint64_t);
     smem = std::max<size_t>(smem, (size_t)NB * 3 * (TILE / 2) * 16);
-    auto kern = k_tensor_sum<NB, TILE, SPLIT, MAXST>;
+    auto kern = k_tensor_sum<NB, TILE, SPLIT, MAXST, MODE>;
     static size_t configured = 0;  // per instantiation: raise the dynamic smem limit once
     if (smem > configured) {
         VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -466,6 +487,14 @@ static void ts_variant(Ctx &c, int v, const uint64_t *const *L, const uint64_t *
         case 2: launch_ts<NB, 128, 2, 8>(c, L, R, n, nl, O); break;
         default: launch_ts<NB, 256, 2, 4>(c, L, R, n, nl, O); break;  // best on B200 (tools/bw_probe.py)
     }
+}
+
+void tensor_sum_mode(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O,
+                     int mode) {
+    if (nb != 1) throw VrError(3, "split tensor_sum supports one row block");
+    if (mode == 1) launch_ts<1, 256, 2, 8, 1>(c, L, R, n, nl, O);
+    else launch_ts<1, 256, 2, 4, 2>(c, L, R, n, nl, O);
+    check_launch("k_tensor_sum");
 }
 
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O) {

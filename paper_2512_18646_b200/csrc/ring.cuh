@@ -24,6 +24,9 @@ void permute(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, in
 void copy_limbs(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl_in, int nl_out, int limb0);
 void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl);
 void bfly_peak(Ctx &c, int blocks, int iters, uint64_t *sink);
+// mode 1: d2 only, mode 2: (d0, d1) only (single row block)
+void tensor_sum_mode(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O,
+                     int mode);
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O);
 
 // rescale: in [polys][l+1][N] -> out [polys][l][N] for each ciphertext
@@ -40,7 +43,10 @@ void keyswitch_poly(Ctx &c, const uint64_t *const *Polys, int count, int level, 
 // Convenience wrappers operating on pointer tables (device) of ciphertexts.
 void relin_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level);  // deg2 -> deg1, same level
 // deg2 at level l -> deg1 at level l-1: (P d + KS-acc) / (P q_l) in one rounding step
-void relin_rescale_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level);
+// d01_ready: event after which (d0, d1) of D3 are valid (they may be computed on another stream while
+// the key switch of d2 runs); nullptr if they are already ordered on c.stream
+void relin_rescale_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out, int count, int level,
+                         cudaEvent_t d01_ready = nullptr);
 void rotate_batch(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int count, int level, int nrot, const uint32_t *gs);
 
 uint64_t *galois_key(Ctx &c, uint32_t g);

@@ -29,6 +29,8 @@ struct NttConst {
 struct Ctx {
     int device = 0;
     cudaStream_t stream = 0;
+    cudaStream_t aux = 0;                    // second stream for intra-driver overlap
+    cudaEvent_t ev_fork = 0, ev_join = 0;    // fork/join events (timing disabled)
     int log_n = 0, n = 0, slots = 0, L = 0, np = 0;  // np = L + 2 (ciphertext chain + special prime)
     uint64_t q[MAXP] = {0};
     DevPrimes primes;
@@ -78,6 +80,9 @@ struct Ctx {
     // stack arena for per-call scratch (LIFO, stream-ordered reuse is safe on one stream)
     char *arena = nullptr;
     size_t arena_cap = 0, arena_top = 0, arena_peak = 0;
+    // free list of big scratch blocks (> 64 MB), reused in stream order; mapping fresh multi-GB
+    // blocks from the pool can stall the host for hundreds of ms
+    std::vector<std::pair<size_t, void *>> big_free;
 
     size_t key_words() const { return (size_t)(L + 1) * 2 * np * n; }
 };
@@ -111,13 +116,26 @@ struct Scratch {
     Ctx &c;
     void *p = nullptr;
     size_t bytes = 0;
-    bool pooled = false;
+    bool pooled = false, big = false;
     static constexpr size_t kArenaMaxBuffer = size_t(64) << 20, kArenaMaxCap = size_t(512) << 20;
     Scratch(Ctx &cx, size_t b) : c(cx) {
         bytes = (b + 255) & ~size_t(255);
         if (!bytes) return;
-        if (bytes > kArenaMaxBuffer) {  // big buffers: the pool's own reuse is cheap relative to their work
-            VR_CUDA(cudaMallocAsync(&p, bytes, c.stream));
+        if (bytes > kArenaMaxBuffer) {  // big buffers: cached free list (best fit within 2x)
+            size_t best = (size_t)-1;
+            int bi = -1;
+            for (int i = 0; i < (int)c.big_free.size(); i++) {
+                const size_t sz = c.big_free[i].first;
+                if (sz >= bytes && sz <= 2 * bytes && sz < best) { best = sz; bi = i; }
+            }
+            if (bi >= 0) {
+                p = c.big_free[bi].second;
+                bytes = c.big_free[bi].first;
+                c.big_free.erase(c.big_free.begin() + bi);
+            } else {
+                VR_CUDA(cudaMallocAsync(&p, bytes, c.stream));
+            }
+            big = true;
             return;
         }
         if (c.arena_top == 0 && c.arena_cap < c.arena_peak) {
@@ -140,6 +158,7 @@ struct Scratch {
     ~Scratch() {
         if (!p) return;
         if (pooled) c.arena_top -= bytes;
+        else if (big) c.big_free.emplace_back(bytes, p);
         else cudaFreeAsync(p, c.stream);
     }
     template <class T>
