@@ -23,6 +23,7 @@
 // another prime), pointer-table gathers and the ModDown / rescale combine
 // "(a - z) * q^-1" run inside the transform instead of as separate kernels.
 #pragma once
+#include <cstdlib>
 #include "vrhe_internal.cuh"
 
 namespace vr {
@@ -144,10 +145,10 @@ struct PassArgs {
     int last;  // this pass writes the final (fully reduced) output through the store functor
 };
 
-template <bool INV, int R>
-__device__ __forceinline__ void group_compute(uint64_t (&x)[8], const int (&base)[8], int d, int s, int logT, int s0, int hi,
-                                              uint64_t q, const ulonglong2 *__restrict__ W, const NttConst &nc) {
-    constexpr int E2 = 1 << R, U = 8 >> R;
+template <bool INV, int R, int EPT>
+__device__ __forceinline__ void group_compute(uint64_t (&x)[EPT], const int (&base)[EPT], int d, int s, int logT, int s0,
+                                              int hi, uint64_t q, const ulonglong2 *__restrict__ W, const NttConst &nc) {
+    constexpr int E2 = 1 << R, U = EPT >> R;
     const uint64_t q2 = 2 * q;
 #pragma unroll
     for (int v = 0; v < U; v++) {
@@ -185,11 +186,14 @@ __device__ __forceinline__ void group_compute(uint64_t (&x)[8], const int (&base
     }
 }
 
-template <bool INV, bool COLS, int LOGT, class LD, class ST>
+// LE = log2(elements per thread): 3 (radix-8 groups) for throughput, 2 (radix-4 groups, twice the
+// threads, half the per-thread dependency chain) for small latency-bound batches.
+template <bool INV, bool COLS, int LOGT, int LE, class LD, class ST>
 __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrimes pr, const ulonglong2 *__restrict__ tw,
                                                 const NttConst *__restrict__ ncs, LD ld, ST st) {
     extern __shared__ uint64_t sm[];
-    constexpr int T = 1 << LOGT, NG = (LOGT + 2) / 3;
+    constexpr int EPT = 1 << LE;
+    constexpr int T = 1 << LOGT, NG = (LOGT + LE - 1) / LE;
     const int logN = a.logN, N = 1 << logN, s0 = a.s0;
     const int lo_bits = logN - s0 - LOGT, TPC = a.TPC;
     const int chunks = (N >> LOGT) / TPC;
@@ -201,39 +205,39 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
     const ulonglong2 *W = tw + (size_t)pidx * N;
     const NttConst nc = ncs[pidx];
     const int tile0 = chunk * TPC, lomask = (1 << lo_bits) - 1;
-    constexpr int tpt = T >> 3;
+    constexpr int tpt = T >> LE;
     int j, sub;
     if (COLS) { j = threadIdx.x % TPC; sub = threadIdx.x / TPC; }
     else { j = threadIdx.x / tpt; sub = threadIdx.x - j * tpt; }
     const int tile = tile0 + j, hi = tile >> lo_bits, lo = tile & lomask;
     const long long ebase = ((long long)hi << (logN - s0)) | lo;
 
-    uint64_t x[8];
-    int base[8];
+    uint64_t x[EPT];
+    int base[EPT];
 #pragma unroll
     for (int step = 0; step < NG; step++) {
         const int gi = INV ? NG - 1 - step : step;
-        const int s = 3 * gi, R = (LOGT - s) < 3 ? (LOGT - s) : 3;
+        const int s = LE * gi, R = (LOGT - s) < LE ? (LOGT - s) : LE;
         const int logd = LOGT - s - R, d = 1 << logd, E2 = 1 << R;
 #pragma unroll
-        for (int v = 0; v < 8; v++) {
-            const int uid = sub * (8 >> R) + v;
-            base[v] = v < (8 >> R) ? (((uid >> logd) << (logd + R)) | (uid & (d - 1))) : 0;
+        for (int v = 0; v < EPT; v++) {
+            const int uid = sub * (EPT >> R) + v;
+            base[v] = v < (EPT >> R) ? (((uid >> logd) << (logd + R)) | (uid & (d - 1))) : 0;
         }
 #pragma unroll
-        for (int e = 0; e < 8; e++) {
+        for (int e = 0; e < EPT; e++) {
             const int L = base[e >> R] + (e & (E2 - 1)) * d;
             if (step == 0) x[e] = ld(ptr, t, ebase | ((long long)L << lo_bits), pr, pidx);
             else x[e] = sm[sidx<COLS>(j, L, T, TPC)];
         }
-        if (R == 3) group_compute<INV, 3>(x, base, d, s, LOGT, s0, hi, q, W, nc);
-        else if (R == 2) group_compute<INV, 2>(x, base, d, s, LOGT, s0, hi, q, W, nc);
-        else group_compute<INV, 1>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+        if (R == 3) group_compute<INV, (LE >= 3 ? 3 : 1), EPT>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+        else if (R == 2) group_compute<INV, 2, EPT>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+        else group_compute<INV, 1, EPT>(x, base, d, s, LOGT, s0, hi, q, W, nc);
         const bool last_group = step == NG - 1;
         if (last_group && a.last) {
             const uint64_t q2 = 2 * q;
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
+            for (int e = 0; e < EPT; e++) {
                 uint64_t v = x[e];
                 if (!INV) v = v >= q2 ? v - q2 : v;
                 x[e] = v >= q ? v - q : v;
@@ -241,28 +245,28 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
         }
         if (last_group && COLS) {
             // consecutive threads own consecutive columns -> coalesced direct stores
-            typename ST::Pre pre[8];
+            typename ST::Pre pre[EPT];
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
+            for (int e = 0; e < EPT; e++) {
                 const int L = base[e >> R] + (e & (E2 - 1)) * d;
                 pre[e] = st.prefetch(t, ebase | ((long long)L << lo_bits), pr, pidx);
             }
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
+            for (int e = 0; e < EPT; e++) {
                 const int L = base[e >> R] + (e & (E2 - 1)) * d;
                 st.finish(ptr, t, ebase | ((long long)L << lo_bits), x[e], pre[e], pr, pidx);
             }
             return;
         }
 #pragma unroll
-        for (int e = 0; e < 8; e++) sm[sidx<COLS>(j, base[e >> R] + (e & (E2 - 1)) * d, T, TPC)] = x[e];
+        for (int e = 0; e < EPT; e++) sm[sidx<COLS>(j, base[e >> R] + (e & (E2 - 1)) * d, T, TPC)] = x[e];
         __syncthreads();  // one owner per element within a group: a single barrier per group boundary
     }
     // rows: coalesced cooperative store out of shared memory (prefetch the epilogue's loads first)
-    long long Es[8];
-    typename ST::Pre pre[8];
+    long long Es[EPT];
+    typename ST::Pre pre[EPT];
 #pragma unroll
-    for (int r = 0; r < 8; r++) {  // blockDim.x * 8 == TPC * T
+    for (int r = 0; r < EPT; r++) {  // blockDim.x * EPT == TPC * T
         const int idx = threadIdx.x + r * blockDim.x;
         const int jj = idx >> LOGT, mid = idx & (T - 1);
         const int tl = tile0 + jj, h2 = tl >> lo_bits, lo2 = tl & lomask;
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
         pre[r] = st.prefetch(t, Es[r], pr, pidx);
     }
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
+    for (int r = 0; r < EPT; r++) {
         const int idx = threadIdx.x + r * blockDim.x;
         const int jj = idx >> LOGT, mid = idx & (T - 1);
         st.finish(ptr, t, Es[r], sm[sidx<COLS>(jj, mid, T, TPC)], pre[r], pr, pidx);
@@ -320,39 +324,46 @@ __global__ void ntt_tiny(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *_
     for (int k = 0; k < N; k++) st.finish(ptr, t, k, a[k], st.prefetch(t, k, pr, pidx), pr, pidx);
 }
 
-template <bool INV, bool COLS, int LOGT, class LD, class ST>
+template <bool INV, bool COLS, int LOGT, int LE, class LD, class ST>
 void launch_pass(Ctx &c, const NttBatch &b, const PassArgs &a, const LD &ld, const ST &st) {
     constexpr int T = 1 << LOGT;
     const int chunks = (c.n >> LOGT) / a.TPC;
-    const int threads = a.TPC * (T >> 3);
+    const int threads = a.TPC * (T >> LE);
     const size_t smem = (size_t)a.TPC * T * sizeof(uint64_t);
     const unsigned blocks = (unsigned)b.count * chunks;
-    ntt_pass<INV, COLS, LOGT, LD, ST><<<blocks, threads, smem, c.stream>>>(b, a, c.primes, INV ? c.itw2 : c.tw2, c.ntt_const,
-                                                                           ld, st);
+    ntt_pass<INV, COLS, LOGT, LE, LD, ST><<<blocks, threads, smem, c.stream>>>(b, a, c.primes, INV ? c.itw2 : c.tw2,
+                                                                               c.ntt_const, ld, st);
     check_launch("ntt_pass");
 }
 
 template <bool INV, bool COLS, class LD, class ST>
-void dispatch_pass(Ctx &c, const NttBatch &b, const PassArgs &a, int logT, const LD &ld, const ST &st) {
+void dispatch_pass(Ctx &c, const NttBatch &b, const PassArgs &a, int logT, int le, const LD &ld, const ST &st) {
+    if (le == 2 && logT >= 6 && logT <= 8) {
+        switch (logT) {
+            case 6: launch_pass<INV, COLS, 6, 2>(c, b, a, ld, st); return;
+            case 7: launch_pass<INV, COLS, 7, 2>(c, b, a, ld, st); return;
+            default: launch_pass<INV, COLS, 8, 2>(c, b, a, ld, st); return;
+        }
+    }
     switch (logT) {
-        case 3: launch_pass<INV, COLS, 3>(c, b, a, ld, st); break;
-        case 4: launch_pass<INV, COLS, 4>(c, b, a, ld, st); break;
-        case 5: launch_pass<INV, COLS, 5>(c, b, a, ld, st); break;
-        case 6: launch_pass<INV, COLS, 6>(c, b, a, ld, st); break;
-        case 7: launch_pass<INV, COLS, 7>(c, b, a, ld, st); break;
-        case 8: launch_pass<INV, COLS, 8>(c, b, a, ld, st); break;
-        case 9: launch_pass<INV, COLS, 9>(c, b, a, ld, st); break;
-        case 10: launch_pass<INV, COLS, 10>(c, b, a, ld, st); break;
+        case 3: launch_pass<INV, COLS, 3, 3>(c, b, a, ld, st); break;
+        case 4: launch_pass<INV, COLS, 4, 3>(c, b, a, ld, st); break;
+        case 5: launch_pass<INV, COLS, 5, 3>(c, b, a, ld, st); break;
+        case 6: launch_pass<INV, COLS, 6, 3>(c, b, a, ld, st); break;
+        case 7: launch_pass<INV, COLS, 7, 3>(c, b, a, ld, st); break;
+        case 8: launch_pass<INV, COLS, 8, 3>(c, b, a, ld, st); break;
+        case 9: launch_pass<INV, COLS, 9, 3>(c, b, a, ld, st); break;
+        case 10: launch_pass<INV, COLS, 10, 3>(c, b, a, ld, st); break;
         default: throw VrError(3, "unsupported NTT tile size");
     }
 }
 
 // Tiles per CTA: as many as fit a 512-thread CTA, reduced for small batches so
 // the launch still spreads over every SM.
-inline int pick_tpc(int count, int tiles_per_tf, int T, int max_tpc, int min_tpc) {
+inline int pick_tpc(int count, int tiles_per_tf, int T, int max_tpc, int min_tpc, int le) {
     int tpc = max_tpc;
     while (tpc > min_tpc && (long long)count * (tiles_per_tf / tpc) < 2 * 148) tpc >>= 1;
-    while (tpc > 1 && tpc * (T >> 3) > 512) tpc >>= 1;
+    while (tpc > 1 && tpc * (T >> le) > 512) tpc >>= 1;
     if (tpc > tiles_per_tf) tpc = tiles_per_tf;
     return tpc;
 }
@@ -368,21 +379,27 @@ void run_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
     }
     if (c.n < 2048) {
         PassArgs a{logN, 0, 1, 1};
-        dispatch_pass<INV, false>(c, b, a, logN, ld, st);
+        dispatch_pass<INV, false>(c, b, a, logN, 3, ld, st);
         return;
     }
     const int la = logN / 2, lb = logN - la;
     const int T1 = 1 << la, T2 = 1 << lb;
-    PassArgs p1{logN, 0, pick_tpc(b.count, 1 << lb, T1, 16, 4), 0};
-    PassArgs p2{logN, la, pick_tpc(b.count, 1 << la, T2, 2048 / T2, 1), 0};
+    // small batches are latency-bound: 4 elements per thread halves each thread's chain
+    static int small_batch = [] {
+        const char *e = getenv("VR_NTT_SMALL");
+        return e ? atoi(e) : 64;
+    }();
+    const int le = b.count <= small_batch ? 2 : 3;
+    PassArgs p1{logN, 0, pick_tpc(b.count, 1 << lb, T1, 16, 4, le), 0};
+    PassArgs p2{logN, la, pick_tpc(b.count, 1 << la, T2, 2048 / T2, 1, le), 0};
     if (!INV) {
         p2.last = 1;
-        dispatch_pass<false, true>(c, b, p1, la, ld, StPlain{});
-        dispatch_pass<false, false>(c, b, p2, lb, LdPlain{}, st);
+        dispatch_pass<false, true>(c, b, p1, la, le, ld, StPlain{});
+        dispatch_pass<false, false>(c, b, p2, lb, le, LdPlain{}, st);
     } else {
         p1.last = 1;
-        dispatch_pass<true, false>(c, b, p2, lb, ld, StPlain{});
-        dispatch_pass<true, true>(c, b, p1, la, LdPlain{}, st);
+        dispatch_pass<true, false>(c, b, p2, lb, le, ld, StPlain{});
+        dispatch_pass<true, true>(c, b, p1, la, le, LdPlain{}, st);
     }
 }
 
