@@ -119,6 +119,9 @@ int vr_matmul_outer(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const
 /* the degree-2 partial sum only (multi-GPU: all-reduce, vr_mod_reduce, then vr_relin + vr_rescale) */
 int vr_tensor_sum(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
                   uint64_t *const *out);
+/* the two halves matmul_outer overlaps: mode 1 writes d2 = sum L1 R1 (poly 2 of out), mode 2 writes
+ * (d0, d1) (polys 0, 1 of out); out is one [3][level+1][N] buffer */
+int vr_tensor_sum_mode(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *R, int n, int level, uint64_t *out, int mode);
 /* conv_columns (multicipher.py:123-162) for C channels x F filters:
  *   Y[f*nout+o] = rescale(mask * (sum_{c,q,p} w[f][c][p][q] * rot(X[c*W + cols[o]+q], p) + bias[f]))
  * w: host int64 [F][C][k][k] (quantised weights), bias_res: host [F][level+1] residues of the bias

@@ -552,6 +552,17 @@ int vr_tensor_sum(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *R,
     });
 }
 
+int vr_tensor_sum_mode(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *R, int n, int level, uint64_t *out, int mode) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (n <= 0) throw vr::VrError(VR_ERR_LAYOUT, "tensor_sum needs at least one column ciphertext");
+        if (mode != 1 && mode != 2) throw vr::VrError(VR_ERR_ENGINE, "mode must be 1 (d2) or 2 (d0, d1)");
+        vr::Ctx &c = h->c;
+        vr::PtrTable tl(c, vec(L, n)), tr(c, vec(R, n)), to(c, std::vector<const uint64_t *>{out});
+        vr::tensor_sum_mode(c, tl.c_(), tr.c_(), n, 1, level + 1, to.m_(), mode);
+    });
+}
+
 int vr_conv_columns(vr_ctx *h, const uint64_t *const *X, int C, int W, int k, const int64_t *w, const uint64_t *bias, int F,
                     const int *out_cols, int nout, const uint64_t *mask_pt, int level, uint64_t *const *Y) {
     return guard([&] {
