@@ -20,8 +20,12 @@ def family(name):
         if k in n:
             if k == 'ntt_pass':
                 import re
-                m = re.search(r'ntt_pass<(\d), (\d), (\d+), ([^,]+), ([^>]+)>', name)
-                return f"ntt_pass inv={m.group(1)} cols={m.group(2)} logT={m.group(3)} {m.group(4).split('::')[-1]}/{m.group(5).split('::')[-1]}" if m else k
+                m = re.search(r'ntt_pass<(\d), (\d), (\d+), (\d), ([^,]+), (.+)>\(', name)
+                if m:
+                    ld = m.group(5).split('::')[-1]
+                    st = m.group(6).split('::')[-1]
+                    return f"ntt_pass inv={m.group(1)} cols={m.group(2)} logT={m.group(3)} ept={1 << int(m.group(4))} {ld}/{st}"
+                return k
             return k
     return n[-40:]
 
