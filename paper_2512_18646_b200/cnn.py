@@ -12,13 +12,16 @@ every output ciphertext.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 from .engine import CkksEngine, EngineError
 from .multicipher import ColumnEncodedImage, conv_columns_multi, encode_image_columns, pad_images
 from .pipeline import poly_activation_batch
 
-__all__ = ["encode_images", "conv_layer", "decode_layer", "square_batch"]
+__all__ = ["encode_images", "conv_layer", "decode_layer", "square_batch", "encode_cfg3_model", "cnn_cfg3", "decode_logits",
+           "dense_columns", "block_sum", "rotate_batch"]
 
 
 def encode_images(engine: CkksEngine, images, padding: int = 0) -> list[ColumnEncodedImage]:
@@ -203,37 +206,58 @@ def block_sum(engine: CkksEngine, cts, terms: int, stride: int):
     return total
 
 
-def cnn_cfg3(engine: CkksEngine, imgs, w, w1, w2):
-    """Config 3 on a batch of (m, 28, 28) images: returns the 10 logit ciphertexts (logit v of image b
-    at slot b*28) and the plaintexts built for the dense layers."""
-    imgs = np.asarray(imgs, dtype=np.float64)
-    m, h, wd = imgs.shape
+@dataclass(frozen=True, eq=False)
+class Cfg3Model:
+    """Plaintext-encoded dense layers of config 3 (the provider encodes the model once, like the
+    reference's encode_model, pipeline.py:339-372)."""
+
+    w: np.ndarray
+    pts1: object  # [ny * F * no][level+1][N] plaintexts of W1 at the dense-1 input level
+    pts2: object  # [nz * ny][level+1][N] constant plaintexts of W2
+    m: int
+    h: int
+    ny: int
+    nz: int
+
+
+def encode_cfg3_model(engine: CkksEngine, w, w1, w2, m: int = 64, h: int = 28) -> Cfg3Model:
+    """Encode config 3's dense weights as plaintexts at the levels the network reaches them."""
     F, _, k, _ = w.shape
-    out_w = wd - k + 1
-    cols = list(range(0, out_w, 2))                      # stride-2 columns: 13
-    rows = list(range(0, h - k + 1, 2))                  # stride-2 rows (slot offsets): 13
-    x = encode_image_columns(engine, imgs)
-    conv = conv_columns_multi(engine, [x], w, np.zeros(F), out_cols=cols)
-    feats = square_batch(engine, [ct for y in conv for ct in y.cts])          # F*13 cts, order (f, o)
-    lv = feats[0].level
+    out_w = h - k + 1
+    nr = no = len(range(0, out_w, 2))
+    L = engine.L
+    lv1, lv2 = L - 2, L - 4  # after conv + square / after dense 1 + square
     S = engine.slots
-    nr, no = len(rows), len(cols)
-    # dense 1: neuron u, input ct (f, o): value W1[u, f*169 + r*13 + o] at slots b*h + 2r
-    ny = w1.shape[0]
+    ny, nz = w1.shape[0], w2.shape[0]
+    rows = list(range(0, h - k + 1, 2))
     masks = np.zeros((ny, F * no, S))
     slot_idx = (np.arange(m)[:, None] * h + np.asarray(rows)[None, :]).reshape(-1)  # (b, r) -> slot
     for f in range(F):
         for o in range(no):
-            wv = w1[:, f * nr * no + np.arange(nr) * no + o]                        # (ny, nr)
+            wv = w1[:, f * nr * no + np.arange(nr) * no + o]  # (ny, nr): W1[u, f*169 + r*13 + o]
             masks[:, f * no + o, slot_idx] = np.tile(wv, (1, m))
-    pts1 = encode_plain_batch(engine, masks.reshape(ny * F * no, S), lv, engine.scales[lv])
-    hid = dense_columns(engine, feats, pts1, ny)
-    hid = block_sum(engine, hid, nr, 2)
+    pts1 = encode_plain_batch(engine, masks.reshape(ny * F * no, S), lv1, engine.scales[lv1])
+    pts2 = encode_plain_batch(engine, np.repeat(np.asarray(w2).reshape(-1, 1), S, axis=1), lv2, engine.scales[lv2])
+    return Cfg3Model(np.asarray(w, dtype=np.float64), pts1, pts2, m, h, ny, nz)
+
+
+def cnn_cfg3(engine: CkksEngine, imgs, w, w1=None, w2=None, model: Cfg3Model | None = None):
+    """Config 3 on a batch of (m, 28, 28) images: returns the 10 logit ciphertexts (logit v of
+    image b at slot b*28).  Pass a pre-encoded ``model`` to skip encoding the dense weights."""
+    imgs = np.asarray(imgs, dtype=np.float64)
+    m, h, wd = imgs.shape
+    if model is None:
+        model = encode_cfg3_model(engine, w, w1, w2, m, h)
+    w = model.w
+    F, _, k, _ = w.shape
+    cols = list(range(0, wd - k + 1, 2))  # stride-2 columns: 13
+    x = encode_image_columns(engine, imgs)
+    conv = conv_columns_multi(engine, [x], w, np.zeros(F), out_cols=cols)
+    feats = square_batch(engine, [ct for y in conv for ct in y.cts])  # F*13 cts, order (f, o)
+    hid = dense_columns(engine, feats, model.pts1, model.ny)
+    hid = block_sum(engine, hid, len(cols), 2)
     hid = square_batch(engine, hid)
-    lv2 = hid[0].level
-    nz = w2.shape[0]
-    pts2 = encode_plain_batch(engine, np.repeat(w2.reshape(-1, 1), S, axis=1), lv2, engine.scales[lv2])
-    return dense_columns(engine, hid, pts2, nz)
+    return dense_columns(engine, hid, model.pts2, model.nz)
 
 
 def decode_logits(engine: CkksEngine, logits, m: int, stride: int) -> np.ndarray:
