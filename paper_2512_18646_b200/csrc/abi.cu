@@ -229,9 +229,27 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
             zr[k] = cos(ang);
             zi[k] = sin(ang);
         }
+        // per-stage twiddles for the slot FFT: stage with half-length hs, butterfly j uses zeta^(4 j S / (2 hs))
+        std::vector<double> ftw(2 * (size_t)c.slots, 0.0);
+        for (int hs = 1; hs < c.slots; hs <<= 1)
+            for (int j = 0; j < hs; j++) {
+                const size_t idx = (size_t)4 * j * (c.slots / (2 * hs));
+                ftw[2 * (hs + j)] = zr[idx];
+                ftw[2 * (hs + j) + 1] = zi[idx];
+            }
         std::vector<int> sp(c.slots);
         uint64_t g = 1;
         for (int j = 0; j < c.slots; j++) { sp[j] = (int)((g - 1) / 4); g = (g * 5) % (2ull * n); }
+        std::vector<int> ps(c.slots);
+        {
+            int logS = 0;
+            while ((1 << logS) < c.slots) logS++;
+            for (int j = 0; j < c.slots; j++) {
+                unsigned x = (unsigned)sp[j], r = 0;
+                for (int b = 0; b < logS; b++) r |= ((x >> b) & 1u) << (logS - 1 - b);
+                ps[r] = j;
+            }
+        }
         std::vector<uint64_t> cdt(vr::CDT_LEN);
         build_cdt(cdt.data());
 
@@ -242,7 +260,9 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         c.rr_tab = upload(c, rr);
         c.zr = upload(c, zr);
         c.zi = upload(c, zi);
+        c.ftw = upload(c, ftw);
         c.slot_pos = upload(c, sp);
+        c.pos_slot = upload(c, ps);
         c.cdt = upload(c, cdt);
         VR_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         VR_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
@@ -271,7 +291,7 @@ int vr_ctx_destroy(vr_ctx *h) {
         vr::Ctx &c = h->c;
         cudaSetDevice(c.device);
         cudaDeviceSynchronize();
-        void *ptrs[] = {c.tw2, c.itw2, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.slot_pos, c.cdt, c.rlk};
+        void *ptrs[] = {c.tw2, c.itw2, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw, c.slot_pos, c.pos_slot, c.cdt, c.rlk};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (c.s_ntt) cudaFree(c.s_ntt);

@@ -14,6 +14,8 @@
 #include "encode.cuh"
 #include "ntt_impl.cuh"
 
+#include <cooperative_groups.h>
+
 namespace vr {
 
 namespace {
@@ -29,23 +31,77 @@ __device__ __forceinline__ int64_t gauss(uint64_t u, const uint64_t *cdt) {
 
 __device__ __forceinline__ unsigned brev_bits(unsigned x, int bits) { return bits ? __brev(x) >> (32 - bits) : 0; }
 
-// In-place radix-2 DIT FFT over re/im (bit-reversed input already in place).
-__device__ void fft_stages(double *re, double *im, int S, const double *zr, const double *zi, bool inverse) {
-    for (int len = 2; len <= S; len <<= 1) {
-        const int half = len >> 1, step = S / len;
-        for (int b = threadIdx.x; b < S / 2; b += blockDim.x) {
-            const int blk = b / half, j = b - blk * half;
-            const int i0 = blk * len + j, i1 = i0 + half;
-            const int idx = 4 * j * step;
-            const double wr = zr[idx], wi = inverse ? -zi[idx] : zi[idx];
-            const double ar = re[i0], ai = im[i0], br = re[i1], bi = im[i1];
-            const double tr = __dsub_rn(__dmul_rn(br, wr), __dmul_rn(bi, wi));
-            const double ti = __dadd_rn(__dmul_rn(br, wi), __dmul_rn(bi, wr));
-            re[i0] = __dadd_rn(ar, tr);
-            im[i0] = __dadd_rn(ai, ti);
-            re[i1] = __dsub_rn(ar, tr);
-            im[i1] = __dsub_rn(ai, ti);
+// Slot FFT: radix-2 DIT over re/im (bit-reversed input already in place), executed as
+// rounds of up to three consecutive stages held in registers (one barrier per round).
+// Every butterfly sees the same operands and twiddle as the stage-by-stage loop of
+// oracle/ckks_oracle.c, so the results are bit-identical; only the schedule differs.
+// Shared-memory copies pad one double per eight so the stride-8 first round is conflict-free.
+template <bool PAD>
+__device__ __forceinline__ int fidx(int i) {
+    return PAD ? i + (i >> 3) : i;
+}
+
+// RB consecutive stages on one register group x[u] = element b + u * h (b = j0 mod h):
+// stage st has half-length hs = h * 2^st, butterfly (u, u + 2^st) uses twiddle j = j0 + (u mod 2^st) * h
+template <int RB>
+__device__ __forceinline__ void fft_group(double *xr, double *xi, int h, int j0, const double2 *tw, bool inverse) {
+    constexpr int R = 1 << RB;
+#pragma unroll
+    for (int st = 0; st < RB; st++) {
+        const int hs = h << st;
+#pragma unroll
+        for (int qb = 0; qb < (1 << st); qb++) {
+            const double2 w = __ldg(tw + hs + j0 + qb * h);
+            const double wr = w.x, wi = inverse ? -w.y : w.y;
+#pragma unroll
+            for (int u = qb; u < R; u += 2 << st) {
+                const int v = u + (1 << st);
+                const double tr = __dsub_rn(__dmul_rn(xr[v], wr), __dmul_rn(xi[v], wi));
+                const double ti = __dadd_rn(__dmul_rn(xr[v], wi), __dmul_rn(xi[v], wr));
+                xr[v] = __dsub_rn(xr[u], tr);
+                xi[v] = __dsub_rn(xi[u], ti);
+                xr[u] = __dadd_rn(xr[u], tr);
+                xi[u] = __dadd_rn(xi[u], ti);
+            }
         }
+    }
+}
+
+// stages with half-lengths h, 2h, .., h * 2^(RB-1) over an S-element block in (padded) shared memory
+template <int RB>
+__device__ __forceinline__ void fft_round(double *re, double *im, int S, int h, const double2 *tw, bool inverse) {
+    constexpr int R = 1 << RB;
+    const int G = S >> RB;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const int j0 = g & (h - 1);
+        const int b = (g - j0) * R + j0;
+        double xr[R], xi[R];
+#pragma unroll
+        for (int u = 0; u < R; u++) {
+            xr[u] = re[fidx<true>(b + u * h)];
+            xi[u] = im[fidx<true>(b + u * h)];
+        }
+        fft_group<RB>(xr, xi, h, j0, tw, inverse);
+#pragma unroll
+        for (int u = 0; u < R; u++) {
+            re[fidx<true>(b + u * h)] = xr[u];
+            im[fidx<true>(b + u * h)] = xi[u];
+        }
+    }
+}
+
+// all stages of length 2 .. S (S = 2^logS), one barrier per round of up to three stages
+__device__ void fft_stages(double *re, double *im, int S, int logS, const double2 *tw, bool inverse) {
+    int h = 1, rem = logS;
+    for (; rem >= 3; rem -= 3, h <<= 3) {
+        fft_round<3>(re, im, S, h, tw, inverse);
+        __syncthreads();
+    }
+    if (rem == 2) {
+        fft_round<2>(re, im, S, h, tw, inverse);
+        __syncthreads();
+    } else if (rem == 1) {
+        fft_round<1>(re, im, S, h, tw, inverse);
         __syncthreads();
     }
 }
@@ -65,49 +121,121 @@ struct SlotSrc {
     }
 };
 
-// one CTA per ciphertext: slot values -> m [count][N] (int64); FFT in shared memory when it fits
-__global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr, const double *zi, const int *slot_pos,
-                         double *wre, double *wim, int64_t *m) {
-    extern __shared__ double fft_sm[];
-    const int c = blockIdx.x;
-    const bool in_smem = wre == nullptr;
-    double *re = in_smem ? fft_sm : wre + (size_t)c * S, *im = in_smem ? fft_sm + S : wim + (size_t)c * S;
-    for (int j = threadIdx.x; j < S; j += blockDim.x) {
-        const int pos = brev_bits((unsigned)slot_pos[j], logS);
-        re[pos] = vs.at(c, j);
-        im[pos] = 0.0;
-    }
-    __syncthreads();
-    fft_stages(re, im, S, zr, zi, true);
-    int64_t *out = m + (size_t)c * 2 * S;
-    for (int k = threadIdx.x; k < S; k += blockDim.x) {
-        const double yr = re[k], yi = im[k];
-        const double xr = __dadd_rn(__dmul_rn(yr, zr[k]), __dmul_rn(yi, zi[k]));
-        const double xi = __dsub_rn(__dmul_rn(yi, zr[k]), __dmul_rn(yr, zi[k]));
-        out[k] = __double2ll_rn(__dmul_rn(xr, f));
-        out[k + S] = __double2ll_rn(__dmul_rn(xi, f));
+// The FFT of one ciphertext is split over a cluster of CL CTAs: CTA r holds positions
+// [r C, (r + 1) C) (C = S / CL) of the bit-reversed array in padded shared memory.  The
+// first log2(C) stages are local; the last log2(CL) = 3 stages form one radix-8 round whose
+// groups {j0 + u C} take element u from CTA u through distributed shared memory.
+constexpr int FFT_CL = 8;
+
+template <int CL>
+__device__ __forceinline__ void fft_cluster(double *re, double *im, int S, int logS, const double2 *tw, bool inverse) {
+    const int C = S / CL;
+    fft_stages(re, im, C, logS - (CL == 8 ? 3 : 0), tw, inverse);
+    if constexpr (CL == 8) {
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+        cluster.sync();
+        const int r = (int)cluster.block_rank(), per = C / 8;
+        for (int g = threadIdx.x; g < per; g += blockDim.x) {
+            const int j0 = r * per + g, jj = fidx<true>(j0);
+            double xr[8], xi[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                xr[u] = cluster.map_shared_rank(re, u)[jj];
+                xi[u] = cluster.map_shared_rank(im, u)[jj];
+            }
+            fft_group<3>(xr, xi, C, j0, tw, inverse);
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                cluster.map_shared_rank(re, u)[jj] = xr[u];
+                cluster.map_shared_rank(im, u)[jj] = xi[u];
+            }
+        }
+        cluster.sync();
     }
 }
 
-// one CTA per ciphertext: centred m [count][N], scales[count] -> real slots [count][S]
-__global__ void k_decode(const int64_t *m, const double *scales, int S, int logS, const double *zr, const double *zi,
-                         const int *slot_pos, double *wre, double *wim, double *out) {
+// Optional fused encryption noise (secret-key path): m += e with e the ciphertext's Gaussian
+// sample (DOM_ENC_E0), so the NTT that follows only reduces m + e into each limb; the
+// stream keys of the uniform a-polynomials are written to keys[c * nl + i].
+struct EncNoise {
+    const uint64_t *cdt;
+    uint64_t seed, nonce0;
+    int nl;
+    uint64_t *keys;  // null: no noise
+};
+
+// cluster of CL CTAs per ciphertext: slot values -> m [count][N] (int64)
+template <int CL>
+__global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr, const double *zi, const double2 *tw,
+                         const int *pos_slot, EncNoise nz, int64_t *m) {
     extern __shared__ double fft_sm[];
-    const int c = blockIdx.x;
-    const bool in_smem = wre == nullptr;
-    double *re = in_smem ? fft_sm : wre + (size_t)c * S, *im = in_smem ? fft_sm + S : wim + (size_t)c * S;
-    const int64_t *mc = m + (size_t)c * 2 * S;
-    const double scale = scales[c];
-    for (int k = threadIdx.x; k < S; k += blockDim.x) {
-        const double ur = __ddiv_rn(__ll2double_rn(mc[k]), scale), ui = __ddiv_rn(__ll2double_rn(mc[k + S]), scale);
-        const int pos = brev_bits((unsigned)k, logS);
-        re[pos] = __dsub_rn(__dmul_rn(ur, zr[k]), __dmul_rn(ui, zi[k]));
-        im[pos] = __dadd_rn(__dmul_rn(ur, zi[k]), __dmul_rn(ui, zr[k]));
+    __shared__ uint64_t cdt_s[CDT_LEN];
+    const int C = S / CL, rank = (int)(blockIdx.x % CL), base = rank * C;
+    const int c = blockIdx.x / CL;
+    double *re = fft_sm, *im = fft_sm + C + C / 8;
+    if (nz.keys) {
+        if (threadIdx.x < CDT_LEN) cdt_s[threadIdx.x] = nz.cdt[threadIdx.x];
+        if (rank == 0 && threadIdx.x < nz.nl)
+            nz.keys[(size_t)c * nz.nl + threadIdx.x] = stream_key(nz.seed, DOM_ENC_A, nz.nonce0 + (uint64_t)c, threadIdx.x);
+    }
+#pragma unroll 4
+    for (int p = threadIdx.x; p < C; p += blockDim.x) {
+        re[fidx<true>(p)] = vs.at(c, pos_slot[base + p]);
+        im[fidx<true>(p)] = 0.0;
     }
     __syncthreads();
-    fft_stages(re, im, S, zr, zi, false);
+    fft_cluster<CL>(re, im, S, logS, tw, true);
+    int64_t *out = m + (size_t)c * 2 * S;
+    const uint64_t ke = nz.keys ? stream_key(nz.seed, DOM_ENC_E0, nz.nonce0 + (uint64_t)c, 0) : 0;
+#pragma unroll 4
+    for (int p = threadIdx.x; p < C; p += blockDim.x) {
+        const int k = base + p;
+        const double yr = re[fidx<true>(p)], yi = im[fidx<true>(p)];
+        const double xr = __dadd_rn(__dmul_rn(yr, zr[k]), __dmul_rn(yi, zi[k]));
+        const double xi = __dsub_rn(__dmul_rn(yi, zr[k]), __dmul_rn(yr, zi[k]));
+        int64_t v0 = __double2ll_rn(__dmul_rn(xr, f)), v1 = __double2ll_rn(__dmul_rn(xi, f));
+        if (nz.keys) {
+            v0 += gauss(rnd(ke, (uint64_t)k), cdt_s);
+            v1 += gauss(rnd(ke, (uint64_t)(k + S)), cdt_s);
+        }
+        out[k] = v0;
+        out[k + S] = v1;
+    }
+}
+
+// cluster of CL CTAs per ciphertext: centred m [count][N], scales[count] -> real slots [count][S]
+template <int CL>
+__global__ void k_decode(const int64_t *m, const double *scales, int S, int logS, const double *zr, const double *zi,
+                         const double2 *tw, const int *slot_pos, double *out) {
+    extern __shared__ double fft_sm[];
+    const int C = S / CL, rank = (int)(blockIdx.x % CL), base = rank * C;
+    const int c = blockIdx.x / CL;
+    double *re = fft_sm, *im = fft_sm + C + C / 8;
+    const int64_t *mc = m + (size_t)c * 2 * S;
+    const double scale = scales[c];
+#pragma unroll 4
+    for (int p = threadIdx.x; p < C; p += blockDim.x) {
+        const int k = (int)brev_bits((unsigned)(base + p), logS);
+        const double ur = __ddiv_rn(__ll2double_rn(mc[k]), scale), ui = __ddiv_rn(__ll2double_rn(mc[k + S]), scale);
+        re[fidx<true>(p)] = __dsub_rn(__dmul_rn(ur, zr[k]), __dmul_rn(ui, zi[k]));
+        im[fidx<true>(p)] = __dadd_rn(__dmul_rn(ur, zi[k]), __dmul_rn(ui, zr[k]));
+    }
+    __syncthreads();
+    fft_cluster<CL>(re, im, S, logS, tw, false);
     double *o = out + (size_t)c * S;
-    for (int j = threadIdx.x; j < S; j += blockDim.x) o[j] = re[slot_pos[j]];
+    if constexpr (CL == 8) {
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+#pragma unroll 4
+        for (int p = threadIdx.x; p < C; p += blockDim.x) {
+            const int pos = slot_pos[base + p];
+            o[base + p] = cluster.map_shared_rank(re, pos / C)[fidx<true>(pos % C)];
+        }
+        cluster.sync();  // peers keep their shared memory until every gather has finished
+    } else {
+        for (int p = threadIdx.x; p < C; p += blockDim.x) o[p] = re[fidx<true>(slot_pos[p])];
+    }
 }
 
 // m [count][N] (int64) -> residues [count][nl][N] (coefficient domain)
@@ -275,33 +403,28 @@ __global__ void k_perm_rows(const uint64_t *in, int rows, int logN, uint32_t g, 
 
 // Fused secret-key encryption: the NTT of (m + e) mod q_i reads its input straight from the
 // sampler, and its store writes c0 = NTT(m + e) - a s and c1 = a (a sampled in the NTT domain).
+// secret-key encryption through one fused forward NTT: load m + e (noise added by k_encode),
+// store c0 = (m + e) - a * s and c1 = a with a uniform from the per-transform stream key
 struct LdSymEnc {
     const int64_t *m;
-    const uint64_t *cdt;
-    uint64_t seed, nonce0;
     int nl, N;
     __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int pidx) const {
-        const int c = t / nl;
-        const int64_t v = gauss(rnd(stream_key(seed, DOM_ENC_E0, nonce0 + (uint64_t)c, 0), (uint64_t)E), cdt) +
-                          m[(long long)c * N + E];
-        return from_i64(v, pr.m[pidx]);
+        return from_i64(m[(long long)(t / nl) * N + E], pr.m[pidx]);
     }
 };
 struct StSymEnc {
-    const uint64_t *s_ntt;
-    uint64_t seed, nonce0;
+    const uint64_t *s_ntt, *keys;
     int nl, N;
     struct Pre {
-        uint64_t s;
+        uint64_t s, key;
     };
     __device__ __forceinline__ Pre prefetch(int t, long long E, const DevPrimes &, int) const {
-        return Pre{s_ntt[(long long)(t % nl) * N + E]};
+        return Pre{s_ntt[(long long)(t % nl) * N + E], keys[t]};
     }
-    __device__ __forceinline__ void finish(uint64_t *ptr, int t, long long E, uint64_t v, const Pre &p, const DevPrimes &pr,
+    __device__ __forceinline__ void finish(uint64_t *ptr, int, long long E, uint64_t v, const Pre &p, const DevPrimes &pr,
                                            int pidx) const {
-        const int c = t / nl, i = t - c * nl;
         const Modulus &m = pr.m[pidx];
-        const uint64_t a = sample_uniform(rnd(stream_key(seed, DOM_ENC_A, nonce0 + (uint64_t)c, i), (uint64_t)E), m.q);
+        const uint64_t a = sample_uniform(rnd(p.key, (uint64_t)E), m.q);
         ptr[E] = sub_mod(v, mul_mod(a, p.s, m), m.q);
         ptr[(long long)nl * N + E] = a;
     }
@@ -313,31 +436,49 @@ int log2i(int x) {
     return l;
 }
 
-int fft_threads(int S) { return S >= 2048 ? 1024 : (S >= 64 ? S / 2 : 32); }
+int fft_cl(int S) { return S >= 64 ? FFT_CL : 1; }
+int fft_threads(int S) {
+    const int C = S / fft_cl(S);
+    return C >= 2048 ? 256 : (C >= 256 ? C / 8 : 32);
+}
+size_t fft_smem(int S) {
+    const int C = S / fft_cl(S);
+    return (size_t)2 * (C + C / 8) * sizeof(double);
+}
 
-// shared-memory FFT when re+im fit (S <= 8192 at 227 KB per CTA)
-bool fft_in_smem(int S) { return (size_t)S * 16 <= (size_t)200 * 1024; }
-void fft_smem_attr(const void *kern, int S) {
-    static int done_enc = 0;
-    (void)done_enc;
-    VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((size_t)S * 16)));
+template <typename K, typename... Args>
+void launch_fft(Ctx &c, K kern, int count, int S, Args... args) {
+    const int cl = fft_cl(S);
+    const size_t sm = fft_smem(S);
+    if (sm > 48 * 1024) VR_CUDA(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(count * cl));
+    cfg.blockDim = dim3((unsigned)fft_threads(S));
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VR_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
 }  // namespace
 
-static void encode_src(Ctx &c, const SlotSrc &vs, int count, double scale, int64_t *d_m) {
+static void encode_src(Ctx &c, const SlotSrc &vs, int count, double scale, int64_t *d_m, EncNoise nz = EncNoise{}) {
     const int S = c.slots;
     const double f = scale / (double)S;
-    if (fft_in_smem(S)) {
-        static int attr_S = 0;
-        if (attr_S < S) { fft_smem_attr((const void *)k_encode, S); attr_S = S; }
-        k_encode<<<count, fft_threads(S), (size_t)S * 16, c.stream>>>(vs, S, log2i(S), f, c.zr, c.zi, c.slot_pos, nullptr,
-                                                                      nullptr, d_m);
-    } else {
-        Scratch wr(c, sizeof(double) * count * S), wi(c, sizeof(double) * count * S);
-        k_encode<<<count, fft_threads(S), 0, c.stream>>>(vs, S, log2i(S), f, c.zr, c.zi, c.slot_pos, wr.as<double>(),
-                                                          wi.as<double>(), d_m);
-    }
+    const double2 *tw = reinterpret_cast<const double2 *>(c.ftw);
+    if (count <= 0) return;
+    if (fft_cl(S) == FFT_CL)
+        launch_fft(c, k_encode<FFT_CL>, count, S, vs, S, log2i(S), f, (const double *)c.zr, (const double *)c.zi, tw,
+                   (const int *)c.pos_slot, nz, d_m);
+    else
+        launch_fft(c, k_encode<1>, count, S, vs, S, log2i(S), f, (const double *)c.zr, (const double *)c.zi, tw,
+                   (const int *)c.pos_slot, nz, d_m);
     check_launch("k_encode");
 }
 
@@ -365,13 +506,16 @@ void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long lon
                  double scale, uint64_t nonce0, uint64_t *d_ct) {
     const int N = c.n, nl = level + 1;
     Scratch m(c, sizeof(int64_t) * count * N);
-    encode_src(c, SlotSrc{src, sc, s1, s2, p > 0 ? p : 1, nvals}, count, scale, m.as<int64_t>());
+    const SlotSrc vs{src, sc, s1, s2, p > 0 ? p : 1, nvals};
     if (c.sym_enc) {
-        // one fused NTT (2 passes): sample -> NTT -> (c0, c1), in place in the output ciphertexts
+        // encode adds e; one fused NTT (2 passes): m + e -> NTT -> (c0, c1), in place in the output ciphertexts
+        Scratch keys(c, sizeof(uint64_t) * count * nl);
+        encode_src(c, vs, count, scale, m.as<int64_t>(), EncNoise{c.cdt, c.seed, nonce0, nl, keys.as<uint64_t>()});
         ntt_forward_fused(c, NttBatch{d_ct, count * nl, nl, (long long)2 * nl * N, nl, 0, 0, 0},
-                          LdSymEnc{m.as<int64_t>(), c.cdt, c.seed, nonce0, nl, N}, StSymEnc{c.s_ntt, c.seed, nonce0, nl, N});
+                          LdSymEnc{m.as<int64_t>(), nl, N}, StSymEnc{c.s_ntt, keys.as<uint64_t>(), nl, N});
         return;
     }
+    encode_src(c, vs, count, scale, m.as<int64_t>());
     const int rows = c.sym_enc ? 2 : 3;
     Scratch buf(c, sizeof(uint64_t) * count * rows * nl * N);
     k_enc_sample<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(m.as<int64_t>(), count, nl, N, c.seed, nonce0,
@@ -400,15 +544,14 @@ void decrypt_decode(Ctx &c, const uint64_t *const *d_cts, const int *d_degs, con
     k_center<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(x.as<uint64_t>(), (long long)count * N, c.q[0], mp);
     check_launch("k_center");
     if (!d_out) return;
-    if (fft_in_smem(S)) {
-        static int attr_S = 0;
-        if (attr_S < S) { fft_smem_attr((const void *)k_decode, S); attr_S = S; }
-        k_decode<<<count, fft_threads(S), (size_t)S * 16, c.stream>>>(mp, d_scales, S, log2i(S), c.zr, c.zi, c.slot_pos,
-                                                                      nullptr, nullptr, d_out);
-    } else {
-        Scratch wr(c, sizeof(double) * count * S), wi(c, sizeof(double) * count * S);
-        k_decode<<<count, fft_threads(S), 0, c.stream>>>(mp, d_scales, S, log2i(S), c.zr, c.zi, c.slot_pos, wr.as<double>(),
-                                                          wi.as<double>(), d_out);
+    const double2 *tw = reinterpret_cast<const double2 *>(c.ftw);
+    if (count > 0) {
+        if (fft_cl(S) == FFT_CL)
+            launch_fft(c, k_decode<FFT_CL>, count, S, (const int64_t *)mp, d_scales, S, log2i(S), (const double *)c.zr,
+                       (const double *)c.zi, tw, (const int *)c.slot_pos, d_out);
+        else
+            launch_fft(c, k_decode<1>, count, S, (const int64_t *)mp, d_scales, S, log2i(S), (const double *)c.zr,
+                       (const double *)c.zi, tw, (const int *)c.slot_pos, d_out);
     }
     check_launch("k_decode");
 }

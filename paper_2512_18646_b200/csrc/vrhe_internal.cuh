@@ -46,7 +46,9 @@ struct Ctx {
     //   [MAXP*8 + 0..3] = P mod q_l (+shoup), P^-1 mod q_l (+shoup)
     uint64_t *rr_tab = nullptr;
     double *zr = nullptr, *zi = nullptr;  // zeta^k, k < N
+    double *ftw = nullptr;  // FFT twiddles by stage: (re, im) pairs at [hs + j], hs = 1, 2, .., S/2, j < hs
     int *slot_pos = nullptr;              // [S]
+    int *pos_slot = nullptr;              // [S] slot j whose bit-reversed FFT position is p
     uint64_t *cdt = nullptr;              // [CDT_LEN]
 
     // keys (device)
