@@ -118,7 +118,12 @@ def check(rc: int) -> None:
 
 def ptr_array(ptrs):
     """Host array of device pointers for a pointer-table argument."""
-    arr = (ctypes.c_void_p * max(1, len(ptrs)))()
-    for i, p in enumerate(ptrs):
-        arr[i] = p
-    return arr
+    ptrs = list(ptrs)
+    return (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs)
+
+
+def row_ptrs(t, count=None):
+    """ptr_array of the leading-index rows of a contiguous device tensor (no per-row views)."""
+    base, step = t.data_ptr(), t.stride(0) * t.element_size()
+    n = t.shape[0] if count is None else count
+    return (ctypes.c_void_p * max(1, n))(*[base + i * step for i in range(n)])

@@ -70,7 +70,7 @@ def square_batch(engine: CkksEngine, cts):
     cts = [engine.adjust(c, lv) for c in cts]
     out = torch.empty((len(cts), 2, lv, engine.N), dtype=torch.int64, device=engine.device)
     ptrs = _lib.ptr_array([c.ptr() for c in cts])
-    _lib.check(engine._lib.vr_mul(engine.handle, ptrs, ptrs, _lib.ptr_array([out[i].data_ptr() for i in range(len(cts))]),
+    _lib.check(engine._lib.vr_mul(engine.handle, ptrs, ptrs, _lib.row_ptrs(out, len(cts)),
                                   len(cts), lv))
     from .engine import Ciphertext
 
@@ -78,7 +78,7 @@ def square_batch(engine: CkksEngine, cts):
     for i, c in enumerate(cts):
         engine._meter.mul_count += 1
         engine._observe(c.depth + 1)
-        res.append(Ciphertext(out[i], lv - 1, engine.scales[lv - 1], c.depth + 1, c.layout, engine._id))
+        res.append(Ciphertext.at(out, i, lv - 1, engine.scales[lv - 1], c.depth + 1, c.layout, engine._id))
     return res
 
 
@@ -128,13 +128,13 @@ def dense_columns(engine: CkksEngine, cts, pts, ny: int):
         raise EngineError("dense_columns inputs must share a level")
     out = torch.empty((ny, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
     _lib.check(engine._lib.vr_pt_matvec(engine.handle, _lib.ptr_array([c.ptr() for c in cts]), nx,
-                                        _lib.ptr_array([pts[i].data_ptr() for i in range(ny * nx)]), ny, lv,
-                                        _lib.ptr_array([out[u].data_ptr() for u in range(ny)])))
+                                        _lib.row_ptrs(pts, ny * nx), ny, lv,
+                                        _lib.row_ptrs(out, ny)))
     depth = max(c.depth for c in cts) + 1
     engine._meter.cmul_count += ny * nx
     engine._meter.add_count += ny * (nx - 1)
     engine._observe(depth)
-    return [Ciphertext(out[u], lv - 1, engine.scales[lv - 1], depth, cts[0].layout, engine._id) for u in range(ny)]
+    return [Ciphertext.at(out, u, lv - 1, engine.scales[lv - 1], depth, cts[0].layout, engine._id) for u in range(ny)]
 
 
 def rotate_batch(engine: CkksEngine, cts, steps):
@@ -152,10 +152,10 @@ def rotate_batch(engine: CkksEngine, cts, steps):
     out = torch.empty((len(cts), len(steps), 2, lv + 1, engine.N), dtype=torch.int64, device=engine.device)
     st = (ctypes.c_int64 * len(steps))(*steps)
     _lib.check(engine._lib.vr_rotate(engine.handle, _lib.ptr_array([c.ptr() for c in cts]),
-                                     _lib.ptr_array([out[i, r].data_ptr() for i in range(len(cts)) for r in range(len(steps))]),
+                                     _lib.row_ptrs(out.flatten(0, 1)),
                                      len(cts), lv, len(steps), st))
     engine._meter.rot_count += len(cts) * len(steps)
-    return [[Ciphertext(out[i, r], lv, c.scale, c.depth, c.layout, engine._id) for r in range(len(steps))]
+    return [[Ciphertext.at(out[i], r, lv, c.scale, c.depth, c.layout, engine._id) for r in range(len(steps))]
             for i, c in enumerate(cts)]
 
 
@@ -169,9 +169,9 @@ def add_batch(engine: CkksEngine, xs, ys):
     lv = xs[0].level
     out = torch.empty((len(xs), 2, lv + 1, engine.N), dtype=torch.int64, device=engine.device)
     _lib.check(engine._lib.vr_add(engine.handle, _lib.ptr_array([x.ptr() for x in xs]), _lib.ptr_array([y.ptr() for y in ys]),
-                                  _lib.ptr_array([out[i].data_ptr() for i in range(len(xs))]), len(xs), 1, lv, 0))
+                                  _lib.row_ptrs(out, len(xs)), len(xs), 1, lv, 0))
     engine._meter.add_count += len(xs)
-    return [Ciphertext(out[i], lv, x.scale, max(x.depth, y.depth), x.layout, engine._id) for i, (x, y) in enumerate(zip(xs, ys))]
+    return [Ciphertext.at(out, i, lv, x.scale, max(x.depth, y.depth), x.layout, engine._id) for i, (x, y) in enumerate(zip(xs, ys))]
 
 
 def block_sum(engine: CkksEngine, cts, terms: int, stride: int):

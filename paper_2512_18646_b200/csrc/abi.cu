@@ -295,6 +295,7 @@ int vr_ctx_destroy(vr_ctx *h) {
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (c.s_ntt) cudaFree(c.s_ntt);
+        if (c.s_sh) cudaFree(c.s_sh);
         if (c.pk) cudaFree(c.pk);
         for (auto &kv : c.gkeys) cudaFree(kv.second);
         for (auto &e : c.tables)

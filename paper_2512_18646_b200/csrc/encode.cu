@@ -12,6 +12,8 @@
 // (seed, domain, nonce/digit, limb): identical integers on CPU and GPU, so
 // ciphertext residues are bit-identical too.
 #include "encode.cuh"
+
+#include <vector>
 #include "ntt_impl.cuh"
 
 #include <cooperative_groups.h>
@@ -413,19 +415,20 @@ struct LdSymEnc {
     }
 };
 struct StSymEnc {
-    const uint64_t *s_ntt, *keys;
+    const uint64_t *s_ntt, *s_sh, *keys;
     int nl, N;
     struct Pre {
-        uint64_t s, key;
+        uint64_t s, s_sh, key;
     };
     __device__ __forceinline__ Pre prefetch(int t, long long E, const DevPrimes &, int) const {
-        return Pre{s_ntt[(long long)(t % nl) * N + E], keys[t]};
+        const long long o = (long long)(t % nl) * N + E;
+        return Pre{s_ntt[o], s_sh[o], keys[t]};
     }
     __device__ __forceinline__ void finish(uint64_t *ptr, int, long long E, uint64_t v, const Pre &p, const DevPrimes &pr,
                                            int pidx) const {
-        const Modulus &m = pr.m[pidx];
-        const uint64_t a = sample_uniform(rnd(p.key, (uint64_t)E), m.q);
-        ptr[E] = sub_mod(v, mul_mod(a, p.s, m), m.q);
+        const uint64_t q = pr.m[pidx].q;
+        const uint64_t a = sample_uniform(rnd(p.key, (uint64_t)E), q);
+        ptr[E] = sub_mod(v, mul_shoup(a, p.s, p.s_sh, q), q);
         ptr[(long long)nl * N + E] = a;
     }
 };
@@ -512,7 +515,7 @@ void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long lon
         Scratch keys(c, sizeof(uint64_t) * count * nl);
         encode_src(c, vs, count, scale, m.as<int64_t>(), EncNoise{c.cdt, c.seed, nonce0, nl, keys.as<uint64_t>()});
         ntt_forward_fused(c, NttBatch{d_ct, count * nl, nl, (long long)2 * nl * N, nl, 0, 0, 0},
-                          LdSymEnc{m.as<int64_t>(), nl, N}, StSymEnc{c.s_ntt, keys.as<uint64_t>(), nl, N});
+                          LdSymEnc{m.as<int64_t>(), nl, N}, StSymEnc{c.s_ntt, c.s_sh, keys.as<uint64_t>(), nl, N});
         return;
     }
     encode_src(c, vs, count, scale, m.as<int64_t>());
@@ -562,6 +565,19 @@ void keygen(Ctx &c) {
     k_sample_secret<<<nblocks((long long)np * n, TB), TB, 0, c.stream>>>(n, np, c.seed, c.primes, c.s_ntt);
     check_launch("k_sample_secret");
     ntt_forward(c, batch_limbs(c.s_ntt, 1, np, n));
+    {
+        // Shoup companions of s (encryption multiplies every a-polynomial by s)
+        std::vector<uint64_t> h((size_t)np * n);
+        VR_CUDA(cudaMemcpyAsync(h.data(), c.s_ntt, sizeof(uint64_t) * h.size(), cudaMemcpyDeviceToHost, c.stream));
+        VR_CUDA(cudaStreamSynchronize(c.stream));
+        for (int i = 0; i < np; i++)
+            for (int k = 0; k < n; k++) {
+                uint64_t &v = h[(size_t)i * n + k];
+                v = (uint64_t)(((unsigned __int128)v << 64) / c.q[i]);
+            }
+        VR_CUDA(cudaMalloc((void **)&c.s_sh, sizeof(uint64_t) * h.size()));
+        VR_CUDA(cudaMemcpy(c.s_sh, h.data(), sizeof(uint64_t) * h.size(), cudaMemcpyHostToDevice));
+    }
     VR_CUDA(cudaMallocAsync((void **)&c.pk, sizeof(uint64_t) * 2 * nl * n, c.stream));
     Scratch e(c, sizeof(uint64_t) * nl * n);
     k_pk_sample<<<nblocks((long long)nl * n, TB), TB, 0, c.stream>>>(n, nl, c.seed, c.cdt, c.primes, c.pk + (size_t)nl * n,

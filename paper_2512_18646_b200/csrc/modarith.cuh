@@ -107,10 +107,11 @@ VR_HD uint64_t mul_shoup(uint64_t x, uint64_t w, uint64_t w_sh, uint64_t q) {
 }
 
 // signed integer -> [0, q)
+// Branch-free: a negative v is shifted by Q = q * floor(2^64 / q) (= q * r_hi, the largest
+// multiple of q below 2^64), which keeps Q + v in [2^63 - q, 2^64) for every int64 v < 0.
 VR_HD uint64_t from_i64(int64_t v, const Modulus &m) {
-    if (v >= 0) return reduce64((uint64_t)v, m);
-    uint64_t r = reduce64((uint64_t)(-(v + 1)) + 1, m);
-    return r ? m.q - r : 0;
+    const uint64_t x = (uint64_t)v + (v < 0 ? m.r_hi * m.q : 0);
+    return reduce64(x, m);
 }
 
 // centered lift of x in [0, from) into [0, m.q)

@@ -53,6 +53,7 @@ struct Ctx {
 
     // keys (device)
     uint64_t *s_ntt = nullptr;  // [np][N]
+    uint64_t *s_sh = nullptr;   // [np][N] Shoup companions floor(s * 2^64 / q) of s_ntt
     uint64_t *pk = nullptr;     // [2][L+1][N]
     uint64_t *rlk = nullptr;    // [L+1][2][np][N]
     std::map<uint32_t, uint64_t *> gkeys;

@@ -95,7 +95,7 @@ def matmul_partials(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -> tu
     if n > 0:
         _lib.check(engine._lib.vr_tensor_sum(engine.handle, _lib.ptr_array([c.ptr() for c in Ls]),
                                              _lib.ptr_array([c.ptr() for c in Rs]), n, nb, lv,
-                                             _lib.ptr_array([part[b].data_ptr() for b in range(nb)])))
+                                             _lib.row_ptrs(part, nb)))
     else:
         part.zero_()
     engine._meter.mul_count += nb * n
@@ -109,10 +109,10 @@ def matmul_finish(engine: CkksEngine, part: torch.Tensor, level: int, m: int, p:
     lib = engine._lib
     _lib.check(lib.vr_mod_reduce(engine.handle, part.data_ptr(), nb * 3, level))
     out = torch.empty((nb, 2, level, engine.N), dtype=torch.int64, device=engine.device)
-    _lib.check(lib.vr_relin_rescale(engine.handle, _lib.ptr_array([part[b].data_ptr() for b in range(nb)]),
-                                    _lib.ptr_array([out[b].data_ptr() for b in range(nb)]), nb, level))
+    _lib.check(lib.vr_relin_rescale(engine.handle, _lib.row_ptrs(part, nb),
+                                    _lib.row_ptrs(out, nb), nb, level))
     engine._observe(engine.L - level + 1)
-    return [Ciphertext(out[b], level - 1, engine.scales[level - 1], engine.L - level + 1, ("grid", m, p), engine._id)
+    return [Ciphertext.at(out, b, level - 1, engine.scales[level - 1], engine.L - level + 1, ("grid", m, p), engine._id)
             for b in range(nb)]
 
 

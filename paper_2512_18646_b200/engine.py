@@ -83,23 +83,77 @@ def _frozen(values) -> np.ndarray:
     return out
 
 
-@dataclass(frozen=True, eq=False)
 class Ciphertext:
-    """Immutable RNS-CKKS ciphertext: residues [degree+1][level+1][N] on the GPU."""
+    """RNS-CKKS ciphertext: residues [degree+1][level+1][N] on the GPU (treated as immutable).
 
-    data: torch.Tensor
-    level: int
-    scale: float
-    depth: int = 0
-    layout: tuple | None = None
-    engine_id: int = 0
+    Ciphertexts produced by one batched kernel share its [count][degree+1][level+1][N] output;
+    each keeps (batch, index) plus its device address and materialises the ``data`` view only
+    when asked, so wrapping a 64-ciphertext batch costs no per-item tensor indexing.
+    """
+
+    __slots__ = ("_data", "_batch", "_idx", "_ptr", "level", "scale", "depth", "layout", "engine_id")
+
+    def __init__(self, data: torch.Tensor, level: int, scale: float, depth: int = 0, layout: tuple | None = None,
+                 engine_id: int = 0):
+        self._data = data
+        self._batch = None
+        self._idx = 0
+        self._ptr = data.data_ptr()
+        self.level = level
+        self.scale = scale
+        self.depth = depth
+        self.layout = layout
+        self.engine_id = engine_id
+
+    @classmethod
+    def at(cls, out: torch.Tensor, i: int, level: int, scale: float, depth: int = 0, layout: tuple | None = None,
+           engine_id: int = 0) -> "Ciphertext":
+        """Ciphertext ``out[i]`` of a contiguous batch, without creating the view."""
+        ct = cls.__new__(cls)
+        ct._data = None
+        ct._batch = out
+        ct._idx = i
+        ct._ptr = out.data_ptr() + i * out.stride(0) * out.element_size()
+        ct.level = level
+        ct.scale = scale
+        ct.depth = depth
+        ct.layout = layout
+        ct.engine_id = engine_id
+        return ct
+
+    @classmethod
+    def batch(cls, out: torch.Tensor, level: int, scale: float, depth: int = 0, layout: tuple | None = None,
+              engine_id: int = 0, count: int | None = None) -> list["Ciphertext"]:
+        """One ciphertext per leading index of ``out`` ([count][deg+1][l+1][N], contiguous)."""
+        base, step = out.data_ptr(), out.stride(0) * out.element_size()
+        res = []
+        new = cls.__new__
+        for i in range(out.shape[0] if count is None else count):
+            ct = new(cls)
+            ct._data = None
+            ct._batch = out
+            ct._idx = i
+            ct._ptr = base + i * step
+            ct.level = level
+            ct.scale = scale
+            ct.depth = depth
+            ct.layout = layout
+            ct.engine_id = engine_id
+            res.append(ct)
+        return res
+
+    @property
+    def data(self) -> torch.Tensor:
+        if self._data is None:
+            self._data = self._batch[self._idx]
+        return self._data
 
     @property
     def degree(self) -> int:
-        return self.data.shape[0] - 1
+        return (self._batch.shape[1] if self._data is None else self._data.shape[0]) - 1
 
     def ptr(self) -> int:
-        return self.data.data_ptr()
+        return self._ptr
 
     def residues(self) -> np.ndarray:
         """Copy of the residues as uint64 numpy (for parity checks)."""
@@ -241,7 +295,7 @@ class CkksEngine:
             self._nonce += count
         self._meter.enc_count += count
         self._observe(0)
-        return [self._wrap(out[i], self.L, 0, layout) for i in range(count)]
+        return Ciphertext.batch(out, self.L, self.scales[self.L], 0, layout, self._id)
 
     def enc_strided(self, src, count: int, nvals: int, p: int, sc: int, s1: int, s2: int, offset: int = 0,
                     layout: tuple | None = None, nonce0: int | None = None) -> list[Ciphertext]:
@@ -263,7 +317,7 @@ class CkksEngine:
             self._nonce += count
         self._meter.enc_count += count
         self._observe(0)
-        return [self._wrap(out[i], self.L, 0, layout) for i in range(count)]
+        return Ciphertext.batch(out, self.L, self.scales[self.L], 0, layout, self._id)
 
     def dec(self, ct: Ciphertext) -> np.ndarray:
         """Full slot vector (real parts), like engine.py:204-206."""

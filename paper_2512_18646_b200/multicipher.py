@@ -153,7 +153,7 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
     outs = torch.empty((nb, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
     _lib.check(engine._lib.vr_matmul_outer(
         engine.handle, _lib.ptr_array(lptrs), _lib.ptr_array(rptrs), n, nb, lv,
-        _lib.ptr_array([outs[b].data_ptr() for b in range(nb)])))
+        _lib.row_ptrs(outs, nb)))
     rdepth = max(c.depth for c in right.cts)
     res = []
     for b, lf in enumerate(lefts):
@@ -161,7 +161,7 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
         engine._meter.mul_count += n
         engine._meter.add_count += n - 1
         engine._observe(depth)
-        res.append(Ciphertext(outs[b], lv - 1, engine.scales[lv - 1], depth, lf.cts[0].layout, engine._id))
+        res.append(Ciphertext.at(outs, b, lv - 1, engine.scales[lv - 1], depth, lf.cts[0].layout, engine._id))
     return res
 
 
@@ -282,7 +282,7 @@ def conv_columns_multi(engine: CkksEngine, imgs, weights, biases, out_cols=None)
         for c in range(C):
             _meter_conv_call(engine, w[f, c], cols, depth_in)
         engine._meter.add_count += C - 1
-        cts = [Ciphertext(Y[f, o], lv - 1, engine.scales[lv - 1], depth_in + 1, ("column", out_h, base.m), engine._id)
+        cts = [Ciphertext.at(Y[f], o, lv - 1, engine.scales[lv - 1], depth_in + 1, ("column", out_h, base.m), engine._id)
                for o in range(nout)]
         out.append(ColumnEncodedImage(cts, out_h, nout, base.m, base.stride))
     return out

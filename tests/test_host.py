@@ -137,6 +137,8 @@ def test_modarith_header_on_host(tmp_path):
             z = min(z, 2 ** 128 - 1)
             rows.append((x, y % (2 ** 64), z >> 64, z & (2 ** 64 - 1), z, y))
         rows.append((q - 1, 2 ** 64 - 1, 2 ** 64 - 1, 2 ** 64 - 1, 2 ** 128 - 1, -1))
+        rows.append((0, 2 ** 63, 0, 0, 0, -(2 ** 63)))  # INT64_MIN through from_i64
+        rows.append((1, 2 ** 63 - 1, 0, 1, 1, 2 ** 63 - 1))
         inp = "\n".join(f"{x} {y} {hi} {lo}" for x, y, hi, lo, _, _ in rows)
         out = subprocess.run([str(exe), str(q), str(w)], input=inp, capture_output=True, text=True, check=True).stdout.split("\n")
         for (x, yu, hi, lo, z, ys), line in zip(rows, out):
