@@ -85,8 +85,15 @@ class OracleEngine:
         lv = a.level
         return OCt(self.c.mul(a.data, b.data), lv - 1, self.scales[lv - 1], max(a.depth, b.depth) + 1, a.layout)
 
+    def mask(self, values, role: str = "constant") -> np.ndarray:
+        """Zero-padded slot vector (engine.py:244-251); cmul accepts it or a PlainMask-like object."""
+        vec = np.asarray(values, dtype=np.float64).reshape(-1)
+        full = np.zeros(self.slots)
+        full[: vec.size] = vec
+        return full
+
     def cmul(self, values, ct: OCt) -> OCt:
-        vals = np.asarray(values, dtype=np.float64).reshape(-1)
+        vals = np.asarray(getattr(values, "values", values), dtype=np.float64).reshape(-1)
         lv = ct.level
         if np.all(vals == vals[0]):
             tmp = self.c.mul_scalar(ct.data, int(round(float(vals[0]) * ct.scale)))

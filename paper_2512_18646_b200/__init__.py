@@ -10,7 +10,21 @@ interface.  There is no CPU fallback.
 from .errors import CapacityError, EngineError, LayoutError
 from .params import EngineParams, config_params, gen_primes, is_pow2, next_pow2
 from .engine import Ciphertext, CkksEngine, OpMeter, PlainMask, SlotEngine
-from .encoding import Encoding, Kernel, MatrixShape, PackedMatrix
+from .encoding import (
+    Encoding,
+    Kernel,
+    MatrixShape,
+    PackedMatrix,
+    encode_db,
+    encode_revolver,
+    encode_row_major,
+    incomplete_col_shift,
+    matrix_from_csv,
+    row_shift,
+    sum_col_vec,
+    sum_row_vec,
+)
+from .matmul import MatmulPlan, build_result_filter, matmul, matmul_tiled, row_shifter
 from .multicipher import (
     ColumnEncodedImage,
     ColumnEncodedMatrix,

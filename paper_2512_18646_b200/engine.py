@@ -411,6 +411,157 @@ class CkksEngine:
         full[: vec.size] = vec
         return PlainMask(_frozen(full), role=role)
 
+    # -- batched forms of the reference ops ----------------------------------
+    # Each computes exactly what the per-op loop would (same kernels, same
+    # residues, same meter increments and depths) in one launch per stage.
+    def _same_level(self, cts) -> bool:
+        lv, sc = cts[0].level, cts[0].scale
+        return all(c.level == lv and c.scale == sc for c in cts)
+
+    def mul_batch(self, xs, ys) -> list[Ciphertext]:
+        """[mul(x, y) for x, y in zip(xs, ys)] (operands may repeat)."""
+        xs, ys = list(xs), list(ys)
+        if len(xs) != len(ys):
+            raise EngineError("mul_batch needs equally many left and right operands")
+        if not xs:
+            return []
+        if not self._same_level(xs + ys):
+            return [self.mul(x, y) for x, y in zip(xs, ys)]
+        for c in xs + ys:
+            self._check(c)
+        lv, count = xs[0].level, len(xs)
+        if lv < 1:
+            raise EngineError("multiplicative depth exhausted: operands are at level 0")
+        out = self._empty(1, lv - 1, count)
+        _lib.check(self._lib.vr_mul(self._h, _lib.ptr_array([x.ptr() for x in xs]), _lib.ptr_array([y.ptr() for y in ys]),
+                                    _lib.row_ptrs(out), count, lv))
+        res = []
+        for i, (x, y) in enumerate(zip(xs, ys)):
+            depth = max(x.depth, y.depth) + 1
+            self._meter.mul_count += 1
+            self._observe(depth)
+            res.append(Ciphertext.at(out, i, lv - 1, self.scales[lv - 1], depth, x.layout, self._id))
+        return res
+
+    def cmul_batch(self, masks, cts) -> list[Ciphertext]:
+        """[cmul(mask_i, ct_i)]; ``masks`` is one PlainMask (shared) or one per ciphertext."""
+        cts = list(cts)
+        if not cts:
+            return []
+        shared = isinstance(masks, PlainMask)
+        masks = [masks] * len(cts) if shared else list(masks)
+        if len(masks) != len(cts):
+            raise EngineError("cmul_batch needs one mask per ciphertext (or one shared mask)")
+        if not self._same_level(cts) or len({c.degree for c in cts}) != 1:
+            return [self.cmul(m, c) for m, c in zip(masks, cts)]
+        uniform = [bool(np.all(m.values == m.values[0])) for m in masks]
+        if any(uniform):
+            # constant masks take cmul's scalar path; the rest go through one batch
+            res = [self.cmul(m, c) if u else None for m, c, u in zip(masks, cts, uniform)]
+            rest = [i for i, u in enumerate(uniform) if not u]
+            if rest:
+                sub = self.cmul_batch(masks[0] if shared else [masks[i] for i in rest], [cts[i] for i in rest])
+                for i, r in zip(rest, sub):
+                    res[i] = r
+            return res
+        for m in masks:
+            if m.values.size != self.slots:
+                raise EngineError(f"mask length {m.values.size} != slot count {self.slots}")
+        for c in cts:
+            self._check(c)
+        lv, deg, count, scale = cts[0].level, cts[0].degree, len(cts), cts[0].scale
+        if lv < 1:
+            raise EngineError("multiplicative depth exhausted: operand is at level 0")
+        rows = [masks[0].values] if shared else [m.values for m in masks]
+        vals = np.stack(rows)
+        d_vals = self._h2d(vals)
+        pts = torch.empty((len(rows), lv + 1, self.N), dtype=torch.int64, device=self.device)
+        _lib.check(self._lib.vr_encode(self._h, d_vals.data_ptr(), len(rows), self.slots, lv, scale, pts.data_ptr()))
+        tmp = self._empty(deg, lv, count)
+        _lib.check(self._lib.vr_mul_plain(self._h, _lib.ptr_array([c.ptr() for c in cts]), _lib.row_ptrs(pts),
+                                          _lib.row_ptrs(tmp), count, deg, lv, 1 if shared else 0))
+        out = self._empty(deg, lv - 1, count)
+        _lib.check(self._lib.vr_rescale(self._h, _lib.row_ptrs(tmp), _lib.row_ptrs(out), count, deg, lv))
+        res = []
+        for i, c in enumerate(cts):
+            self._meter.cmul_count += 1
+            self._observe(c.depth + 1)
+            res.append(Ciphertext.at(out, i, lv - 1, self.scales[lv - 1], c.depth + 1, c.layout, self._id))
+        return res
+
+    def add_batch(self, xs, ys) -> list[Ciphertext]:
+        """[add(x, y) for x, y in zip(xs, ys)]."""
+        xs, ys = list(xs), list(ys)
+        if len(xs) != len(ys):
+            raise EngineError("add_batch needs equally many operands")
+        if not xs:
+            return []
+        if not self._same_level(xs + ys) or len({c.degree for c in xs + ys}) != 1:
+            return [self.add(x, y) for x, y in zip(xs, ys)]
+        for c in xs + ys:
+            self._check(c)
+        lv, deg, count = xs[0].level, xs[0].degree, len(xs)
+        out = self._empty(deg, lv, count)
+        _lib.check(self._lib.vr_add(self._h, _lib.ptr_array([x.ptr() for x in xs]), _lib.ptr_array([y.ptr() for y in ys]),
+                                    _lib.row_ptrs(out), count, deg, lv, 0))
+        res = []
+        for i, (x, y) in enumerate(zip(xs, ys)):
+            depth = max(x.depth, y.depth)
+            self._meter.add_count += 1
+            self._observe(depth)
+            res.append(Ciphertext.at(out, i, lv, x.scale, depth, x.layout, self._id))
+        return res
+
+    def rot_batch(self, cts, steps) -> list[list[Ciphertext]]:
+        """[[rot(ct, s) for s in steps] for ct in cts]: one hoisted ModUp per ciphertext."""
+        cts, steps = list(cts), [int(s) for s in steps]
+        if not cts or not steps:
+            return [[] for _ in cts]
+        if not self._same_level(cts) or any(c.degree != 1 for c in cts):
+            return [[self.rot(c, s) for s in steps] for c in cts]
+        for c in cts:
+            self._check(c)
+        lv, count = cts[0].level, len(cts)
+        out = torch.empty((count, len(steps), 2, lv + 1, self.N), dtype=torch.int64, device=self.device)
+        st = (ctypes.c_int64 * len(steps))(*steps)
+        _lib.check(self._lib.vr_rotate(self._h, _lib.ptr_array([c.ptr() for c in cts]), _lib.row_ptrs(out.flatten(0, 1)),
+                                       count, lv, len(steps), st))
+        res = []
+        for i, c in enumerate(cts):
+            self._meter.rot_count += len(steps)
+            self._observe(c.depth)
+            res.append([Ciphertext.at(out[i], r, lv, c.scale, c.depth, c.layout, self._id) for r in range(len(steps))])
+        return res
+
+    def sum_batch(self, acc: Ciphertext, cts) -> Ciphertext:
+        """acc + cts[0] + cts[1] + ... (``len(cts)`` adds, like the sequential loop).
+
+        Modular addition is exact, so a pairwise tree over the aligned operands gives the
+        same residues as the left-to-right chain.
+        """
+        cts = list(cts)
+        if not cts:
+            return acc
+        lv = min([acc.level] + [c.level for c in cts])
+        terms = [self.adjust(c, lv) for c in cts]
+        if not self._same_level(terms) or terms[0].scale != self.scales[lv]:
+            out = acc
+            for c in cts:
+                out = self.add(out, c)
+            return out
+        base = self.adjust(acc, lv)
+        depth = max([acc.depth] + [c.depth for c in cts])
+        m = self._meter
+        before = m.add_count
+        while len(terms) > 1:
+            half = len(terms) // 2
+            paired = self.add_batch(terms[:half], terms[half:2 * half])
+            terms = paired + terms[2 * half:]
+        out = self.add(base, terms[0])
+        m.add_count = before + len(cts)
+        self._observe(depth)
+        return Ciphertext(out.data, out.level, out.scale, depth, acc.layout, self._id)
+
     # -- device-level helpers (no metering) --------------------------------
     def encode_plain(self, values, level: int, scale: float) -> torch.Tensor:
         vals = self._pad([values])

@@ -86,6 +86,35 @@ def main():
     data["rot_x"] = x
     data["rot_steps"] = np.array([1, -1, 3, 8, -9])
     data["rot_out"] = np.stack([eng.dec(eng.rot(ct, s)) for s in data["rot_steps"]])
+    # Algorithm 3 (revolver matmul, matmul.py) cases: (m, n, p, slots); operands padded like
+    # test_matmul.py:12-25 (row width max(n, p), layout height max(m, p)).  Separate generator so
+    # the fixtures above keep their draws.
+    from packedhe.encoding import encode_revolver, encode_row_major
+    from packedhe.matmul import matmul as alg3
+
+    r3 = np.random.default_rng(0xA163)
+    a3 = [(4, 4, 4, 16), (3, 4, 2, 32), (8, 8, 8, 64), (8, 8, 4, 256), (2, 4, 2, 8), (1, 2, 1, 8), (4, 4, 2, 16),
+          (16, 16, 16, 256)]
+    for idx, (m, n, p, slots) in enumerate(a3):
+        if idx == len(a3) - 1:
+            a, b = r3.uniform(-1, 1, (m, n)), r3.uniform(-1, 1, (n, p))
+        else:
+            a, b = r3.integers(-4, 5, size=(m, n)).astype(float), r3.integers(-4, 5, size=(n, p)).astype(float)
+        width = max(n, p)
+        ap = np.zeros((m, width))
+        ap[:, :n] = a
+        bp = np.zeros((width, p))
+        bp[:n] = b
+        eng = SlotEngine(EngineParams(slots=slots))
+        ca, cb = encode_row_major(eng, ap), encode_revolver(eng, bp, target_m=max(m, p))
+        before = eng.meter_snapshot()
+        out = alg3(eng, ca, cb)
+        d = eng.meter_snapshot().delta_since(before)
+        data[f"a3_{idx}_shape"] = np.array([m, n, p, slots])
+        data[f"a3_{idx}_a"], data[f"a3_{idx}_b"] = a, b
+        data[f"a3_{idx}_out"] = out.decode(eng)
+        data[f"a3_{idx}_meter"] = meter_tuple(d)
+        data[f"a3_{idx}_depth"] = np.array([out.ct.depth])
     np.savez_compressed(OUT, **data)
     print(f"wrote {OUT} ({len(data)} arrays)")
 
