@@ -306,7 +306,7 @@ def run_ours(args, ws, rank, local):
         cfg5["cfg5b"] = bench_cfg5b(ws, rank, local, max_over_ranks, barrier)
     if not args.no_extra and rank == 0:
         extra["ntt"] = bench_ntt(eng, peak)
-        extra["configs"] = {"cfg1": bench_cfg1(), "cfg3": bench_cfg3(), "cfg4": bench_cfg4(steps=3), **cfg5}
+        extra["configs"] = {"cfg1": bench_cfg1(), "cfg2_alg3": bench_cfg2_alg3(), "cfg3": bench_cfg3(), "cfg4": bench_cfg4(steps=3), **cfg5}
     line = None
     if rank == 0:
         cpu = None
@@ -364,6 +364,41 @@ def bench_cfg1(steps=50):
     torch.cuda.synchronize()
     t = st.elapsed_time(en) / 1e3 / steps
     return {"metric": "HE matmul/s (cfg1 8x8, N=2^13)", "value": 1.0 / t, "ms_per_matmul": t * 1e3, "max_abs_err": err}
+
+
+def bench_cfg2_alg3(steps=5):
+    """Config 2, Algorithm 3 (revolver matmul, the rotation-heavy single-ciphertext product):
+    A, B 64x64 padded to row width 128 so the 64x128 layout fills 8192 slots (fast path,
+    depth 3).  64 hoisted rotations of B, 64 products, 64 x 14 cascade rotations, 128 cmuls."""
+    import torch
+
+    from paper_2512_18646_b200 import CkksEngine, config_params, encode_revolver, encode_row_major, matmul
+    from tools.workloads import cfg_matmul
+
+    a, b = cfg_matmul(2)
+    eng = CkksEngine(config_params(2))
+    ap = np.zeros((64, 128))
+    ap[:, :64] = a
+    bp = np.zeros((128, 64))
+    bp[:64] = b
+    ca, cb = encode_row_major(eng, ap), encode_revolver(eng, bp, target_m=64)
+    err = float(np.max(np.abs(matmul(eng, ca, cb).decode(eng)[:, :64] - a @ b)))
+    for _ in range(2):
+        matmul(eng, ca, cb)
+    before = eng.meter_snapshot()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    st.record(eng._stream)
+    for _ in range(steps):
+        matmul(eng, ca, cb)
+    en.record(eng._stream)
+    torch.cuda.synchronize()
+    t = st.elapsed_time(en) / 1e3 / steps
+    d = eng.meter_snapshot().delta_since(before)
+    return {"metric": "HE matmul/s (cfg2 Algorithm 3 revolver, 64x64 at width 128, N=2^14)", "value": 1.0 / t,
+            "ms_per_matmul": t * 1e3, "max_abs_err": err,
+            "ops_per_matmul": {"rot": d.rot_count // steps, "mul": d.mul_count // steps, "cmul": d.cmul_count // steps,
+                               "add": d.add_count // steps}}
 
 
 def bench_cfg4(steps=2):
