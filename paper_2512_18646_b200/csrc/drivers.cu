@@ -31,6 +31,8 @@ template <int FG>
 __global__ void __launch_bounds__(128) k_conv_mac(const uint64_t *const *T, const int *cols, int nout, int C, int W, int k,
                                                   int F, const uint64_t *wq, const uint64_t *bq, const uint64_t *mask, int nl,
                                                   int N, DevPrimes pr, uint64_t *Yp) {
+    pdl_wait();
+    pdl_trigger();
     const int kk = blockIdx.x * blockDim.x + threadIdx.x;
     if (kk >= N) return;
     const int poly = blockIdx.y / nl, i = blockIdx.y - poly * nl;
@@ -81,6 +83,8 @@ template <int FG>
 __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T, const int *cols, int nout, int C, int W,
                                                         int k, int F, const uint32_t *wb, uint64_t bb_pow, const uint64_t *bq,
                                                         const uint64_t *mask, int nl, int N, DevPrimes pr, uint64_t *Yp) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) uint64_t smc[];
     const int taps = C * k * k;
     const uint64_t **sptr = (const uint64_t **)smc;
@@ -164,6 +168,8 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
 template <int UG>
 __global__ void __launch_bounds__(128) k_pt_matvec(const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int nl,
                                                    int N, DevPrimes pr, uint64_t *Yp) {
+    pdl_wait();
+    pdl_trigger();
     const int kk = blockIdx.x * blockDim.x + threadIdx.x;
     if (kk >= N) return;
     const int i = blockIdx.y;
@@ -330,18 +336,18 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
             const uint64_t bpow = uint64_t(1) << bb;
             dim3 gs(nblocks(N / 2, 128), 2 * nl, (unsigned)no * (F / FG));
             switch (FG) {
-                case 8: k_conv_mac_small<8><<<gs, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-                case 4: k_conv_mac_small<4><<<gs, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-                case 2: k_conv_mac_small<2><<<gs, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-                default: k_conv_mac_small<1><<<gs, 128, sm, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                case 8: launch_pdl(k_conv_mac_small<8>, dim3(gs), dim3(128), sm, c.stream, tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                case 4: launch_pdl(k_conv_mac_small<4>, dim3(gs), dim3(128), sm, c.stream, tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                case 2: launch_pdl(k_conv_mac_small<2>, dim3(gs), dim3(128), sm, c.stream, tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+                default: launch_pdl(k_conv_mac_small<1>, dim3(gs), dim3(128), sm, c.stream, tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
             }
             check_launch("k_conv_mac_small");
         } else {
         switch (FG) {
-            case 8: k_conv_mac<8><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-            case 4: k_conv_mac<4><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-            case 2: k_conv_mac<2><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
-            default: k_conv_mac<1><<<grid, 128, 0, c.stream>>>(tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+            case 8: launch_pdl(k_conv_mac<8>, dim3(grid), dim3(128), 0, c.stream, tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+            case 4: launch_pdl(k_conv_mac<4>, dim3(grid), dim3(128), 0, c.stream, tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+            case 2: launch_pdl(k_conv_mac<2>, dim3(grid), dim3(128), 0, c.stream, tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
+            default: launch_pdl(k_conv_mac<1>, dim3(grid), dim3(128), 0, c.stream, tt.c_(), colp, no, C, W, k, F, dwq.get(), dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
         }
         check_launch("k_conv_mac");
         }
@@ -408,7 +414,7 @@ void pt_matvec(Ctx &c, const uint64_t *const *X, int nx, const uint64_t *const *
     for (int u0 = 0; u0 < ny; u0 += chunk) {
         const int nu = std::min(chunk, ny - u0);
         dim3 grid(nblocks(N, 128), nl, (nu + UG - 1) / UG);
-        k_pt_matvec<UG><<<grid, 128, 0, c.stream>>>(X, nx, PT + (size_t)u0 * nx, nu, nl, N, c.primes, yp.as<uint64_t>());
+        launch_pdl(k_pt_matvec<UG>, dim3(grid), dim3(128), 0, c.stream, X, nx, PT + (size_t)u0 * nx, nu, nl, N, c.primes, yp.as<uint64_t>());
         check_launch("k_pt_matvec");
         std::vector<const uint64_t *> ins(nu);
         for (int u = 0; u < nu; u++) ins[u] = yp.as<uint64_t>() + (size_t)u * ctw;

@@ -171,6 +171,8 @@ struct EncNoise {
 template <int CL>
 __global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr, const double *zi, const double2 *tw,
                          const int *pos_slot, EncNoise nz, int64_t *m) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ double fft_sm[];
     __shared__ uint64_t cdt_s[CDT_LEN];
     const int C = S / CL, rank = (int)(blockIdx.x % CL), base = rank * C;
@@ -210,6 +212,8 @@ __global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr
 template <int CL>
 __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS, const double *zr, const double *zi,
                          const double2 *tw, const int *slot_pos, double *out) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ double fft_sm[];
     const int C = S / CL, rank = (int)(blockIdx.x % CL), base = rank * C;
     const int c = blockIdx.x / CL;
@@ -242,6 +246,8 @@ __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS
 
 // m [count][N] (int64) -> residues [count][nl][N] (coefficient domain)
 __global__ void k_reduce_coeffs(const int64_t *m, int count, int nl, int N, DevPrimes pr, uint64_t *out) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (long long)count * nl * N) return;
     const int k = (int)(e % N);
@@ -255,6 +261,8 @@ __global__ void k_reduce_coeffs(const int64_t *m, int count, int nl, int N, DevP
 // secret-key encryption:          buf [count][2][nl][N] = (m + e, a (already NTT))
 __global__ void k_enc_sample(const int64_t *m, int count, int nl, int N, uint64_t seed, uint64_t nonce0, int sym,
                              const uint64_t *cdt, DevPrimes pr, uint64_t *buf) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (long long)count * N) return;
     const long long c = e / N;
@@ -282,6 +290,8 @@ __global__ void k_enc_sample(const int64_t *m, int count, int nl, int N, uint64_
 // combine NTT'd samples into ciphertexts out [count][2][nl][N]
 __global__ void k_enc_combine(const uint64_t *buf, int count, int nl, int N, int Ltop, int sym, const uint64_t *pk,
                               const uint64_t *s_ntt, DevPrimes pr, uint64_t *out) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (long long)count * nl * N) return;
     const int k = (int)(e % N);
@@ -307,6 +317,8 @@ __global__ void k_enc_combine(const uint64_t *buf, int count, int nl, int N, int
 // x[c][k] = c0 + c1 s (+ c2 s^2) on limb q0 (NTT domain)
 __global__ void k_dec_limb0(const uint64_t *const *C, const int *degs, const int *levels, int count, int N,
                             const uint64_t *s_ntt, DevPrimes pr, uint64_t *x) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (long long)count * N) return;
     const long long c = e / N;
@@ -321,6 +333,8 @@ __global__ void k_dec_limb0(const uint64_t *const *C, const int *degs, const int
 }
 
 __global__ void k_center(const uint64_t *x, long long total, uint64_t q, int64_t *m) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= total) return;
     const uint64_t v = x[e];
@@ -459,13 +473,15 @@ void launch_fft(Ctx &c, K kern, int count, int S, Args... args) {
     cfg.blockDim = dim3((unsigned)fft_threads(S));
     cfg.dynamicSmemBytes = sm;
     cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = (unsigned)cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     VR_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
@@ -493,7 +509,7 @@ void encode_plain(Ctx &c, const double *d_vals, int count, int nvals, int level,
     const int N = c.n, nl = level + 1;
     Scratch m(c, sizeof(int64_t) * count * N);
     encode_coeffs(c, d_vals, count, nvals, scale, m.as<int64_t>());
-    k_reduce_coeffs<<<nblocks((long long)count * nl * N, TB), TB, 0, c.stream>>>(m.as<int64_t>(), count, nl, N, c.primes, d_pt);
+    launch_pdl(k_reduce_coeffs, dim3(nblocks((long long)count * nl * N, TB)), dim3(TB), 0, c.stream, m.as<int64_t>(), count, nl, N, c.primes, d_pt);
     check_launch("k_reduce_coeffs");
     ntt_forward(c, batch_limbs(d_pt, count, nl, N));
 }
@@ -521,7 +537,7 @@ void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long lon
     encode_src(c, vs, count, scale, m.as<int64_t>());
     const int rows = c.sym_enc ? 2 : 3;
     Scratch buf(c, sizeof(uint64_t) * count * rows * nl * N);
-    k_enc_sample<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(m.as<int64_t>(), count, nl, N, c.seed, nonce0,
+    launch_pdl(k_enc_sample, dim3(nblocks((long long)count * N, TB)), dim3(TB), 0, c.stream, m.as<int64_t>(), count, nl, N, c.seed, nonce0,
                                                                          c.sym_enc, c.cdt, c.primes, buf.as<uint64_t>());
     check_launch("k_enc_sample");
     if (c.sym_enc) {
@@ -530,7 +546,7 @@ void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long lon
     } else {
         ntt_forward(c, batch_limbs(buf.as<uint64_t>(), count * 3, nl, N));
     }
-    k_enc_combine<<<nblocks((long long)count * nl * N, TB), TB, 0, c.stream>>>(buf.as<uint64_t>(), count, nl, N, c.L,
+    launch_pdl(k_enc_combine, dim3(nblocks((long long)count * nl * N, TB)), dim3(TB), 0, c.stream, buf.as<uint64_t>(), count, nl, N, c.L,
                                                                                c.sym_enc, c.pk, c.s_ntt, c.primes, d_ct);
     check_launch("k_enc_combine");
 }
@@ -539,12 +555,12 @@ void decrypt_decode(Ctx &c, const uint64_t *const *d_cts, const int *d_degs, con
                     int count, double *d_out, int64_t *d_coeffs_out) {
     const int N = c.n, S = c.slots;
     Scratch x(c, sizeof(uint64_t) * count * N), m(c, sizeof(int64_t) * count * N);
-    k_dec_limb0<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(d_cts, d_degs, d_levels, count, N, c.s_ntt, c.primes,
+    launch_pdl(k_dec_limb0, dim3(nblocks((long long)count * N, TB)), dim3(TB), 0, c.stream, d_cts, d_degs, d_levels, count, N, c.s_ntt, c.primes,
                                                                         x.as<uint64_t>());
     check_launch("k_dec_limb0");
     ntt_inverse(c, NttBatch{x.as<uint64_t>(), count, 1, (long long)N, 1, 0, 0, 0});
     int64_t *mp = d_coeffs_out ? d_coeffs_out : m.as<int64_t>();
-    k_center<<<nblocks((long long)count * N, TB), TB, 0, c.stream>>>(x.as<uint64_t>(), (long long)count * N, c.q[0], mp);
+    launch_pdl(k_center, dim3(nblocks((long long)count * N, TB)), dim3(TB), 0, c.stream, x.as<uint64_t>(), (long long)count * N, c.q[0], mp);
     check_launch("k_center");
     if (!d_out) return;
     const double2 *tw = reinterpret_cast<const double2 *>(c.ftw);

@@ -49,6 +49,8 @@ template <int KS_MAXD, int KS_CG>
 __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint64_t *const *P, long long poly_off, int count,
                                                   int level, int N, int logN, int np, const uint64_t *key, uint32_t g,
                                                   DevPrimes pr, uint64_t *A) {
+    pdl_wait();
+    pdl_trigger();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int nl = level + 1, nt = level + 2;
     if (e >= (long long)nt * N) return;
@@ -192,12 +194,14 @@ static void launch_ks_inner_cg(Ctx &c, const uint64_t *D, const uint64_t *const 
     const int N = c.n, nl = level + 1, nt = level + 2;
     const dim3 blocks(nblocks((long long)nt * N, 128), (count + CG - 1) / CG);
     if (nl <= 8)
-        k_ks_inner<8, CG><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
+        launch_pdl(k_ks_inner<8, CG>, blocks, dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g,
+                   c.primes, A);
     else if (nl <= 16)
-        k_ks_inner<16, CG><<<blocks, 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g, c.primes, A);
+        launch_pdl(k_ks_inner<16, CG>, blocks, dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N, c.log_n, c.np, key,
+                   g, c.primes, A);
     else
-        k_ks_inner<40, 1><<<dim3(blocks.x, count), 128, 0, c.stream>>>(D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g,
-                                                                         c.primes, A);
+        launch_pdl(k_ks_inner<40, 1>, dim3(blocks.x, count), dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N,
+                   c.log_n, c.np, key, g, c.primes, A);
     check_launch("k_ks_inner");
 }
 

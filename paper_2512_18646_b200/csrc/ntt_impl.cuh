@@ -200,6 +200,8 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
     const int t = blockIdx.x / chunks, chunk = blockIdx.x - t * chunks;
     uint64_t *ptr;
     int pidx;
+    pdl_wait();
+    pdl_trigger();
     if (!locate(b, t, N, ptr, pidx)) return;
     const uint64_t q = pr.m[pidx].q;
     const ulonglong2 *W = tw + (size_t)pidx * N;
@@ -331,8 +333,8 @@ void launch_pass(Ctx &c, const NttBatch &b, const PassArgs &a, const LD &ld, con
     const int threads = a.TPC * (T >> LE);
     const size_t smem = (size_t)a.TPC * T * sizeof(uint64_t);
     const unsigned blocks = (unsigned)b.count * chunks;
-    ntt_pass<INV, COLS, LOGT, LE, LD, ST><<<blocks, threads, smem, c.stream>>>(b, a, c.primes, INV ? c.itw2 : c.tw2,
-                                                                               c.ntt_const, ld, st);
+    launch_pdl(ntt_pass<INV, COLS, LOGT, LE, LD, ST>, dim3(blocks), dim3(threads), smem, c.stream, b, a, c.primes,
+               (const ulonglong2 *)(INV ? c.itw2 : c.tw2), (const NttConst *)c.ntt_const, ld, st);
     check_launch("ntt_pass");
 }
 

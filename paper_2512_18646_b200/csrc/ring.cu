@@ -38,6 +38,8 @@ __device__ __forceinline__ bool decompose(long long pair, int polys, int nl, int
 
 __global__ void k_binop(const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *O, int count, int polys,
                         int nl, int N, int op, DevPrimes pr) {
+    pdl_wait();
+    pdl_trigger();
     const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= (long long)count * polys * nl * (N / 2)) return;
     Idx x;
@@ -53,6 +55,8 @@ __global__ void k_binop(const uint64_t *const *A, const uint64_t *const *B, uint
 
 __global__ void k_tensor(const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *O, int count, int nl, int N,
                          DevPrimes pr) {
+    pdl_wait();
+    pdl_trigger();
     const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= (long long)count * nl * (N / 2)) return;
     Idx x;
@@ -73,6 +77,8 @@ __global__ void k_tensor(const uint64_t *const *A, const uint64_t *const *B, uin
 // out[ct][p][i] = ct[p][i] * pt[ct or shared][i]
 __global__ void k_mul_plain(const uint64_t *const *C, const uint64_t *const *P, uint64_t *const *O, int count, int polys,
                             int nl, int N, int shared_pt, DevPrimes pr) {
+    pdl_wait();
+    pdl_trigger();
     const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= (long long)count * polys * nl * (N / 2)) return;
     Idx x;
@@ -85,6 +91,8 @@ __global__ void k_mul_plain(const uint64_t *const *C, const uint64_t *const *P, 
 
 __global__ void k_mul_scalar(const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, int N,
                              LimbScalars s, DevPrimes pr) {
+    pdl_wait();
+    pdl_trigger();
     const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= (long long)count * polys * nl * (N / 2)) return;
     Idx x;
@@ -98,6 +106,8 @@ __global__ void k_mul_scalar(const uint64_t *const *C, uint64_t *const *O, int c
 // O[c][p][i] += B[c][p][i] * s_i  where B has nlb >= nl limbs per poly (level-dropped read)
 __global__ void k_axpy(uint64_t *const *O, const uint64_t *const *B, int count, int polys, int nl, int nlb, int N,
                        LimbScalars s, DevPrimes pr) {
+    pdl_wait();
+    pdl_trigger();
     const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= (long long)count * polys * nl * (N / 2)) return;
     Idx x;
@@ -110,6 +120,8 @@ __global__ void k_axpy(uint64_t *const *O, const uint64_t *const *B, int count, 
 }
 
 __global__ void k_add_const(uint64_t *const *C, int count, int nl, int N, LimbScalars s, DevPrimes pr) {
+    pdl_wait();
+    pdl_trigger();
     const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= (long long)count * nl * (N / 2)) return;
     Idx x;
@@ -128,6 +140,8 @@ __device__ __forceinline__ int galois_src(int k, uint32_t g, int logN) {
 }
 
 __global__ void k_permute(const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, int logN, uint32_t g) {
+    pdl_wait();
+    pdl_trigger();
     const int N = 1 << logN;
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (long long)count * polys * nl * N) return;
@@ -140,6 +154,8 @@ __global__ void k_permute(const uint64_t *const *C, uint64_t *const *O, int coun
 
 __global__ void k_copy_limbs(const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl_in, int nl_out,
                              int limb0, int N) {
+    pdl_wait();
+    pdl_trigger();
     const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= (long long)count * polys * nl_out * (N / 2)) return;
     Idx x;
@@ -149,6 +165,8 @@ __global__ void k_copy_limbs(const uint64_t *const *C, uint64_t *const *O, int c
 }
 
 __global__ void k_mod_fixup(uint64_t *data, long long count_polys, int nl, int N, DevPrimes pr) {
+    pdl_wait();
+    pdl_trigger();
     const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= count_polys * nl * (N / 2)) return;
     Idx x;
@@ -206,6 +224,8 @@ __host__ __device__ constexpr int ts_stages() {
 template <int NB, int TS_TILE, int TS_SPLIT, int MAXST, int MODE>
 __global__ void __launch_bounds__(TS_TILE / 2 + 32)
     k_tensor_sum(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int TS_CONSUMERS = TS_TILE / 2;  // 2 coefficients per consumer thread
     constexpr int TS_STAGES = ts_stages<NB, TS_TILE, MAXST>();
     // limb tiles per stage: L[b] poly0/poly1 ..., R poly0/poly1 (MODE 1: L[b] poly1 ..., R poly1)
@@ -398,57 +418,57 @@ LimbScalars limb_scalars(const Ctx &c, int64_t s, int nl) {
 void binop(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *O, int count, int polys, int nl, int op) {
     const long long pairs = (long long)count * polys * nl * (c.n / 2);
     if (!pairs) return;
-    k_binop<<<nblocks(pairs, TB), TB, 0, c.stream>>>(A, B, O, count, polys, nl, c.n, op, c.primes);
+    launch_pdl(k_binop, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, A, B, O, count, polys, nl, c.n, op, c.primes);
     check_launch("k_binop");
 }
 
 void tensor(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *O, int count, int nl) {
     const long long pairs = (long long)count * nl * (c.n / 2);
-    k_tensor<<<nblocks(pairs, TB), TB, 0, c.stream>>>(A, B, O, count, nl, c.n, c.primes);
+    launch_pdl(k_tensor, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, A, B, O, count, nl, c.n, c.primes);
     check_launch("k_tensor");
 }
 
 void mul_plain(Ctx &c, const uint64_t *const *C, const uint64_t *const *P, uint64_t *const *O, int count, int polys, int nl,
                int shared_pt) {
     const long long pairs = (long long)count * polys * nl * (c.n / 2);
-    k_mul_plain<<<nblocks(pairs, TB), TB, 0, c.stream>>>(C, P, O, count, polys, nl, c.n, shared_pt, c.primes);
+    launch_pdl(k_mul_plain, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, C, P, O, count, polys, nl, c.n, shared_pt, c.primes);
     check_launch("k_mul_plain");
 }
 
 void mul_scalar(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, const LimbScalars &s) {
     const long long pairs = (long long)count * polys * nl * (c.n / 2);
-    k_mul_scalar<<<nblocks(pairs, TB), TB, 0, c.stream>>>(C, O, count, polys, nl, c.n, s, c.primes);
+    launch_pdl(k_mul_scalar, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, C, O, count, polys, nl, c.n, s, c.primes);
     check_launch("k_mul_scalar");
 }
 
 void axpy(Ctx &c, uint64_t *const *O, const uint64_t *const *B, int count, int polys, int nl, int nlb, const LimbScalars &s) {
     const long long pairs = (long long)count * polys * nl * (c.n / 2);
-    k_axpy<<<nblocks(pairs, TB), TB, 0, c.stream>>>(O, B, count, polys, nl, nlb, c.n, s, c.primes);
+    launch_pdl(k_axpy, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, O, B, count, polys, nl, nlb, c.n, s, c.primes);
     check_launch("k_axpy");
 }
 
 void add_const(Ctx &c, uint64_t *const *C, int count, int nl, const LimbScalars &s) {
     const long long pairs = (long long)count * nl * (c.n / 2);
-    k_add_const<<<nblocks(pairs, TB), TB, 0, c.stream>>>(C, count, nl, c.n, s, c.primes);
+    launch_pdl(k_add_const, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, C, count, nl, c.n, s, c.primes);
     check_launch("k_add_const");
 }
 
 void permute(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, uint32_t g) {
     const long long el = (long long)count * polys * nl * c.n;
-    k_permute<<<nblocks(el, TB), TB, 0, c.stream>>>(C, O, count, polys, nl, c.log_n, g);
+    launch_pdl(k_permute, dim3(nblocks(el, TB)), dim3(TB), 0, c.stream, C, O, count, polys, nl, c.log_n, g);
     check_launch("k_permute");
 }
 
 void copy_limbs(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl_in, int nl_out, int limb0) {
     const long long pairs = (long long)count * polys * nl_out * (c.n / 2);
     if (!pairs) return;
-    k_copy_limbs<<<nblocks(pairs, TB), TB, 0, c.stream>>>(C, O, count, polys, nl_in, nl_out, limb0, c.n);
+    launch_pdl(k_copy_limbs, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, C, O, count, polys, nl_in, nl_out, limb0, c.n);
     check_launch("k_copy_limbs");
 }
 
 void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl) {
     const long long pairs = count_polys * nl * (c.n / 2);
-    k_mod_fixup<<<nblocks(pairs, TB), TB, 0, c.stream>>>(data, count_polys, nl, c.n, c.primes);
+    launch_pdl(k_mod_fixup, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, data, count_polys, nl, c.n, c.primes);
     check_launch("k_mod_fixup");
 }
 
@@ -470,13 +490,15 @@ static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
     cfg.blockDim = dim3(TILE / 2 + 32, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = SPLIT;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     VR_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, n, nl, c.n, c.primes, O));
 }
 

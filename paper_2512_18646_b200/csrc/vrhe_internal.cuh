@@ -2,6 +2,8 @@
 // CUDA translation units of libvrhe.so.  Nothing here is exported; the C-ABI
 // lives in abi.cu and is declared in include/vrhe.h.
 #pragma once
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -208,6 +210,36 @@ void ntt_forward(Ctx &c, const NttBatch &b);
 void ntt_inverse(Ctx &c, const NttBatch &b);
 
 // grid helper
+// Programmatic dependent launch (sm_90+).  A kernel started through launch_pdl may become
+// resident while its predecessor on the stream is still draining; it must execute pdl_wait()
+// (griddepcontrol.wait: full completion + visibility of the predecessor grid) before touching
+// global memory.  pdl_trigger() lets the successor launch early.  VR_PDL=0 disables the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("VR_PDL");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    VR_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 inline unsigned nblocks(long long work, int per_block) { return (unsigned)((work + per_block - 1) / per_block); }
 
 }  // namespace vr
