@@ -268,6 +268,13 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         VR_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
         VR_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
         VR_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+        {
+            int least = 0, greatest = 0;
+            VR_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            VR_CUDA(cudaStreamCreateWithPriority(&c.hi, cudaStreamNonBlocking, greatest));
+        }
+        VR_CUDA(cudaEventCreateWithFlags(&c.ev_hi, cudaEventDisableTiming));
+        VR_CUDA(cudaEventCreateWithFlags(&c.ev_hi_done, cudaEventDisableTiming));
         VR_CUDA(cudaMallocHost((void **)&c.stage, (size_t)vr::Ctx::kStageSlots * vr::Ctx::kStageBytes));
         for (int i = 0; i < vr::Ctx::kStageSlots; i++)
             VR_CUDA(cudaEventCreateWithFlags(&c.stage_evt[i], cudaEventDisableTiming));
@@ -303,6 +310,9 @@ int vr_ctx_destroy(vr_ctx *h) {
         if (c.arena) cudaFree(c.arena);
         if (c.ev_fork) cudaEventDestroy(c.ev_fork);
         if (c.ev_join) cudaEventDestroy(c.ev_join);
+        if (c.ev_hi) cudaEventDestroy(c.ev_hi);
+        if (c.ev_hi_done) cudaEventDestroy(c.ev_hi_done);
+        if (c.hi) cudaStreamDestroy(c.hi);
         for (auto &b : c.big_free) cudaFree(b.second);
         for (int i = 0; i < vr::Ctx::kStageSlots; i++)
             if (c.stage_evt[i]) cudaEventDestroy(c.stage_evt[i]);

@@ -221,16 +221,33 @@ void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, in
     Scratch d3(c, sizeof(uint64_t) * nb * 3 * nl * N);
     PtrTable td(c, strided(d3.as<uint64_t>(), nb, (size_t)3 * nl * N));
     if (nb == 1 && n >= 8) {
-        // overlap: d2 = sum L1 R1 first (half the operand bytes) so the key switch starts early,
-        // while (d0, d1) accumulate on the auxiliary stream; the final combine waits for them.
+        // overlap: d2 = sum L1 R1 (half the operand bytes) feeds the key switch, while (d0, d1)
+        // accumulate on the auxiliary stream; the final combine waits for them.  Order 1 (default)
+        // runs d2 alone at full bandwidth and forks (d0, d1) behind it, under the key switch.
+        static const int order = [] {
+            const char *e = getenv("VR_MM_ORDER");
+            return e ? atoi(e) : 0;
+        }();
+        cudaStream_t main = c.stream;
+        if (order == 1) tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
         VR_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         VR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
-        cudaStream_t main = c.stream;
         c.stream = c.aux;
         tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 2);
         VR_CUDA(cudaEventRecord(c.ev_join, c.aux));
         c.stream = main;
-        tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
+        if (order != 1) tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
+        if (order >= 2) {
+            // the latency-bound key-switch chain on the highest-priority stream
+            VR_CUDA(cudaEventRecord(c.ev_hi, main));
+            VR_CUDA(cudaStreamWaitEvent(c.hi, c.ev_hi, 0));
+            c.stream = c.hi;
+            relin_rescale_batch(c, td.c_(), Out, nb, level, c.ev_join);
+            VR_CUDA(cudaEventRecord(c.ev_hi_done, c.hi));
+            c.stream = main;
+            VR_CUDA(cudaStreamWaitEvent(main, c.ev_hi_done, 0));
+            return;
+        }
         relin_rescale_batch(c, td.c_(), Out, nb, level, c.ev_join);
         return;
     }

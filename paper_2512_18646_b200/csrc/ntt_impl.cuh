@@ -26,6 +26,8 @@
 #include <cstdlib>
 #include "vrhe_internal.cuh"
 
+#include <cooperative_groups.h>
+
 namespace vr {
 namespace nttk {
 
@@ -370,9 +372,168 @@ inline int pick_tpc(int count, int tiles_per_tf, int T, int max_tpc, int min_tpc
     return tpc;
 }
 
+// ---- one-kernel transform: a cluster of 8 CTAs per transform ------------------------------
+// CTA r of the cluster owns the contiguous chunk [r C, (r+1) C), C = N / 8, in shared memory.
+// Forward: the first three stages (distances N/2, N/4, N/8) pair elements {j + u C : u < 8}
+// across the cluster: thread j of CTA r loads that column straight from global memory (through
+// the Load functor), runs the three stages in registers and scatters element u into CTA u's
+// shared memory (DSMEM).  The remaining log2(C) stages stay inside each chunk (radix-8 groups,
+// exactly the rows pass of ntt_pass with s0 = 3), and the chunk leaves through the Store functor.
+// Inverse: the local Gentleman-Sande stages first (input through the Load functor), then the
+// last three stages gather each column from the eight CTAs.  One launch and one global round
+// trip per transform instead of two.
+__device__ __forceinline__ int sidx_row(int L) { return L ^ ((L >> 4) & 15); }
+
+template <bool INV, int LOGC, class LD, class ST>
+__global__ void __launch_bounds__((1 << LOGC) / 8) ntt_cl8(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *__restrict__ tw,
+                                                const NttConst *__restrict__ ncs, LD ld, ST st) {
+    namespace cg = cooperative_groups;
+    extern __shared__ uint64_t sm[];
+    constexpr int LE = 3, EPT = 8, C = 1 << LOGC, NG = (LOGC + LE - 1) / LE;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int r = (int)cluster.block_rank(), t = blockIdx.x >> 3, sub = threadIdx.x;
+    const int N = 1 << logN;
+    pdl_wait();
+    pdl_trigger();
+    uint64_t *ptr;
+    int pidx;
+    if (!locate(b, t, N, ptr, pidx)) return;  // uniform over the cluster (same transform)
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    const uint64_t q = pr.m[pidx].q, q2 = 2 * q;
+    const ulonglong2 *W = tw + (size_t)pidx * N;
+    const NttConst nc = ncs[pidx];
+    const int col = r * (C / 8) + sub;  // this thread's cross-cluster column
+    uint64_t x[EPT];
+    int base[EPT];
+
+    auto local_stages = [&](bool from_global) {
+#pragma unroll
+        for (int step = 0; step < NG; step++) {
+            const int gi = INV ? NG - 1 - step : step;
+            const int s = LE * gi, R = (LOGC - s) < LE ? (LOGC - s) : LE;
+            const int logd = LOGC - s - R, d = 1 << logd, E2 = 1 << R;
+#pragma unroll
+            for (int v = 0; v < EPT; v++) {
+                const int uid = sub * (EPT >> R) + v;
+                base[v] = v < (EPT >> R) ? (((uid >> logd) << (logd + R)) | (uid & (d - 1))) : 0;
+            }
+#pragma unroll
+            for (int e = 0; e < EPT; e++) {
+                const int L = base[e >> R] + (e & (E2 - 1)) * d;
+                x[e] = (from_global && step == 0) ? ld(ptr, t, (long long)r * C + L, pr, pidx) : sm[sidx_row(L)];
+            }
+            if (R == 3) group_compute<INV, 3, EPT>(x, base, d, s, LOGC, 3, r, q, W, nc);
+            else if (R == 2) group_compute<INV, 2, EPT>(x, base, d, s, LOGC, 3, r, q, W, nc);
+            else group_compute<INV, 1, EPT>(x, base, d, s, LOGC, 3, r, q, W, nc);
+            if (!INV && step == NG - 1) {
+#pragma unroll
+                for (int e = 0; e < EPT; e++) {
+                    uint64_t v = x[e] >= q2 ? x[e] - q2 : x[e];
+                    x[e] = v >= q ? v - q : v;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < EPT; e++) sm[sidx_row(base[e >> R] + (e & (E2 - 1)) * d)] = x[e];
+            __syncthreads();
+        }
+    };
+    const int zero_base[EPT] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+    if (!INV) {
+#pragma unroll
+        for (int u = 0; u < 8; u++) x[u] = ld(ptr, t, (long long)col + ((long long)u << LOGC), pr, pidx);
+        group_compute<false, 3, EPT>(x, zero_base, 1, 0, 3, 0, 0, q, W, nc);
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer is resident
+#pragma unroll
+        for (int u = 0; u < 8; u++) cluster.map_shared_rank(sm, u)[sidx_row(col)] = x[u];
+        cluster.sync();
+        local_stages(false);
+        // coalesced store of the chunk through the Store functor (prefetch its loads first)
+        typename ST::Pre pre[EPT];
+#pragma unroll
+        for (int k = 0; k < EPT; k++) pre[k] = st.prefetch(t, (long long)r * C + sub + k * (C / 8), pr, pidx);
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int mid = sub + k * (C / 8);
+            st.finish(ptr, t, (long long)r * C + mid, sm[sidx_row(mid)], pre[k], pr, pidx);
+        }
+    } else {
+        local_stages(true);
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+        cluster.sync();
+#pragma unroll
+        for (int u = 0; u < 8; u++) x[u] = cluster.map_shared_rank(sm, u)[sidx_row(col)];
+        group_compute<true, 3, EPT>(x, zero_base, 1, 0, 3, 0, 0, q, W, nc);
+        typename ST::Pre pre[EPT];
+#pragma unroll
+        for (int u = 0; u < 8; u++) pre[u] = st.prefetch(t, (long long)col + ((long long)u << LOGC), pr, pidx);
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const uint64_t v = x[u] >= q ? x[u] - q : x[u];
+            st.finish(ptr, t, (long long)col + ((long long)u << LOGC), v, pre[u], pr, pidx);
+        }
+        cluster.sync();  // peers keep their shared memory until every gather has finished
+    }
+}
+
+template <bool INV, int LOGC, class LD, class ST>
+void launch_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
+    constexpr int C = 1 << LOGC;
+    const size_t smem = (size_t)C * sizeof(uint64_t);
+    auto kern = ntt_cl8<INV, LOGC, LD, ST>;
+    static bool configured = false;
+    if (!configured && smem > 48 * 1024) {
+        VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)b.count * 8);
+    cfg.blockDim = dim3(C / 8);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 8;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    VR_CUDA(cudaLaunchKernelEx(&cfg, kern, b, c.log_n, c.primes, (const ulonglong2 *)(INV ? c.itw2 : c.tw2),
+                               (const NttConst *)c.ntt_const, ld, st));
+    check_launch("ntt_cl8");
+}
+
+// Policy (measured on B200, tools/cl_probe.sh): the cluster kernel beats the two passes for
+// large batches at N <= 2^14 (0.243 -> 0.226 us per 2^14 transform at 1280 transforms) but
+// not for the short latency-bound batches of a key switch (relin chain 49 -> 54 us) nor at
+// N = 2^15 (512-thread CTAs at 80 registers: one CTA per SM).  VR_NTT_CL = minimum batch
+// (default 256; 0 disables).
+inline int ntt_cl_min() {
+    static const int v = [] {
+        const char *e = getenv("VR_NTT_CL");
+        return e ? atoi(e) : 256;
+    }();
+    return v;
+}
+
+template <bool INV, class LD, class ST>
+bool try_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
+    const int lim = ntt_cl_min();
+    if (lim <= 0 || b.count < lim) return false;
+    switch (c.log_n) {
+        case 12: launch_cl8<INV, 9>(c, b, ld, st); return true;
+        case 13: launch_cl8<INV, 10>(c, b, ld, st); return true;
+        case 14: launch_cl8<INV, 11>(c, b, ld, st); return true;
+        default: return false;
+    }
+}
+
 template <bool INV, class LD, class ST>
 void run_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
     if (b.count <= 0) return;
+    if (try_cl8<INV>(c, b, ld, st)) return;
     const int logN = c.log_n;
     if (c.n <= 4) {
         ntt_tiny<INV><<<nblocks(b.count, 64), 64, 0, c.stream>>>(b, logN, c.primes, INV ? c.itw2 : c.tw2, c.ntt_const, ld, st);

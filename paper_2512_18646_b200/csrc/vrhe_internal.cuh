@@ -33,6 +33,8 @@ struct Ctx {
     cudaStream_t stream = 0;
     cudaStream_t aux = 0;                    // second stream for intra-driver overlap
     cudaEvent_t ev_fork = 0, ev_join = 0;    // fork/join events (timing disabled)
+    cudaStream_t hi = 0;                     // highest-priority stream for latency-bound chains
+    cudaEvent_t ev_hi = 0, ev_hi_done = 0;
     int log_n = 0, n = 0, slots = 0, L = 0, np = 0;  // np = L + 2 (ciphertext chain + special prime)
     uint64_t q[MAXP] = {0};
     DevPrimes primes;

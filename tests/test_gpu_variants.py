@@ -1,0 +1,28 @@
+"""The parity suite rerun under the library's alternative code paths (each is selected once per
+process from the environment, so every variant runs in its own interpreter):
+
+* VR_NTT_CL=1  -- every NTT through the one-kernel 8-CTA cluster transform (default: batches >= 256)
+* VR_PDL=0     -- plain stream ordering instead of programmatic dependent launch
+* VR_MM_ORDER=2 -- matmul_outer's key-switch chain on the high-priority stream
+"""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.parametrize("env", [{"VR_NTT_CL": "1"}, {"VR_PDL": "0"}, {"VR_MM_ORDER": "2", "VR_NTT_CL": "1"}],
+                         ids=["cluster-ntt", "no-pdl", "hi-prio-chain"])
+def test_parity_suite_under_variant(env):
+    pytest.importorskip("torch").cuda.is_available() or pytest.skip("no CUDA device")
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_parity.py", "tests/test_gpu_configs.py", "tests/test_gpu_alg3.py"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
