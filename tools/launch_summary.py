@@ -15,6 +15,12 @@ def load(path, limit=None):
 
 def family(name):
     n = name.split('(')[0].replace('void ', '')
+    if 'ntt_cl8' in name:
+        import re
+        m = re.search(r'ntt_cl8<(\d), (\d+), ([^,]+), (.+)>\(', name)
+        if m:
+            return f"ntt_cl8 inv={m.group(1)} logC={m.group(2)} {m.group(3).split('::')[-1]}/{m.group(4).split('::')[-1]}"
+        return 'ntt_cl8'
     for k in ('ntt_pass', 'k_tensor_sum', 'k_conv_mac', 'k_ks_inner', 'k_tensor', 'k_binop', 'k_mul_scalar', 'k_add_const',
               'k_copy_limbs', 'k_encode', 'k_decode', 'k_enc', 'k_mul_plain'):
         if k in n:
