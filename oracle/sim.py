@@ -211,6 +211,36 @@ def oracle_poly(x, coeffs):  # oracle.py:52-56
     return c0 + c1 * x + c2 * x * x + c3 * x * x * x
 
 
+def oracle_flatten(maps):  # oracle.py:59-61
+    return np.concatenate([np.asarray(m, dtype=np.float64).reshape(-1) for m in maps])
+
+
+def oracle_forward(weights, images):  # oracle.py:64-82
+    """Plaintext conv -> act -> flatten -> fc -> act -> fc of the Table-1 CNN."""
+    images = np.asarray(images, dtype=np.float64)
+    out = []
+    for img in images:
+        maps = [oracle_poly(conv_fast(img[None], k.weights, k.bias)[0], weights.act1) for k in weights.conv_kernels]
+        h1 = oracle_poly(np.asarray(weights.fc1_weight) @ oracle_flatten(maps) + weights.fc1_bias, weights.act2)
+        out.append(np.asarray(weights.fc2_weight) @ h1 + weights.fc2_bias)
+    return np.stack(out)
+
+
+def table1_weights(seed: int):
+    """Seeded Table-1 model in the reference suite's distribution (test_pipeline.py:32-46);
+    returns plain arrays: (kernels [4][3][3], kernel biases [4], fc1_w, fc1_b, fc2_w, fc2_b)."""
+    rng = np.random.default_rng(seed)
+    kw, kb = [], []
+    for _ in range(4):
+        kw.append(rng.uniform(-0.4, 0.4, size=(3, 3)))
+        kb.append(float(rng.uniform(-0.1, 0.1)))
+    fc1_w = rng.uniform(-0.05, 0.05, size=(64, 2704))
+    fc1_b = rng.uniform(-0.1, 0.1, size=64)
+    fc2_w = rng.uniform(-0.3, 0.3, size=(10, 64))
+    fc2_b = rng.uniform(-0.1, 0.1, size=10)
+    return np.array(kw), np.array(kb), fc1_w, fc1_b, fc2_w, fc2_b
+
+
 def conv_fast(images, weights, bias=0.0):
     """Vectorised valid conv for large fixtures (same values as oracle_conv up to fp reassociation)."""
     images = np.asarray(images, dtype=np.float64)

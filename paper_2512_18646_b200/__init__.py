@@ -38,6 +38,24 @@ from .multicipher import (
     pad_images,
     reassemble_columns,
 )
-from .pipeline import activation_constants, poly_activation, poly_activation_batch
+from .conv import ImageShape, KernelSpan, build_offset_filter, conv, kernel_spanner, sum_for_conv
+from .virtual import VirtualLayout, batched_conv, reform, tile_kernel_span, vadd, vmul, vrot
+from .pipeline import (
+    PIPELINE_DEPTH,
+    BatchPlan,
+    ChunkedDataset,
+    EncodedModel,
+    ModelWeights,
+    activation_constants,
+    argmax_decide,
+    encode_model,
+    fc_layer,
+    flatten_maps,
+    forward,
+    forward_encoded,
+    pack_batch,
+    poly_activation,
+    poly_activation_batch,
+)
 
 __version__ = "0.1.0"

@@ -115,6 +115,78 @@ def main():
         data[f"a3_{idx}_out"] = out.decode(eng)
         data[f"a3_{idx}_meter"] = meter_tuple(d)
         data[f"a3_{idx}_depth"] = np.array([out.ct.depth])
+    # conv.py / virtual.py / pipeline.py (the dataset-layout CNN); own generator
+    from packedhe.conv import ImageShape, conv, kernel_spanner
+    from packedhe.encoding import encode_db
+    from packedhe.pipeline import ModelWeights, conv_layer, encode_model, fc_layer, flatten_maps, forward_encoded, pack_batch
+    from packedhe.virtual import VirtualLayout, batched_conv, reform, tile_kernel_span, vrot
+
+    rc = np.random.default_rng(0xC0DE)
+    for idx, (h, w, k) in enumerate([(4, 4, 2), (6, 6, 3), (5, 7, 2), (8, 8, 3)]):
+        img = rc.integers(-3, 5, size=(h, w)).astype(float)
+        kw = rc.integers(-3, 4, size=(k, k)).astype(float)
+        bias = float(rc.integers(-2, 3)) / 2
+        slots = max(2, 1 << (h * w - 1).bit_length())
+        eng = SlotEngine(EngineParams(slots=slots))
+        span = kernel_spanner(eng, Kernel(kw, bias=bias), ImageShape(h, w))
+        ct = eng.enc(img.reshape(-1))
+        before = eng.meter_snapshot()
+        out = conv(eng, ct, span, ImageShape(h, w))
+        d = eng.meter_snapshot().delta_since(before)
+        data[f"cs{idx}_img"], data[f"cs{idx}_w"], data[f"cs{idx}_bias"] = img, kw, np.array([bias])
+        data[f"cs{idx}_out"] = eng.dec(out)[: h * w].reshape(h, w)
+        data[f"cs{idx}_meter"] = meter_tuple(d)
+        data[f"cs{idx}_depth"] = np.array([out.depth])
+    # batched conv + reform + vrot on a 4 x 128 layout of 8x8 images
+    lay = VirtualLayout(4, 128, 8, 8)
+    imgs = rc.integers(0, 4, size=(4, 8, 8)).astype(float)
+    kw = rc.integers(-3, 4, size=(3, 3)).astype(float)
+    eng = SlotEngine(EngineParams(slots=512))
+    ct = pack_batch(eng, imgs, lay)
+    span = tile_kernel_span(eng, Kernel(kw, bias=0.25), lay)
+    before = eng.meter_snapshot()
+    out = batched_conv(eng, ct, lay, span)
+    d = eng.meter_snapshot().delta_since(before)
+    data["bc_imgs"], data["bc_w"], data["bc_out"] = imgs, kw, eng.dec(out)
+    data["bc_meter"], data["bc_depth"] = meter_tuple(d), np.array([out.depth])
+    before = eng.meter_snapshot()
+    flat, _ = reform(eng, out, lay, 6, 6)
+    d = eng.meter_snapshot().delta_since(before)
+    data["rf_out"], data["rf_meter"] = eng.dec(flat), meter_tuple(d)
+    before = eng.meter_snapshot()
+    vr = vrot(eng, ct, lay, 5)
+    d = eng.meter_snapshot().delta_since(before)
+    data["vr_out"], data["vr_meter"] = eng.dec(vr), meter_tuple(d)
+    # fc_layer: plain, and neuron blocks wider than the row count
+    for idx, (rows, width, outs, slots) in enumerate([(4, 8, 4, 32), (4, 16, 8, 64)]):
+        x = rc.integers(-4, 5, size=(rows, width)).astype(float)
+        wmat = rc.uniform(-1, 1, size=(outs, width))
+        b = rc.uniform(-1, 1, size=outs)
+        eng = SlotEngine(EngineParams(slots=slots))
+        pm = encode_db(eng, x)
+        before = eng.meter_snapshot()
+        out = fc_layer(eng, pm, wmat, b)
+        d = eng.meter_snapshot().delta_since(before)
+        data[f"fc{idx}_x"], data[f"fc{idx}_w"], data[f"fc{idx}_b"] = x, wmat, b
+        data[f"fc{idx}_out"], data[f"fc{idx}_meter"] = out.decode(eng), meter_tuple(d)
+        data[f"fc{idx}_depth"] = np.array([out.ct.depth])
+    # Table-1 forward at the paper's layout (32 images of 28x28 per 32768 slots), seeded model
+    sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+    from oracle.sim import table1_weights
+
+    act1 = (-0.00015120704, 0.4610149, 2.0225089, -1.4511951)
+    act2 = (-1.5650465, -0.9943767, 1.6794522, 0.5350255)
+    kw4, kb4, f1w, f1b, f2w, f2b = table1_weights(7)
+    weights = ModelWeights([Kernel(kw4[i], bias=float(kb4[i])) for i in range(4)], f1w, f1b, f2w, f2b, act1, act2)
+    imgs = np.random.default_rng(8).uniform(0, 1, size=(32, 28, 28))
+    eng = SlotEngine(EngineParams(slots=32768))
+    model = encode_model(eng, weights)
+    ct = pack_batch(eng, imgs)
+    sm = {}
+    scores = forward_encoded(eng, ct, model, stage_meters=sm)
+    data["t1_scores"] = scores.decode(eng)[:, :10]
+    data["t1_stage_meters"] = np.stack([meter_tuple(sm[k]) for k in ("conv", "act1", "flatten", "fc1", "act2", "fc2")])
+    data["t1_depth"] = np.array([eng.meter_snapshot().max_depth, model.ciphertext_count])
     np.savez_compressed(OUT, **data)
     print(f"wrote {OUT} ({len(data)} arrays)")
 
