@@ -306,7 +306,7 @@ def run_ours(args, ws, rank, local):
         cfg5["cfg5b"] = bench_cfg5b(ws, rank, local, max_over_ranks, barrier)
     if not args.no_extra and rank == 0:
         extra["ntt"] = bench_ntt(eng, peak)
-        extra["configs"] = {"cfg1": bench_cfg1(), "cfg2_alg3": bench_cfg2_alg3(), "cfg3": bench_cfg3(), "cfg4": bench_cfg4(steps=3), **cfg5}
+        extra["configs"] = {"cfg1": bench_cfg1(), "cfg2_alg3": bench_cfg2_alg3(), "table1_cnn": bench_table1(), "cfg3": bench_cfg3(), "cfg4": bench_cfg4(steps=3), **cfg5}
     line = None
     if rank == 0:
         cpu = None
@@ -399,6 +399,55 @@ def bench_cfg2_alg3(steps=5):
             "ms_per_matmul": t * 1e3, "max_abs_err": err,
             "ops_per_matmul": {"rot": d.rot_count // steps, "mul": d.mul_count // steps, "cmul": d.cmul_count // steps,
                                "add": d.add_count // steps}}
+
+
+def bench_table1(steps=3):
+    """The paper's Table-1 encrypted CNN (pipeline.forward_encoded): 32 MNIST-sized images per
+    32768-slot ciphertext, conv 4x3x3 -> act -> ReForm -> FC 2704->64 -> act -> FC 64->10, depth 13,
+    N = 2^16 on q0 60b + 13 x 45b + P 60b.  Model encoded once; per batch: encrypt the images,
+    forward, decode the scores.  Synthetic seeded images/weights in the reference suite's ranges."""
+    import torch
+
+    sys.path.insert(0, str(ROOT))
+    from oracle.sim import table1_weights
+    from paper_2512_18646_b200 import EngineParams, Kernel, ModelWeights, SlotEngine, encode_model, forward_encoded, pack_batch
+
+    act1 = (-0.00015120704, 0.4610149, 2.0225089, -1.4511951)
+    act2 = (-1.5650465, -0.9943767, 1.6794522, 0.5350255)
+    kw, kb, f1w, f1b, f2w, f2b = table1_weights(7)
+    weights = ModelWeights([Kernel(kw[i], bias=float(kb[i])) for i in range(4)], f1w, f1b, f2w, f2b, act1, act2)
+    imgs = np.random.default_rng(8).uniform(0, 1, size=(32, 28, 28))
+    eng = SlotEngine(EngineParams(slots=32768, prime_bits=(60,) + (45,) * 13))
+    model = encode_model(eng, weights)
+    scores = forward_encoded(eng, pack_batch(eng, imgs), model).decode(eng)[:, :10]
+    want = np.stack([weights.fc2_weight @ _t1_hidden(weights, im) + weights.fc2_bias for im in imgs])
+    err = float(np.max(np.abs(scores - want)))
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    st.record(eng._stream)
+    for _ in range(steps):
+        forward_encoded(eng, pack_batch(eng, imgs), model).decode(eng)
+    en.record(eng._stream)
+    torch.cuda.synchronize()
+    t = st.elapsed_time(en) / 1e3 / steps
+    return {"metric": "encrypted-CNN images/s (paper Table 1: 32 images x 28x28 per ciphertext, depth 13, N=2^16)",
+            "value": 32.0 / t, "s_per_batch": t, "max_abs_err": err,
+            "note": "per batch: encrypt images, forward (36 conv products, ~5.8k rotations), decode; model encoded once"}
+
+
+def _t1_hidden(weights, img):
+    def poly(x, c):
+        return c[0] + c[1] * x + c[2] * x * x + c[3] * x * x * x
+
+    maps = []
+    for kern in weights.conv_kernels:
+        k = kern.k
+        out = np.full((28 - k + 1, 28 - k + 1), float(kern.bias))
+        for p in range(k):
+            for q in range(k):
+                out += kern.weights[p, q] * img[p:p + 28 - k + 1, q:q + 28 - k + 1]
+        maps.append(poly(out, weights.act1).reshape(-1))
+    return poly(weights.fc1_weight @ np.concatenate(maps) + weights.fc1_bias, weights.act2)
 
 
 def bench_cfg4(steps=2):
