@@ -58,4 +58,6 @@ from .pipeline import (
     poly_activation_batch,
 )
 
+from .serial import SerialError, load_batch, load_ciphertext, load_model, read_ciphertext, write_batch, write_ciphertext, write_model
+
 __version__ = "0.1.0"
