@@ -177,6 +177,7 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
             c.primes.m[p] = vr::Modulus{q, (uint64_t)(r >> 64), (uint64_t)r};
         }
         std::vector<ulonglong2> tw((size_t)np * n), itw((size_t)np * n);
+        std::vector<double> twd((size_t)np * n), itwd((size_t)np * n);
         c.h_ntt_const.resize(np);
         for (int p = 0; p < np; p++) {
             const uint64_t q = c.q[p];
@@ -188,10 +189,20 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
                 const uint32_t r = h_brev(i, log_n);
                 tw[(size_t)p * n + i] = make_ulonglong2(pw[r], h_shoup(pw[r], q));
                 itw[(size_t)p * n + i] = make_ulonglong2(ipw[r], h_shoup(ipw[r], q));
+                twd[(size_t)p * n + i] = (double)pw[r];
+                itwd[(size_t)p * n + i] = (double)ipw[r];
             }
             const uint64_t ninv = h_inv((uint64_t)n % q, q);
             const uint64_t w0n = h_mulmod(itw[(size_t)p * n + 1].x, ninv, q);
-            c.h_ntt_const[p] = vr::NttConst{ninv, h_shoup(ninv, q), w0n, h_shoup(w0n, q)};
+            // FP64 path when every intermediate of a transform stays an exact integer below 2^51
+            // (|values| <= 16 q through 14 forward stages); VR_NTT_F64=0 keeps every prime integer.
+            static const bool f64_on = [] {
+                const char *e = getenv("VR_NTT_F64");
+                return e == nullptr || atoi(e) != 0;
+            }();
+            const int f64 = (f64_on && q < (1ull << 46)) ? 1 : 0;
+            c.h_ntt_const[p] = vr::NttConst{ninv, h_shoup(ninv, q), w0n, h_shoup(w0n, q), (double)q, 1.0 / (double)q,
+                                            (double)ninv, (double)w0n, f64};
         }
         c.h_inv_tab.assign((size_t)np * np * 2, 0);
         for (int a = 0; a < np; a++)
@@ -255,6 +266,8 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
 
         c.tw2 = upload(c, tw);
         c.itw2 = upload(c, itw);
+        c.twd = upload(c, twd);
+        c.itwd = upload(c, itwd);
         c.ntt_const = upload(c, c.h_ntt_const);
         c.inv_tab = upload(c, c.h_inv_tab);
         c.rr_tab = upload(c, rr);
@@ -298,7 +311,7 @@ int vr_ctx_destroy(vr_ctx *h) {
         vr::Ctx &c = h->c;
         cudaSetDevice(c.device);
         cudaDeviceSynchronize();
-        void *ptrs[] = {c.tw2, c.itw2, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw, c.slot_pos, c.pos_slot, c.cdt, c.rlk};
+        void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw, c.slot_pos, c.pos_slot, c.cdt, c.rlk};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (c.s_ntt) cudaFree(c.s_ntt);

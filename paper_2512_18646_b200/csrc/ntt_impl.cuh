@@ -24,6 +24,7 @@
 // "(a - z) * q^-1" run inside the transform instead of as separate kernels.
 #pragma once
 #include <cstdlib>
+#include <type_traits>
 #include "vrhe_internal.cuh"
 
 #include <cooperative_groups.h>
@@ -144,7 +145,9 @@ struct StCombine {
 
 struct PassArgs {
     int logN, s0, TPC;
-    int last;  // this pass writes the final (fully reduced) output through the store functor
+    int last;     // this pass writes the final (fully reduced) output through the store functor
+    int raw_in;   // input is the other pass's intermediate (FP64 body: raw double bits)
+    int raw_out;  // output is an intermediate for the other pass
 };
 
 template <bool INV, int R, int EPT>
@@ -188,26 +191,102 @@ __device__ __forceinline__ void group_compute(uint64_t (&x)[EPT], const int (&ba
     }
 }
 
+// ---- FP64-pipe arithmetic (primes q < 2^46; NttConst::f64) ------------------------------------
+// Values are exact integers held in doubles.  t = y*w mod q is computed Shoup-style on the FP64
+// pipe: h = fl(y w), l = y w - h (exact, FMA), qt = rint(h / q) (FMA with 1.5*2^52), and
+// r = (h - qt q) + l, exact because h - qt q is an integer of magnitude <= 0.75 q; |r| <= q
+// whenever |y| < 2^51.  Forward stages therefore grow |x| by at most q each (<= 17 q after 16
+// stages), Gentleman-Sande stages fold their sums; every transform ends with a canonical
+// reduction to [0, q), so the output residues are exactly those of the integer path.
+constexpr double kF64Magic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kTwo52 = 4503599627370496.0;
+
+__device__ __forceinline__ double u2d(uint64_t v) {  // v < 2^52
+    return __dadd_rn(__longlong_as_double((long long)(v | 0x4330000000000000ull)), -kTwo52);
+}
+__device__ __forceinline__ uint64_t d2u(double x) {  // integer x in [0, 2^52)
+    return (uint64_t)__double_as_longlong(__dadd_rn(x, kTwo52)) & 0x000FFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ double rint_f(double x, double qinv) {
+    return __dadd_rn(__fma_rn(x, qinv, kF64Magic), -kF64Magic);
+}
+__device__ __forceinline__ double mulmod_f(double y, double w, double q, double qinv) {
+    const double h = __dmul_rn(y, w);
+    const double l = __fma_rn(y, w, -h);
+    return __dadd_rn(__fma_rn(-rint_f(h, qinv), q, h), l);
+}
+__device__ __forceinline__ double fold_f(double x, double q, double qinv) { return __fma_rn(-rint_f(x, qinv), q, x); }
+__device__ __forceinline__ uint64_t canon_f(double x, double q, double qinv) {
+    double r = fold_f(x, q, qinv);
+    r = r < 0.0 ? __dadd_rn(r, q) : r;
+    return d2u(r);
+}
+
+template <bool INV, int R, int EPT>
+__device__ __forceinline__ void group_compute_f(double (&x)[EPT], const int (&base)[EPT], int d, int s, int logT, int s0,
+                                                int hi, const double *__restrict__ W, const NttConst &nc) {
+    constexpr int E2 = 1 << R, U = EPT >> R;
+    const double q = nc.qd, qinv = nc.qinv;
+#pragma unroll
+    for (int v = 0; v < U; v++) {
+        double tw[E2 - 1];
+#pragma unroll
+        for (int r = 0, n = 0; r < R; r++) {
+            const int g = s0 + s + r, half = E2 >> (r + 1), shift = logT - (s + r);
+#pragma unroll
+            for (int w = 0; w < E2; w += 2 * half, n++) {
+                if (INV && g == 0) continue;
+                tw[n] = __ldg(W + (1 << g) + (hi << (g - s0)) + ((base[v] + w * d) >> shift));
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; rr++) {
+            const int r = INV ? R - 1 - rr : rr;
+            const int g = s0 + s + r, half = E2 >> (r + 1);
+            const int n0 = (1 << r) - 1;
+#pragma unroll
+            for (int w = 0; w < E2; w++) {
+                if (w & half) continue;
+                double &X = x[v * E2 + w], &Y = x[v * E2 + w + half];
+                if (INV && g == 0) {
+                    const double a = X, b = Y;
+                    X = mulmod_f(__dadd_rn(a, b), nc.ninv_d, q, qinv);
+                    Y = mulmod_f(__dsub_rn(a, b), nc.w0n_d, q, qinv);
+                } else if (INV) {
+                    const double a = X, b = Y;
+                    X = fold_f(__dadd_rn(a, b), q, qinv);
+                    Y = mulmod_f(__dsub_rn(a, b), tw[n0 + w / (2 * half)], q, qinv);
+                } else {
+                    const double t = mulmod_f(Y, tw[n0 + w / (2 * half)], q, qinv);
+                    const double a = X;
+                    X = __dadd_rn(a, t);
+                    Y = __dsub_rn(a, t);
+                }
+            }
+        }
+    }
+}
+
 // LE = log2(elements per thread): 3 (radix-8 groups) for throughput, 2 (radix-4 groups, twice the
 // threads, half the per-thread dependency chain) for small latency-bound batches.
-template <bool INV, bool COLS, int LOGT, int LE, class LD, class ST>
-__global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrimes pr, const ulonglong2 *__restrict__ tw,
-                                                const NttConst *__restrict__ ncs, LD ld, ST st) {
-    extern __shared__ uint64_t sm[];
+// The CTA's prime picks the integer (Harvey/Shoup, IMAD pipe) or the FP64-pipe body; a.raw_in /
+// a.raw_out mark the intermediate between the two passes of one transform, which the FP64 body
+// keeps as raw double bits (the integer body as lazy [0, 4q) residues).
+template <bool INV, bool COLS, int LOGT, int LE, bool F64, class LD, class ST>
+__device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs &a, const DevPrimes &pr,
+                                              const ulonglong2 *__restrict__ tw, const double *__restrict__ twd,
+                                              const NttConst &nc, uint64_t *ptr, int t, int pidx, const LD &ld,
+                                              const ST &st, uint64_t *sm) {
+    using V = typename std::conditional<F64, double, uint64_t>::type;
     constexpr int EPT = 1 << LE;
     constexpr int T = 1 << LOGT, NG = (LOGT + LE - 1) / LE;
     const int logN = a.logN, N = 1 << logN, s0 = a.s0;
     const int lo_bits = logN - s0 - LOGT, TPC = a.TPC;
     const int chunks = (N >> LOGT) / TPC;
-    const int t = blockIdx.x / chunks, chunk = blockIdx.x - t * chunks;
-    uint64_t *ptr;
-    int pidx;
-    pdl_wait();
-    pdl_trigger();
-    if (!locate(b, t, N, ptr, pidx)) return;
+    const int chunk = blockIdx.x - t * chunks;
     const uint64_t q = pr.m[pidx].q;
     const ulonglong2 *W = tw + (size_t)pidx * N;
-    const NttConst nc = ncs[pidx];
+    const double *Wd = twd + (size_t)pidx * N;
     const int tile0 = chunk * TPC, lomask = (1 << lo_bits) - 1;
     constexpr int tpt = T >> LE;
     int j, sub;
@@ -215,8 +294,28 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
     else { j = threadIdx.x / tpt; sub = threadIdx.x - j * tpt; }
     const int tile = tile0 + j, hi = tile >> lo_bits, lo = tile & lomask;
     const long long ebase = ((long long)hi << (logN - s0)) | lo;
+    V *smv = reinterpret_cast<V *>(sm);
 
-    uint64_t x[EPT];
+    // element conversion at the pass boundaries
+    auto in = [&](uint64_t u) -> V {
+        if constexpr (F64) return a.raw_in ? __longlong_as_double((long long)u) : u2d(u);
+        else return u;
+    };
+    auto out_final = [&](V v) -> uint64_t {
+        if constexpr (F64) return canon_f(v, nc.qd, nc.qinv);
+        else {
+            const uint64_t q2 = 2 * q;
+            uint64_t w = v;
+            if (!INV) w = w >= q2 ? w - q2 : w;
+            return w >= q ? w - q : w;
+        }
+    };
+    auto out_raw = [&](V v) -> uint64_t {
+        if constexpr (F64) return (uint64_t)__double_as_longlong(v);
+        else return v;
+    };
+
+    V x[EPT];
     int base[EPT];
 #pragma unroll
     for (int step = 0; step < NG; step++) {
@@ -231,22 +330,19 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
 #pragma unroll
         for (int e = 0; e < EPT; e++) {
             const int L = base[e >> R] + (e & (E2 - 1)) * d;
-            if (step == 0) x[e] = ld(ptr, t, ebase | ((long long)L << lo_bits), pr, pidx);
-            else x[e] = sm[sidx<COLS>(j, L, T, TPC)];
+            if (step == 0) x[e] = in(ld(ptr, t, ebase | ((long long)L << lo_bits), pr, pidx));
+            else x[e] = smv[sidx<COLS>(j, L, T, TPC)];
         }
-        if (R == 3) group_compute<INV, (LE >= 3 ? 3 : 1), EPT>(x, base, d, s, LOGT, s0, hi, q, W, nc);
-        else if (R == 2) group_compute<INV, 2, EPT>(x, base, d, s, LOGT, s0, hi, q, W, nc);
-        else group_compute<INV, 1, EPT>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+        if constexpr (F64) {
+            if (R == 3) group_compute_f<INV, (LE >= 3 ? 3 : 1), EPT>(x, base, d, s, LOGT, s0, hi, Wd, nc);
+            else if (R == 2) group_compute_f<INV, 2, EPT>(x, base, d, s, LOGT, s0, hi, Wd, nc);
+            else group_compute_f<INV, 1, EPT>(x, base, d, s, LOGT, s0, hi, Wd, nc);
+        } else {
+            if (R == 3) group_compute<INV, (LE >= 3 ? 3 : 1), EPT>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+            else if (R == 2) group_compute<INV, 2, EPT>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+            else group_compute<INV, 1, EPT>(x, base, d, s, LOGT, s0, hi, q, W, nc);
+        }
         const bool last_group = step == NG - 1;
-        if (last_group && a.last) {
-            const uint64_t q2 = 2 * q;
-#pragma unroll
-            for (int e = 0; e < EPT; e++) {
-                uint64_t v = x[e];
-                if (!INV) v = v >= q2 ? v - q2 : v;
-                x[e] = v >= q ? v - q : v;
-            }
-        }
         if (last_group && COLS) {
             // consecutive threads own consecutive columns -> coalesced direct stores
             typename ST::Pre pre[EPT];
@@ -258,12 +354,13 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
 #pragma unroll
             for (int e = 0; e < EPT; e++) {
                 const int L = base[e >> R] + (e & (E2 - 1)) * d;
-                st.finish(ptr, t, ebase | ((long long)L << lo_bits), x[e], pre[e], pr, pidx);
+                const uint64_t v = a.last ? out_final(x[e]) : (a.raw_out ? out_raw(x[e]) : out_final(x[e]));
+                st.finish(ptr, t, ebase | ((long long)L << lo_bits), v, pre[e], pr, pidx);
             }
             return;
         }
 #pragma unroll
-        for (int e = 0; e < EPT; e++) sm[sidx<COLS>(j, base[e >> R] + (e & (E2 - 1)) * d, T, TPC)] = x[e];
+        for (int e = 0; e < EPT; e++) smv[sidx<COLS>(j, base[e >> R] + (e & (E2 - 1)) * d, T, TPC)] = x[e];
         __syncthreads();  // one owner per element within a group: a single barrier per group boundary
     }
     // rows: coalesced cooperative store out of shared memory (prefetch the epilogue's loads first)
@@ -281,8 +378,29 @@ __global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrime
     for (int r = 0; r < EPT; r++) {
         const int idx = threadIdx.x + r * blockDim.x;
         const int jj = idx >> LOGT, mid = idx & (T - 1);
-        st.finish(ptr, t, Es[r], sm[sidx<COLS>(jj, mid, T, TPC)], pre[r], pr, pidx);
+        const V v = smv[sidx<COLS>(jj, mid, T, TPC)];
+        st.finish(ptr, t, Es[r], a.last ? out_final(v) : (a.raw_out ? out_raw(v) : out_final(v)), pre[r], pr, pidx);
     }
+}
+
+template <bool INV, bool COLS, int LOGT, int LE, class LD, class ST>
+__global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrimes pr, const ulonglong2 *__restrict__ tw,
+                                                const double *__restrict__ twd, const NttConst *__restrict__ ncs, LD ld,
+                                                ST st) {
+    extern __shared__ uint64_t sm[];
+    constexpr int T = 1 << LOGT;
+    const int N = 1 << a.logN;
+    const int chunks = (N >> LOGT) / a.TPC;
+    const int t = blockIdx.x / chunks;
+    uint64_t *ptr;
+    int pidx;
+    pdl_wait();
+    pdl_trigger();
+    if (!locate(b, t, N, ptr, pidx)) return;
+    const NttConst nc = ncs[pidx];
+    (void)T;
+    if (nc.f64) ntt_pass_body<INV, COLS, LOGT, LE, true>(b, a, pr, tw, twd, nc, ptr, t, pidx, ld, st, sm);
+    else ntt_pass_body<INV, COLS, LOGT, LE, false>(b, a, pr, tw, twd, nc, ptr, t, pidx, ld, st, sm);
 }
 
 // one thread per transform for N <= 4 (slots = 2, test-only parameter sets)
@@ -336,7 +454,8 @@ void launch_pass(Ctx &c, const NttBatch &b, const PassArgs &a, const LD &ld, con
     const size_t smem = (size_t)a.TPC * T * sizeof(uint64_t);
     const unsigned blocks = (unsigned)b.count * chunks;
     launch_pdl(ntt_pass<INV, COLS, LOGT, LE, LD, ST>, dim3(blocks), dim3(threads), smem, c.stream, b, a, c.primes,
-               (const ulonglong2 *)(INV ? c.itw2 : c.tw2), (const NttConst *)c.ntt_const, ld, st);
+               (const ulonglong2 *)(INV ? c.itw2 : c.tw2), (const double *)(INV ? c.itwd : c.twd),
+               (const NttConst *)c.ntt_const, ld, st);
     check_launch("ntt_pass");
 }
 
@@ -384,28 +503,42 @@ inline int pick_tpc(int count, int tiles_per_tf, int T, int max_tpc, int min_tpc
 // trip per transform instead of two.
 __device__ __forceinline__ int sidx_row(int L) { return L ^ ((L >> 4) & 15); }
 
-template <bool INV, int LOGC, class LD, class ST>
-__global__ void __launch_bounds__((1 << LOGC) / 8) ntt_cl8(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *__restrict__ tw,
-                                                const NttConst *__restrict__ ncs, LD ld, ST st) {
+template <bool INV, int LOGC, bool F64, class LD, class ST>
+__device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, const ulonglong2 *__restrict__ tw,
+                                             const double *__restrict__ twd, const NttConst &nc, uint64_t *ptr, int t,
+                                             int pidx, const LD &ld, const ST &st, uint64_t *sm) {
     namespace cg = cooperative_groups;
-    extern __shared__ uint64_t sm[];
+    using V = typename std::conditional<F64, double, uint64_t>::type;
     constexpr int LE = 3, EPT = 8, C = 1 << LOGC, NG = (LOGC + LE - 1) / LE;
     cg::cluster_group cluster = cg::this_cluster();
-    const int r = (int)cluster.block_rank(), t = blockIdx.x >> 3, sub = threadIdx.x;
+    const int r = (int)cluster.block_rank(), sub = threadIdx.x;
     const int N = 1 << logN;
-    pdl_wait();
-    pdl_trigger();
-    uint64_t *ptr;
-    int pidx;
-    if (!locate(b, t, N, ptr, pidx)) return;  // uniform over the cluster (same transform)
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     const uint64_t q = pr.m[pidx].q, q2 = 2 * q;
     const ulonglong2 *W = tw + (size_t)pidx * N;
-    const NttConst nc = ncs[pidx];
+    const double *Wd = twd + (size_t)pidx * N;
     const int col = r * (C / 8) + sub;  // this thread's cross-cluster column
-    uint64_t x[EPT];
+    V *smv = reinterpret_cast<V *>(sm);
+    V x[EPT];
     int base[EPT];
+    const int zero_base[EPT] = {0, 0, 0, 0, 0, 0, 0, 0};
 
+    auto in = [&](uint64_t u) -> V {
+        if constexpr (F64) return u2d(u);
+        else return u;
+    };
+    auto final_value = [&](V v) -> uint64_t {
+        if constexpr (F64) return canon_f(v, nc.qd, nc.qinv);
+        else {
+            uint64_t w = v;
+            if (!INV) w = w >= q2 ? w - q2 : w;
+            return w >= q ? w - q : w;
+        }
+    };
+    auto compute = [&](auto rtag, int d, int s, int logT, int s0, int hi, const int(&bs)[EPT]) {
+        constexpr int RR = decltype(rtag)::value;
+        if constexpr (F64) group_compute_f<INV, RR, EPT>(x, bs, d, s, logT, s0, hi, Wd, nc);
+        else group_compute<INV, RR, EPT>(x, bs, d, s, logT, s0, hi, q, W, nc);
+    };
     auto local_stages = [&](bool from_global) {
 #pragma unroll
         for (int step = 0; step < NG; step++) {
@@ -420,32 +553,24 @@ __global__ void __launch_bounds__((1 << LOGC) / 8) ntt_cl8(NttBatch b, int logN,
 #pragma unroll
             for (int e = 0; e < EPT; e++) {
                 const int L = base[e >> R] + (e & (E2 - 1)) * d;
-                x[e] = (from_global && step == 0) ? ld(ptr, t, (long long)r * C + L, pr, pidx) : sm[sidx_row(L)];
+                x[e] = (from_global && step == 0) ? in(ld(ptr, t, (long long)r * C + L, pr, pidx)) : smv[sidx_row(L)];
             }
-            if (R == 3) group_compute<INV, 3, EPT>(x, base, d, s, LOGC, 3, r, q, W, nc);
-            else if (R == 2) group_compute<INV, 2, EPT>(x, base, d, s, LOGC, 3, r, q, W, nc);
-            else group_compute<INV, 1, EPT>(x, base, d, s, LOGC, 3, r, q, W, nc);
-            if (!INV && step == NG - 1) {
+            if (R == 3) compute(std::integral_constant<int, 3>{}, d, s, LOGC, 3, r, base);
+            else if (R == 2) compute(std::integral_constant<int, 2>{}, d, s, LOGC, 3, r, base);
+            else compute(std::integral_constant<int, 1>{}, d, s, LOGC, 3, r, base);
 #pragma unroll
-                for (int e = 0; e < EPT; e++) {
-                    uint64_t v = x[e] >= q2 ? x[e] - q2 : x[e];
-                    x[e] = v >= q ? v - q : v;
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < EPT; e++) sm[sidx_row(base[e >> R] + (e & (E2 - 1)) * d)] = x[e];
+            for (int e = 0; e < EPT; e++) smv[sidx_row(base[e >> R] + (e & (E2 - 1)) * d)] = x[e];
             __syncthreads();
         }
     };
-    const int zero_base[EPT] = {0, 0, 0, 0, 0, 0, 0, 0};
 
     if (!INV) {
 #pragma unroll
-        for (int u = 0; u < 8; u++) x[u] = ld(ptr, t, (long long)col + ((long long)u << LOGC), pr, pidx);
-        group_compute<false, 3, EPT>(x, zero_base, 1, 0, 3, 0, 0, q, W, nc);
+        for (int u = 0; u < 8; u++) x[u] = in(ld(ptr, t, (long long)col + ((long long)u << LOGC), pr, pidx));
+        compute(std::integral_constant<int, 3>{}, 1, 0, 3, 0, 0, zero_base);
         asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer is resident
 #pragma unroll
-        for (int u = 0; u < 8; u++) cluster.map_shared_rank(sm, u)[sidx_row(col)] = x[u];
+        for (int u = 0; u < 8; u++) cluster.map_shared_rank(smv, u)[sidx_row(col)] = x[u];
         cluster.sync();
         local_stages(false);
         // coalesced store of the chunk through the Store functor (prefetch its loads first)
@@ -455,25 +580,40 @@ __global__ void __launch_bounds__((1 << LOGC) / 8) ntt_cl8(NttBatch b, int logN,
 #pragma unroll
         for (int k = 0; k < EPT; k++) {
             const int mid = sub + k * (C / 8);
-            st.finish(ptr, t, (long long)r * C + mid, sm[sidx_row(mid)], pre[k], pr, pidx);
+            st.finish(ptr, t, (long long)r * C + mid, final_value(smv[sidx_row(mid)]), pre[k], pr, pidx);
         }
     } else {
         local_stages(true);
         asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
         cluster.sync();
 #pragma unroll
-        for (int u = 0; u < 8; u++) x[u] = cluster.map_shared_rank(sm, u)[sidx_row(col)];
-        group_compute<true, 3, EPT>(x, zero_base, 1, 0, 3, 0, 0, q, W, nc);
+        for (int u = 0; u < 8; u++) x[u] = cluster.map_shared_rank(smv, u)[sidx_row(col)];
+        compute(std::integral_constant<int, 3>{}, 1, 0, 3, 0, 0, zero_base);
         typename ST::Pre pre[EPT];
 #pragma unroll
         for (int u = 0; u < 8; u++) pre[u] = st.prefetch(t, (long long)col + ((long long)u << LOGC), pr, pidx);
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
-            const uint64_t v = x[u] >= q ? x[u] - q : x[u];
-            st.finish(ptr, t, (long long)col + ((long long)u << LOGC), v, pre[u], pr, pidx);
-        }
+        for (int u = 0; u < 8; u++)
+            st.finish(ptr, t, (long long)col + ((long long)u << LOGC), final_value(x[u]), pre[u], pr, pidx);
         cluster.sync();  // peers keep their shared memory until every gather has finished
     }
+}
+
+template <bool INV, int LOGC, class LD, class ST>
+__global__ void __launch_bounds__((1 << LOGC) / 8) ntt_cl8(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *__restrict__ tw,
+                                                           const double *__restrict__ twd,
+                                                           const NttConst *__restrict__ ncs, LD ld, ST st) {
+    extern __shared__ uint64_t sm[];
+    const int t = blockIdx.x >> 3;
+    pdl_wait();
+    pdl_trigger();
+    uint64_t *ptr;
+    int pidx;
+    if (!locate(b, t, 1 << logN, ptr, pidx)) return;  // uniform over the cluster (same transform)
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    const NttConst nc = ncs[pidx];
+    if (nc.f64) ntt_cl8_body<INV, LOGC, true>(logN, pr, tw, twd, nc, ptr, t, pidx, ld, st, sm);
+    else ntt_cl8_body<INV, LOGC, false>(logN, pr, tw, twd, nc, ptr, t, pidx, ld, st, sm);
 }
 
 template <bool INV, int LOGC, class LD, class ST>
@@ -501,7 +641,7 @@ void launch_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     VR_CUDA(cudaLaunchKernelEx(&cfg, kern, b, c.log_n, c.primes, (const ulonglong2 *)(INV ? c.itw2 : c.tw2),
-                               (const NttConst *)c.ntt_const, ld, st));
+                               (const double *)(INV ? c.itwd : c.twd), (const NttConst *)c.ntt_const, ld, st));
     check_launch("ntt_cl8");
 }
 
@@ -541,7 +681,7 @@ void run_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
         return;
     }
     if (c.n < 2048) {
-        PassArgs a{logN, 0, 1, 1};
+        PassArgs a{logN, 0, 1, 1, 0, 0};
         dispatch_pass<INV, false>(c, b, a, logN, 3, ld, st);
         return;
     }
@@ -553,8 +693,11 @@ void run_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
         return e ? atoi(e) : 64;
     }();
     const int le = b.count <= small_batch ? 2 : 3;
-    PassArgs p1{logN, 0, pick_tpc(b.count, 1 << lb, T1, 16, 4, le), 0};
-    PassArgs p2{logN, la, pick_tpc(b.count, 1 << la, T2, 2048 / T2, 1, le), 0};
+    PassArgs p1{logN, 0, pick_tpc(b.count, 1 << lb, T1, 16, 4, le), 0, 0, 0};
+    PassArgs p2{logN, la, pick_tpc(b.count, 1 << la, T2, 2048 / T2, 1, le), 0, 0, 0};
+    // the first pass hands its intermediate to the second (raw doubles on the FP64 body)
+    (INV ? p2 : p1).raw_out = 1;
+    (INV ? p1 : p2).raw_in = 1;
     if (!INV) {
         p2.last = 1;
         dispatch_pass<false, true>(c, b, p1, la, le, ld, StPlain{});

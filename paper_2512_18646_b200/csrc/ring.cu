@@ -204,6 +204,23 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
+// same, with an L2 eviction-priority policy (createpolicy) attached to the transfer
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+                     "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 // Fused sum_k tensor(L[b][k], R[k]) for NB row blocks sharing the right operand.
 // Grid (coefficient tiles of TS_TILE, limbs, TS_SPLIT): the TS_SPLIT CTAs of a
 // thread-block cluster take disjoint parts of the k range.  Inside a CTA one
@@ -223,7 +240,8 @@ __host__ __device__ constexpr int ts_stages() {
 // MODE 0: (d0, d1, d2); MODE 1: d2 = sum L1 R1 only (reads half the operands); MODE 2: (d0, d1) only.
 template <int NB, int TS_TILE, int TS_SPLIT, int MAXST, int MODE>
 __global__ void __launch_bounds__(TS_TILE / 2 + 32)
-    k_tensor_sum(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O) {
+    k_tensor_sum(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O,
+                 int hint) {
     pdl_wait();
     pdl_trigger();
     constexpr int TS_CONSUMERS = TS_TILE / 2;  // 2 coefficients per consumer thread
@@ -258,6 +276,9 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
     const Modulus m = pr.m[i];
     if (warp == producer_warp) {
         if (lane == 0) {
+            const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+            (void)pol_keep;
+            (void)pol_drop;
             const uint32_t bytes = (uint32_t)tile * 8;
             const size_t o0 = (size_t)i * N + k0, o1 = (size_t)(nl + i) * N + k0;
             for (int t = tb, it = 0; t < te; t++, it++) {
@@ -266,9 +287,27 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
                 uint64_t *st = ring + (size_t)s * ARR * tile;
                 mbar_expect_tx(&full[s], bytes * ARR);
                 if constexpr (MODE == 1) {
+                    // hint: keep the c1 halves in L2 for the (d0, d1) pass that follows
+                    if (hint) {
 #pragma unroll
-                    for (int b = 0; b < NB; b++) bulk_g2s(st + b * tile, L[b * n + t] + o1, bytes, &full[s]);
-                    bulk_g2s(st + NB * tile, R[t] + o1, bytes, &full[s]);
+                        for (int b = 0; b < NB; b++) bulk_g2s_hint(st + b * tile, L[b * n + t] + o1, bytes, &full[s], pol_keep);
+                        bulk_g2s_hint(st + NB * tile, R[t] + o1, bytes, &full[s], pol_keep);
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < NB; b++) bulk_g2s(st + b * tile, L[b * n + t] + o1, bytes, &full[s]);
+                        bulk_g2s(st + NB * tile, R[t] + o1, bytes, &full[s]);
+                    }
+                } else if (MODE == 2 && hint) {
+                    // last use of every operand: stream them through L2 at the lowest priority
+#pragma unroll
+                    for (int b = 0; b < NB; b++) {
+                        const uint64_t *l = L[b * n + t];
+                        bulk_g2s_hint(st + (2 * b) * tile, l + o0, bytes, &full[s], pol_drop);
+                        bulk_g2s_hint(st + (2 * b + 1) * tile, l + o1, bytes, &full[s], pol_drop);
+                    }
+                    const uint64_t *r = R[t];
+                    bulk_g2s_hint(st + (2 * NB) * tile, r + o0, bytes, &full[s], pol_drop);
+                    bulk_g2s_hint(st + (2 * NB + 1) * tile, r + o1, bytes, &full[s], pol_drop);
                 } else {
 #pragma unroll
                     for (int b = 0; b < NB; b++) {
@@ -499,7 +538,11 @@ static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    VR_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, n, nl, c.n, c.primes, O));
+    static const int hint = [] {
+        const char *e = getenv("VR_TS_HINT");
+        return e ? atoi(e) : 1;
+    }();
+    VR_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, n, nl, c.n, c.primes, O, hint));
 }
 
 template <int NB>

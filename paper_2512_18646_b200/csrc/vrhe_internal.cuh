@@ -26,6 +26,9 @@ struct DevPrimes {
 // Per-prime NTT scalars: n^-1 and (psi^-1_br[1] * n^-1), each with Shoup companion.
 struct NttConst {
     uint64_t ninv, ninv_sh, w0n, w0n_sh;
+    // FP64-pipe transform (primes below 2^46, see ntt_impl.cuh): q, 1/q, n^-1 and w0n as doubles
+    double qd, qinv, ninv_d, w0n_d;
+    int f64;
 };
 
 struct Ctx {
@@ -50,6 +53,7 @@ struct Ctx {
     //   [MAXP*8 + 0..3] = P mod q_l (+shoup), P^-1 mod q_l (+shoup)
     uint64_t *rr_tab = nullptr;
     double *zr = nullptr, *zi = nullptr;  // zeta^k, k < N
+    double *twd = nullptr, *itwd = nullptr;  // NTT twiddles as doubles [np][N] (FP64-pipe transforms)
     double *ftw = nullptr;  // FFT twiddles by stage: (re, im) pairs at [hs + j], hs = 1, 2, .., S/2, j < hs
     int *slot_pos = nullptr;              // [S]
     int *pos_slot = nullptr;              // [S] slot j whose bit-reversed FFT position is p

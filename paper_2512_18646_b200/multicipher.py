@@ -98,7 +98,8 @@ def _common_level(engine: CkksEngine, cts):
 
 
 def _checked_ptrs(engine: CkksEngine, cem: ColumnEncodedMatrix):
-    """(level, [device pointers]) of a column-encoded operand, validated and cached on the object."""
+    """(level, [device pointers]) of a column-encoded operand, validated and cached on the object
+    (operands are immutable; the cache also holds the ctypes pointer array and the max depth)."""
     cached = getattr(cem, "_vr_ptrs", None)
     if cached is not None and cached[0] == engine._id:
         return cached[1], cached[2]
@@ -108,8 +109,16 @@ def _checked_ptrs(engine: CkksEngine, cem: ColumnEncodedMatrix):
     ptrs = None
     if all(c.level == lv for c in cem.cts):
         ptrs = [c.ptr() for c in cem.cts]
-        object.__setattr__(cem, "_vr_ptrs", (engine._id, lv, ptrs))
+        object.__setattr__(cem, "_vr_ptrs", (engine._id, lv, ptrs, _lib.ptr_array(ptrs), max(c.depth for c in cem.cts)))
     return lv, ptrs
+
+
+def _fast_operand(engine: CkksEngine, cem: ColumnEncodedMatrix):
+    """(level, ctypes pointer array, max depth) from the cache, or None."""
+    cached = getattr(cem, "_vr_ptrs", None)
+    if cached is not None and cached[0] == engine._id:
+        return cached[1], cached[3], cached[4]
+    return None
 
 
 def matmul_outer(engine: CkksEngine, left: ColumnEncodedMatrix, right: ColumnEncodedMatrix) -> PackedMatrix:
@@ -133,6 +142,20 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
     if nb not in (1, 2, 4):
         raise EngineError("matmul_outer_blocks supports 1, 2 or 4 row blocks")
     n = right.n
+    if nb == 1:
+        # steady state (operands already validated once): cached pointer arrays, no per-call scans
+        fl, fr = _fast_operand(engine, lefts[0]), _fast_operand(engine, right)
+        lf = lefts[0]
+        if (fl is not None and fr is not None and fl[0] == fr[0] and fl[0] >= 1 and lf.role == "left"
+                and right.role == "right" and lf.n == n and lf.p == right.p):
+            lv = fl[0]
+            outs = torch.empty((1, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
+            _lib.check(engine._lib.vr_matmul_outer(engine.handle, fl[1], fr[1], n, 1, lv, _lib.row_ptrs(outs, 1)))
+            depth = max(fl[2], fr[2]) + 1
+            engine._meter.mul_count += n
+            engine._meter.add_count += n - 1
+            engine._observe(depth)
+            return [Ciphertext.at(outs, 0, lv - 1, engine.scales[lv - 1], depth, lf.cts[0].layout, engine._id)]
     for lf in lefts:
         if lf.role != "left" or right.role != "right":
             raise LayoutError("operands must be a (left, right) column-encoded pair")

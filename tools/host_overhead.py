@@ -21,3 +21,13 @@ pr = cProfile.Profile(); pr.enable()
 for _ in range(100): matmul_outer(eng, L, R)
 pr.disable(); torch.cuda.synchronize()
 pstats.Stats(pr).sort_stats("tottime").print_stats(12)
+# C-ABI call alone (pre-built pointer arrays): host cost of the C++ driver + its launches
+from paper_2512_18646_b200 import _lib
+lp = _lib.ptr_array([c.ptr() for c in L.cts]); rp = _lib.ptr_array([c.ptr() for c in R.cts])
+outs = torch.empty((1, 2, eng.L, eng.N), dtype=torch.int64, device=eng.device); op = _lib.row_ptrs(outs, 1)
+for _ in range(20): eng._lib.vr_matmul_outer(eng.handle, lp, rp, 64, 1, eng.L, op)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(200): eng._lib.vr_matmul_outer(eng.handle, lp, rp, 64, 1, eng.L, op)
+t1 = time.perf_counter(); torch.cuda.synchronize()
+print(f"C-ABI vr_matmul_outer host submit {1e3*(t1-t0)/200:.3f} ms/call")
