@@ -204,6 +204,14 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
             c.h_ntt_const[p] = vr::NttConst{ninv, h_shoup(ninv, q), w0n, h_shoup(w0n, q), (double)q, 1.0 / (double)q,
                                             (double)ninv, (double)w0n, f64};
         }
+        std::vector<uint64_t> liftk((size_t)vr::MAXP * vr::MAXP, 0);
+        for (int a = 0; a < np; a++) {
+            if (c.h_ntt_const[a].f64) c.f64mask |= 1ull << a;
+            for (int b = 0; b < np; b++) {
+                const uint64_t qa = c.q[a], qb = c.q[b];
+                liftk[(size_t)a * vr::MAXP + b] = (qb - qa % qb) % qb;  // == qb * ceil(qa / qb) - qa
+            }
+        }
         c.h_inv_tab.assign((size_t)np * np * 2, 0);
         for (int a = 0; a < np; a++)
             for (int b = 0; b < np; b++) {
@@ -267,6 +275,7 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         c.tw2 = upload(c, tw);
         c.itw2 = upload(c, itw);
         c.twd = upload(c, twd);
+        c.liftk = upload(c, liftk);
         c.itwd = upload(c, itwd);
         c.ntt_const = upload(c, c.h_ntt_const);
         c.inv_tab = upload(c, c.h_inv_tab);
@@ -311,7 +320,7 @@ int vr_ctx_destroy(vr_ctx *h) {
         vr::Ctx &c = h->c;
         cudaSetDevice(c.device);
         cudaDeviceSynchronize();
-        void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw, c.slot_pos, c.pos_slot, c.cdt, c.rlk};
+        void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.liftk, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw, c.slot_pos, c.pos_slot, c.cdt, c.rlk};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (c.s_ntt) cudaFree(c.s_ntt);

@@ -68,13 +68,21 @@ struct LdPlain {
     }
 };
 // centred lift of src[(t / div) * N + E] from prime (from_fixed >= 0 ? from_fixed : (t/div) % mod) into the target prime
+// When source and target primes both run the FP64 body (Ctx::f64mask), the FP64 transform takes
+// any integer input below 2^51, so the centred lift needs no reduction: x - q_src is represented
+// as x + liftk[src][dst] with liftk = q_dst * ceil(q_src / q_dst) - q_src (< q_dst), an exact
+// non-negative value congruent to x - q_src.
 struct LdLift {
     const uint64_t *src;
     int div, mod, from_fixed, N;
+    uint64_t f64mask;
+    const uint64_t *liftk;  // [MAXP][MAXP]
     __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int pidx) const {
         const int row = t / div;
         const int fp = from_fixed >= 0 ? from_fixed : row % mod;
-        return lift_centered(src[(long long)row * N + E], pr.m[fp].q, pr.m[pidx]);
+        const uint64_t x = src[(long long)row * N + E], from = pr.m[fp].q;
+        if ((f64mask >> fp) & (f64mask >> pidx) & 1ull) return x > (from >> 1) ? x + liftk[fp * MAXP + pidx] : x;
+        return lift_centered(x, from, pr.m[pidx]);
     }
 };
 // ptrs[t / div] + (t % div) * stride + off + E
