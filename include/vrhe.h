@@ -108,6 +108,8 @@ int vr_rotate(vr_ctx *ctx, const uint64_t *const *in, uint64_t *const *out, int 
 int vr_keyswitch(vr_ctx *ctx, const uint64_t *poly, int level, uint32_t g, uint64_t *out);
 /* integer-pipe roofline probe: blocks x 256 threads x iters x 8 register-only NTT butterflies */
 int vr_bench_butterflies(vr_ctx *ctx, int blocks, int iters, uint64_t *d_sink);
+/* FP64-pipe roofline probe (the FP64 NTT butterfly for primes < 2^46): blocks x 256 threads x iters x 64 butterflies */
+int vr_bench_butterflies_f64(vr_ctx *ctx, int blocks, int iters, uint64_t *d_sink);
 /* reduce residue sums (< 2^64) mod q_i in place: [polys][level+1][N] (after an NCCL uint64 sum) */
 int vr_mod_reduce(vr_ctx *ctx, uint64_t *data, long long polys, int level);
 

@@ -57,6 +57,7 @@ _SIGS = {
     "vr_keyswitch": [c_vp, c_vp, ctypes.c_int, ctypes.c_uint32, c_vp],
     "vr_mod_reduce": [c_vp, c_vp, ctypes.c_longlong, ctypes.c_int],
     "vr_bench_butterflies": [c_vp, ctypes.c_int, ctypes.c_int, c_vp],
+    "vr_bench_butterflies_f64": [c_vp, ctypes.c_int, ctypes.c_int, c_vp],
     "vr_matmul_outer": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp],
     "vr_tensor_sum": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp],
     "vr_tensor_sum_mode": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int],

@@ -577,6 +577,10 @@ int vr_bench_butterflies(vr_ctx *h, int blocks, int iters, uint64_t *d_sink) {
     return guard([&] { vr::bfly_peak(h->c, blocks, iters, d_sink); });
 }
 
+int vr_bench_butterflies_f64(vr_ctx *h, int blocks, int iters, uint64_t *d_sink) {
+    return guard([&] { vr::bfly_peak_f64(h->c, blocks, iters, d_sink); });
+}
+
 int vr_mod_reduce(vr_ctx *h, uint64_t *data, long long polys, int level) {
     return guard([&] {
         check_level(h->c, level);

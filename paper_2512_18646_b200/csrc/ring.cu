@@ -10,6 +10,7 @@
 #include <cstdlib>
 
 #include "ring.cuh"
+#include "ntt_impl.cuh"
 
 namespace vr {
 
@@ -434,7 +435,47 @@ __global__ void __launch_bounds__(256) k_bfly_peak(uint64_t q, uint64_t w, uint6
     if (acc == 0x12345) sink[0] = acc;  // keep the chains alive
 }
 
+// FP64-pipe peak: the NTT's FP64 butterfly (nttk::mulmod_f, x + t, x - t) on registers only; one fold
+// per 8 butterflies keeps |x| bounded (a forward pass folds never, so this peak is conservative).
+__global__ void __launch_bounds__(256) k_bfly_peak_f64(double q, double w, double qinv, int iters, double *sink) {
+    double x[8], y[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+        x[e] = (double)((threadIdx.x * 977u + e * 131u) % 1000003u);
+        y[e] = (double)((blockIdx.x * 613u + e * 71u) % 1000003u);
+    }
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const double t = nttk::mulmod_f(y[e], w, q, qinv);
+                const double a = x[e];
+                x[e] = __dadd_rn(a, t);
+                y[e] = __dsub_rn(a, t);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            x[e] = nttk::fold_f(x[e], q, qinv);
+            y[e] = nttk::fold_f(y[e], q, qinv);
+        }
+    }
+    double acc = 0;
+#pragma unroll
+    for (int e = 0; e < 8; e++) acc += x[e] + y[e];
+    if (acc == 12345.0) sink[0] = acc;
+}
+
 }  // namespace
+
+void bfly_peak_f64(Ctx &c, int blocks, int iters, uint64_t *sink) {
+    int p = 0;
+    while (p + 1 < c.np && c.q[p] >= (1ull << 46)) p++;
+    const double q = (double)c.q[p];
+    k_bfly_peak_f64<<<blocks, 256, 0, c.stream>>>(q, (double)(1234567 % c.q[p]), 1.0 / q, iters, (double *)sink);
+    check_launch("k_bfly_peak_f64");
+}
 
 void bfly_peak(Ctx &c, int blocks, int iters, uint64_t *sink) {
     const uint64_t q = c.q[1 < c.np ? 1 : 0];

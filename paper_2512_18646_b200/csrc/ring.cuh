@@ -24,6 +24,7 @@ void permute(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, in
 void copy_limbs(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl_in, int nl_out, int limb0);
 void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl);
 void bfly_peak(Ctx &c, int blocks, int iters, uint64_t *sink);
+void bfly_peak_f64(Ctx &c, int blocks, int iters, uint64_t *sink);  // iters x 64 butterflies per thread
 // mode 1: d2 only, mode 2: (d0, d1) only (single row block)
 void tensor_sum_mode(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O,
                      int mode);
