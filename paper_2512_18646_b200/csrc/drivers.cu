@@ -229,14 +229,15 @@ void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, in
             return e ? atoi(e) : 0;
         }();
         cudaStream_t main = c.stream;
-        if (order == 1) tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
+        const bool d2_first = order == 1 || order == 3;
+        if (d2_first) tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
         VR_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         VR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
         c.stream = c.aux;
         tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 2);
         VR_CUDA(cudaEventRecord(c.ev_join, c.aux));
         c.stream = main;
-        if (order != 1) tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
+        if (!d2_first) tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
         if (order >= 2) {
             // the latency-bound key-switch chain on the highest-priority stream
             VR_CUDA(cudaEventRecord(c.ev_hi, main));
