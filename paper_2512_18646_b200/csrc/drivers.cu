@@ -222,13 +222,34 @@ void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, in
     PtrTable td(c, strided(d3.as<uint64_t>(), nb, (size_t)3 * nl * N));
     if (nb == 1 && n >= 8) {
         // overlap: d2 = sum L1 R1 (half the operand bytes) feeds the key switch, while (d0, d1)
-        // accumulate on the auxiliary stream; the final combine waits for them.  Order 1 (default)
-        // runs d2 alone at full bandwidth and forks (d0, d1) behind it, under the key switch.
+        // accumulate on the auxiliary stream; the final combine waits for them.  VR_MM_ORDER:
+        // 4 (default, measured best: 87.7 vs 94 us at cfg 2) d2 + key switch on the highest-priority
+        // stream, so their CTAs are placed before the concurrent (d0, d1) pass; 0 both sums forked
+        // together, chain on the caller's stream; 1/3 d2 first then fork; 2/3 chain on the
+        // high-priority stream.
         static const int order = [] {
             const char *e = getenv("VR_MM_ORDER");
-            return e ? atoi(e) : 0;
+            return e ? atoi(e) : 4;
         }();
         cudaStream_t main = c.stream;
+        if (order == 4) {
+            // d2 and its key switch on the highest-priority stream (the block scheduler places their
+            // CTAs before those of the concurrent (d0, d1) pass on the auxiliary stream)
+            VR_CUDA(cudaEventRecord(c.ev_fork, main));
+            VR_CUDA(cudaStreamWaitEvent(c.hi, c.ev_fork, 0));
+            VR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
+            c.stream = c.hi;
+            tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
+            c.stream = c.aux;
+            tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 2);
+            VR_CUDA(cudaEventRecord(c.ev_join, c.aux));
+            c.stream = c.hi;
+            relin_rescale_batch(c, td.c_(), Out, nb, level, c.ev_join);
+            VR_CUDA(cudaEventRecord(c.ev_hi_done, c.hi));
+            c.stream = main;
+            VR_CUDA(cudaStreamWaitEvent(main, c.ev_hi_done, 0));
+            return;
+        }
         const bool d2_first = order == 1 || order == 3;
         if (d2_first) tensor_sum_mode(c, L, R, n, nb, nl, td.m_(), 1);
         VR_CUDA(cudaEventRecord(c.ev_fork, c.stream));

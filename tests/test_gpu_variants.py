@@ -4,6 +4,8 @@ process from the environment, so every variant runs in its own interpreter):
 * VR_NTT_CL=1  -- every NTT through the one-kernel 8-CTA cluster transform (default: batches >= 256)
 * VR_PDL=0     -- plain stream ordering instead of programmatic dependent launch
 * VR_MM_ORDER=2 -- matmul_outer's key-switch chain on the high-priority stream
+* VR_MM_ORDER=0, VR_NTT_F64=0 -- both tensor sums forked together on normal-priority streams, and
+  every NTT on the integer (IMAD-pipe) body
 """
 
 import os
@@ -17,8 +19,8 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-@pytest.mark.parametrize("env", [{"VR_NTT_CL": "1"}, {"VR_PDL": "0"}, {"VR_MM_ORDER": "2", "VR_NTT_CL": "1"}],
-                         ids=["cluster-ntt", "no-pdl", "hi-prio-chain"])
+@pytest.mark.parametrize("env", [{"VR_NTT_CL": "1"}, {"VR_PDL": "0"}, {"VR_MM_ORDER": "2", "VR_NTT_CL": "1"}, {"VR_MM_ORDER": "0", "VR_NTT_F64": "0"}],
+                         ids=["cluster-ntt", "no-pdl", "hi-prio-chain", "order0-int-ntt"])
 def test_parity_suite_under_variant(env):
     pytest.importorskip("torch").cuda.is_available() or pytest.skip("no CUDA device")
     e = dict(os.environ, **env)
