@@ -23,6 +23,7 @@ float64 simulator with no cryptography and is reported as
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -107,7 +108,7 @@ class ClockSampler:
             self._stop.wait(self.period)
 
     def __enter__(self):
-        if self._nv is not None:
+        if self._nv is not None and not os.environ.get("VR_BENCH_NO_NVML"):
             self._sample()  # first sample before the timed region starts
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
@@ -243,19 +244,43 @@ def run_ours(args, ws, rank, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    # setup: let clocks, allocator pools and pointer-table caches settle (untimed)
+    # the warm-up loops hold the previous result exactly like the timed loop, so the allocator has
+    # both output buffers before timing starts (the first second buffer cost one cudaMalloc: ~90 ms)
+    t_settle = time.perf_counter()
+    out = None
+    while time.perf_counter() - t_settle < 0.25:
+        out = matmul_outer(eng, left, right)
+        torch.cuda.synchronize()
     for _ in range(args.warmup):
-        matmul_outer(eng, left, right)
+        out = matmul_outer(eng, left, right)
     barrier()
     torch.cuda.synchronize()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = lib.vr_launch_count()
+    chunks = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if os.environ.get("VR_BENCH_CHUNKS") else None
+    # no Python garbage-collection pauses inside the timed regions (as timeit does): a gen-2
+    # collection stalled the host for up to ~25 ms and starved the device in some runs
+    gc.collect()
+    gc.disable()
     with ClockSampler(local) as clk:
         st.record(stream)
-        for _ in range(args.steps):
+        slow = []
+        for i in range(args.steps):
+            if chunks is not None and i % max(1, args.steps // 4) == 0 and i // max(1, args.steps // 4) < 4:
+                chunks[i // max(1, args.steps // 4)].record(stream)
+            hc = time.perf_counter()
             out = matmul_outer(eng, left, right)
+            if chunks is not None and time.perf_counter() - hc > 1e-3:
+                slow.append((i, round((time.perf_counter() - hc) * 1e3, 2)))
         en.record(stream)
         torch.cuda.synchronize()
+    if chunks is not None:
+        chunks[4] = en
+        print("chunk ms:", [round(chunks[j].elapsed_time(chunks[j + 1]), 3) for j in range(4)], "slow host calls:", slow,
+              file=sys.stderr)
     launches = lib.vr_launch_count() - l0
+    gc.enable()
     barrier()
     step_s = max_over_ranks(st.elapsed_time(en) / 1e3 / args.steps)
     value = ws / step_s
@@ -284,16 +309,21 @@ def run_ours(args, ws, rank, local):
     pin_a = torch.from_numpy(a).pin_memory()
     pin_b = torch.from_numpy(b).pin_memory()
     e2e_steps = max(3, min(50, args.steps // 4))
-    for _ in range(2):
-        matmul_outer(eng, encode_left(eng, pin_a.numpy(), DIM), encode_right(eng, pin_b.numpy(), DIM)).decode(eng)
+    res = None
+    t_settle = time.perf_counter()
+    while time.perf_counter() - t_settle < 0.25:  # same statement as the timed loop
+        res = matmul_outer(eng, encode_left(eng, pin_a.numpy(), DIM), encode_right(eng, pin_b.numpy(), DIM)).decode(eng)
     barrier()
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()
     t0 = time.perf_counter()
     st.record(stream)
     for _ in range(e2e_steps):
         res = matmul_outer(eng, encode_left(eng, pin_a.numpy(), DIM), encode_right(eng, pin_b.numpy(), DIM)).decode(eng)
     en.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     e2e_s = max_over_ranks(max(st.elapsed_time(en) / 1e3, time.perf_counter() - t0) / e2e_steps)
     h2d = 2 * DIM * DIM * 8  # the raw A and B (broadcast/tiling happens in the encode kernel)
     d2h = eng.slots * 8
