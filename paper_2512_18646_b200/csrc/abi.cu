@@ -204,7 +204,8 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
             c.h_ntt_const[p] = vr::NttConst{ninv, h_shoup(ninv, q), w0n, h_shoup(w0n, q), (double)q, 1.0 / (double)q,
                                             (double)ninv, (double)w0n, f64};
         }
-        std::vector<uint64_t> liftk((size_t)vr::MAXP * vr::MAXP, 0);
+        std::vector<uint64_t> liftk((size_t)vr::MAXP * vr::MAXP, 0), kshift(vr::MAXP, 0);
+        for (int a = 0; a < np; a++) kshift[a] = c.q[a] * (((1ull << 47) + c.q[a] - 1) / c.q[a]);
         for (int a = 0; a < np; a++) {
             if (c.h_ntt_const[a].f64) c.f64mask |= 1ull << a;
             for (int b = 0; b < np; b++) {
@@ -276,6 +277,7 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         c.itw2 = upload(c, itw);
         c.twd = upload(c, twd);
         c.liftk = upload(c, liftk);
+        c.kshift = upload(c, kshift);
         c.itwd = upload(c, itwd);
         c.ntt_const = upload(c, c.h_ntt_const);
         c.inv_tab = upload(c, c.h_inv_tab);
@@ -320,7 +322,7 @@ int vr_ctx_destroy(vr_ctx *h) {
         vr::Ctx &c = h->c;
         cudaSetDevice(c.device);
         cudaDeviceSynchronize();
-        void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.liftk, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw, c.slot_pos, c.pos_slot, c.cdt, c.rlk};
+        void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.liftk, c.kshift, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw, c.slot_pos, c.pos_slot, c.cdt, c.rlk};
         for (void *p : ptrs)
             if (p) cudaFree(p);
         if (c.s_ntt) cudaFree(c.s_ntt);

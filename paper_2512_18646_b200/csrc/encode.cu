@@ -421,11 +421,17 @@ __global__ void k_perm_rows(const uint64_t *in, int rows, int logN, uint32_t g, 
 // sampler, and its store writes c0 = NTT(m + e) - a s and c1 = a (a sampled in the NTT domain).
 // secret-key encryption through one fused forward NTT: load m + e (noise added by k_encode),
 // store c0 = (m + e) - a * s and c1 = a with a uniform from the per-transform stream key
+// On an FP64-body prime any |m + e| < 2^47 enters the transform unreduced, shifted by
+// kshift[p] = q ceil(2^47 / q) (== 0 mod q) into [0, 2^48 + q); larger values are reduced.
 struct LdSymEnc {
     const int64_t *m;
     int nl, N;
+    uint64_t f64mask;
+    const uint64_t *kshift;
     __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int pidx) const {
-        return from_i64(m[(long long)(t / nl) * N + E], pr.m[pidx]);
+        const int64_t v = m[(long long)(t / nl) * N + E];
+        if (((f64mask >> pidx) & 1ull) && v > -(1ll << 47) && v < (1ll << 47)) return (uint64_t)(v + (int64_t)kshift[pidx]);
+        return from_i64(v, pr.m[pidx]);
     }
 };
 struct StSymEnc {
@@ -531,7 +537,7 @@ void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long lon
         Scratch keys(c, sizeof(uint64_t) * count * nl);
         encode_src(c, vs, count, scale, m.as<int64_t>(), EncNoise{c.cdt, c.seed, nonce0, nl, keys.as<uint64_t>()});
         ntt_forward_fused(c, NttBatch{d_ct, count * nl, nl, (long long)2 * nl * N, nl, 0, 0, 0},
-                          LdSymEnc{m.as<int64_t>(), nl, N}, StSymEnc{c.s_ntt, c.s_sh, keys.as<uint64_t>(), nl, N});
+                          LdSymEnc{m.as<int64_t>(), nl, N, c.f64mask, c.kshift}, StSymEnc{c.s_ntt, c.s_sh, keys.as<uint64_t>(), nl, N});
         return;
     }
     encode_src(c, vs, count, scale, m.as<int64_t>());

@@ -48,7 +48,7 @@ struct LdStrided {
 template <int KS_MAXD, int KS_CG>
 __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint64_t *const *P, long long poly_off, int count,
                                                   int level, int N, int logN, int np, const uint64_t *key, uint32_t g,
-                                                  DevPrimes pr, uint64_t *A) {
+                                                  DevPrimes pr, uint64_t *A, const NttConst *__restrict__ ncs) {
     pdl_wait();
     pdl_trigger();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -76,6 +76,33 @@ __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint6
         for (int j = 0; j < KS_MAXD; j++)
             if (j < nl)
                 dv[cc][j] = (t == j) ? P[c][poly_off + (long long)j * N + src] : D[(((long long)c * nl + j) * nt + t) * N + src];
+    }
+    const NttConst nc = ncs[pidx];
+    if (nc.f64) {
+        // FP64 pipe (prime < 2^46): exact Shoup-style products, sums of |r| <= q stay exact in a double
+        double kd0[KS_MAXD], kd1[KS_MAXD];
+#pragma unroll
+        for (int j = 0; j < KS_MAXD; j++)
+            if (j < nl) {
+                kd0[j] = nttk::u2d(k0[j]);
+                kd1[j] = nttk::u2d(k1[j]);
+            }
+#pragma unroll
+        for (int cc = 0; cc < KS_CG; cc++) {
+            const int c = c0 + cc;
+            if (c >= count) break;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < KS_MAXD; j++)
+                if (j < nl) {
+                    const double dd = nttk::u2d(dv[cc][j]);
+                    a0 = __dadd_rn(a0, nttk::mulmod_f(dd, kd0[j], nc.qd, nc.qinv));
+                    a1 = __dadd_rn(a1, nttk::mulmod_f(dd, kd1[j], nc.qd, nc.qinv));
+                }
+            A[(((long long)c * 2 + 0) * nt + t) * N + k] = nttk::canon_f(a0, nc.qd, nc.qinv);
+            A[(((long long)c * 2 + 1) * nt + t) * N + k] = nttk::canon_f(a1, nc.qd, nc.qinv);
+        }
+        return;
     }
 #pragma unroll
     for (int cc = 0; cc < KS_CG; cc++) {
@@ -195,13 +222,13 @@ static void launch_ks_inner_cg(Ctx &c, const uint64_t *D, const uint64_t *const 
     const dim3 blocks(nblocks((long long)nt * N, 128), (count + CG - 1) / CG);
     if (nl <= 8)
         launch_pdl(k_ks_inner<8, CG>, blocks, dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g,
-                   c.primes, A);
+                   c.primes, A, (const NttConst *)c.ntt_const);
     else if (nl <= 16)
         launch_pdl(k_ks_inner<16, CG>, blocks, dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N, c.log_n, c.np, key,
-                   g, c.primes, A);
+                   g, c.primes, A, (const NttConst *)c.ntt_const);
     else
         launch_pdl(k_ks_inner<40, 1>, dim3(blocks.x, count), dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N,
-                   c.log_n, c.np, key, g, c.primes, A);
+                   c.log_n, c.np, key, g, c.primes, A, (const NttConst *)c.ntt_const);
     check_launch("k_ks_inner");
 }
 

@@ -54,6 +54,7 @@ struct Ctx {
     uint64_t *rr_tab = nullptr;
     double *zr = nullptr, *zi = nullptr;  // zeta^k, k < N
     uint64_t f64mask = 0;          // bit p: prime p runs the FP64 NTT body
+    uint64_t *kshift = nullptr;    // [MAXP] q ceil(2^47 / q): signed inputs of FP64-body transforms
     uint64_t *liftk = nullptr;     // [MAXP][MAXP] centred-lift offsets for FP64 transforms (ntt_impl.cuh LdLift)
     double *twd = nullptr, *itwd = nullptr;  // NTT twiddles as doubles [np][N] (FP64-pipe transforms)
     double *ftw = nullptr;  // FFT twiddles by stage: (re, im) pairs at [hs + j], hs = 1, 2, .., S/2, j < hs
