@@ -235,8 +235,8 @@ __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS
         cg::cluster_group cluster = cg::this_cluster();
 #pragma unroll 4
         for (int p = threadIdx.x; p < C; p += blockDim.x) {
-            const int pos = slot_pos[base + p];
-            o[base + p] = cluster.map_shared_rank(re, pos / C)[fidx<true>(pos % C)];
+            const int pos = slot_pos[base + p];  // C = 2^(logS - 3)
+            o[base + p] = cluster.map_shared_rank(re, pos >> (logS - 3))[fidx<true>(pos & (C - 1))];
         }
         cluster.sync();  // peers keep their shared memory until every gather has finished
     } else {
@@ -312,33 +312,6 @@ __global__ void k_enc_combine(const uint64_t *buf, int count, int nl, int N, int
     const uint64_t p0 = pk[(size_t)i * N + k], p1 = pk[(size_t)(Ltop + 1 + i) * N + k];
     o[(size_t)i * N + k] = add_mod(mul_mod(v, p0, m), me0, m.q);
     o[(size_t)(nl + i) * N + k] = add_mod(mul_mod(v, p1, m), e1, m.q);
-}
-
-// x[c][k] = c0 + c1 s (+ c2 s^2) on limb q0 (NTT domain)
-__global__ void k_dec_limb0(const uint64_t *const *C, const int *degs, const int *levels, int count, int N,
-                            const uint64_t *s_ntt, DevPrimes pr, uint64_t *x) {
-    pdl_wait();
-    pdl_trigger();
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= (long long)count * N) return;
-    const long long c = e / N;
-    const int k = (int)(e - c * N);
-    const Modulus m = pr.m[0];
-    const uint64_t *ct = C[c];
-    const size_t nl = (size_t)levels[c] + 1;
-    const uint64_t s = s_ntt[k];
-    uint64_t v = add_mod(ct[k], mul_mod(ct[nl * N + k], s, m), m.q);
-    if (degs[c] == 2) v = add_mod(v, mul_mod(ct[2 * nl * N + k], mul_mod(s, s, m), m), m.q);
-    x[e] = v;
-}
-
-__global__ void k_center(const uint64_t *x, long long total, uint64_t q, int64_t *m) {
-    pdl_wait();
-    pdl_trigger();
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= total) return;
-    const uint64_t v = x[e];
-    m[e] = v > (q >> 1) ? -(int64_t)(q - v) : (int64_t)v;
 }
 
 // ---- key generation ----
@@ -557,17 +530,41 @@ void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long lon
     check_launch("k_enc_combine");
 }
 
+// decryption fused into the limb-0 inverse NTT: the load computes c0 + c1 s (+ c2 s^2) mod q0 in the
+// NTT domain, the store centres the coefficients into int64
+struct LdDec {
+    const uint64_t *const *C;
+    const int *degs, *levels;
+    const uint64_t *s_ntt;
+    int N;
+    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int) const {
+        const Modulus m = pr.m[0];
+        const uint64_t *ct = C[t];
+        const long long nlN = (long long)(levels[t] + 1) * N;
+        const uint64_t s = s_ntt[E];
+        uint64_t v = add_mod(ct[E], mul_mod(ct[nlN + E], s, m), m.q);
+        if (degs[t] == 2) v = add_mod(v, mul_mod(ct[2 * nlN + E], mul_mod(s, s, m), m), m.q);
+        return v;
+    }
+};
+struct StCenter {
+    int64_t *m;
+    uint64_t q;
+    int N;
+    struct Pre {};
+    __device__ __forceinline__ Pre prefetch(int, long long, const DevPrimes &, int) const { return Pre{}; }
+    __device__ __forceinline__ void finish(uint64_t *, int t, long long E, uint64_t v, const Pre &, const DevPrimes &, int) const {
+        m[(long long)t * N + E] = v > (q >> 1) ? -(int64_t)(q - v) : (int64_t)v;
+    }
+};
+
 void decrypt_decode(Ctx &c, const uint64_t *const *d_cts, const int *d_degs, const int *d_levels, const double *d_scales,
                     int count, double *d_out, int64_t *d_coeffs_out) {
     const int N = c.n, S = c.slots;
     Scratch x(c, sizeof(uint64_t) * count * N), m(c, sizeof(int64_t) * count * N);
-    launch_pdl(k_dec_limb0, dim3(nblocks((long long)count * N, TB)), dim3(TB), 0, c.stream, d_cts, d_degs, d_levels, count, N, c.s_ntt, c.primes,
-                                                                        x.as<uint64_t>());
-    check_launch("k_dec_limb0");
-    ntt_inverse(c, NttBatch{x.as<uint64_t>(), count, 1, (long long)N, 1, 0, 0, 0});
     int64_t *mp = d_coeffs_out ? d_coeffs_out : m.as<int64_t>();
-    launch_pdl(k_center, dim3(nblocks((long long)count * N, TB)), dim3(TB), 0, c.stream, x.as<uint64_t>(), (long long)count * N, c.q[0], mp);
-    check_launch("k_center");
+    ntt_inverse_fused(c, NttBatch{x.as<uint64_t>(), count, 1, (long long)N, 1, 0, 0, 0},
+                      LdDec{d_cts, d_degs, d_levels, c.s_ntt, N}, StCenter{mp, c.q[0], N});
     if (!d_out) return;
     const double2 *tw = reinterpret_cast<const double2 *>(c.ftw);
     if (count > 0) {

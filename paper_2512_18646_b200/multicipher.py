@@ -76,7 +76,7 @@ def encode_left(engine: CkksEngine, a, p: int) -> ColumnEncodedMatrix:
         raise CapacityError(f"{m}x{p} broadcast needs {m * p} slots, engine has {engine.slots}")
     # ct k, slot i*p + j = A[i, k]: broadcast done on the device from the raw m x n matrix
     cts = engine.enc_strided(a, count=n, nvals=m * p, p=p, sc=1, s1=n, s2=0, layout=("grid", m, p))
-    return ColumnEncodedMatrix(cts, "left", m, n, p)
+    return _fresh(engine, ColumnEncodedMatrix(cts, "left", m, n, p))
 
 
 def encode_right(engine: CkksEngine, b, m: int) -> ColumnEncodedMatrix:
@@ -87,7 +87,15 @@ def encode_right(engine: CkksEngine, b, m: int) -> ColumnEncodedMatrix:
         raise CapacityError(f"{m}x{p} tiling needs {m * p} slots, engine has {engine.slots}")
     # ct k, slot i*p + j = B[k, j]: tiling done on the device from the raw n x p matrix
     cts = engine.enc_strided(b, count=n, nvals=m * p, p=p, sc=p, s1=0, s2=1, layout=("grid", m, p))
-    return ColumnEncodedMatrix(cts, "right", m, n, p)
+    return _fresh(engine, ColumnEncodedMatrix(cts, "right", m, n, p))
+
+
+def _fresh(engine: CkksEngine, cem: ColumnEncodedMatrix) -> ColumnEncodedMatrix:
+    """Operand fresh from one encryption batch: same engine, top level, depth 0 for every
+    ciphertext, so the validated pointer cache of _checked_ptrs can be filled directly."""
+    ptrs = [c._ptr for c in cem.cts]
+    object.__setattr__(cem, "_vr_ptrs", (engine._id, engine.L, ptrs, _lib.ptr_array(ptrs), 0))
+    return cem
 
 
 def _common_level(engine: CkksEngine, cts):
