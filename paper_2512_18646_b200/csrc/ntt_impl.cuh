@@ -45,6 +45,20 @@ __device__ __forceinline__ int sidx(int j, int L, int T, int TPC) {
     if (COLS) return L * TPC + j;
     return j * T + (L ^ ((L >> 4) & 15));
 }
+// The row swizzle sw(L) = L ^ ((L >> 4) & 15) is linear over GF(2), so for an element
+// L = base | c (disjoint bits, c a compile-time constant) sw(L) = sw(base) ^ sw(c); with the row
+// offset j*T above every swizzled bit, the index is (j*T | sw(base)) ^ sw(c): one XOR per access.
+__host__ __device__ constexpr int swz(int L) { return L ^ ((L >> 4) & 15); }
+template <bool COLS>
+__device__ __forceinline__ int sidx_base(int j, int base, int T, int TPC) {
+    if (COLS) return base * TPC + j;
+    return (j * T) | swz(base);
+}
+template <bool COLS>
+__device__ __forceinline__ int sidx_off(int sb, int c, int TPC) {
+    if (COLS) return sb + c * TPC;
+    return sb ^ swz(c);
+}
 
 __device__ __forceinline__ void bf_fwd(uint64_t &X, uint64_t &Y, ulonglong2 w, uint64_t q, uint64_t q2) {
     const uint64_t x = X >= q2 ? X - q2 : X;
@@ -158,6 +172,10 @@ struct PassArgs {
     int raw_out;  // output is an intermediate for the other pass
 };
 
+// Index algebra shared by every caller: a unit's elements sit at base | (w << log2(d)), w < 2^R,
+// where base has no bits in [log2 d, log2 d + R).  So (base + w d) >> shift splits into
+// (base >> shift) + (w >> (R - r)) for every stage r (shift = log2 d + R - r): one runtime twiddle
+// address per stage, the w part a compile-time offset in the load's immediate.
 template <bool INV, int R, int EPT>
 __device__ __forceinline__ void group_compute(uint64_t (&x)[EPT], const int (&base)[EPT], int d, int s, int logT, int s0,
                                               int hi, uint64_t q, const ulonglong2 *__restrict__ W, const NttConst &nc) {
@@ -173,7 +191,7 @@ __device__ __forceinline__ void group_compute(uint64_t (&x)[EPT], const int (&ba
 #pragma unroll
             for (int w = 0; w < E2; w += 2 * half, n++) {
                 if (INV && g == 0) continue;
-                tw[n] = __ldg(W + (1 << g) + (hi << (g - s0)) + ((base[v] + w * d) >> shift));
+                tw[n] = __ldg(W + ((1 << g) + (hi << (g - s0)) + (base[v] >> shift)) + (w >> (R - r)));
             }
         }
 #pragma unroll
@@ -244,7 +262,7 @@ __device__ __forceinline__ void group_compute_f(double (&x)[EPT], const int (&ba
 #pragma unroll
             for (int w = 0; w < E2; w += 2 * half, n++) {
                 if (INV && g == 0) continue;
-                tw[n] = __ldg(W + (1 << g) + (hi << (g - s0)) + ((base[v] + w * d) >> shift));
+                tw[n] = __ldg(W + ((1 << g) + (hi << (g - s0)) + (base[v] >> shift)) + (w >> (R - r)));
             }
         }
 #pragma unroll
@@ -335,11 +353,14 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
             const int uid = sub * (EPT >> R) + v;
             base[v] = v < (EPT >> R) ? (((uid >> logd) << (logd + R)) | (uid & (d - 1))) : 0;
         }
+        int sb[EPT];
+#pragma unroll
+        for (int v = 0; v < EPT; v++) sb[v] = sidx_base<COLS>(j, base[v], T, TPC);
 #pragma unroll
         for (int e = 0; e < EPT; e++) {
-            const int L = base[e >> R] + (e & (E2 - 1)) * d;
+            const int L = base[e >> R] | ((e & (E2 - 1)) << logd);
             if (step == 0) x[e] = in(ld(ptr, t, ebase | ((long long)L << lo_bits), pr, pidx));
-            else x[e] = smv[sidx<COLS>(j, L, T, TPC)];
+            else x[e] = smv[sidx_off<COLS>(sb[e >> R], (e & (E2 - 1)) << logd, TPC)];
         }
         if constexpr (F64) {
             if (R == 3) group_compute_f<INV, (LE >= 3 ? 3 : 1), EPT>(x, base, d, s, LOGT, s0, hi, Wd, nc);
@@ -368,7 +389,7 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
             return;
         }
 #pragma unroll
-        for (int e = 0; e < EPT; e++) smv[sidx<COLS>(j, base[e >> R] + (e & (E2 - 1)) * d, T, TPC)] = x[e];
+        for (int e = 0; e < EPT; e++) smv[sidx_off<COLS>(sb[e >> R], (e & (E2 - 1)) << logd, TPC)] = x[e];
         __syncthreads();  // one owner per element within a group: a single barrier per group boundary
     }
     // rows: coalesced cooperative store out of shared memory (prefetch the epilogue's loads first)
@@ -391,8 +412,19 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
     }
 }
 
+// Register cap for the transforms whose prologue/epilogue are plain loads/stores: the integer and
+// FP64 bodies share one kernel, and uncapped the inverse passes took 108-118 registers (23%
+// occupancy, ncu) against 60-64 for the forward ones.  Fused functors keep the compiler's choice.
+template <class LD, class ST>
+struct LightIO {
+    static constexpr bool value = std::is_same<ST, StPlain>::value &&
+                                  (std::is_same<LD, LdPlain>::value || std::is_same<LD, LdGather>::value ||
+                                   std::is_same<LD, LdLift>::value);
+};
+constexpr int kCapRegs = 64;
+
 template <bool INV, bool COLS, int LOGT, int LE, class LD, class ST>
-__global__ void __launch_bounds__(512) ntt_pass(NttBatch b, PassArgs a, DevPrimes pr, const ulonglong2 *__restrict__ tw,
+__global__ void __launch_bounds__(512, LightIO<LD, ST>::value ? 65536 / (512 * kCapRegs) : 1) ntt_pass(NttBatch b, PassArgs a, DevPrimes pr, const ulonglong2 *__restrict__ tw,
                                                 const double *__restrict__ twd, const NttConst *__restrict__ ncs, LD ld,
                                                 ST st) {
     extern __shared__ uint64_t sm[];
@@ -558,16 +590,20 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
                 const int uid = sub * (EPT >> R) + v;
                 base[v] = v < (EPT >> R) ? (((uid >> logd) << (logd + R)) | (uid & (d - 1))) : 0;
             }
+            int sb[EPT];
+#pragma unroll
+            for (int v = 0; v < EPT; v++) sb[v] = swz(base[v]);
 #pragma unroll
             for (int e = 0; e < EPT; e++) {
-                const int L = base[e >> R] + (e & (E2 - 1)) * d;
-                x[e] = (from_global && step == 0) ? in(ld(ptr, t, (long long)r * C + L, pr, pidx)) : smv[sidx_row(L)];
+                const int L = base[e >> R] | ((e & (E2 - 1)) << logd);
+                x[e] = (from_global && step == 0) ? in(ld(ptr, t, (long long)r * C + L, pr, pidx))
+                                                  : smv[sb[e >> R] ^ swz((e & (E2 - 1)) << logd)];
             }
             if (R == 3) compute(std::integral_constant<int, 3>{}, d, s, LOGC, 3, r, base);
             else if (R == 2) compute(std::integral_constant<int, 2>{}, d, s, LOGC, 3, r, base);
             else compute(std::integral_constant<int, 1>{}, d, s, LOGC, 3, r, base);
 #pragma unroll
-            for (int e = 0; e < EPT; e++) smv[sidx_row(base[e >> R] + (e & (E2 - 1)) * d)] = x[e];
+            for (int e = 0; e < EPT; e++) smv[sb[e >> R] ^ swz((e & (E2 - 1)) << logd)] = x[e];
             __syncthreads();
         }
     };
@@ -608,7 +644,7 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
 }
 
 template <bool INV, int LOGC, class LD, class ST>
-__global__ void __launch_bounds__((1 << LOGC) / 8) ntt_cl8(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *__restrict__ tw,
+__global__ void __launch_bounds__((1 << LOGC) / 8, LightIO<LD, ST>::value ? 65536 / (((1 << LOGC) / 8) * kCapRegs) : 1) ntt_cl8(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *__restrict__ tw,
                                                            const double *__restrict__ twd,
                                                            const NttConst *__restrict__ ncs, LD ld, ST st) {
     extern __shared__ uint64_t sm[];
