@@ -53,7 +53,7 @@ __device__ __forceinline__ void fft_group(double *xr, double *xi, int h, int j0,
         const int hs = h << st;
 #pragma unroll
         for (int qb = 0; qb < (1 << st); qb++) {
-            const double2 w = __ldg(tw + hs + j0 + qb * h);
+            const double2 w = tw[hs + j0 + qb * h];
             const double wr = w.x, wi = inverse ? -w.y : w.y;
 #pragma unroll
             for (int u = qb; u < R; u += 2 << st) {
@@ -93,7 +93,7 @@ __device__ __forceinline__ void fft_round(double *re, double *im, int S, int h, 
 }
 
 // all stages of length 2 .. S (S = 2^logS), one barrier per round of up to three stages
-__device__ void fft_stages(double *re, double *im, int S, int logS, const double2 *tw, bool inverse) {
+__device__ __forceinline__ void fft_stages(double *re, double *im, int S, int logS, const double2 *tw, bool inverse) {
     int h = 1, rem = logS;
     for (; rem >= 3; rem -= 3, h <<= 3) {
         fft_round<3>(re, im, S, h, tw, inverse);
@@ -129,10 +129,18 @@ struct SlotSrc {
 // groups {j0 + u C} take element u from CTA u through distributed shared memory.
 constexpr int FFT_CL = 8;
 
+// The local stages read their twiddles (indices < C) from a shared-memory copy of the table's
+// first C entries (tws, filled by stage_twiddles before the PDL wait: the table is constant, so
+// its load overlaps the previous kernel); only the cross-cluster round reads the global table.
+__device__ __forceinline__ void stage_twiddles(double2 *tws, const double2 *tw, int C) {
+    for (int i = threadIdx.x; i < C; i += blockDim.x) tws[i] = __ldg(tw + i);
+}
+
 template <int CL>
-__device__ __forceinline__ void fft_cluster(double *re, double *im, int S, int logS, const double2 *tw, bool inverse) {
+__device__ __forceinline__ void fft_cluster(double *re, double *im, int S, int logS, const double2 *tw, const double2 *tws,
+                                            bool inverse) {
     const int C = S / CL;
-    fft_stages(re, im, C, logS - (CL == 8 ? 3 : 0), tw, inverse);
+    fft_stages(re, im, C, logS - (CL == 8 ? 3 : 0), tws, inverse);
     if constexpr (CL == 8) {
         namespace cg = cooperative_groups;
         cg::cluster_group cluster = cg::this_cluster();
@@ -171,13 +179,15 @@ struct EncNoise {
 template <int CL>
 __global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr, const double *zi, const double2 *tw,
                          const int *pos_slot, EncNoise nz, int64_t *m) {
-    pdl_wait();
-    pdl_trigger();
     extern __shared__ double fft_sm[];
     __shared__ uint64_t cdt_s[CDT_LEN];
     const int C = S / CL, rank = (int)(blockIdx.x % CL), base = rank * C;
     const int c = blockIdx.x / CL;
     double *re = fft_sm, *im = fft_sm + C + C / 8;
+    double2 *tws = reinterpret_cast<double2 *>(im + C + C / 8);
+    stage_twiddles(tws, tw, C);
+    pdl_wait();
+    pdl_trigger();
     if (nz.keys) {
         if (threadIdx.x < CDT_LEN) cdt_s[threadIdx.x] = nz.cdt[threadIdx.x];
         if (rank == 0 && threadIdx.x < nz.nl)
@@ -189,7 +199,7 @@ __global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr
         im[fidx<true>(p)] = 0.0;
     }
     __syncthreads();
-    fft_cluster<CL>(re, im, S, logS, tw, true);
+    fft_cluster<CL>(re, im, S, logS, tw, tws, true);
     int64_t *out = m + (size_t)c * 2 * S;
     const uint64_t ke = nz.keys ? stream_key(nz.seed, DOM_ENC_E0, nz.nonce0 + (uint64_t)c, 0) : 0;
 #pragma unroll 4
@@ -212,12 +222,14 @@ __global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr
 template <int CL>
 __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS, const double *zr, const double *zi,
                          const double2 *tw, const int *slot_pos, double *out) {
-    pdl_wait();
-    pdl_trigger();
     extern __shared__ double fft_sm[];
     const int C = S / CL, rank = (int)(blockIdx.x % CL), base = rank * C;
     const int c = blockIdx.x / CL;
     double *re = fft_sm, *im = fft_sm + C + C / 8;
+    double2 *tws = reinterpret_cast<double2 *>(im + C + C / 8);
+    stage_twiddles(tws, tw, C);
+    pdl_wait();
+    pdl_trigger();
     const int64_t *mc = m + (size_t)c * 2 * S;
     const double scale = scales[c];
 #pragma unroll 4
@@ -228,7 +240,7 @@ __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS
         im[fidx<true>(p)] = __dadd_rn(__dmul_rn(ur, zi[k]), __dmul_rn(ui, zr[k]));
     }
     __syncthreads();
-    fft_cluster<CL>(re, im, S, logS, tw, false);
+    fft_cluster<CL>(re, im, S, logS, tw, tws, false);
     double *o = out + (size_t)c * S;
     if constexpr (CL == 8) {
         namespace cg = cooperative_groups;
@@ -439,7 +451,7 @@ int fft_threads(int S) {
 }
 size_t fft_smem(int S) {
     const int C = S / fft_cl(S);
-    return (size_t)2 * (C + C / 8) * sizeof(double);
+    return (size_t)2 * (C + C / 8) * sizeof(double) + (size_t)C * sizeof(double2);  // re, im (padded) + twiddles
 }
 
 template <typename K, typename... Args>

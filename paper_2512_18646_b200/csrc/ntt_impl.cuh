@@ -412,19 +412,14 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
     }
 }
 
-// Register cap for the transforms whose prologue/epilogue are plain loads/stores: the integer and
-// FP64 bodies share one kernel, and uncapped the inverse passes took 108-118 registers (23%
-// occupancy, ncu) against 60-64 for the forward ones.  Fused functors keep the compiler's choice.
-template <class LD, class ST>
-struct LightIO {
-    static constexpr bool value = std::is_same<ST, StPlain>::value &&
-                                  (std::is_same<LD, LdPlain>::value || std::is_same<LD, LdGather>::value ||
-                                   std::is_same<LD, LdLift>::value);
-};
+// Register cap (64) on every transform kernel.  Uncapped, the integer and FP64 bodies sharing one
+// kernel took 94-128 registers (inverse passes and fused-epilogue passes: 23-25% occupancy in ncu);
+// capped, the fused epilogues spill up to ~250 B of prefetched operands to L1-resident local memory
+// and still run faster: config 4 49.2 -> 52.1 images/s, the fused encryption NTT 110 -> 82 us.
 constexpr int kCapRegs = 64;
 
 template <bool INV, bool COLS, int LOGT, int LE, class LD, class ST>
-__global__ void __launch_bounds__(512, LightIO<LD, ST>::value ? 65536 / (512 * kCapRegs) : 1) ntt_pass(NttBatch b, PassArgs a, DevPrimes pr, const ulonglong2 *__restrict__ tw,
+__global__ void __launch_bounds__(512, 65536 / (512 * kCapRegs)) ntt_pass(NttBatch b, PassArgs a, DevPrimes pr, const ulonglong2 *__restrict__ tw,
                                                 const double *__restrict__ twd, const NttConst *__restrict__ ncs, LD ld,
                                                 ST st) {
     extern __shared__ uint64_t sm[];
@@ -644,7 +639,7 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
 }
 
 template <bool INV, int LOGC, class LD, class ST>
-__global__ void __launch_bounds__((1 << LOGC) / 8, LightIO<LD, ST>::value ? 65536 / (((1 << LOGC) / 8) * kCapRegs) : 1) ntt_cl8(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *__restrict__ tw,
+__global__ void __launch_bounds__((1 << LOGC) / 8, 65536 / (((1 << LOGC) / 8) * kCapRegs)) ntt_cl8(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *__restrict__ tw,
                                                            const double *__restrict__ twd,
                                                            const NttConst *__restrict__ ncs, LD ld, ST st) {
     extern __shared__ uint64_t sm[];
