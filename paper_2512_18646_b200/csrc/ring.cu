@@ -598,8 +598,41 @@ static void ts_variant(Ctx &c, int v, const uint64_t *const *L, const uint64_t *
 void tensor_sum_mode(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O,
                      int mode) {
     if (nb != 1) throw VrError(3, "split tensor_sum supports one row block");
-    if (mode == 1) launch_ts<1, 256, 2, 8, 1>(c, L, R, n, nl, O);
-    else launch_ts<1, 256, 2, 4, 2>(c, L, R, n, nl, O);
+    static const int v2 = [] {
+        const char *e = getenv("VR_TS2_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    // launch shapes swept on B200 with tools/ts2_sweep.sh (VR_TS1_VARIANT / VR_TS2_VARIANT override)
+    static const int v1 = [] {
+        const char *e = getenv("VR_TS1_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    if (mode == 1) {
+        switch (v1) {
+            case 1: launch_ts<1, 512, 2, 8, 1>(c, L, R, n, nl, O); break;
+            case 2: launch_ts<1, 512, 2, 4, 1>(c, L, R, n, nl, O); break;
+            case 3: launch_ts<1, 1024, 2, 4, 1>(c, L, R, n, nl, O); break;
+            case 4: launch_ts<1, 256, 4, 8, 1>(c, L, R, n, nl, O); break;
+            case 5: launch_ts<1, 256, 2, 8, 1>(c, L, R, n, nl, O); break;
+            case 6: launch_ts<1, 128, 4, 8, 1>(c, L, R, n, nl, O); break;
+            case 7: launch_ts<1, 256, 8, 8, 1>(c, L, R, n, nl, O); break;
+            default: launch_ts<1, 512, 4, 4, 1>(c, L, R, n, nl, O); break;  // 17.9 us alone (was 20.5)
+        }
+    } else {
+        switch (v2) {
+            case 1: launch_ts<1, 256, 1, 4, 2>(c, L, R, n, nl, O); break;
+            case 2: launch_ts<1, 256, 2, 8, 2>(c, L, R, n, nl, O); break;
+            case 3: launch_ts<1, 256, 2, 4, 2>(c, L, R, n, nl, O); break;
+            case 4: launch_ts<1, 128, 2, 8, 2>(c, L, R, n, nl, O); break;
+            case 5: launch_ts<1, 256, 4, 4, 2>(c, L, R, n, nl, O); break;
+            case 6: launch_ts<1, 512, 1, 4, 2>(c, L, R, n, nl, O); break;
+            case 7: launch_ts<1, 1024, 2, 2, 2>(c, L, R, n, nl, O); break;
+            case 8: launch_ts<1, 512, 2, 6, 2>(c, L, R, n, nl, O); break;
+            case 9: launch_ts<1, 512, 4, 4, 2>(c, L, R, n, nl, O); break;
+            case 10: launch_ts<1, 512, 2, 3, 2>(c, L, R, n, nl, O); break;
+            default: launch_ts<1, 512, 2, 4, 2>(c, L, R, n, nl, O); break;  // 34.4 us alone (was 37.1)
+        }
+    }
     check_launch("k_tensor_sum");
 }
 

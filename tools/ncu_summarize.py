@@ -35,5 +35,6 @@ for row in rows[2:]:
         "dram_pct_of_peak": f(d, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
         "warps_active_pct": f(d, "sm__warps_active.avg.pct_of_peak_sustained_active"),
         "registers_per_thread": f(d, "launch__registers_per_thread"), "algorithmic_bytes_per_launch": alg}
-(ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(out, indent=1) + "\n")
+out_path = Path(sys.argv[2]) if len(sys.argv) > 2 else ROOT / "profiles" / "ncu_summary.json"
+out_path.write_text(json.dumps(out, indent=1) + "\n")
 print(json.dumps(out, indent=1))
