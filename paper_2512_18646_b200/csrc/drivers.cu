@@ -33,11 +33,11 @@ __global__ void __launch_bounds__(128) k_conv_mac(const uint64_t *const *T, cons
                                                   int N, DevPrimes pr, uint64_t *Yp) {
     pdl_wait();
     pdl_trigger();
-    const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+    const int kk = blockIdx.z * blockDim.x + threadIdx.x;
     if (kk >= N) return;
     const int poly = blockIdx.y / nl, i = blockIdx.y - poly * nl;
     const int nfg = F / FG;
-    const int o = blockIdx.z / nfg, f0 = (blockIdx.z - o * nfg) * FG;
+    const int o = blockIdx.x / nfg, f0 = (blockIdx.x - o * nfg) * FG;
     const Modulus m = pr.m[i];
     u128 acc[FG];
 #pragma unroll
@@ -90,14 +90,14 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
     const uint64_t **sptr = (const uint64_t **)smc;
     uint32_t *sw = (uint32_t *)(smc + ((taps + 1) & ~1));  // [taps][FG], 16-byte aligned rows for FG % 4 == 0
     const int nfg = F / FG;
-    const int o = blockIdx.z / nfg, f0 = (blockIdx.z - o * nfg) * FG;
+    const int o = blockIdx.x / nfg, f0 = (blockIdx.x - o * nfg) * FG;
     for (int t = threadIdx.x; t < taps; t += blockDim.x) {
         const int c = t / (k * k), r = t - c * k * k, q = r / k, p = r - q * k;  // tap order (c, q, p)
         sptr[t] = T[((size_t)c * W + cols[o] + q) * k + p];
         for (int f = 0; f < FG; f++) sw[t * FG + f] = wb[((size_t)(f0 + f) * C + c) * k * k + p * k + q];
     }
     __syncthreads();
-    const int kk = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    const int kk = (blockIdx.z * blockDim.x + threadIdx.x) * 2;
     if (kk >= N) return;
     const int poly = blockIdx.y / nl, i = blockIdx.y - poly * nl;
     const Modulus m = pr.m[i];
@@ -368,12 +368,16 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
     Scratch yp(c, sizeof(uint64_t) * (size_t)F * ocols * ctw);
     for (int o0 = 0; o0 < nout; o0 += ocols) {
         const int no = std::min(ocols, nout - o0);
-        dim3 grid(nblocks(N, 128), 2 * nl, (unsigned)no * (F / FG));
+        // grid x = (output column, filter group) fastest, z = coefficient tile: CTAs resident together
+        // share one coefficient tile, so a rotated tap read by k output columns and F / FG filter
+        // groups is served from L2 after its first read (measured 5.35 -> 5.19 ms per cfg-4 launch;
+        // the MAC is instruction-bound: ncu 3.2 G warp instructions, 7x the IMAD.WIDE count)
+        dim3 grid((unsigned)no * (F / FG), 2 * nl, nblocks(N, 128));
         const int *colp = dcols.get() + o0;
         if (small) {
             const size_t sm = (size_t)((taps + 1) & ~1) * 8 + (size_t)taps * FG * 4 + 16;
             const uint64_t bpow = uint64_t(1) << bb;
-            dim3 gs(nblocks(N / 2, 128), 2 * nl, (unsigned)no * (F / FG));
+            dim3 gs((unsigned)no * (F / FG), 2 * nl, nblocks(N / 2, 128));
             switch (FG) {
                 case 8: launch_pdl(k_conv_mac_small<8>, dim3(gs), dim3(128), sm, c.stream, tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
                 case 4: launch_pdl(k_conv_mac_small<4>, dim3(gs), dim3(128), sm, c.stream, tt.c_(), colp, no, C, W, k, F, dwb.get(), bpow, dbq.get(), mask_pt, nl, N, c.primes, yp.as<uint64_t>()); break;
