@@ -164,45 +164,71 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
 }
 
 // Plaintext mat-vec: Yp[u] = sum_j PT[u*nx + j] (.) X[j] (both polys), 128-bit accumulation.
-// One thread = (limb, coefficient) x UG outputs; each plaintext word feeds two MACs.
-template <int UG>
+// HBM-bound on the plaintext stream (cfg 3 dense 845->64: 2.2 GB per pass).  A thread owns two
+// adjacent coefficients (16-byte loads) of one limb for UG outputs; the CTA stages the pointers of
+// a chunk of JC inputs in shared memory (no dependent pointer load in the loop) and the j loop is
+// unrolled by two so the next input's loads are in flight during the current MACs.
+__device__ __forceinline__ ulonglong2 ld2(const uint64_t *p) { return *reinterpret_cast<const ulonglong2 *>(p); }
+__device__ __forceinline__ void st2(uint64_t *p, uint64_t a, uint64_t b) {
+    *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(a, b);
+}
+constexpr int PMV_JC = 128;
+template <int UG, int JU>
 __global__ void __launch_bounds__(128) k_pt_matvec(const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int nl,
                                                    int N, DevPrimes pr, uint64_t *Yp) {
+    __shared__ const uint64_t *sp[PMV_JC][UG + 1];  // [j][u] plaintext pointers, [j][UG] the input
     pdl_wait();
     pdl_trigger();
-    const int kk = blockIdx.x * blockDim.x + threadIdx.x;
-    if (kk >= N) return;
+    const int kk = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
     const int i = blockIdx.y;
     const int u0 = blockIdx.z * UG;
     const Modulus m = pr.m[i];
     const size_t o0 = (size_t)i * N + kk, o1 = (size_t)(nl + i) * N + kk;
-    u128 acc[UG][2];
+    const bool live = kk < N;
+    u128 acc[UG][2][2];  // [output][poly][coefficient]
 #pragma unroll
-    for (int u = 0; u < UG; u++) acc[u][0] = acc[u][1] = u128{0, 0};
-    for (int j = 0; j < nx; j++) {
-        const uint64_t x0 = X[j][o0], x1 = X[j][o1];
+    for (int u = 0; u < UG; u++)
 #pragma unroll
-        for (int u = 0; u < UG; u++) {
-            if (u0 + u < ny) {
-                const uint64_t pt = PT[(size_t)(u0 + u) * nx + j][o0];
-                mac_to(acc[u][0], pt, x0);
-                mac_to(acc[u][1], pt, x1);
-            }
+        for (int p = 0; p < 2; p++) acc[u][p][0] = acc[u][p][1] = u128{0, 0};
+    for (int jc = 0; jc < nx; jc += PMV_JC) {
+        const int nj = min(PMV_JC, nx - jc);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nj * (UG + 1); t += blockDim.x) {
+            const int jj = t / (UG + 1), u = t - jj * (UG + 1);
+            sp[jj][u] = u == UG ? X[jc + jj] : (u0 + u < ny ? PT[(size_t)(u0 + u) * nx + jc + jj] : nullptr);
         }
-        if ((j & 7) == 7) {
+        __syncthreads();
+        if (!live) continue;
+#pragma unroll JU
+        for (int jj = 0; jj < nj; jj++) {
+            const ulonglong2 x0 = ld2(sp[jj][UG] + o0), x1 = ld2(sp[jj][UG] + o1);
+            ulonglong2 pt[UG];
+#pragma unroll
+            for (int u = 0; u < UG; u++) pt[u] = sp[jj][u] ? ld2(sp[jj][u] + o0) : make_ulonglong2(0, 0);
 #pragma unroll
             for (int u = 0; u < UG; u++) {
-                acc[u][0] = u128{reduce128(acc[u][0], m), 0};
-                acc[u][1] = u128{reduce128(acc[u][1], m), 0};
+                mac_to(acc[u][0][0], pt[u].x, x0.x);
+                mac_to(acc[u][0][1], pt[u].y, x0.y);
+                mac_to(acc[u][1][0], pt[u].x, x1.x);
+                mac_to(acc[u][1][1], pt[u].y, x1.y);
+            }
+            if (((jc + jj) & 7) == 7) {
+#pragma unroll
+                for (int u = 0; u < UG; u++)
+#pragma unroll
+                    for (int p = 0; p < 2; p++)
+#pragma unroll
+                        for (int e = 0; e < 2; e++) acc[u][p][e] = u128{reduce128(acc[u][p][e], m), 0};
             }
         }
     }
+    if (!live) return;
 #pragma unroll
     for (int u = 0; u < UG; u++) {
         if (u0 + u >= ny) break;
         uint64_t *y = Yp + (size_t)(u0 + u) * 2 * nl * N;
-        y[o0] = reduce128(acc[u][0], m);
-        y[o1] = reduce128(acc[u][1], m);
+        st2(y + o0, reduce128(acc[u][0][0], m), reduce128(acc[u][0][1], m));
+        st2(y + o1, reduce128(acc[u][1][0], m), reduce128(acc[u][1][1], m));
     }
 }
 
@@ -448,21 +474,35 @@ void poly_activation(Ctx &c, const uint64_t *const *X, int count, int level, con
     }
 }
 
-void pt_matvec(Ctx &c, const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int level, uint64_t *const *Y) {
+template <int UG, int JU>
+static void pt_matvec_ug(Ctx &c, const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int level,
+                         uint64_t *const *Y) {
     const int N = c.n, nl = level + 1;
     const size_t ctw = (size_t)2 * nl * N;
-    constexpr int UG = 8;
     const int chunk = (int)std::max<size_t>(UG, std::min<size_t>((size_t)ny, ((size_t)2 << 30) / (ctw * 8)));
     Scratch yp(c, sizeof(uint64_t) * (size_t)std::min(chunk, ny) * ctw);
     for (int u0 = 0; u0 < ny; u0 += chunk) {
         const int nu = std::min(chunk, ny - u0);
-        dim3 grid(nblocks(N, 128), nl, (nu + UG - 1) / UG);
-        launch_pdl(k_pt_matvec<UG>, dim3(grid), dim3(128), 0, c.stream, X, nx, PT + (size_t)u0 * nx, nu, nl, N, c.primes, yp.as<uint64_t>());
+        dim3 grid(nblocks(N / 2, 128), nl, (nu + UG - 1) / UG);
+        launch_pdl(k_pt_matvec<UG, JU>, dim3(grid), dim3(128), 0, c.stream, X, nx, PT + (size_t)u0 * nx, nu, nl, N, c.primes, yp.as<uint64_t>());
         check_launch("k_pt_matvec");
         std::vector<const uint64_t *> ins(nu);
         for (int u = 0; u < nu; u++) ins[u] = yp.as<uint64_t>() + (size_t)u * ctw;
         PtrTable ti(c, ins);
         rescale(c, ti.c_(), Y + u0, nu, 2, level);
+    }
+}
+
+void pt_matvec(Ctx &c, const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int level, uint64_t *const *Y) {
+    static const int ug = [] {
+        const char *e = getenv("VR_PMV_UG");
+        return e ? atoi(e) : 2;
+    }();
+    switch (ug) {
+        case 1: pt_matvec_ug<1, 4>(c, X, nx, PT, ny, level, Y); break;
+        case 3: pt_matvec_ug<2, 4>(c, X, nx, PT, ny, level, Y); break;
+        case 4: pt_matvec_ug<4, 2>(c, X, nx, PT, ny, level, Y); break;
+        default: pt_matvec_ug<2, 2>(c, X, nx, PT, ny, level, Y); break;
     }
 }
 
