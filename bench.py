@@ -200,7 +200,7 @@ def run_reference(args, ws, rank):
         "data": "synthetic (seed 1, U[-1,1])",
         "config": {"workload": "cfg2 HE matmul 64x64 (n=64 column ciphertexts), N=2^14, 5 primes + P"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} cfg-2 HE matmuls (matmul_outer on resident ciphertexts) in the C RNS-CKKS oracle, OpenMP over limbs",
+                         "sample": f"{args.steps} cfg-2 HE matmuls (matmul_outer on resident ciphertexts) in the C RNS-CKKS oracle, OpenMP over (limb, coefficient chunk) work items and key-switch target primes",
                          "max_abs_err": err},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_simulator": {"value": 1.0 / sim_t, "unit": UNIT, "cores": 1,
@@ -344,7 +344,7 @@ def run_ours(args, ws, rank, local):
             times, cerr = cpu_port_matmul(reps=2)
             cv = 1.0 / statistics.median(times)
             cpu = {"value": cv, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-                   "sample": "2 cfg-2 HE matmuls (matmul_outer on resident ciphertexts) in the C RNS-CKKS oracle, OpenMP",
+                   "sample": "2 cfg-2 HE matmuls (matmul_outer on resident ciphertexts) in the C RNS-CKKS oracle, OpenMP over (limb, coefficient chunk) work items and key-switch target primes",
                    "max_abs_err": cerr}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port", "sample": f"failed: {exc}"}

@@ -651,13 +651,21 @@ static void keyswitch_acc(orc_ctx *c, const uint64_t *cpoly, int level, const ui
     const int n = c->n, nl = level + 1, np = c->np, P = np - 1;
     const int nt = nl + 1; /* target primes q0..ql, P */
     memset(acc, 0, 16ull * nt * n);
-    uint64_t *x = malloc(8ull * n), *d = malloc(8ull * n);
+    /* the digits' coefficient forms first, then one independent work item per target prime
+       (threads never share an accumulator; per-target accumulation order is j = 0..l) */
+    uint64_t *xs = malloc(8ull * nl * n);
+#pragma omp parallel for schedule(static)
     for (int j = 0; j < nl; j++) {
-        memcpy(x, cpoly + (size_t)j * n, 8ull * n);
-        orc_intt(c, j, x);
-        for (int t = 0; t < nt; t++) {
-            const int pidx = t < nl ? t : P;
-            const uint64_t q = c->q[pidx];
+        memcpy(xs + (size_t)j * n, cpoly + (size_t)j * n, 8ull * n);
+        orc_intt(c, j, xs + (size_t)j * n);
+    }
+#pragma omp parallel for schedule(dynamic)
+    for (int t = 0; t < nt; t++) {
+        uint64_t *d = malloc(8ull * n);
+        const int pidx = t < nl ? t : P;
+        const uint64_t q = c->q[pidx];
+        for (int j = 0; j < nl; j++) {
+            const uint64_t *x = xs + (size_t)j * n;
             if (t == j) memcpy(d, cpoly + (size_t)j * n, 8ull * n);
             else {
                 for (int k = 0; k < n; k++) d[k] = lift_centered(x[k], c->q[j], q);
@@ -669,8 +677,9 @@ static void keyswitch_acc(orc_ctx *c, const uint64_t *cpoly, int level, const ui
                 for (int k = 0; k < n; k++) a[k] = addmod(a[k], mulmod(d[k], kk[k], q), q);
             }
         }
+        free(d);
     }
-    free(x); free(d);
+    free(xs);
 }
 
 /* hybrid key switch, dnum = l+1 single-prime digits, one special prime P.
@@ -722,17 +731,25 @@ void orc_relin_rescale(orc_ctx *c, const uint64_t *d3, int level, uint64_t *out)
     const uint64_t Pq = c->q[P], ql = c->q[level];
     uint64_t *acc = malloc(16ull * nt * n);
     keyswitch_acc(c, d3 + (size_t)2 * nl * n, level, get_rlk(c), acc);
-    uint64_t *yq = malloc(8ull * n), *yp = malloc(8ull * n), *z = malloc(8ull * n);
+    uint64_t *yqs = malloc(16ull * n), *yps = malloc(16ull * n);
     const uint64_t pinv_ql = invmod(Pq % ql, ql), p_ql = Pq % ql;
+#pragma omp parallel for schedule(static)
     for (int b = 0; b < 2; b++) {
         const uint64_t *ab = acc + (size_t)b * nt * n, *db = d3 + (size_t)b * nl * n;
+        uint64_t *yq = yqs + (size_t)b * n, *yp = yps + (size_t)b * n;
         for (int k = 0; k < n; k++) {
             yq[k] = addmod(mulmod(p_ql, db[(size_t)level * n + k], ql), ab[(size_t)level * n + k], ql);
             yp[k] = ab[(size_t)nl * n + k];
         }
         orc_intt(c, level, yq);
         orc_intt(c, P, yp);
+    }
+#pragma omp parallel for schedule(dynamic) collapse(2)
+    for (int b = 0; b < 2; b++) {
         for (int i = 0; i < level; i++) {
+            const uint64_t *ab = acc + (size_t)b * nt * n, *db = d3 + (size_t)b * nl * n;
+            const uint64_t *yq = yqs + (size_t)b * n, *yp = yps + (size_t)b * n;
+            uint64_t *z = malloc(8ull * n);
             const uint64_t q = c->q[i], pm = Pq % q, pqm = mulmod(pm, ql % q, q);
             const uint64_t inv = invmod(pqm, q);
             for (int k = 0; k < n; k++) {
@@ -749,9 +766,10 @@ void orc_relin_rescale(orc_ctx *c, const uint64_t *d3, int level, uint64_t *out)
                 const uint64_t x = addmod(mulmod(pm, db[(size_t)i * n + k], q), ab[(size_t)i * n + k], q);
                 o[k] = mulmod(submod(x, z[k], q), inv, q);
             }
+            free(z);
         }
     }
-    free(acc); free(yq); free(yp); free(z);
+    free(acc); free(yqs); free(yps);
 }
 
 uint32_t orc_galois_elt(const orc_ctx *c, int64_t steps) {
@@ -807,18 +825,24 @@ void orc_mul(orc_ctx *c, const uint64_t *a, const uint64_t *b, int level, uint64
 void orc_matmul_outer(orc_ctx *c, const uint64_t *const *Ls, const uint64_t *const *Rs, int count, int level, uint64_t *out) {
     const int n = c->n, nl = level + 1;
     uint64_t *d = calloc((size_t)3 * nl * n, 8);
-#pragma omp parallel for schedule(static)
+    /* (limb, coefficient chunk) work items so every host thread has work (the per-coefficient
+       accumulation order over t is unchanged) */
+    const int nch = n >= 64 ? 32 : 1;
+#pragma omp parallel for schedule(static) collapse(2)
     for (int i = 0; i < nl; i++) {
+        for (int ch = 0; ch < nch; ch++) {
         const uint64_t q = c->q[i];
         const size_t o0 = (size_t)i * n, o1 = (size_t)(nl + i) * n, o2 = (size_t)(2 * nl + i) * n;
+        const int k0 = ch * (n / nch), k1 = k0 + n / nch;
         for (int t = 0; t < count; t++) {
             const uint64_t *a = Ls[t], *b = Rs[t];
-            for (int k = 0; k < n; k++) {
+            for (int k = k0; k < k1; k++) {
                 uint64_t a0 = a[o0 + k], a1 = a[o1 + k], b0 = b[o0 + k], b1 = b[o1 + k];
                 d[o0 + k] = addmod(d[o0 + k], mulmod(a0, b0, q), q);
                 d[o1 + k] = addmod(d[o1 + k], addmod(mulmod(a0, b1, q), mulmod(a1, b0, q), q), q);
                 d[o2 + k] = addmod(d[o2 + k], mulmod(a1, b1, q), q);
             }
+        }
         }
     }
     orc_relin_rescale(c, d, level, out);
