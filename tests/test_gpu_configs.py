@@ -131,3 +131,27 @@ def test_cfg3_full_size_decoded():
     assert got.shape == (64, 10)
     assert float(np.max(np.abs(got - want))) < TOL
     assert all(c.level == 0 and c.depth == 5 for c in logits)
+
+
+@pytest.mark.parametrize("slots,nx,ny", [(1024, 131, 3), (4, 5, 3)])
+def test_dense_columns_bit_exact(slots, nx, ny):
+    """k_pt_matvec: more inputs than one shared-memory pointer chunk (128), an odd output count,
+    and a ring smaller than one CTA's coefficient tile; residues vs the oracle's cmul/add/rescale."""
+    from paper_2512_18646_b200 import EngineParams
+    from paper_2512_18646_b200.cnn import dense_columns, encode_plain_batch
+
+    p = EngineParams(slots=slots, prime_bits=(60, 40, 40), delta=40, seed=5)
+    g, o = CkksEngine(p), OracleEngine.from_params(p)
+    rng = np.random.default_rng(11)
+    xs = rng.uniform(-1, 1, (nx, slots))
+    ws = rng.uniform(-1, 1, (ny * nx, slots))
+    gx, ox = [g.enc(v) for v in xs], [o.enc(v) for v in xs]
+    lv = gx[0].level
+    ys = dense_columns(g, gx, encode_plain_batch(g, ws, lv, g.scales[lv]), ny)
+    for u in range(ny):
+        acc = None
+        for j in range(nx):
+            term = o.c.mul_plain(ox[j].data, o.c.encode(ws[u * nx + j], lv, o.scales[lv]))
+            acc = term if acc is None else o.c.add(acc, term)
+        np.testing.assert_array_equal(ys[u].residues(), o.c.rescale(acc))
+        np.testing.assert_allclose(g.dec(ys[u]), (xs * ws[u * nx:(u + 1) * nx]).sum(axis=0), atol=TOL)
