@@ -93,10 +93,13 @@ __device__ __forceinline__ void fft_round(double *re, double *im, int S, int h, 
 }
 
 // all stages of length 2 .. S (S = 2^logS), one barrier per round of up to three stages
+// RBMAX = 2: radix-4 rounds (twice the threads per round, half the dependent chain per thread) for
+// the latency-bound single-ciphertext decode; the butterflies and their order are unchanged.
+template <int RBMAX = 3>
 __device__ __forceinline__ void fft_stages(double *re, double *im, int S, int logS, const double2 *tw, bool inverse) {
     int h = 1, rem = logS;
-    for (; rem >= 3; rem -= 3, h <<= 3) {
-        fft_round<3>(re, im, S, h, tw, inverse);
+    for (; rem >= RBMAX; rem -= RBMAX, h <<= RBMAX) {
+        fft_round<RBMAX>(re, im, S, h, tw, inverse);
         __syncthreads();
     }
     if (rem == 2) {
@@ -136,11 +139,11 @@ __device__ __forceinline__ void stage_twiddles(double2 *tws, const double2 *tw, 
     for (int i = threadIdx.x; i < C; i += blockDim.x) tws[i] = __ldg(tw + i);
 }
 
-template <int CL>
+template <int CL, int RBMAX = 3>
 __device__ __forceinline__ void fft_cluster(double *re, double *im, int S, int logS, const double2 *tw, const double2 *tws,
                                             bool inverse) {
     const int C = S / CL;
-    fft_stages(re, im, C, logS - (CL == 8 ? 3 : 0), tws, inverse);
+    fft_stages<RBMAX>(re, im, C, logS - (CL == 8 ? 3 : 0), tws, inverse);
     if constexpr (CL == 8) {
         namespace cg = cooperative_groups;
         cg::cluster_group cluster = cg::this_cluster();
@@ -176,7 +179,7 @@ struct EncNoise {
 };
 
 // cluster of CL CTAs per ciphertext: slot values -> m [count][N] (int64)
-template <int CL>
+template <int CL, int RBMAX = 3>
 __global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr, const double *zi, const double2 *tw,
                          const int *pos_slot, EncNoise nz, int64_t *m) {
     extern __shared__ double fft_sm[];
@@ -199,7 +202,7 @@ __global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr
         im[fidx<true>(p)] = 0.0;
     }
     __syncthreads();
-    fft_cluster<CL>(re, im, S, logS, tw, tws, true);
+    fft_cluster<CL, RBMAX>(re, im, S, logS, tw, tws, true);
     int64_t *out = m + (size_t)c * 2 * S;
     const uint64_t ke = nz.keys ? stream_key(nz.seed, DOM_ENC_E0, nz.nonce0 + (uint64_t)c, 0) : 0;
 #pragma unroll 4
@@ -219,7 +222,7 @@ __global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr
 }
 
 // cluster of CL CTAs per ciphertext: centred m [count][N], scales[count] -> real slots [count][S]
-template <int CL>
+template <int CL, int RBMAX = 3>
 __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS, const double *zr, const double *zi,
                          const double2 *tw, const int *slot_pos, double *out) {
     extern __shared__ double fft_sm[];
@@ -240,7 +243,7 @@ __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS
         im[fidx<true>(p)] = __dadd_rn(__dmul_rn(ur, zi[k]), __dmul_rn(ui, zr[k]));
     }
     __syncthreads();
-    fft_cluster<CL>(re, im, S, logS, tw, tws, false);
+    fft_cluster<CL, RBMAX>(re, im, S, logS, tw, tws, false);
     double *o = out + (size_t)c * S;
     if constexpr (CL == 8) {
         namespace cg = cooperative_groups;
@@ -455,13 +458,13 @@ size_t fft_smem(int S) {
 }
 
 template <typename K, typename... Args>
-void launch_fft(Ctx &c, K kern, int count, int S, Args... args) {
+void launch_fft_t(Ctx &c, K kern, int count, int S, int tmul, Args... args) {
     const int cl = fft_cl(S);
     const size_t sm = fft_smem(S);
     if (sm > 48 * 1024) VR_CUDA(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(count * cl));
-    cfg.blockDim = dim3((unsigned)fft_threads(S));
+    cfg.blockDim = dim3((unsigned)(fft_threads(S) * tmul));
     cfg.dynamicSmemBytes = sm;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[2];
@@ -476,6 +479,11 @@ void launch_fft(Ctx &c, K kern, int count, int S, Args... args) {
     VR_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
+template <typename K, typename... Args>
+void launch_fft(Ctx &c, K kern, int count, int S, Args... args) {
+    launch_fft_t(c, kern, count, S, 1, args...);
+}
+
 }  // namespace
 
 static void encode_src(Ctx &c, const SlotSrc &vs, int count, double scale, int64_t *d_m, EncNoise nz = EncNoise{}) {
@@ -483,12 +491,23 @@ static void encode_src(Ctx &c, const SlotSrc &vs, int count, double scale, int64
     const double f = scale / (double)S;
     const double2 *tw = reinterpret_cast<const double2 *>(c.ftw);
     if (count <= 0) return;
-    if (fft_cl(S) == FFT_CL)
-        launch_fft(c, k_encode<FFT_CL>, count, S, vs, S, log2i(S), f, (const double *)c.zr, (const double *)c.zi, tw,
-                   (const int *)c.pos_slot, nz, d_m);
-    else
+    // VR_ENC_R4=1: radix-4 rounds with twice the threads (measured slower for the 64-ciphertext
+    // batches of cfg 2: 24 -> 30.5 us; the decode of <= 4 ciphertexts uses them, 25 -> 17 us)
+    static const int enc_r4 = [] {
+        const char *e = getenv("VR_ENC_R4");
+        return e ? atoi(e) : 0;
+    }();
+    if (fft_cl(S) == FFT_CL) {
+        if (enc_r4 && fft_threads(S) <= 512)
+            launch_fft_t(c, k_encode<FFT_CL, 2>, count, S, 2, vs, S, log2i(S), f, (const double *)c.zr, (const double *)c.zi,
+                         tw, (const int *)c.pos_slot, nz, d_m);
+        else
+            launch_fft(c, k_encode<FFT_CL>, count, S, vs, S, log2i(S), f, (const double *)c.zr, (const double *)c.zi, tw,
+                       (const int *)c.pos_slot, nz, d_m);
+    } else {
         launch_fft(c, k_encode<1>, count, S, vs, S, log2i(S), f, (const double *)c.zr, (const double *)c.zi, tw,
                    (const int *)c.pos_slot, nz, d_m);
+    }
     check_launch("k_encode");
 }
 
@@ -580,10 +599,14 @@ void decrypt_decode(Ctx &c, const uint64_t *const *d_cts, const int *d_degs, con
     if (!d_out) return;
     const double2 *tw = reinterpret_cast<const double2 *>(c.ftw);
     if (count > 0) {
-        if (fft_cl(S) == FFT_CL)
-            launch_fft(c, k_decode<FFT_CL>, count, S, (const int64_t *)mp, d_scales, S, log2i(S), (const double *)c.zr,
-                       (const double *)c.zi, tw, (const int *)c.slot_pos, d_out);
-        else
+        if (fft_cl(S) == FFT_CL) {
+            if (count <= 4 && fft_threads(S) <= 512)  // latency-bound: radix-4 rounds, twice the threads
+                launch_fft_t(c, k_decode<FFT_CL, 2>, count, S, 2, (const int64_t *)mp, d_scales, S, log2i(S),
+                             (const double *)c.zr, (const double *)c.zi, tw, (const int *)c.slot_pos, d_out);
+            else
+                launch_fft(c, k_decode<FFT_CL>, count, S, (const int64_t *)mp, d_scales, S, log2i(S), (const double *)c.zr,
+                           (const double *)c.zi, tw, (const int *)c.slot_pos, d_out);
+        } else
             launch_fft(c, k_decode<1>, count, S, (const int64_t *)mp, d_scales, S, log2i(S), (const double *)c.zr,
                        (const double *)c.zi, tw, (const int *)c.slot_pos, d_out);
     }
