@@ -49,16 +49,19 @@ template <int KS_MAXD, int KS_CG>
 __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint64_t *const *P, long long poly_off, int count,
                                                   int level, int N, int logN, int np, const uint64_t *key, uint32_t g,
                                                   DevPrimes pr, uint64_t *A, const NttConst *__restrict__ ncs) {
-    pdl_wait();
-    pdl_trigger();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int nl = level + 1, nt = level + 2;
-    if (e >= (long long)nt * N) return;
+    if (e >= (long long)nt * N) {
+        pdl_wait();
+        pdl_trigger();
+        return;
+    }
     const int k = (int)(e % N), t = (int)(e / N);
     const int c0 = blockIdx.y * KS_CG;
     const int pidx = t < nl ? t : np - 1;
     const Modulus m = pr.m[pidx];
     const int src = galois_src(k, g, logN);
+    // the key is constant: its loads are issued before the PDL wait (they overlap the ModUp tail)
     uint64_t k0[KS_MAXD], k1[KS_MAXD];
 #pragma unroll
     for (int j = 0; j < KS_MAXD; j++) {
@@ -67,6 +70,8 @@ __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint6
             k1[j] = __ldg(key + (((size_t)j * 2 + 1) * np + pidx) * N + k);
         }
     }
+    pdl_wait();
+    pdl_trigger();
     uint64_t dv[KS_CG][KS_MAXD];
 #pragma unroll
     for (int cc = 0; cc < KS_CG; cc++) {

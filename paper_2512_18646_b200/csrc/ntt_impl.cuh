@@ -170,6 +170,7 @@ struct PassArgs {
     int last;     // this pass writes the final (fully reduced) output through the store functor
     int raw_in;   // input is the other pass's intermediate (FP64 body: raw double bits)
     int raw_out;  // output is an intermediate for the other pass
+    int prefetch = 0;  // pull this CTA's twiddles into L2 before the PDL wait (small latency-bound batches)
 };
 
 // Index algebra shared by every caller: a unit's elements sit at base | (w << log2(d)), w < 2^R,
@@ -418,6 +419,26 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
 // and still run faster: config 4 49.2 -> 52.1 images/s, the fused encryption NTT 110 -> 82 us.
 constexpr int kCapRegs = 64;
 
+// Pull the twiddles a pass's CTA will read into L2 before the PDL wait (the tables are constant,
+// so this overlaps the previous kernel's tail).  Between the steps of a workload the streaming
+// passes (the tensor sums read 250 MB per cfg-2 step) evict them, and the small latency-bound
+// batches of a key switch otherwise pay one HBM round trip per radix group (cfg-2 chain 47.5 ->
+// 44.8 us).  Only the small-batch (radix-4) passes do it: for large batches the twiddles stay in
+// L2 and the extra instructions cost throughput (cfg 4 52.4 -> 47.7 images/s when unconditional).  Stage g of this CTA
+// reads entries [2^g + h_lo 2^(g-s0), 2^g + (h_hi + 1) 2^(g-s0)) with h = tile >> lo_bits.
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+template <int LOGT>
+__device__ __forceinline__ void prefetch_pass_twiddles(const PassArgs &a, const char *table, int esz, int tile0) {
+    const int lo_bits = a.logN - a.s0 - LOGT;
+    const long long hlo = tile0 >> lo_bits, hhi = (tile0 + a.TPC - 1) >> lo_bits;
+#pragma unroll 1
+    for (int s = 0; s < LOGT; s++) {
+        const long long g0 = 1ll << (a.s0 + s);
+        const long long l0 = ((g0 + (hlo << s)) * esz) >> 7, l1 = ((g0 + ((hhi + 1) << s)) * esz - 1) >> 7;
+        for (long long l = l0 + threadIdx.x; l <= l1; l += blockDim.x) prefetch_l2(table + (l << 7));
+    }
+}
+
 template <bool INV, bool COLS, int LOGT, int LE, class LD, class ST>
 __global__ void __launch_bounds__(512, 65536 / (512 * kCapRegs)) ntt_pass(NttBatch b, PassArgs a, DevPrimes pr, const ulonglong2 *__restrict__ tw,
                                                 const double *__restrict__ twd, const NttConst *__restrict__ ncs, LD ld,
@@ -429,9 +450,15 @@ __global__ void __launch_bounds__(512, 65536 / (512 * kCapRegs)) ntt_pass(NttBat
     const int t = blockIdx.x / chunks;
     uint64_t *ptr;
     int pidx;
+    const bool live = locate(b, t, N, ptr, pidx);  // batch metadata only (no global reads)
+    if (live && a.prefetch) {
+        const bool f64 = ncs[pidx].f64;  // constant table
+        prefetch_pass_twiddles<LOGT>(a, f64 ? (const char *)(twd + (size_t)pidx * N) : (const char *)(tw + (size_t)pidx * N),
+                                     f64 ? 8 : 16, ((int)blockIdx.x - t * chunks) * a.TPC);
+    }
     pdl_wait();
     pdl_trigger();
-    if (!locate(b, t, N, ptr, pidx)) return;
+    if (!live) return;
     const NttConst nc = ncs[pidx];
     (void)T;
     if (nc.f64) ntt_pass_body<INV, COLS, LOGT, LE, true>(b, a, pr, tw, twd, nc, ptr, t, pidx, ld, st, sm);
@@ -732,8 +759,8 @@ void run_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
         return e ? atoi(e) : 64;
     }();
     const int le = b.count <= small_batch ? 2 : 3;
-    PassArgs p1{logN, 0, pick_tpc(b.count, 1 << lb, T1, 16, 4, le), 0, 0, 0};
-    PassArgs p2{logN, la, pick_tpc(b.count, 1 << la, T2, 2048 / T2, 1, le), 0, 0, 0};
+    PassArgs p1{logN, 0, pick_tpc(b.count, 1 << lb, T1, 16, 4, le), 0, 0, 0, le == 2};
+    PassArgs p2{logN, la, pick_tpc(b.count, 1 << la, T2, 2048 / T2, 1, le), 0, 0, 0, le == 2};
     // the first pass hands its intermediate to the second (raw doubles on the FP64 body)
     (INV ? p2 : p1).raw_out = 1;
     (INV ? p1 : p2).raw_in = 1;
