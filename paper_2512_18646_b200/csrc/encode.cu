@@ -231,6 +231,16 @@ __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS
     double *re = fft_sm, *im = fft_sm + C + C / 8;
     double2 *tws = reinterpret_cast<double2 *>(im + C + C / 8);
     stage_twiddles(tws, tw, C);
+    if constexpr (RBMAX == 2) {
+        // latency-bound single-ciphertext decode: the constant twist tables zr/zi (read at bit-reversed
+        // positions spread over every line) and this CTA's slot map go to L2 before the PDL wait
+        const int lines = S / 16;  // 128-byte lines of one [S] double table
+        for (int l = rank * (lines / CL) + threadIdx.x; l < (rank + 1) * (lines / CL); l += blockDim.x) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(zr + 16 * l));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(zi + 16 * l));
+        }
+        for (int l = threadIdx.x; l < C / 32; l += blockDim.x) asm volatile("prefetch.global.L2 [%0];" ::"l"(slot_pos + base + 32 * l));
+    }
     pdl_wait();
     pdl_trigger();
     const int64_t *mc = m + (size_t)c * 2 * S;
