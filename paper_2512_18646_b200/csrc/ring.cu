@@ -644,7 +644,25 @@ void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int 
     switch (nb) {
         case 1: ts_variant<1>(c, variant, L, R, n, nl, O); break;
         case 2: ts_variant<2>(c, variant, L, R, n, nl, O); break;
-        case 4: ts_variant<4>(c, variant, L, R, n, nl, O); break;
+        case 4: {
+            // four row blocks sharing R (cfg 5a): two launches of two row blocks.  R is streamed twice,
+            // but each CTA holds half the 128-bit accumulators (104 instead of 188 registers, 3 CTAs
+            // per SM instead of 2): cfg-5a matmul 2.12 -> 1.56 ms.  Swept on B200 (tools/prof_5a.sh):
+            // one NB=4 kernel 2.12 ms (tiles 128 / split 4: 2.81; tile 256 / split 4: 2.52), two NB=2
+            // launches with 512-tiles 1.76, 8 stages 1.96, split 4 1.70, four NB=1 launches 1.69.
+            // VR_TS4=1 restores the single NB=4 kernel.
+            static const int v4 = [] {
+                const char *e = getenv("VR_TS4");
+                return e ? atoi(e) : 0;
+            }();
+            if (v4 == 1) {
+                ts_variant<4>(c, variant, L, R, n, nl, O);
+            } else {
+                launch_ts<2, 256, 2, 4>(c, L, R, n, nl, O);
+                launch_ts<2, 256, 2, 4>(c, L + 2 * (size_t)n, R, n, nl, O + 2);
+            }
+            break;
+        }
         default: throw VrError(3, "tensor_sum: nblocks must be 1, 2 or 4");
     }
     check_launch("k_tensor_sum");
