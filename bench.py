@@ -515,7 +515,7 @@ def bench_cfg4(steps=2):
     te = time.perf_counter() - t0
     return {"metric": "encrypted-CNN images/s (cfg4 conv 16x3x3x3 + degree-2 activation, 16 images/batch, N=2^15)",
             "value": 16 / t, "s_per_batch": t, "max_abs_err": err, "launches_per_batch": launches,
-            "e2e_images_per_s": 16 / te, "e2e_h2d_bytes": 3 * 226 * 16 * 226 * 8, "e2e_d2h_bytes": 16 * 224 * eng.slots * 8}
+            "e2e_images_per_s": 16 / te, "e2e_h2d_bytes": 3 * 226 * 16 * 226 * 8, "e2e_d2h_bytes": 16 * 224 * 16 * 224 * 8}
 
 
 def bench_cfg3(steps=3):

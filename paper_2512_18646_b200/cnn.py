@@ -86,8 +86,10 @@ def decode_layer(engine: CkksEngine, ys, stride: int = 1) -> np.ndarray:
     """Decrypt a conv layer's output to (m, F, out_h, out_w) (rows subsampled by ``stride``)."""
     outs = []
     for y in ys:
-        vecs = engine.dec_batch(y.cts)  # [w][slots]
-        img = np.stack([vecs[:, b * y.stride: b * y.stride + y.h].T for b in range(y.m)])  # (m, h, w)
+        # only the valid slots (b * stride + i, i < h) leave the device: [w][m * h]
+        sel = (np.arange(y.m)[:, None] * y.stride + np.arange(y.h)[None, :]).reshape(-1)
+        vecs = engine.dec_batch(y.cts, select=sel)
+        img = vecs.reshape(len(y.cts), y.m, y.h).transpose(1, 2, 0)  # (m, h, w)
         outs.append(img[:, ::stride, :])
     return np.stack(outs, axis=1)
 

@@ -323,7 +323,9 @@ class CkksEngine:
         """Full slot vector (real parts), like engine.py:204-206."""
         return self.dec_batch([ct])[0]
 
-    def dec_batch(self, cts) -> np.ndarray:
+    def dec_batch(self, cts, select=None) -> np.ndarray:
+        """Decrypt + decode many ciphertexts -> [count][slots] (real parts).  ``select`` (slot
+        indices) keeps only those slots, gathered on the device before the copy to the host."""
         cts = list(cts)
         for ct in cts:
             self._check(ct)
@@ -334,6 +336,9 @@ class CkksEngine:
         scl = (ctypes.c_double * count)(*[ct.scale for ct in cts])
         _lib.check(self._lib.vr_decrypt_decode(self._h, _lib.ptr_array([ct.ptr() for ct in cts]), degs, lvls, scl,
                                                count, out.data_ptr(), None))
+        if select is not None:
+            idx = torch.as_tensor(np.asarray(select, dtype=np.int64), device=self.device)
+            out = out.index_select(1, idx)
         return out.cpu().numpy()
 
     def add(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:

@@ -321,8 +321,7 @@ def conv_columns_multi(engine: CkksEngine, imgs, weights, biases, out_cols=None)
 
 def reassemble_columns(engine: CkksEngine, img: ColumnEncodedImage) -> np.ndarray:
     """Decode to an (m, h, w) array (multicipher.py:165-172); one batched decrypt."""
-    vecs = engine.dec_batch(img.cts)  # [w][slots]
-    out = np.empty((img.m, img.h, img.w), dtype=np.float64)
-    for b in range(img.m):
-        out[b, :, :] = vecs[:, b * img.stride: b * img.stride + img.h].T
-    return out
+    # only the slots the reference reads (b * stride + i, i < h) are copied to the host
+    sel = (np.arange(img.m)[:, None] * img.stride + np.arange(img.h)[None, :]).reshape(-1)
+    vecs = engine.dec_batch(img.cts, select=sel)  # [w][m * h]
+    return np.ascontiguousarray(vecs.reshape(len(img.cts), img.m, img.h).transpose(1, 2, 0))
