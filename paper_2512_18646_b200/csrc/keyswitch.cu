@@ -239,10 +239,13 @@ static void launch_ks_inner_cg(Ctx &c, const uint64_t *D, const uint64_t *const 
 
 static void launch_ks_inner(Ctx &c, const uint64_t *D, const uint64_t *const *Polys, long long poly_off, int count, int level,
                             const uint64_t *key, uint32_t g, uint64_t *A) {
-    static int cg = [] {
+    static int cg_env = [] {
         const char *e = getenv("VR_KS_CG");
-        return e ? atoi(e) : 2;  // swept on B200: 1/2/4/8 within 2%
+        return e ? atoi(e) : 0;
     }();
+    // swept on B200: 1/2/4/8 within 2% for <= 8 digits; above 8 digits (Table 1, 14 limbs) one
+    // ciphertext per thread (146 instead of 175 registers) is ~1.5% faster
+    const int cg = cg_env ? cg_env : (level + 1 > 8 ? 1 : 2);
     switch (cg) {
         case 1: launch_ks_inner_cg<1>(c, D, Polys, poly_off, count, level, key, g, A); break;
         case 2: launch_ks_inner_cg<2>(c, D, Polys, poly_off, count, level, key, g, A); break;

@@ -288,8 +288,8 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
                 uint64_t *st = ring + (size_t)s * ARR * tile;
                 mbar_expect_tx(&full[s], bytes * ARR);
                 if constexpr (MODE == 1) {
-                    // hint: keep the c1 halves in L2 for the (d0, d1) pass that follows
-                    if (hint) {
+                    // hint bit 0: keep the c1 halves in L2 for the (d0, d1) pass that follows
+                    if (hint & 1) {
 #pragma unroll
                         for (int b = 0; b < NB; b++) bulk_g2s_hint(st + b * tile, L[b * n + t] + o1, bytes, &full[s], pol_keep);
                         bulk_g2s_hint(st + NB * tile, R[t] + o1, bytes, &full[s], pol_keep);

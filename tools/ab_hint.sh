@@ -1,0 +1,1 @@
+for h in 1 2 1 2; do echo -n "VR_TS_HINT=$h "; VR_TS_HINT=$h timeout 300 python tools/chain_probe.py 2>&1 | tail -1; done
