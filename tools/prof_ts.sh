@@ -1,5 +1,5 @@
 python tools/step_profile.py --cfg 2 --steps 2 > gpurun_out/plain_ts.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_tensor_sum -s 0 -c 2 -o /tmp/prof_ts python tools/step_profile.py --cfg 2 --steps 2 > gpurun_out/ncu_ts.log 2>&1; echo "ncu rc=$?"
+ncu -f --set full --clock-control none --import-source on -k regex:k_tensor_sum -s 0 -c 2 -o /tmp/prof_ts python tools/step_profile.py --cfg 2 --steps 2 > gpurun_out/ncu_ts.log 2>&1; echo "ncu rc=$?"
 python tools/ncu_summarize.py /tmp/prof_ts.ncu-rep gpurun_out/ncu_summary.json
 ncu -i /tmp/prof_ts.ncu-rep --page raw --csv > gpurun_out/ts_raw.csv 2>&1
 python tools/step_profile.py --cfg 2 --steps 3 > gpurun_out/prof_plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -s $(grep launches_before gpurun_out/prof_plain.log | cut -d= -f2) -c 40 --csv --log-file gpurun_out/launches_cfg2.csv python tools/step_profile.py --cfg 2 --steps 3 > gpurun_out/ncu_launch.log 2>&1; echo "ncu2 rc=$?"
