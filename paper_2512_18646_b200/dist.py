@@ -3,11 +3,13 @@
 * HE matmul (config 5a): C = sum_k L_k * R_k is a sum over independent column
   ciphertexts (multicipher.py:100-102).  Rank g owns a contiguous
   k range, computes the degree-2 partial sum locally (one fused tensor-sum
-  launch for every row block), the partials are summed with ONE NCCL
-  all-reduce in int64 (every residue is < 2^60, so up to 8 ranks cannot
-  overflow), reduced mod q, then relinearised and rescaled once.  Because the
-  modular sum is exact and relinearisation happens after it, the result is
-  bit-identical for 1, 2, 4 or 8 ranks.
+  launch for every row block), the partials are summed in int64 (every
+  residue is < 2^60, so up to 8 ranks cannot overflow) -- either one NCCL
+  all-reduce (every rank finishes every block) or one reduce per row block to
+  its owner rank (``matmul_outer_sharded_owned``: each rank relinearises only
+  its own blocks) -- then reduced mod q, relinearised and rescaled once.
+  Because the modular sum is exact and relinearisation happens after it, the
+  result is bit-identical for 1, 2, 4 or 8 ranks.
 * HE conv (config 5b): images are independent; groups of images shard across
   ranks with no collective at all.
 
@@ -24,8 +26,9 @@ from . import _lib
 from .engine import Ciphertext, CkksEngine, EngineError, LayoutError
 from .multicipher import ColumnEncodedMatrix
 
-__all__ = ["shard_range", "matmul_nonce_plan", "encode_operands_sharded", "allreduce_partials", "matmul_partials",
-           "matmul_finish", "matmul_outer_sharded", "image_groups"]
+__all__ = ["shard_range", "matmul_nonce_plan", "encode_operands_sharded", "allreduce_partials", "block_owner",
+           "reduce_partials_to_owners", "matmul_partials", "matmul_finish", "matmul_outer_sharded",
+           "matmul_outer_sharded_owned", "image_groups"]
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -72,6 +75,30 @@ def allreduce_partials(partial: torch.Tensor, group=None) -> torch.Tensor:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
     return partial
+
+
+def block_owner(block: int, world: int) -> int:
+    """Rank that finishes (relinearises + rescales) row block ``block``: round robin."""
+    return block % world
+
+
+def reduce_partials_to_owners(partial: torch.Tensor, group=None) -> list[int]:
+    """Sum each row block's degree-2 partial onto its owner rank only (one reduce per block, int64, no
+    modular reduction) and return the blocks this rank owns.  Every rank then relinearises only its
+    own blocks instead of all of them: the finishing work is sharded too."""
+    import torch.distributed as dist
+
+    if partial.dtype != torch.int64:
+        raise EngineError("partials must be int64 residues")
+    nb = partial.shape[0]
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return list(range(nb))
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    for b in range(nb):
+        owner = block_owner(b, world)
+        dst = owner if group is None else dist.get_global_rank(group, owner)
+        dist.reduce(partial[b], dst=dst, op=dist.ReduceOp.SUM, group=group)
+    return [b for b in range(nb) if block_owner(b, world) == rank]
 
 
 def matmul_partials(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -> tuple[torch.Tensor, int]:
@@ -121,6 +148,18 @@ def matmul_outer_sharded(engine: CkksEngine, lefts, right: ColumnEncodedMatrix, 
     part, lv = matmul_partials(engine, lefts, right)
     allreduce_partials(part, group)
     return matmul_finish(engine, part, lv, right.m, right.p)
+
+
+def matmul_outer_sharded_owned(engine: CkksEngine, lefts, right: ColumnEncodedMatrix, group=None) -> dict[int, Ciphertext]:
+    """Distributed matmul_outer with the finish sharded as well: local tensor-sum, per-block reduce to the
+    block's owner, then each rank relinearises + rescales only the blocks it owns ({block: ciphertext};
+    empty on ranks that own none).  Residues are identical to matmul_outer_sharded's."""
+    part, lv = matmul_partials(engine, lefts, right)
+    mine = reduce_partials_to_owners(part, group)
+    if not mine:
+        return {}
+    sub = part if len(mine) == part.shape[0] else part[mine].contiguous()
+    return dict(zip(mine, matmul_finish(engine, sub, lv, right.m, right.p)))
 
 
 def image_groups(n_images: int, group: int, rank: int, world: int) -> list[tuple[int, int]]:

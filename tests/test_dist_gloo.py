@@ -13,7 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2512_18646_b200.dist import allreduce_partials, image_groups, matmul_nonce_plan, shard_range
+from paper_2512_18646_b200.dist import (allreduce_partials, block_owner, image_groups, matmul_nonce_plan,
+                                        reduce_partials_to_owners, shard_range)
 
 SLOTS, BITS, DELTA, SEED = 64, (60, 40, 40), 40, 7
 NB, M, N_K, P = 2, 4, 6, 8
@@ -127,3 +128,44 @@ def test_sharded_matmul_bit_exact_world2():
             np.testing.assert_array_equal(got[rank][bi], want[bi])
     dec = o.dec(type("C", (), {"data": want[0], "scale": o.scales[o.L - 1]})())
     np.testing.assert_allclose(dec[: M * P].reshape(M, P), a[0] @ b, atol=1e-3)
+
+
+def _worker_owned(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b = _inputs()
+        o = _oracle()
+        lo, hi = shard_range(N_K, rank, world)
+        L, R = _encrypt(o, a, b, range(lo, hi))
+        part = torch.from_numpy(_partial(o, L, R, range(lo, hi)))
+        mine = reduce_partials_to_owners(part)
+        res = _finish(o, part.numpy())  # only the owned blocks hold the full sum
+        q.put((rank, mine, {bi: res[bi].copy() for bi in mine}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_owner_reduce_bit_exact_world2():
+    """Per-block reduce to the owner rank (the finish sharded over ranks): every block is owned by
+    exactly one rank and its finished residues equal the unsharded result."""
+    a, b = _inputs()
+    o = _oracle()
+    L, R = _encrypt(o, a, b, range(N_K))
+    want = _finish(o, _partial(o, L, R, range(N_K)))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_owned, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    owned = sorted(bi for _, mine, _ in got for bi in mine)
+    assert owned == list(range(NB))
+    for rank, mine, res in got:
+        assert mine == [bi for bi in range(NB) if block_owner(bi, 2) == rank]
+        for bi in mine:
+            np.testing.assert_array_equal(res[bi], want[bi])

@@ -37,3 +37,21 @@ def test_cfg5a_sharded_equals_unsharded():
         outs = matmul_finish(eng, total, lv, 64, 256)
         for o, r in zip(outs, ref):
             np.testing.assert_array_equal(o.residues(), r)
+
+
+def test_cfg5a_owned_world1_equals_unsharded():
+    """matmul_outer_sharded_owned on one rank finishes every block, bit-identical to matmul_outer_blocks."""
+    from paper_2512_18646_b200.dist import matmul_outer_sharded_owned
+
+    a, b = cfg_matmul(5)
+    blocks = [a[64 * i: 64 * (i + 1)] for i in range(4)]
+    eng = CkksEngine(config_params(5))
+    lefts = [encode_left(eng, blk, 256) for blk in blocks]
+    right = encode_right(eng, b, 64)
+    ref = [w.residues() for w in matmul_outer_blocks(eng, lefts, right)]
+    del lefts, right
+    ls, rs = encode_operands_sharded(eng, blocks, b, 0, 256)
+    outs = matmul_outer_sharded_owned(eng, ls, rs)
+    assert sorted(outs) == [0, 1, 2, 3]
+    for bi, r in enumerate(ref):
+        np.testing.assert_array_equal(outs[bi].residues(), r)
