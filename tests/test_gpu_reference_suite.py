@@ -195,3 +195,44 @@ def test_depth_exhaustion_raises():
     b = eng.mul(a, a)
     with pytest.raises(EngineError):
         eng.mul(b, b)
+
+
+def test_encode_left_right_layouts():  # test_multicipher.py:21-33
+    eng = make_engine(8)
+    left = encode_left(eng, [[1, 2], [3, 4]], p=2)
+    assert len(left.cts) == 2
+    np.testing.assert_allclose(eng.dec(left.cts[0])[:4], [1, 1, 3, 3], atol=TOL)
+    np.testing.assert_allclose(eng.dec(left.cts[1])[:4], [2, 2, 4, 4], atol=TOL)
+    right = encode_right(eng, [[5, 6], [7, 8]], m=2)
+    np.testing.assert_allclose(eng.dec(right.cts[0])[:4], [5, 6, 5, 6], atol=TOL)
+    np.testing.assert_allclose(eng.dec(right.cts[1])[:4], [7, 8, 7, 8], atol=TOL)
+
+
+def test_encode_right_identity_and_zero_left():  # test_multicipher.py:36-50
+    eng = make_engine(16)
+    cem = encode_right(eng, np.eye(3), m=2)
+    for k in range(3):
+        want = np.zeros((2, 3))
+        want[:, k] = 1.0
+        np.testing.assert_allclose(eng.dec(cem.cts[k])[:6].reshape(2, 3), want, atol=TOL)
+    eng8 = make_engine(8)
+    for ct in encode_left(eng8, np.zeros((2, 3)), p=2).cts:
+        assert float(np.max(np.abs(eng8.dec(ct)))) < TOL
+
+
+def test_capacity_checks():  # test_multicipher.py:53-58
+    eng = make_engine(4)
+    with pytest.raises(CapacityError):
+        encode_left(eng, np.ones((3, 2)), p=2)
+    with pytest.raises(CapacityError):
+        encode_image_columns(eng, np.ones((5, 3)))
+
+
+def test_matmul_outer_single_term(rng):  # test_multicipher.py:69-74
+    eng = make_engine(8)
+    a, b = rand_int_matrix(rng, 2, 1), rand_int_matrix(rng, 1, 3)
+    before = eng.meter_snapshot()
+    got = matmul_outer(eng, encode_left(eng, a, 3), encode_right(eng, b, 2)).decode(eng)
+    d = eng.meter_snapshot().delta_since(before)
+    np.testing.assert_allclose(got, a @ b, atol=TOL)
+    assert (d.mul_count, d.add_count, d.rot_count) == (1, 0, 0)
