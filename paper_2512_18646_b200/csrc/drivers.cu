@@ -442,8 +442,8 @@ static void poly_activation_chunk(Ctx &c, const uint64_t *const *X, int count, i
     PtrTable tx2(c, strided(x2.as<uint64_t>(), count, w1)), tpre(c, strided(pre.as<uint64_t>(), count, w1));
     mul_batch(c, X, X, tx2.m_(), count, level);  // x^2 at level-1
     if (c3_zero) {
-        mul_scalar(c, tx2.c_(), tpre.m_(), count, 2, level, limb_scalars(c, kc[1], level));
-        axpy(c, tpre.m_(), X, count, 2, level, level + 1, limb_scalars(c, kc[2], level));
+        scale_axpy(c, tx2.c_(), X, tpre.m_(), count, 2, level, level + 1, limb_scalars(c, kc[1], level),
+                   limb_scalars(c, kc[2], level));
         rescale(c, tpre.c_(), Out, count, 2, level - 1);
     } else {
         Scratch inner(c, sizeof(uint64_t) * count * w1), xs(c, sizeof(uint64_t) * count * 2 * (level + 1) * N),

@@ -120,6 +120,22 @@ __global__ void k_axpy(uint64_t *const *O, const uint64_t *const *B, int count, 
     st2(o, add_mod(a.x, mul_shoup(b.x, w, wsh, q), q), add_mod(a.y, mul_shoup(b.y, w, wsh, q), q));
 }
 
+// O[c][p][i] = C[c][p][i] * s_i + B[c][p][i] * t_i  (B with nlb >= nl limbs): mul_scalar + axpy in one pass
+__global__ void k_scale_axpy(const uint64_t *const *C, const uint64_t *const *B, uint64_t *const *O, int count, int polys,
+                             int nl, int nlb, int N, LimbScalars s, LimbScalars t, DevPrimes pr) {
+    pdl_wait();
+    pdl_trigger();
+    const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pair >= (long long)count * polys * nl * (N / 2)) return;
+    Idx x;
+    decompose(pair, polys, nl, N, x);
+    const uint64_t q = pr.m[x.limb].q, w = s.v[x.limb], wsh = s.sh[x.limb], u = t.v[x.limb], ush = t.sh[x.limb];
+    const size_t off = ((size_t)x.poly * nl + x.limb) * N + x.k;
+    const ulonglong2 a = ld2(C[x.ct] + off), b = ld2(B[x.ct] + ((size_t)x.poly * nlb + x.limb) * N + x.k);
+    st2(O[x.ct] + off, add_mod(mul_shoup(a.x, w, wsh, q), mul_shoup(b.x, u, ush, q), q),
+        add_mod(mul_shoup(a.y, w, wsh, q), mul_shoup(b.y, u, ush, q), q));
+}
+
 __global__ void k_add_const(uint64_t *const *C, int count, int nl, int N, LimbScalars s, DevPrimes pr) {
     pdl_wait();
     pdl_trigger();
@@ -525,6 +541,14 @@ void axpy(Ctx &c, uint64_t *const *O, const uint64_t *const *B, int count, int p
     const long long pairs = (long long)count * polys * nl * (c.n / 2);
     launch_pdl(k_axpy, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, O, B, count, polys, nl, nlb, c.n, s, c.primes);
     check_launch("k_axpy");
+}
+
+void scale_axpy(Ctx &c, const uint64_t *const *C, const uint64_t *const *B, uint64_t *const *O, int count, int polys, int nl,
+                int nlb, const LimbScalars &s, const LimbScalars &t) {
+    const long long pairs = (long long)count * polys * nl * (c.n / 2);
+    launch_pdl(k_scale_axpy, dim3(nblocks(pairs, TB)), dim3(TB), 0, c.stream, C, B, O, count, polys, nl, nlb, c.n, s, t,
+               c.primes);
+    check_launch("k_scale_axpy");
 }
 
 void add_const(Ctx &c, uint64_t *const *C, int count, int nl, const LimbScalars &s) {

@@ -20,6 +20,9 @@ void mul_scalar(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count,
 void add_const(Ctx &c, uint64_t *const *C, int count, int nl, const LimbScalars &s);
 // O[c][p][i] += B[c][p][i] * s_i for i < nl (B has nlb >= nl limbs per poly)
 void axpy(Ctx &c, uint64_t *const *O, const uint64_t *const *B, int count, int polys, int nl, int nlb, const LimbScalars &s);
+// O = C * s + B * t per limb (B with nlb >= nl limbs): one pass instead of mul_scalar + axpy
+void scale_axpy(Ctx &c, const uint64_t *const *C, const uint64_t *const *B, uint64_t *const *O, int count, int polys, int nl,
+                int nlb, const LimbScalars &s, const LimbScalars &t);
 void permute(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl, uint32_t g);
 void copy_limbs(Ctx &c, const uint64_t *const *C, uint64_t *const *O, int count, int polys, int nl_in, int nl_out, int limb0);
 void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl);
