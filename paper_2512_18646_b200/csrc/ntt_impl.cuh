@@ -711,15 +711,16 @@ void launch_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
     check_launch("ntt_cl8");
 }
 
-// Policy (measured on B200, tools/cl_probe.sh): the cluster kernel beats the two passes for
-// large batches at N <= 2^14 (0.243 -> 0.226 us per 2^14 transform at 1280 transforms) but
-// not for the short latency-bound batches of a key switch (relin chain 49 -> 54 us) nor at
+// Policy (measured on B200, tools/cl_probe.sh, tools/ab_cl.sh): the cluster kernel beats the two
+// passes for batches of 32+ transforms at N <= 2^14 (0.243 -> 0.226 us per 2^14 transform at 1280
+// transforms; cfg 3 +1.5% with the threshold at 32 instead of 256) but not for the short
+// latency-bound batches of a single key switch (25-30 transforms; relin chain 49 -> 54 us) nor at
 // N = 2^15 (512-thread CTAs at 80 registers: one CTA per SM).  VR_NTT_CL = minimum batch
-// (default 256; 0 disables).
+// (default 32; 0 disables).
 inline int ntt_cl_min() {
     static const int v = [] {
         const char *e = getenv("VR_NTT_CL");
-        return e ? atoi(e) : 256;
+        return e ? atoi(e) : 32;
     }();
     return v;
 }
