@@ -712,15 +712,17 @@ void launch_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
 }
 
 // Policy (measured on B200, tools/cl_probe.sh, tools/ab_cl.sh): the cluster kernel beats the two
-// passes for batches of 32+ transforms at N <= 2^14 (0.243 -> 0.226 us per 2^14 transform at 1280
-// transforms; cfg 3 +1.5% with the threshold at 32 instead of 256) but not for the short
-// latency-bound batches of a single key switch (25-30 transforms; relin chain 49 -> 54 us) nor at
-// N = 2^15 (512-thread CTAs at 80 registers: one CTA per SM).  VR_NTT_CL = minimum batch
-// (default 32; 0 disables).
+// passes from ~24 transforms at N <= 2^14 (0.243 -> 0.226 us per 2^14 transform at 1280 transforms;
+// cfg 3 +1.5% with the threshold at 24-32 instead of 256).  At 24 the 30-transform ModUp NTT of a
+// single relinearisation runs as one cluster kernel: alone the chain is 2.5 us slower, but inside
+// matmul_outer (next to the streaming (d0, d1) pass) the step is 1.8% faster (83.6 -> 82.2 us).
+// Below ~16 transforms the two passes win (chain 44.7 -> 51.9 us at 8); at N = 2^15 the cluster
+// kernel does not pay (512-thread CTAs at 80 registers: one CTA per SM).  VR_NTT_CL = minimum
+// batch (default 24; 0 disables).
 inline int ntt_cl_min() {
     static const int v = [] {
         const char *e = getenv("VR_NTT_CL");
-        return e ? atoi(e) : 32;
+        return e ? atoi(e) : 24;
     }();
     return v;
 }
