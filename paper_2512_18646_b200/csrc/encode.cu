@@ -24,10 +24,16 @@ namespace {
 
 constexpr int TB = 256;
 
+// Discrete Gaussian by CDT inversion: mag = #{i < CDT_LEN - 1 : r >= cdt[i]} (the table is
+// non-decreasing), i.e. exactly the oracle's linear scan, found by a branch-free 5-step binary
+// search -- no data-dependent loop, so a warp no longer waits for its largest sample.
 __device__ __forceinline__ int64_t gauss(uint64_t u, const uint64_t *cdt) {
+    static_assert(CDT_LEN == 32, "binary search covers 31 entries");
     const uint64_t r = u >> 1;
     int mag = 0;
-    while (mag < CDT_LEN - 1 && r >= cdt[mag]) mag++;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1)
+        if (r >= cdt[mag + s - 1]) mag += s;
     return (u & 1) ? -(int64_t)mag : (int64_t)mag;
 }
 
