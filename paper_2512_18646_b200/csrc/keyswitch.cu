@@ -209,11 +209,25 @@ void rescale(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int count,
     ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), rows, level, N), nttk::LdLift{y.as<uint64_t>(), level, 1, level, N, c.f64mask, c.liftk}, st);
 }
 
-static void modup_impl(Ctx &c, const uint64_t *const *Polys, long long poly_off, int count, int level, uint64_t *D) {
+// cl_intt: run the INTT of the digits as one cluster kernel whatever the batch size.  Measured on
+// B200 for the relinearisation inside matmul_outer, next to the streaming (d0, d1) pass: cfg-2 step
+// 82.6 -> 79.9 us, cfg 1 +5%; for the isolated small ModUps of hoisted rotations it is slower
+// (Algorithm 3 84 -> 74 HE matmul/s), so only the relinearisation path asks for it.
+// VR_MODUP_INTT_CL=0 disables it.
+static void modup_impl(Ctx &c, const uint64_t *const *Polys, long long poly_off, int count, int level, uint64_t *D,
+                       bool cl_intt_wanted = false) {
     const int N = c.n, nl = level + 1, nt = level + 2;
     Scratch x(c, sizeof(uint64_t) * count * nl * N);
-    ntt_inverse_fused(c, batch_limbs(x.as<uint64_t>(), count, nl, N), nttk::LdGather{Polys, nl, (long long)N, poly_off},
-                      nttk::StPlain{});
+    static const int cl_env = [] {
+        const char *e = getenv("VR_MODUP_INTT_CL");
+        return e ? atoi(e) : 1;
+    }();
+    if (cl_intt_wanted && cl_env)
+        ntt_inverse_cl(c, batch_limbs(x.as<uint64_t>(), count, nl, N), nttk::LdGather{Polys, nl, (long long)N, poly_off},
+                       nttk::StPlain{});
+    else
+        ntt_inverse_fused(c, batch_limbs(x.as<uint64_t>(), count, nl, N), nttk::LdGather{Polys, nl, (long long)N, poly_off},
+                          nttk::StPlain{});
     ntt_forward_fused(c, NttBatch{D, count * nl * nt, nt, (long long)nt * N, nl, 0, c.np - 1, nl},
                       nttk::LdLift{x.as<uint64_t>(), nt, nl, -1, N, c.f64mask, c.liftk}, nttk::StPlain{});
 }
@@ -283,11 +297,12 @@ void relin_rescale_batch(Ctx &c, const uint64_t *const *D3, uint64_t *const *Out
     const uint64_t *key = relin_key(c);
     const long long off = (long long)2 * nl * N;
     Scratch d(c, sizeof(uint64_t) * count * nl * nt * N), a(c, sizeof(uint64_t) * count * 2 * nt * N);
-    modup_impl(c, D3, off, count, level, d.as<uint64_t>());
+    modup_impl(c, D3, off, count, level, d.as<uint64_t>(), true);
     launch_ks_inner(c, d.as<uint64_t>(), D3, off, count, level, key, 1, a.as<uint64_t>());
     const uint64_t *rr = c.rr_tab + (size_t)level * RR_STRIDE;
     Scratch y(c, sizeof(uint64_t) * count * 4 * N), z(c, sizeof(uint64_t) * count * 2 * level * N);
     if (d01_ready) VR_CUDA(cudaStreamWaitEvent(c.stream, d01_ready, 0));  // (d0, d1) produced on another stream
+    // (a cluster kernel here measured slower inside matmul_outer: 79.9 -> 84.5 us)
     ntt_inverse_fused(c, NttBatch{y.as<uint64_t>(), count * 4, 2, (long long)2 * N, 1, level, P, 0},
                       LdXrow{a.as<uint64_t>(), D3, rr, level, nt, N}, nttk::StPlain{});
     ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), count * 2, level, N), LdCrt{y.as<uint64_t>(), rr, level, N},

@@ -728,9 +728,9 @@ inline int ntt_cl_min() {
 }
 
 template <bool INV, class LD, class ST>
-bool try_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
+bool try_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st, bool force = false) {
     const int lim = ntt_cl_min();
-    if (lim <= 0 || b.count < lim) return false;
+    if (!force && (lim <= 0 || b.count < lim)) return false;
     switch (c.log_n) {
         case 12: launch_cl8<INV, 9>(c, b, ld, st); return true;
         case 13: launch_cl8<INV, 10>(c, b, ld, st); return true;
@@ -784,5 +784,10 @@ template <class LD, class ST>
 void ntt_forward_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) { nttk::run_fused<false>(c, b, ld, st); }
 template <class LD, class ST>
 void ntt_inverse_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) { nttk::run_fused<true>(c, b, ld, st); }
+// one-kernel cluster transform regardless of the batch threshold (N <= 2^14; else the two passes)
+template <class LD, class ST>
+void ntt_inverse_cl(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
+    if (b.count > 0 && !nttk::try_cl8<true>(c, b, ld, st, true)) nttk::run_fused<true>(c, b, ld, st);
+}
 
 }  // namespace vr
