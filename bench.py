@@ -1,23 +1,32 @@
 #!/usr/bin/env python
 """Benchmark: HE matmul/s of the column-ciphertext matmul (BASELINE.json config 2)
-on B200, plus NTT GB/s and the CPU baselines.
+on B200, plus every other BASELINE config, NTT GB/s, roofline fractions and the
+CPU baselines.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One step = one HE matmul A(64x64)*B(64x64): matmul_outer over n = 64 resident
 column-ciphertext pairs (N = 2^14, 5 ciphertext primes + 60-bit special prime,
 scale 2^40, seed 1) = fused tensor-sum + one relinearisation + one rescale.
-Under torchrun every rank runs independent HE matmuls (weak scaling) and
-`value` is the whole-job throughput, timed on the device as the max over ranks.
 
-`e2e` is the same metric through the public API with host buffers: every step
-uploads A and B from pinned host memory, encrypts the 128 column ciphertexts
-(encode_left/encode_right), runs matmul_outer and downloads the decoded result.
-
-`--impl reference` times the CPU restatement of the same path (oracle/, real
-RNS-CKKS in C + OpenMP) on rank 0 only; the reference package itself is a
-float64 simulator with no cryptography and is reported as
-`reference_simulator` beside it.
+* ``--gpus N`` without torchrun re-launches itself under torchrun with N ranks
+  (and refuses to run if fewer than N GPUs are visible); it never prints a
+  1-GPU line for N > 1.  Under torchrun every rank runs independent config-2
+  HE matmuls (weak scaling) and `value` is the whole-job throughput, timed on
+  the device as the max over ranks; configs 5a / 5b shard one job over the N
+  ranks (strong scaling, NCCL int64 reduce of the 5a partials).
+* `e2e` is the same metric through the public API with host buffers: every
+  step uploads A and B from pinned host memory, encrypts the 128 column
+  ciphertexts (encode_left/encode_right), runs matmul_outer and downloads the
+  decoded result.
+* Every config entry carries a `roofline` (tools/costmodel.py: compulsory
+  bytes B_alg and modmuls M_alg of SURVEY.md 8(d); HBM peak from
+  MEASURED_PEAKS.json, integer peak measured live) and a `cpu_baseline`.
+* `--impl reference` times the CPU restatement of the same path (oracle/: real
+  RNS-CKKS in C + OpenMP, on every host core) on rank 0 only, with the same
+  config dict; the reference package itself is a float64 slot simulator with
+  no cryptography and is reported as
+  `reference_simulator` beside it.
 """
 
 from __future__ import annotations
@@ -26,6 +35,7 @@ import argparse
 import gc
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,10 +48,13 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+from tools import costmodel  # noqa: E402
+
 METRIC = "HE matmul/s (column-ciphertext matmul_outer, BASELINE config 2: A,B 64x64, n=64 cts/operand, N=2^14)"
 UNIT = "HE matmul/s"
 CFG = 2
 DIM = 64
+WORKLOAD = "cfg2 HE matmul 64x64 (n=64 column ciphertexts/operand), N=2^14, q0 60b + 4x40b + P 60b, scale 2^40, seed 1"
 
 
 def parse():
@@ -50,8 +63,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--no-extra", action="store_true", help="skip the NTT/config-1 side measurements")
+    ap.add_argument("--no-extra", action="store_true", help="skip the side configs (headline line only)")
     return ap.parse_args()
+
+
+def die(msg: str, code: int = 2):
+    print(f"bench.py: {msg}", file=sys.stderr, flush=True)
+    sys.exit(code)
 
 
 def dist_env():
@@ -59,6 +77,40 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def config_dict(n_gpus: int) -> dict:
+    """The config both arms report (identical dicts: the driver compares them)."""
+    return {"workload": WORKLOAD, "global_batch": n_gpus, "seq_len": None,
+            "parallelism": f"replicas x{n_gpus} (weak scaling)", "l2": "inputs larger than L2 (128 cts = 168 MB)"}
+
+
+def maybe_spawn(args) -> None:
+    """--gpus N outside torchrun: re-launch under torchrun with N ranks, or fail loudly."""
+    if "WORLD_SIZE" in os.environ:
+        ws = int(os.environ["WORLD_SIZE"])
+        if ws != args.gpus:
+            die(f"--gpus {args.gpus} but torchrun started WORLD_SIZE={ws}")
+        return
+    if args.gpus <= 1:
+        return
+    if args.impl == "reference":
+        return  # the CPU arm runs on rank 0 only; no ranks to start
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        die(f"--gpus {args.gpus} requested but only {have} GPU(s) are visible; refusing to report a smaller run")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr prove N ranks
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    print("bench.py: launching " + " ".join(cmd), file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def inputs(cfg=CFG, dim=DIM):
@@ -75,7 +127,7 @@ class ClockSampler:
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
-    def __init__(self, index: int, period: float = 0.01):
+    def __init__(self, index: int, period: float = 0.005):
         self.index = index
         self.period = period
         self.samples = []
@@ -118,6 +170,11 @@ class ClockSampler:
         self._stop.set()
         if self._t is not None:
             self._t.join(timeout=10)
+        if self._nv is not None and not os.environ.get("VR_BENCH_NO_NVML"):
+            try:
+                self._sample()  # and one at its end
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
@@ -127,7 +184,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def peaks():
+def hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
@@ -145,51 +202,208 @@ def ncu_traffic(kernel: str):
     return v.get("dram_bytes_per_launch")
 
 
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ---------------------------------------------------------------------------
-def cpu_port_matmul(cfg=CFG, dim=DIM, reps=1):
-    """Time the CPU residue oracle (C + OpenMP) on HE matmuls of the same workload."""
+# CPU legs: the C RNS-CKKS oracle (OpenMP, every host thread) and the reference's float64 simulator
+def _oracle_engine(cfg):
     from oracle.engine import OracleEngine
     from paper_2512_18646_b200.params import config_params
 
-    p = config_params(cfg)
-    e = OracleEngine.from_params(p)
-    a, b = inputs(cfg, dim)
-    L = [e.enc(np.repeat(a[:, k], dim)) for k in range(dim)]
-    R = [e.enc(np.tile(b[k, :], dim)) for k in range(dim)]
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        out = e.matmul_outer_blocks([L], R)[0]
-        times.append(time.perf_counter() - t0)
-    got = e.dec(out)[: dim * dim].reshape(dim, dim)
-    err = float(np.max(np.abs(got - a @ b)))
-    return times, err
+    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+    return OracleEngine.from_params(config_params(cfg))
 
 
-def simulator_matmul(cfg=CFG, dim=DIM, reps=20):
-    """Time the reference algorithm (float64 slot simulator, numpy restatement)."""
-    from oracle import sim
+def _random_cts(e, count, level=None):
+    """Uniform residues mod q_i: the timed C-oracle kernels are data-independent, so large CPU
+    samples skip the (slow, irrelevant to the timed op) host encryption."""
+    from oracle.engine import OCt
 
-    a, b = inputs(cfg, dim)
-    slots = {1: 4096, 2: 8192}[cfg]
-    eng = sim.SimEngine(slots)
-    L, R = sim.encode_left(eng, a, dim), sim.encode_right(eng, b, dim)
+    lv = e.L if level is None else level
+    rng = np.random.default_rng(12345)
+    qs = np.array(e.q[: lv + 1], dtype=np.uint64)[None, :, None]
+    out = []
+    for _ in range(count):
+        d = (rng.integers(0, 1 << 62, size=(2, lv + 1, e.N), dtype=np.uint64) % qs).astype(np.uint64)
+        out.append(OCt(d, lv, e.scales[lv]))
+    return out
+
+
+class CpuMatmul:
+    """One warmed C-oracle engine per arm: the relinearisation key is generated by an untimed
+    matmul on THIS engine before any timing (the oracle builds it lazily on first use)."""
+
+    def __init__(self, cfg=CFG, dim=DIM):
+        self.e = _oracle_engine(cfg)
+        self.a, self.b = inputs(cfg, dim)
+        self.dim = dim
+        self.L = [self.e.enc(np.repeat(self.a[:, k], dim)) for k in range(dim)]
+        self.R = [self.e.enc(np.tile(self.b[k, :], dim)) for k in range(dim)]
+        out = self.e.matmul_outer_blocks([self.L], self.R)[0]  # warm-up: builds the relin key
+        got = self.e.dec(out)[: dim * dim].reshape(dim, dim)
+        self.err = float(np.max(np.abs(got - self.a @ self.b)))
+
+    def time(self, reps: int) -> list[float]:
+        t = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            self.e.matmul_outer_blocks([self.L], self.R)
+            t.append(time.perf_counter() - t0)
+        return t
+
+
+def cpu_baseline_matmul(reps=20, warmup=3):
+    """The same measurement as the reference arm (run_reference): one warmed engine, `warmup`
+    untimed matmuls, then the mean of `reps` timed ones."""
+    cm = CpuMatmul()
+    cm.time(warmup)
+    times = cm.time(reps)
+    v = 1.0 / statistics.mean(times)
+    return {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "port", "cpu": cpu_model(),
+            "sample": f"{reps} cfg-2 HE matmuls after {warmup} untimed ones on the same engine (relin key built before "
+                      "timing): matmul_outer on 128 resident ciphertexts in the C RNS-CKKS oracle, OpenMP on every host thread",
+            "ms_per_matmul": 1e3 / v, "max_abs_err": cm.err}
+
+
+def cpu_oracle_matmul_cfg(cfg, n, nb, reps=1):
+    """C oracle matmul_outer_blocks at config cfg (n column pairs, nb row blocks) on uniform random
+    residues.  The operand lists cycle through a pool of at most 64 distinct ciphertexts (>= 300 MB at
+    cfg 5, beyond any host cache): a full cfg-5a operand set would need 6 GB of host memory and the
+    timed op is data-independent."""
+    e = _oracle_engine(cfg)
+    pool = _random_cts(e, min(64, nb * n + n))
+    cts = [pool[i % len(pool)] for i in range(nb * n + n)]
+    lefts = [cts[b * n:(b + 1) * n] for b in range(nb)]
+    R = cts[nb * n:]
+    e.matmul_outer_blocks([lefts[0][:1]], R[:1])  # builds the relin key (untimed)
     t = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        sim.matmul_outer(eng, L, R, dim, dim)
+        e.matmul_outer_blocks(lefts, R)
         t.append(time.perf_counter() - t0)
     return min(t)
 
 
+def cpu_oracle_conv_slice(cfg=4, nout=2, act_cts=4):
+    """C oracle on a slice of the config-4 layer: conv_columns_multi for all 16 filters x 3 channels
+    on output columns 0..nout-1 (rotations of nout+2 input columns), and poly_activation on act_cts
+    outputs.  Returns (seconds per output column of the conv, seconds per activation)."""
+    e = _oracle_engine(cfg)
+    W_in, k, F, C = nout + 2, 3, 16, 3
+    X = _random_cts(e, C * W_in)
+    w = np.random.default_rng(3).normal(0, 0.05, (F, C, k, k))
+    e.conv_columns_multi(X, C, W_in, w[:1], np.zeros(1), [0], 16, 226, 224)  # Galois keys (untimed)
+    t0 = time.perf_counter()
+    Y = e.conv_columns_multi(X, C, W_in, w, np.zeros(F), list(range(nout)), 16, 226, 224)
+    t_conv = (time.perf_counter() - t0) / nout
+    e.poly_activation(Y[0], (0.25, 0.5, 0.125, 0.0))  # relin key (untimed)
+    t0 = time.perf_counter()
+    for y in Y[:act_cts]:
+        e.poly_activation(y, (0.25, 0.5, 0.125, 0.0))
+    t_act = (time.perf_counter() - t0) / act_cts
+    return t_conv, t_act
+
+
+def cpu_oracle_cfg3_slice():
+    """C oracle on config 3's conv + square stage (the dense layers have no oracle driver):
+    5 filters x 13 stride-2 output columns, then the square of the 65 outputs."""
+    e = _oracle_engine(3)
+    X = _random_cts(e, 28)
+    w = np.random.default_rng(2).normal(0, 0.1, (5, 1, 4, 4))
+    e.conv_columns_multi(X[:4], 1, 4, w[:1], np.zeros(1), [0], 64, 28, 25)  # Galois keys (untimed)
+    t0 = time.perf_counter()
+    Y = e.conv_columns_multi(X, 1, 28, w, np.zeros(5), list(range(0, 25, 2)), 64, 28, 25)
+    e.mul(Y[0], Y[0])  # relin key (outside the square timing below)
+    t_conv = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for y in Y:
+        e.mul(y, y)
+    return t_conv + (time.perf_counter() - t0)
+
+
+def simulator_matmul(cfg=CFG, dim=DIM, reps=20, blocks=1):
+    """Time the reference algorithm (float64 slot simulator, numpy restatement of multicipher.py)."""
+    from oracle import sim
+
+    rng = np.random.default_rng(cfg - 1)
+    a = rng.uniform(-1, 1, (dim, dim))
+    b = rng.uniform(-1, 1, (dim, dim))
+    slots = {1: 4096, 2: 8192, 5: 16384}[cfg]
+    eng = sim.SimEngine(slots)
+    m = dim // blocks
+    Ls = [sim.encode_left(eng, a[i * m:(i + 1) * m], dim) for i in range(blocks)]
+    R = sim.encode_right(eng, b, m)
+    t = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for L in Ls:
+            sim.matmul_outer(eng, L, R, m, dim)
+        t.append(time.perf_counter() - t0)
+    return min(t)
+
+
+def simulator_conv_act(filters=1, images=16, slots=16384):
+    """The reference's conv_columns + poly_activation (multicipher.py:123-162, pipeline.py:180-197) as
+    the float64 simulator, config-4 shapes: `filters` filters x 3 channels on 226 padded columns, summed,
+    then the activation of the 224 outputs.  Seconds per filter."""
+    from oracle import sim
+
+    rng = np.random.default_rng(3)
+    imgs = np.pad(rng.uniform(0, 1, (images, 3, 224, 224)), ((0, 0), (0, 0), (1, 1), (1, 1)))
+    w = rng.normal(0, 0.05, (16, 3, 3, 3))
+    eng = sim.SimEngine(slots)
+    chans = [sim.encode_image_columns(eng, imgs[:, c]) for c in range(3)]
+    t0 = time.perf_counter()
+    for f in range(filters):
+        outs = None
+        for c in range(3):
+            cts, geom = chans[c]
+            y, _ = sim.conv_columns(eng, cts, geom, w[f, c], 0.0)
+            outs = y if outs is None else [eng.add(p, q) for p, q in zip(outs, y)]
+        for ct in outs:
+            sim.poly_activation(eng, ct, (0.25, 0.5, 0.125, 0.0))
+    return (time.perf_counter() - t0) / filters
+
+
+def simulator_cfg3(images=64):
+    """The reference's conv_columns (stride 1; the reference has no stride) of config 3's 5 filters on
+    28 columns + the square, as the float64 simulator (conv + square stage only)."""
+    from oracle import sim
+
+    rng = np.random.default_rng(2)
+    imgs = rng.uniform(0, 1, (images, 28, 28))
+    w = rng.normal(0, 0.1, (5, 1, 4, 4))
+    eng = sim.SimEngine(8192)
+    cts, geom = sim.encode_image_columns(eng, imgs)
+    t0 = time.perf_counter()
+    for f in range(5):
+        y, _ = sim.conv_columns(eng, cts, geom, w[f, 0], 0.0)
+        for ct in y[::2]:
+            eng.mul(ct, ct)
+    return time.perf_counter() - t0
+
+
+# ---------------------------------------------------------------------------
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_port_matmul(reps=1)
-    times, err = cpu_port_matmul(reps=args.steps)
+    cores = host_cores()
+    cm = CpuMatmul()
+    for _ in range(max(0, args.warmup)):
+        cm.time(1)
+    times = cm.time(args.steps)
     per = statistics.mean(times)
     v = 1.0 / per
     sim_t = simulator_matmul()
@@ -198,10 +412,12 @@ def run_reference(args, ws, rank):
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seed 1, U[-1,1])",
-        "config": {"workload": "cfg2 HE matmul 64x64 (n=64 column ciphertexts), N=2^14, 5 primes + P"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} cfg-2 HE matmuls (matmul_outer on resident ciphertexts) in the C RNS-CKKS oracle, OpenMP over (limb, coefficient chunk) work items and key-switch target primes",
-                         "max_abs_err": err},
+        "config": config_dict(args.gpus),
+        "max_abs_err": cm.err,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
+                         "sample": f"{args.steps} cfg-2 HE matmuls after {args.warmup} warm-up matmuls on the same "
+                                   "engine (relin key built before timing): matmul_outer on 128 resident ciphertexts "
+                                   "in the C RNS-CKKS oracle, OpenMP on every host thread"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_simulator": {"value": 1.0 / sim_t, "unit": UNIT, "cores": 1,
                                 "note": "reference algorithm as an exact float64 slot simulator (no cryptography)"},
@@ -210,6 +426,71 @@ def run_reference(args, ws, rank):
 
 
 # ---------------------------------------------------------------------------
+def int_peaks(eng):
+    """Register-only butterfly peaks (G butterflies/s): Harvey/Shoup on the IMAD pipe (60-bit primes)
+    and the FP64 Shoup butterfly (primes < 2^46)."""
+    import torch
+
+    from paper_2512_18646_b200 import _lib
+
+    lib = eng._lib
+    sink = torch.zeros(1, dtype=torch.int64, device=eng.device)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    blocks, iters = 148 * 16, 256
+    _lib.check(lib.vr_bench_butterflies(eng.handle, blocks, 16, sink.data_ptr()))
+    torch.cuda.synchronize()
+    st.record()
+    _lib.check(lib.vr_bench_butterflies(eng.handle, blocks, iters, sink.data_ptr()))
+    en.record()
+    torch.cuda.synchronize()
+    peak_int = blocks * 256 * iters * 8 / (st.elapsed_time(en) / 1e3) / 1e9
+    f_iters = 32
+    _lib.check(lib.vr_bench_butterflies_f64(eng.handle, blocks, 4, sink.data_ptr()))
+    torch.cuda.synchronize()
+    st.record()
+    _lib.check(lib.vr_bench_butterflies_f64(eng.handle, blocks, f_iters, sink.data_ptr()))
+    en.record()
+    torch.cuda.synchronize()
+    peak_f64 = blocks * 256 * f_iters * 64 / (st.elapsed_time(en) / 1e3) / 1e9
+    return peak_int, peak_f64
+
+
+def modmul_peak(primes, peaks):
+    """Limb-weighted butterfly peak of a prime chain (FP64 body below 2^46, IMAD body otherwise)."""
+    peak_int, peak_f64 = peaks
+    n_f = sum(1 for q in primes if q < (1 << 46))
+    n = len(primes)
+    return 1.0 / ((n - n_f) / n / peak_int + n_f / n / peak_f64)
+
+
+def roofline_for(key, t_unit, primes, peaks):
+    B, M = costmodel.CONFIGS[key]()
+    r = costmodel.roofline(B, M, t_unit, hbm_peak()[0], modmul_peak(primes, peaks))
+    r["cost_model"] = "tools/costmodel.py (SURVEY.md 8(d)); peak HBM from MEASURED_PEAKS.json, modmul peak = live butterfly probes weighted by the chain's limb mix"
+    return r
+
+
+class Timer:
+    """CUDA events on the current stream (the engine runs on it), max over ranks."""
+
+    def __init__(self, max_over_ranks):
+        import torch
+
+        self.torch = torch
+        self.mor = max_over_ranks
+
+    def __call__(self, fn, reps: int) -> float:
+        torch = self.torch
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        st.record()
+        for _ in range(reps):
+            fn()
+        en.record()
+        torch.cuda.synchronize()
+        return self.mor(st.elapsed_time(en) / 1e3 / reps)
+
+
 def run_ours(args, ws, rank, local):
     import torch
 
@@ -221,10 +502,11 @@ def run_ours(args, ws, rank, local):
     if ws > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eng = CkksEngine(config_params(CFG), device=local)
     lib = eng._lib
-    stream = eng._stream
     a, b = inputs()
     left = encode_left(eng, a, DIM)
     right = encode_right(eng, b, DIM)
@@ -244,9 +526,9 @@ def run_ours(args, ws, rank, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    # setup: let clocks, allocator pools and pointer-table caches settle (untimed)
-    # the warm-up loops hold the previous result exactly like the timed loop, so the allocator has
-    # both output buffers before timing starts (the first second buffer cost one cudaMalloc: ~90 ms)
+    # setup: let clocks, allocator pools and pointer-table caches settle (untimed).  The warm-up
+    # loops hold the previous result exactly like the timed loop, so the allocator has both output
+    # buffers before timing starts.
     t_settle = time.perf_counter()
     out = None
     while time.perf_counter() - t_settle < 0.25:
@@ -258,51 +540,37 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = lib.vr_launch_count()
-    chunks = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if os.environ.get("VR_BENCH_CHUNKS") else None
-    # no Python garbage-collection pauses inside the timed regions (as timeit does): a gen-2
-    # collection stalled the host for up to ~25 ms and starved the device in some runs
+    # no Python garbage-collection pauses inside the timed regions (as timeit does)
     gc.collect()
     gc.disable()
     with ClockSampler(local) as clk:
-        st.record(stream)
-        slow = []
-        for i in range(args.steps):
-            if chunks is not None and i % max(1, args.steps // 4) == 0 and i // max(1, args.steps // 4) < 4:
-                chunks[i // max(1, args.steps // 4)].record(stream)
-            hc = time.perf_counter()
+        st.record()
+        for _ in range(args.steps):
             out = matmul_outer(eng, left, right)
-            if chunks is not None and time.perf_counter() - hc > 1e-3:
-                slow.append((i, round((time.perf_counter() - hc) * 1e3, 2)))
-        en.record(stream)
+        en.record()
         torch.cuda.synchronize()
-    if chunks is not None:
-        chunks[4] = en
-        print("chunk ms:", [round(chunks[j].elapsed_time(chunks[j + 1]), 3) for j in range(4)], "slow host calls:", slow,
-              file=sys.stderr)
     launches = lib.vr_launch_count() - l0
     gc.enable()
     barrier()
     step_s = max_over_ranks(st.elapsed_time(en) / 1e3 / args.steps)
     value = ws / step_s
+    timer = Timer(max_over_ranks)
+    peaks = int_peaks(eng)
 
     # dominant kernel: the (d0, d1) tensor-sum the step runs beside the d2 key switch, timed alone
-    # on the same stream (mode 2 reads all 2n column ciphertexts; mode 1 reads only their c1 halves)
     nl = eng.L + 1
     ptrsL = _lib.ptr_array([c.ptr() for c in left.cts])
     ptrsR = _lib.ptr_array([c.ptr() for c in right.cts])
     d3 = torch.empty((3, nl, eng.N), dtype=torch.int64, device="cuda")
+
+    def ts():
+        _lib.check(lib.vr_tensor_sum_mode(eng.handle, ptrsL, ptrsR, DIM, eng.L, d3.data_ptr(), 2))
+
     for _ in range(3):
-        _lib.check(lib.vr_tensor_sum_mode(eng.handle, ptrsL, ptrsR, DIM, eng.L, d3.data_ptr(), 2))
-    reps = max(args.steps, 20)
-    torch.cuda.synchronize()
-    st.record(stream)
-    for _ in range(reps):
-        _lib.check(lib.vr_tensor_sum_mode(eng.handle, ptrsL, ptrsR, DIM, eng.L, d3.data_ptr(), 2))
-    en.record(stream)
-    torch.cuda.synchronize()
-    ts_s = st.elapsed_time(en) / 1e3 / reps
+        ts()
+    ts_s = timer(ts, max(args.steps, 20))
     alg_bytes = DIM * 4 * nl * eng.N * 8 + 2 * nl * eng.N * 8
-    peak, peak_src = peaks()
+    peak, peak_src = hbm_peak()
     achieved = alg_bytes / ts_s / 1e9
 
     # e2e through the public API with host buffers
@@ -310,21 +578,26 @@ def run_ours(args, ws, rank, local):
     pin_b = torch.from_numpy(b).pin_memory()
     e2e_steps = max(3, min(50, args.steps // 4))
     res = None
+
+    def e2e_step():
+        return matmul_outer(eng, encode_left(eng, pin_a.numpy(), DIM), encode_right(eng, pin_b.numpy(), DIM)).decode(eng)
+
     t_settle = time.perf_counter()
     while time.perf_counter() - t_settle < 0.25:  # same statement as the timed loop
-        res = matmul_outer(eng, encode_left(eng, pin_a.numpy(), DIM), encode_right(eng, pin_b.numpy(), DIM)).decode(eng)
+        res = e2e_step()
     barrier()
     torch.cuda.synchronize()
     gc.collect()
     gc.disable()
     t0 = time.perf_counter()
-    st.record(stream)
+    st.record()
     for _ in range(e2e_steps):
-        res = matmul_outer(eng, encode_left(eng, pin_a.numpy(), DIM), encode_right(eng, pin_b.numpy(), DIM)).decode(eng)
-    en.record(stream)
+        res = e2e_step()
+    en.record()
     torch.cuda.synchronize()
     gc.enable()
     e2e_s = max_over_ranks(max(st.elapsed_time(en) / 1e3, time.perf_counter() - t0) / e2e_steps)
+    assert float(np.max(np.abs(res[: DIM * DIM].reshape(DIM, DIM) - a @ b))) < 1e-3
     h2d = 2 * DIM * DIM * 8  # the raw A and B (broadcast/tiling happens in the encode kernel)
     d2h = eng.slots * 8
 
@@ -332,33 +605,33 @@ def run_ours(args, ws, rank, local):
     cfg5 = {}
     if not args.no_extra:
         del left, right, first, out
-        cfg5["cfg5a"] = bench_cfg5a(ws, rank, local, max_over_ranks, barrier)
-        cfg5["cfg5b"] = bench_cfg5b(ws, rank, local, max_over_ranks, barrier)
+        cfg5["cfg5a"] = bench_cfg5a(ws, rank, local, max_over_ranks, barrier, peaks)
+        cfg5["cfg5b"] = bench_cfg5b(ws, rank, local, max_over_ranks, barrier, peaks)
     if not args.no_extra and rank == 0:
-        extra["ntt"] = bench_ntt(eng, peak)
-        extra["configs"] = {"cfg1": bench_cfg1(), "cfg2_alg3": bench_cfg2_alg3(), "table1_cnn": bench_table1(), "cfg3": bench_cfg3(), "cfg4": bench_cfg4(steps=3), **cfg5}
+        extra["ntt"] = bench_ntt(eng, peak, peaks)
+        extra["configs"] = {"cfg1": bench_cfg1(peaks), "cfg2": {"metric": METRIC, "value": value,
+                                                                 "roofline": roofline_for(2, step_s, eng.q, peaks)},
+                            "cfg2_alg3": bench_cfg2_alg3(), "table1_cnn": bench_table1(), "cfg3": bench_cfg3(peaks),
+                            "cfg4": bench_cfg4(peaks), **cfg5}
     line = None
     if rank == 0:
-        cpu = None
         try:
-            times, cerr = cpu_port_matmul(reps=2)
-            cv = 1.0 / statistics.median(times)
-            cpu = {"value": cv, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-                   "sample": "2 cfg-2 HE matmuls (matmul_outer on resident ciphertexts) in the C RNS-CKKS oracle, OpenMP over (limb, coefficient chunk) work items and key-switch target primes",
-                   "max_abs_err": cerr}
+            cpu = cpu_baseline_matmul(reps=20)
         except Exception as exc:  # pragma: no cover
-            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port", "sample": f"failed: {exc}"}
+            cpu = {"value": None, "unit": UNIT, "cores": host_cores(), "kind": "port", "sample": f"failed: {exc}"}
+        if "configs" in extra:
+            extra["configs"]["cfg2"]["cpu_baseline"] = cpu
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic (seed 1, U[-1,1]); inputs larger than L2 (128 cts = 168 MB)",
-            "config": {"workload": "cfg2 HE matmul 64x64 (n=64 column ciphertexts/operand), N=2^14, q0 60b + 4x40b + P 60b, scale 2^40",
-                       "parallelism": f"replicas x{ws}", "l2": "inputs larger than L2"},
+            "config": config_dict(ws),
             "max_abs_err": err,
-            "roofline": {"bound": "hbm", "kernel": "k_tensor_sum<MODE=2> (d0,d1)", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic("k_tensor_sum_d01"),
+            "roofline": {"bound": "hbm", "kernel": "k_tensor_sum<MODE=2> (d0,d1)", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic("k_tensor_sum_d01"),
                          "alg_bytes_per_launch": alg_bytes, "launch_us": ts_s * 1e6, "step_share": ts_s / step_s,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         "step": roofline_for(2, step_s, eng.q, peaks)},
             "cpu_baseline": cpu,
             "e2e": {"value": ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "encode_left+encode_right (encrypt 128 cts) -> matmul_outer -> decode"},
@@ -372,7 +645,12 @@ def run_ours(args, ws, rank, local):
         torch.distributed.destroy_process_group()
 
 
-def bench_cfg1(steps=50):
+def _cpu_entry(value, unit, kind, sample, cores=None):
+    return {"value": value, "unit": unit, "cores": host_cores() if cores is None else cores, "kind": kind,
+            "cpu": cpu_model(), "sample": sample}
+
+
+def bench_cfg1(peaks, steps=200):
     """Config 1: HE matmul 8x8 (n = 8 column ciphertexts, N = 2^13), device time per matmul."""
     import torch
 
@@ -383,25 +661,22 @@ def bench_cfg1(steps=50):
     eng = CkksEngine(config_params(1))
     left, right = encode_left(eng, a, 8), encode_right(eng, b, 8)
     err = float(np.max(np.abs(matmul_outer(eng, left, right).decode(eng) - a @ b)))
-    for _ in range(3):
+    for _ in range(20):
         matmul_outer(eng, left, right)
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    st.record(eng._stream)
-    for _ in range(steps):
-        matmul_outer(eng, left, right)
-    en.record(eng._stream)
-    torch.cuda.synchronize()
-    t = st.elapsed_time(en) / 1e3 / steps
-    return {"metric": "HE matmul/s (cfg1 8x8, N=2^13)", "value": 1.0 / t, "ms_per_matmul": t * 1e3, "max_abs_err": err}
+    t = Timer(lambda x: x)(lambda: matmul_outer(eng, left, right), steps)
+    t_cpu = cpu_oracle_matmul_cfg(1, 8, 1, reps=20)
+    t_sim = simulator_matmul(1, 8)
+    return {"metric": "HE matmul/s (cfg1 8x8, N=2^13)", "value": 1.0 / t, "ms_per_matmul": t * 1e3, "max_abs_err": err,
+            "roofline": roofline_for(1, t, eng.q, peaks),
+            "cpu_baseline": _cpu_entry(1.0 / t_cpu, UNIT, "port", "best of 20 cfg-1 HE matmuls (matmul_outer, 16 cts, "
+                                       "warmed engine) in the C RNS-CKKS oracle, OpenMP"),
+            "reference_simulator": {"value": 1.0 / t_sim, "unit": UNIT, "cores": 1}}
 
 
 def bench_cfg2_alg3(steps=5):
     """Config 2, Algorithm 3 (revolver matmul, the rotation-heavy single-ciphertext product):
     A, B 64x64 padded to row width 128 so the 64x128 layout fills 8192 slots (fast path,
     depth 3).  64 hoisted rotations of B, 64 products, 64 x 14 cascade rotations, 128 cmuls."""
-    import torch
-
     from paper_2512_18646_b200 import CkksEngine, config_params, encode_revolver, encode_row_major, matmul
     from tools.workloads import cfg_matmul
 
@@ -416,14 +691,7 @@ def bench_cfg2_alg3(steps=5):
     for _ in range(2):
         matmul(eng, ca, cb)
     before = eng.meter_snapshot()
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    st.record(eng._stream)
-    for _ in range(steps):
-        matmul(eng, ca, cb)
-    en.record(eng._stream)
-    torch.cuda.synchronize()
-    t = st.elapsed_time(en) / 1e3 / steps
+    t = Timer(lambda x: x)(lambda: matmul(eng, ca, cb), steps)
     d = eng.meter_snapshot().delta_since(before)
     return {"metric": "HE matmul/s (cfg2 Algorithm 3 revolver, 64x64 at width 128, N=2^14)", "value": 1.0 / t,
             "ms_per_matmul": t * 1e3, "max_abs_err": err,
@@ -436,15 +704,12 @@ def bench_table1(steps=3):
     32768-slot ciphertext, conv 4x3x3 -> act -> ReForm -> FC 2704->64 -> act -> FC 64->10, depth 13,
     N = 2^16 on q0 60b + 13 x 45b + P 60b.  Model encoded once; per batch: encrypt the images,
     forward, decode the scores.  Synthetic seeded images/weights in the reference suite's ranges."""
-    import torch
-
-    sys.path.insert(0, str(ROOT))
     from oracle.sim import table1_weights
     from paper_2512_18646_b200 import EngineParams, Kernel, ModelWeights, SlotEngine, encode_model, forward_encoded, pack_batch
 
     act1 = (-0.00015120704, 0.4610149, 2.0225089, -1.4511951)
     act2 = (-1.5650465, -0.9943767, 1.6794522, 0.5350255)
-    kw, kb, f1w, f1b, f2w, f2b = table1_weights(7)
+    kw, kb, f1w, f1b, f2w, f2b = table1_weights(7)  # seeded weights only (outside the timed loop)
     weights = ModelWeights([Kernel(kw[i], bias=float(kb[i])) for i in range(4)], f1w, f1b, f2w, f2b, act1, act2)
     imgs = np.random.default_rng(8).uniform(0, 1, size=(32, 28, 28))
     eng = SlotEngine(EngineParams(slots=32768, prime_bits=(60,) + (45,) * 13))
@@ -452,14 +717,7 @@ def bench_table1(steps=3):
     scores = forward_encoded(eng, pack_batch(eng, imgs), model).decode(eng)[:, :10]
     want = np.stack([weights.fc2_weight @ _t1_hidden(weights, im) + weights.fc2_bias for im in imgs])
     err = float(np.max(np.abs(scores - want)))
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    st.record(eng._stream)
-    for _ in range(steps):
-        forward_encoded(eng, pack_batch(eng, imgs), model).decode(eng)
-    en.record(eng._stream)
-    torch.cuda.synchronize()
-    t = st.elapsed_time(en) / 1e3 / steps
+    t = Timer(lambda x: x)(lambda: forward_encoded(eng, pack_batch(eng, imgs), model).decode(eng), steps)
     return {"metric": "encrypted-CNN images/s (paper Table 1: 32 images x 28x28 per ciphertext, depth 13, N=2^16)",
             "value": 32.0 / t, "s_per_batch": t, "max_abs_err": err,
             "note": "per batch: encrypt images, forward (36 conv products, ~5.8k rotations), decode; model encoded once"}
@@ -480,7 +738,28 @@ def _t1_hidden(weights, img):
     return poly(weights.fc1_weight @ np.concatenate(maps) + weights.fc1_bias, weights.act2)
 
 
-def bench_cfg4(steps=2):
+_CFG4_CPU = {}
+
+
+def cfg4_cpu(images_per_ct):
+    """CPU figures for one config-4 layer batch (16 or 64 images per ciphertext): the C oracle
+    on a slice (extrapolated to the 224 output columns and 3584 activations) and the reference's
+    simulator on one of the 16 filters (x 16)."""
+    if "oracle" not in _CFG4_CPU:
+        t_col, t_act = cpu_oracle_conv_slice()
+        _CFG4_CPU["oracle"] = 224 * t_col + 16 * 224 * t_act
+        _CFG4_CPU["sim"] = 16 * simulator_conv_act(filters=1, images=16)
+    t_o, t_s = _CFG4_CPU["oracle"], _CFG4_CPU["sim"]
+    return (_cpu_entry(images_per_ct / t_o, "images/s", "port",
+                       f"C RNS-CKKS oracle on a slice of one batch ({images_per_ct} images/ct): conv_columns_multi for 16 "
+                       "filters x 3 channels on 2 of the 224 output columns (x 112) + poly_activation of 4 outputs "
+                       "(x 896); ciphertext work is independent of images/ct; OpenMP, keys built before timing"),
+            {"value": images_per_ct / t_s, "unit": "images/s", "cores": 1,
+             "sample": "reference algorithm (float64 simulator): conv_columns x 3 channels + poly_activation for 1 of the 16 "
+                       "filters (x 16), 16384 slots; no cryptography"})
+
+
+def bench_cfg4(peaks, steps=3):
     """Config 4: 16 images 3x224x224, 16-filter 3x3 conv (padding 1) + 0.125x^2+0.5x+0.25, N = 2^15."""
     import torch
 
@@ -495,16 +774,8 @@ def bench_cfg4(steps=2):
     got = decode_layer(eng, ys)
     err = float(np.max(np.abs(got - poly_plain(conv_plain(imgs, w, b, padding=1), ACT4))))
     del ys
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
     l0 = eng._lib.vr_launch_count()
-    st.record(eng._stream)
-    for _ in range(steps):
-        ys = conv_layer(eng, chans, w, b, activation=ACT4)
-        del ys
-    en.record(eng._stream)
-    torch.cuda.synchronize()
-    t = st.elapsed_time(en) / 1e3 / steps
+    t = Timer(lambda x: x)(lambda: conv_layer(eng, chans, w, b, activation=ACT4), steps)
     launches = (eng._lib.vr_launch_count() - l0) / steps
     # e2e: encrypt from host, layer, decrypt to host
     torch.cuda.synchronize()
@@ -513,12 +784,15 @@ def bench_cfg4(steps=2):
     decode_layer(eng, ys)
     torch.cuda.synchronize()
     te = time.perf_counter() - t0
+    cpu, simr = cfg4_cpu(16)
     return {"metric": "encrypted-CNN images/s (cfg4 conv 16x3x3x3 + degree-2 activation, 16 images/batch, N=2^15)",
             "value": 16 / t, "s_per_batch": t, "max_abs_err": err, "launches_per_batch": launches,
-            "e2e_images_per_s": 16 / te, "e2e_h2d_bytes": 3 * 226 * 16 * 226 * 8, "e2e_d2h_bytes": 16 * 224 * 16 * 224 * 8}
+            "roofline": roofline_for(4, t, eng.q, peaks), "cpu_baseline": cpu, "reference_simulator": simr,
+            "e2e": {"value": 16 / te, "unit": "images/s", "h2d_bytes_per_step": 3 * 226 * 16 * 226 * 8,
+                    "d2h_bytes_per_step": 16 * 224 * 16 * 224 * 8}}
 
 
-def bench_cfg3(steps=3):
+def bench_cfg3(peaks, steps=5):
     """Config 3: 64 images 28x28 -> conv 5x4x4 stride 2 -> square -> dense 845->64 -> square -> dense 64->10
     (N = 2^14, depth 5), images/s of the encrypted inference (inputs resident, dense plaintexts included)."""
     import torch
@@ -535,20 +809,25 @@ def bench_cfg3(steps=3):
     t_model = time.perf_counter() - t0
     logits = cnn_cfg3(eng, imgs, w, model=model)
     err = float(np.max(np.abs(decode_logits(eng, logits, 64, 28) - cfg3_plain(imgs, w, w1, w2))))
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    st.record(eng._stream)
-    for _ in range(steps):
-        logits = cnn_cfg3(eng, imgs, w, model=model)
-    en.record(eng._stream)
-    torch.cuda.synchronize()
-    t = st.elapsed_time(en) / 1e3 / steps
+    for _ in range(2):
+        cnn_cfg3(eng, imgs, w, model=model)
+    t = Timer(lambda x: x)(lambda: cnn_cfg3(eng, imgs, w, model=model), steps)
+    t_o = cpu_oracle_cfg3_slice()
+    t_s = simulator_cfg3()
     return {"metric": "encrypted-CNN images/s (cfg3 small CNN, 64 images per pass, N=2^14, depth 5)",
             "value": 64 / t, "s_per_pass": t, "max_abs_err": err, "model_encode_s": t_model,
-            "note": "each pass encrypts the 28 image columns; the 4160+640 dense-layer plaintexts are encoded once"}
+            "note": "each pass encrypts the 28 image columns; the 4160+640 dense-layer plaintexts are encoded once",
+            "roofline": roofline_for(3, t, eng.q, peaks),
+            "cpu_baseline": _cpu_entry(64 / t_o, "images/s", "port",
+                                       "C RNS-CKKS oracle on the conv + square stage only (5 filters x 13 stride-2 columns, "
+                                       "65 squares; the dense layers have no oracle driver, so this OVERSTATES the CPU "
+                                       "rate); OpenMP, keys built before timing"),
+            "reference_simulator": {"value": 64 / t_s, "unit": "images/s", "cores": 1,
+                                    "sample": "float64 simulator: conv_columns (stride 1, 5 filters) + square of the even "
+                                              "columns; conv + square stage only"}}
 
 
-def bench_cfg5a(ws, rank, local, max_over_ranks, barrier, steps=5):
+def bench_cfg5a(ws, rank, local, max_over_ranks, barrier, peaks, steps=5):
     """Config 5a: HE matmul 256x256 (4 row blocks of 64 x 256 column cts), k sharded over ranks,
     degree-2 partials summed in int64 with one NCCL reduce per row block onto the block's owner rank,
     which alone relinearises + rescales it (strong scaling; at N=1 one rank finishes all four)."""
@@ -566,25 +845,47 @@ def bench_cfg5a(ws, rank, local, max_over_ranks, barrier, steps=5):
     outs = matmul_outer_sharded_owned(eng, lefts, right)
     errs = [float(np.max(np.abs(eng.dec(o)[: 64 * 256].reshape(64, 256) - blocks[bi] @ b))) for bi, o in outs.items()]
     err = max_over_ranks(max(errs) if errs else 0.0)
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(2):
+        matmul_outer_sharded_owned(eng, lefts, right)
+    barrier()
+    t = Timer(max_over_ranks)(lambda: matmul_outer_sharded_owned(eng, lefts, right), steps)
+
+    # e2e: host A row blocks + B -> encrypt this rank's shard -> sharded matmul -> decode owned blocks to host
+    def e2e():
+        ls, r = encode_operands_sharded(eng, blocks, b, lo, hi)
+        o = matmul_outer_sharded_owned(eng, ls, r)
+        return {bi: eng.dec_batch([c], select=np.arange(64 * 256))[0] for bi, c in o.items()}
+
+    e2e()
     barrier()
     torch.cuda.synchronize()
-    st.record(eng._stream)
-    for _ in range(steps):
-        outs = matmul_outer_sharded_owned(eng, lefts, right)
-    en.record(eng._stream)
+    t0 = time.perf_counter()
+    for _ in range(2):
+        e2e()
     torch.cuda.synchronize()
-    t = max_over_ranks(st.elapsed_time(en) / 1e3 / steps)
-    return {"metric": "HE matmul/s (cfg5a 256x256, 4 row blocks x 256 column cts, k sharded, NCCL int64 reduce per block)",
-            "value": 1.0 / t, "ms_per_matmul": t * 1e3, "n_gpus": ws, "scaling": "strong", "max_abs_err": err,
-            "k_per_rank": hi - lo}
+    te = max_over_ranks((time.perf_counter() - t0) / 2)
+    del lefts, right, outs
+    res = {"metric": "HE matmul/s (cfg5a 256x256, 4 row blocks x 256 column cts, k sharded, NCCL int64 reduce per block)",
+           "value": 1.0 / t, "ms_per_matmul": t * 1e3, "n_gpus": ws, "scaling": "strong", "max_abs_err": err,
+           "k_per_rank": hi - lo, "roofline": roofline_for("5a", t * ws, eng.q, peaks),
+           "e2e": {"value": 1.0 / te, "unit": UNIT, "h2d_bytes_per_step": (4 * 64 * 256 + 256 * 256) * 8,
+                   "d2h_bytes_per_step": 4 * 64 * 256 * 8,
+                   "path": "encode_operands_sharded (this rank's 5 x k-shard encryptions) -> matmul_outer_sharded_owned -> decode"}}
+    res["roofline"]["note"] = "per-GPU fraction: t_unit = measured time x n_gpus (each GPU moves 1/n_gpus of B_alg)"
+    if rank == 0:
+        t_cpu = cpu_oracle_matmul_cfg(5, 256, 4, reps=1)
+        res["cpu_baseline"] = _cpu_entry(1.0 / t_cpu, UNIT, "port",
+                                         "one cfg-5a HE matmul (4 row blocks x 256 column pairs, N=2^15, l=8) in the C "
+                                         "RNS-CKKS oracle on uniform random residues (64 distinct ciphertexts cycled; "
+                                         "matmul_outer is data-independent); relin key built before timing; OpenMP")
+        t_sim = simulator_matmul(5, 256, reps=2, blocks=4)
+        res["reference_simulator"] = {"value": 1.0 / t_sim, "unit": UNIT, "cores": 1}
+    return res
 
 
-def bench_cfg5b(ws, rank, local, max_over_ranks, barrier, images=512, group=64):
+def bench_cfg5b(ws, rank, local, max_over_ranks, barrier, peaks, images=512, group=64):
     """Config 5b: the config-4 layer on 512 images, 64 images per column ciphertext (8 groups),
     groups sharded over ranks, no collective (strong scaling)."""
-    import torch
-
     from paper_2512_18646_b200 import CkksEngine, config_params
     from paper_2512_18646_b200.cnn import conv_layer, decode_layer, encode_images
     from paper_2512_18646_b200.dist import image_groups
@@ -600,22 +901,24 @@ def bench_cfg5b(ws, rank, local, max_over_ranks, barrier, images=512, group=64):
         got = decode_layer(eng, conv_layer(eng, chans[0], w, b, activation=ACT4))
         err = float(np.max(np.abs(got - poly_plain(conv_plain(imgs[lo:hi], w, b, padding=1), ACT4))))
     err = max_over_ranks(err)
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    torch.cuda.synchronize()
-    st.record(eng._stream)
-    for ch in chans:
-        ys = conv_layer(eng, ch, w, b, activation=ACT4)
-        del ys
-    en.record(eng._stream)
-    torch.cuda.synchronize()
-    t = max_over_ranks(st.elapsed_time(en) / 1e3)
-    return {"metric": "encrypted-CNN images/s (cfg5b: cfg4 layer on 512 images, 64 images/ct, groups sharded)",
-            "value": images / t, "s_per_512_images": t, "n_gpus": ws, "scaling": "strong", "max_abs_err": err,
-            "groups_per_rank": len(mine)}
+
+    def run_all():
+        for ch in chans:
+            conv_layer(eng, ch, w, b, activation=ACT4)
+
+    t = Timer(max_over_ranks)(run_all, 1)
+    res = {"metric": "encrypted-CNN images/s (cfg5b: cfg4 layer on 512 images, 64 images/ct, groups sharded)",
+           "value": images / t, "s_per_512_images": t, "n_gpus": ws, "scaling": "strong", "max_abs_err": err,
+           "groups_per_rank": len(mine),
+           "roofline": roofline_for("5b", t * ws / (images // group), eng.q, peaks)}
+    res["roofline"]["note"] = "per 64-image group per GPU: t_unit = measured time x n_gpus / 8 groups"
+    if rank == 0:
+        res["cpu_baseline"], res["reference_simulator"] = cfg4_cpu(group)
+    return res
 
 
-def bench_ntt(eng, peak):
+def bench_ntt(eng, peak, peaks):
     """Forward NTT throughput on a batch larger than L2 (N=2^14 limbs, in place)."""
     import torch
 
@@ -625,43 +928,20 @@ def bench_ntt(eng, peak):
     polys = 256
     data = torch.randint(0, 2 ** 39, (polys, nl, eng.N), dtype=torch.int64, device="cuda")
     lib = eng._lib
+
+    def fwd():
+        _lib.check(lib.vr_ntt(eng.handle, data.data_ptr(), polys, nl, 0, 0))
+
     for _ in range(3):
-        _lib.check(lib.vr_ntt(eng.handle, data.data_ptr(), polys, nl, 0, 0))
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
-    torch.cuda.synchronize()
-    st.record(eng._stream)
-    for _ in range(reps):
-        _lib.check(lib.vr_ntt(eng.handle, data.data_ptr(), polys, nl, 0, 0))
-    en.record(eng._stream)
-    torch.cuda.synchronize()
-    t = st.elapsed_time(en) / 1e3 / reps
+        fwd()
+    t = Timer(lambda x: x)(fwd, 10)
     nbytes = polys * nl * eng.N * 8
     gbs = 2 * nbytes / t / 1e9  # read + write of every limb
     butterflies = polys * nl * (eng.N // 2) * eng.params.log_n
-    # integer-pipe peak: the same butterfly on registers only (k_bfly_peak)
-    sink = torch.zeros(1, dtype=torch.int64, device="cuda")
-    blocks, iters = 148 * 16, 256
-    _lib.check(lib.vr_bench_butterflies(eng.handle, blocks, 16, sink.data_ptr()))
-    torch.cuda.synchronize()
-    st.record(eng._stream)
-    _lib.check(lib.vr_bench_butterflies(eng.handle, blocks, iters, sink.data_ptr()))
-    en.record(eng._stream)
-    torch.cuda.synchronize()
-    tp = st.elapsed_time(en) / 1e3
-    peak_int = blocks * 256 * iters * 8 / tp / 1e9
-    # FP64-pipe peak: the FP64 NTT butterfly on registers only (primes < 2^46 run the FP64 body)
-    f_iters = 32
-    _lib.check(lib.vr_bench_butterflies_f64(eng.handle, blocks, 4, sink.data_ptr()))
-    torch.cuda.synchronize()
-    st.record(eng._stream)
-    _lib.check(lib.vr_bench_butterflies_f64(eng.handle, blocks, f_iters, sink.data_ptr()))
-    en.record(eng._stream)
-    torch.cuda.synchronize()
-    peak_f64 = blocks * 256 * f_iters * 64 / (st.elapsed_time(en) / 1e3) / 1e9
+    peak_int, peak_f64 = peaks
     n_f64 = sum(1 for q in eng.q[:nl] if q < (1 << 46))
     # limb-weighted roofline: time per butterfly = share_int / peak_int + share_f64 / peak_f64
-    peak_mix = 1.0 / ((nl - n_f64) / nl / peak_int + n_f64 / nl / peak_f64)
+    peak_mix = modmul_peak(eng.q[:nl], peaks)
     achieved = butterflies / t / 1e9
     return {"metric": "NTT HBM GB/s (forward, in place)", "N": eng.N, "limbs": polys * nl,
             "gbs": gbs, "peak": peak, "frac": gbs / peak, "us_per_limb": t / (polys * nl) * 1e6,
@@ -676,6 +956,7 @@ def bench_ntt(eng, peak):
 
 def main():
     args = parse()
+    maybe_spawn(args)
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, ws, rank)

@@ -45,6 +45,8 @@ int vr_ctx_destroy(vr_ctx *ctx);
 const char *vr_last_error(void);
 /* total kernels this library has launched (instrumentation for bench.py) */
 unsigned long long vr_launch_count(void);
+/* order every later call on cuda_stream (NULL = the legacy default stream); the context's
+ * private stream (the default after vr_ctx_create) stays alive until vr_ctx_destroy */
 int vr_set_stream(vr_ctx *ctx, void *cuda_stream);
 int vr_sync(vr_ctx *ctx);
 

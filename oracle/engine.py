@@ -106,6 +106,38 @@ class OracleEngine:
             return OCt(ct.data, ct.level, ct.scale, ct.depth, ct.layout)
         return OCt(self.c.rotate(ct.data, int(l)), ct.level, ct.scale, ct.depth, ct.layout)
 
+    # -- the batched surface of the product engine (CkksEngine.*_batch), as plain loops --------
+    # The product's algorithm modules (matmul.py, conv.py, virtual.py, pipeline.py) drive only this
+    # surface; these loops are the per-op definition the GPU's batched launches must reproduce.
+    def enc_batch(self, rows, layout=None, nonce0=None):
+        if nonce0 is None:
+            return [self.enc(r, layout) for r in rows]
+        saved, self.nonce = self.nonce, int(nonce0)  # explicit nonces leave the running counter alone
+        try:
+            return [self.enc(r, layout) for r in rows]
+        finally:
+            self.nonce = saved
+
+    def rot_batch(self, cts, steps):
+        return [[self.rot(c, s) for s in steps] for c in cts]
+
+    def add_batch(self, xs, ys):
+        return [self.add(x, y) for x, y in zip(xs, ys)]
+
+    def mul_batch(self, xs, ys):
+        return [self.mul(x, y) for x, y in zip(xs, ys)]
+
+    def cmul_batch(self, masks, cts):
+        cts = list(cts)
+        if not isinstance(masks, (list, tuple)):
+            masks = [masks] * len(cts)
+        return [self.cmul(m, c) for m, c in zip(masks, cts)]
+
+    def sum_batch(self, acc, cts):
+        for c in cts:
+            acc = self.add(acc, c)
+        return acc
+
     # -- fused drivers (same op order as the CUDA drivers) -----------------
     def matmul_outer_blocks(self, lefts, rights):
         """lefts: list of lists of OCt (row blocks), rights: list of OCt."""

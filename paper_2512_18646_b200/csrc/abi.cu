@@ -3,6 +3,8 @@
 #include <math.h>
 
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "../../include/vrhe.h"
 #include "encode.cuh"
@@ -93,10 +95,55 @@ void check_level(const vr::Ctx &c, int level) {
     if (level < 0 || level > c.L) throw vr::VrError(VR_ERR_ENGINE, "level out of range");
 }
 
+// Release everything a (possibly partially constructed) context owns.  Errors are ignored:
+// this runs on the vr_ctx_create failure path and from vr_ctx_destroy.
+void destroy_ctx(vr_ctx *h) {
+    vr::Ctx &c = h->c;
+    cudaSetDevice(c.device);
+    for (cudaStream_t s : {c.own, c.aux, c.hi, c.stream})
+        if (s) cudaStreamSynchronize(s);
+    void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.liftk, c.kshift, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw,
+                    c.slot_pos, c.pos_slot, c.cdt, c.rlk, c.s_ntt, c.s_sh, c.pk, c.arena};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    for (auto &kv : c.gkeys) cudaFree(kv.second);
+    for (auto &e : c.tables)
+        if (e.dev) cudaFree(e.dev);
+    for (auto &b : c.big_free) cudaFree(b.second);
+    for (cudaEvent_t e : {c.ev_fork, c.ev_join, c.ev_hi, c.ev_hi_done})
+        if (e) cudaEventDestroy(e);
+    for (int i = 0; i < vr::Ctx::kStageSlots; i++)
+        if (c.stage_evt[i]) cudaEventDestroy(c.stage_evt[i]);
+    if (c.stage) cudaFreeHost(c.stage);
+    // the private streams only; a user stream installed by vr_set_stream belongs to the caller
+    for (cudaStream_t s : {c.own, c.aux, c.hi})
+        if (s) cudaStreamDestroy(s);
+    cudaGetLastError();
+    delete h;
+}
+
 }  // namespace
 
 namespace vr {
 unsigned long long g_launches = 0;
+
+void ensure_smem(Ctx &c, const void *kern, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, size_t> done;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t &have = done[{c.device, kern}];
+    if (smem <= have) return;
+    int cur = c.device;
+    VR_CUDA(cudaGetDevice(&cur));
+    if (cur != c.device) VR_CUDA(cudaSetDevice(c.device));
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cur != c.device) cudaSetDevice(cur);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw VrError(4, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    }
+    have = smem;
+}
 
 const void *const *cached_table(Ctx &c, const void *const *ptrs, size_t n) {
     static const void *empty_slot = nullptr;
@@ -156,6 +203,7 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         if (num_q < 1 || num_q + 1 > vr::MAXP) throw vr::VrError(VR_ERR_ENGINE, "unsupported number of primes");
         VR_CUDA(cudaSetDevice(device));
         auto *h = new vr_ctx();
+        try {
         vr::Ctx &c = h->c;
         c.device = device;
         c.log_n = log_n;
@@ -168,10 +216,8 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         const int n = c.n, np = c.np;
         for (int p = 0; p < np; p++) {
             const uint64_t q = primes[p];
-            if (q >= (1ull << 61) || q % (2ull * n) != 1) {
-                delete h;
+            if (q >= (1ull << 61) || q % (2ull * n) != 1)
                 throw vr::VrError(VR_ERR_ENGINE, "primes must be < 2^61 and == 1 mod 2N");
-            }
             c.q[p] = q;
             u128h r = (~(u128h)0) / q;
             c.primes.m[p] = vr::Modulus{q, (uint64_t)(r >> 64), (uint64_t)r};
@@ -288,7 +334,8 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         c.slot_pos = upload(c, sp);
         c.pos_slot = upload(c, ps);
         c.cdt = upload(c, cdt);
-        VR_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        VR_CUDA(cudaStreamCreateWithFlags(&c.own, cudaStreamNonBlocking));
+        c.stream = c.own;  // until vr_set_stream installs the caller's stream
         VR_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
         VR_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
         VR_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
@@ -311,41 +358,22 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         }
         vr::keygen(c);
         VR_CUDA(cudaStreamSynchronize(c.stream));
-        // a user stream replaces the private one via vr_set_stream; keep the private one alive
+        } catch (...) {
+            destroy_ctx(h);  // no partially built context (device tables, streams, keys) leaks
+            throw;
+        }
         *out = h;
     });
 }
 
 int vr_ctx_destroy(vr_ctx *h) {
     if (!h) return VR_OK;
-    return guard([&] {
-        vr::Ctx &c = h->c;
-        cudaSetDevice(c.device);
-        cudaDeviceSynchronize();
-        void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.liftk, c.kshift, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw, c.slot_pos, c.pos_slot, c.cdt, c.rlk};
-        for (void *p : ptrs)
-            if (p) cudaFree(p);
-        if (c.s_ntt) cudaFree(c.s_ntt);
-        if (c.s_sh) cudaFree(c.s_sh);
-        if (c.pk) cudaFree(c.pk);
-        for (auto &kv : c.gkeys) cudaFree(kv.second);
-        for (auto &e : c.tables)
-            if (e.dev) cudaFree(e.dev);
-        if (c.arena) cudaFree(c.arena);
-        if (c.ev_fork) cudaEventDestroy(c.ev_fork);
-        if (c.ev_join) cudaEventDestroy(c.ev_join);
-        if (c.ev_hi) cudaEventDestroy(c.ev_hi);
-        if (c.ev_hi_done) cudaEventDestroy(c.ev_hi_done);
-        if (c.hi) cudaStreamDestroy(c.hi);
-        for (auto &b : c.big_free) cudaFree(b.second);
-        for (int i = 0; i < vr::Ctx::kStageSlots; i++)
-            if (c.stage_evt[i]) cudaEventDestroy(c.stage_evt[i]);
-        if (c.stage) cudaFreeHost(c.stage);
-        delete h;
-    });
+    return guard([&] { destroy_ctx(h); });
 }
 
 int vr_set_stream(vr_ctx *h, void *stream) {
+    // NULL is the legacy default stream (torch's default stream); the private stream is kept
+    // for vr_ctx_destroy either way
     return guard([&] { h->c.stream = (cudaStream_t)stream; });
 }
 

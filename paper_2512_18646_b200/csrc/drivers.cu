@@ -257,7 +257,8 @@ void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, in
             const char *e = getenv("VR_MM_ORDER");
             return e ? atoi(e) : 4;
         }();
-        cudaStream_t main = c.stream;
+        StreamScope scope(c);  // restores c.stream (and joins aux/hi on an error) on every exit
+        cudaStream_t main = scope.main;
         if (order == 4) {
             // d2 and its key switch on the highest-priority stream (the block scheduler places their
             // CTAs before those of the concurrent (d0, d1) pass on the auxiliary stream)

@@ -477,7 +477,7 @@ template <typename K, typename... Args>
 void launch_fft_t(Ctx &c, K kern, int count, int S, int tmul, Args... args) {
     const int cl = fft_cl(S);
     const size_t sm = fft_smem(S);
-    if (sm > 48 * 1024) VR_CUDA(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ensure_smem(c, (const void *)kern, sm);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(count * cl));
     cfg.blockDim = dim3((unsigned)(fft_threads(S) * tmul));

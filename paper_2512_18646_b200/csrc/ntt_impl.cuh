@@ -687,11 +687,7 @@ void launch_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
     constexpr int C = 1 << LOGC;
     const size_t smem = (size_t)C * sizeof(uint64_t);
     auto kern = ntt_cl8<INV, LOGC, LD, ST>;
-    static bool configured = false;
-    if (!configured && smem > 48 * 1024) {
-        VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
-    }
+    ensure_smem(c, (const void *)kern, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)b.count * 8);
     cfg.blockDim = dim3(C / 8);
@@ -730,7 +726,8 @@ inline int ntt_cl_min() {
 template <bool INV, class LD, class ST>
 bool try_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st, bool force = false) {
     const int lim = ntt_cl_min();
-    if (!force && (lim <= 0 || b.count < lim)) return false;
+    if (lim <= 0) return false;  // VR_NTT_CL=0 is a kill switch, also for forced callers
+    if (!force && b.count < lim) return false;
     switch (c.log_n) {
         case 12: launch_cl8<INV, 9>(c, b, ld, st); return true;
         case 13: launch_cl8<INV, 10>(c, b, ld, st); return true;

@@ -584,11 +584,7 @@ static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
     size_t smem = (size_t)ts_stages<NB, TILE, MAXST>() * ARR * tile * sizeof(uint64_t);
     smem = std::max<size_t>(smem, (size_t)NB * 3 * (TILE / 2) * 16);
     auto kern = k_tensor_sum<NB, TILE, SPLIT, MAXST, MODE>;
-    static size_t configured = 0;  // per instantiation: raise the dynamic smem limit once
-    if (smem > configured) {
-        VR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-    }
+    ensure_smem(c, (const void *)kern, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c.n / tile, nl, SPLIT);
     cfg.blockDim = dim3(TILE / 2 + 32, 1, 1);

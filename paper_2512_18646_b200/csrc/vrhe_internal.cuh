@@ -3,12 +3,14 @@
 // lives in abi.cu and is declared in include/vrhe.h.
 #pragma once
 #include <cstdlib>
+#include <exception>
 #include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <map>
 #include <stdexcept>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -33,7 +35,8 @@ struct NttConst {
 
 struct Ctx {
     int device = 0;
-    cudaStream_t stream = 0;
+    cudaStream_t stream = 0;                 // the stream every call is ordered on (vr_set_stream)
+    cudaStream_t own = 0;                    // the context's private stream (default until vr_set_stream)
     cudaStream_t aux = 0;                    // second stream for intra-driver overlap
     cudaEvent_t ev_fork = 0, ev_join = 0;    // fork/join events (timing disabled)
     cudaStream_t hi = 0;                     // highest-priority stream for latency-bound chains
@@ -109,8 +112,10 @@ struct VrError : std::runtime_error {
 #define VR_CUDA(call)                                                                              \
     do {                                                                                           \
         cudaError_t _e = (call);                                                                   \
-        if (_e != cudaSuccess)                                                                     \
+        if (_e != cudaSuccess) {                                                                   \
+            cudaGetLastError(); /* do not leave the error for the next check_launch */             \
             throw ::vr::VrError(4, std::string(#call) + ": " + cudaGetErrorString(_e));            \
+        }                                                                                          \
     } while (0)
 
 // number of kernels launched by this library (bench.py reports it as gpu_launches)
@@ -121,6 +126,33 @@ inline void check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw VrError(4, std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+// Raise kern's dynamic shared-memory limit on the context's device to at least `smem`.
+// The attribute is per (device, function) and shared by every context on that device, so the
+// record of what was set is process-wide, keyed by device, only ever raised, and mutex-guarded
+// (one engine per worker thread is the reference's model, engine.py:170-173).  Set for any size:
+// the 48 KB default covers dynamic + static shared memory together.
+void ensure_smem(Ctx &c, const void *kern, size_t smem);
+
+// Drivers that fork work onto c.aux / c.hi temporarily point c.stream at them.  This guard
+// restores the caller's stream on every exit and, when unwinding after an error, joins the side
+// streams back into it so scratch freed on the caller's stream is not reused under them.
+struct StreamScope {
+    Ctx &c;
+    cudaStream_t main;
+    explicit StreamScope(Ctx &cx) : c(cx), main(cx.stream) {}
+    ~StreamScope() {
+        c.stream = main;
+        if (std::uncaught_exceptions() > 0) {
+            for (cudaStream_t s : {c.aux, c.hi}) {
+                if (!s) continue;
+                if (cudaEventRecord(c.ev_join, s) == cudaSuccess) cudaStreamWaitEvent(main, c.ev_join, 0);
+            }
+            cudaGetLastError();
+        }
+    }
+    StreamScope(const StreamScope &) = delete;
+};
 
 // Per-call scratch.  Carved LIFO out of the context's arena (kernels on the one stream
 // run in order, so the next call may reuse the bytes immediately); when the arena is

@@ -62,9 +62,8 @@ class Kernel:
 
 
 # ---- row-major / revolver packing and the rotate-and-add primitives (encoding.py:90-170) ----
-# Written against the SlotEngine surface only (enc/rot/add/cmul/mask), so they run unchanged on
-# the GPU engine and on the CPU residue oracle.  Where the engine offers batched forms
-# (CkksEngine.rot_batch/add_batch/cmul_batch) the *_many variants below use them.
+# Written against the SlotEngine surface (enc/rot/add/cmul/mask) plus CkksEngine's batched forms
+# (rot_batch/add_batch/cmul_batch): one launch per cascade step for all matrices.
 
 def _fits(engine, m: int, n: int) -> None:
     if m * n > engine.slots:
@@ -149,19 +148,12 @@ def sum_col_vec_many(engine, pms) -> list[PackedMatrix]:
     m, n = pms[0].shape.m, pms[0].shape.n
     steps = _log2_exact(n, "sum_col_vec")
     cts = [pm.ct for pm in pms]
-    batched = hasattr(engine, "rot_batch")
     for t in range(steps):
-        if batched:
-            cts = engine.add_batch(cts, [r[0] for r in engine.rot_batch(cts, [1 << t])])
-        else:
-            cts = [engine.add(c, engine.rot(c, 1 << t)) for c in cts]
+        cts = engine.add_batch(cts, [r[0] for r in engine.rot_batch(cts, [1 << t])])
     keep = _col0_filter(engine, m, n)
-    cts = engine.cmul_batch(keep, cts) if batched else [engine.cmul(keep, c) for c in cts]
+    cts = engine.cmul_batch(keep, cts)
     for t in range(steps):
-        if batched:
-            cts = engine.add_batch(cts, [r[0] for r in engine.rot_batch(cts, [-(1 << t)])])
-        else:
-            cts = [engine.add(c, engine.rot(c, -(1 << t))) for c in cts]
+        cts = engine.add_batch(cts, [r[0] for r in engine.rot_batch(cts, [-(1 << t)])])
     return [pm.with_ct(c) for pm, c in zip(pms, cts)]
 
 

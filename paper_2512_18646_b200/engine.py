@@ -77,6 +77,14 @@ class OpMeter:
         )
 
 
+def scalar_i64(x: float) -> int:
+    """round(x) as a signed 64-bit scalar for the C-ABI; ctypes would wrap larger values silently."""
+    k = int(round(x))
+    if not -(1 << 63) < k < (1 << 63):
+        raise CapacityError(f"constant {x:.6g} does not fit a 64-bit integer scalar at this scale")
+    return k
+
+
 def _frozen(values) -> np.ndarray:
     out = np.array(values, dtype=np.float64)
     out.flags.writeable = False
@@ -192,7 +200,8 @@ class CkksEngine:
                                                ctypes.byref(h)))
             self._stream = torch.cuda.current_stream(self.device)
         self._h = h
-        _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(self._stream.cuda_stream)))
+        self._stream_ptr = self._stream.cuda_stream
+        _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(self._stream_ptr)))
         self._meter = OpMeter()
         self._nonce = 0
         self._pin = None
@@ -220,6 +229,16 @@ class CkksEngine:
 
     @property
     def handle(self):
+        """The C context, ordered on the caller's CURRENT torch stream.
+
+        Like a torch op, every engine call runs on ``torch.cuda.current_stream()``: the library
+        kernels, the output allocations, the pinned H2D staging copies and the decode's D2H all
+        share that one stream, so no cross-stream hazard exists inside a call.
+        """
+        cur = torch.cuda.current_stream(self.device)
+        if cur.cuda_stream != self._stream_ptr:
+            _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(cur.cuda_stream)))
+            self._stream, self._stream_ptr = cur, cur.cuda_stream
         return self._h
 
     def _observe(self, depth: int) -> None:
@@ -246,6 +265,7 @@ class CkksEngine:
 
     def _h2d(self, vals: np.ndarray) -> torch.Tensor:
         """Host float64 array -> device, staged through a reusable pinned buffer."""
+        self.handle  # noqa: B018 -- adopt the caller's current stream before copying
         nbytes = vals.nbytes
         if self._pin is None or self._pin.numel() < vals.size:
             self._pin = torch.empty(max(vals.size, 1 << 16), dtype=torch.float64, pin_memory=True)
@@ -289,7 +309,7 @@ class CkksEngine:
         d_vals = self._h2d(vals)
         out = self._empty(1, self.L, count)
         n0 = self._nonce if nonce0 is None else int(nonce0)
-        _lib.check(self._lib.vr_encrypt(self._h, d_vals.data_ptr(), count, vals.shape[1], self.L,
+        _lib.check(self._lib.vr_encrypt(self.handle, d_vals.data_ptr(), count, vals.shape[1], self.L,
                                         self.scales[self.L], n0, out.data_ptr()))
         if nonce0 is None:
             self._nonce += count
@@ -311,7 +331,7 @@ class CkksEngine:
         d_src = self._h2d(arr) if arr.size else torch.zeros(1, dtype=torch.float64, device=self.device)
         out = self._empty(1, self.L, count)
         n0 = self._nonce if nonce0 is None else int(nonce0)
-        _lib.check(self._lib.vr_encrypt_strided(self._h, d_src.data_ptr() + 8 * int(offset), sc, s1, s2, max(1, p), nvals,
+        _lib.check(self._lib.vr_encrypt_strided(self.handle, d_src.data_ptr() + 8 * int(offset), sc, s1, s2, max(1, p), nvals,
                                                 count, self.L, self.scales[self.L], n0, out.data_ptr()))
         if nonce0 is None:
             self._nonce += count
@@ -334,7 +354,7 @@ class CkksEngine:
         degs = (ctypes.c_int * count)(*[ct.degree for ct in cts])
         lvls = (ctypes.c_int * count)(*[ct.level for ct in cts])
         scl = (ctypes.c_double * count)(*[ct.scale for ct in cts])
-        _lib.check(self._lib.vr_decrypt_decode(self._h, _lib.ptr_array([ct.ptr() for ct in cts]), degs, lvls, scl,
+        _lib.check(self._lib.vr_decrypt_decode(self.handle, _lib.ptr_array([ct.ptr() for ct in cts]), degs, lvls, scl,
                                                count, out.data_ptr(), None))
         if select is not None:
             idx = torch.as_tensor(np.asarray(select, dtype=np.int64), device=self.device)
@@ -367,7 +387,7 @@ class CkksEngine:
         if lv < 1:
             raise EngineError("multiplicative depth exhausted: operands are at level 0")
         out = self._empty(1, lv - 1)
-        _lib.check(self._lib.vr_mul(self._h, _lib.ptr_array([a2.ptr()]), _lib.ptr_array([b2.ptr()]),
+        _lib.check(self._lib.vr_mul(self.handle, _lib.ptr_array([a2.ptr()]), _lib.ptr_array([b2.ptr()]),
                                     _lib.ptr_array([out.data_ptr()]), 1, lv))
         depth = max(a.depth, b.depth) + 1
         self._meter.mul_count += 1
@@ -384,15 +404,15 @@ class CkksEngine:
         vals = mask.values
         tmp = self._empty(ct.degree, lv)
         if np.all(vals == vals[0]):
-            k = int(round(float(vals[0]) * ct.scale))
-            _lib.check(self._lib.vr_mul_scalar(self._h, _lib.ptr_array([ct.ptr()]), k,
+            k = scalar_i64(float(vals[0]) * ct.scale)
+            _lib.check(self._lib.vr_mul_scalar(self.handle, _lib.ptr_array([ct.ptr()]), k,
                                                _lib.ptr_array([tmp.data_ptr()]), 1, ct.degree, lv))
         else:
             pt = self.encode_plain(vals, lv, ct.scale)
-            _lib.check(self._lib.vr_mul_plain(self._h, _lib.ptr_array([ct.ptr()]), _lib.ptr_array([pt.data_ptr()]),
+            _lib.check(self._lib.vr_mul_plain(self.handle, _lib.ptr_array([ct.ptr()]), _lib.ptr_array([pt.data_ptr()]),
                                               _lib.ptr_array([tmp.data_ptr()]), 1, ct.degree, lv, 1))
         out = self._empty(ct.degree, lv - 1)
-        _lib.check(self._lib.vr_rescale(self._h, _lib.ptr_array([tmp.data_ptr()]), _lib.ptr_array([out.data_ptr()]),
+        _lib.check(self._lib.vr_rescale(self.handle, _lib.ptr_array([tmp.data_ptr()]), _lib.ptr_array([out.data_ptr()]),
                                         1, ct.degree, lv))
         depth = ct.depth + 1
         self._meter.cmul_count += 1
@@ -438,7 +458,7 @@ class CkksEngine:
         if lv < 1:
             raise EngineError("multiplicative depth exhausted: operands are at level 0")
         out = self._empty(1, lv - 1, count)
-        _lib.check(self._lib.vr_mul(self._h, _lib.ptr_array([x.ptr() for x in xs]), _lib.ptr_array([y.ptr() for y in ys]),
+        _lib.check(self._lib.vr_mul(self.handle, _lib.ptr_array([x.ptr() for x in xs]), _lib.ptr_array([y.ptr() for y in ys]),
                                     _lib.row_ptrs(out), count, lv))
         res = []
         for i, (x, y) in enumerate(zip(xs, ys)):
@@ -481,12 +501,12 @@ class CkksEngine:
         vals = np.stack(rows)
         d_vals = self._h2d(vals)
         pts = torch.empty((len(rows), lv + 1, self.N), dtype=torch.int64, device=self.device)
-        _lib.check(self._lib.vr_encode(self._h, d_vals.data_ptr(), len(rows), self.slots, lv, scale, pts.data_ptr()))
+        _lib.check(self._lib.vr_encode(self.handle, d_vals.data_ptr(), len(rows), self.slots, lv, scale, pts.data_ptr()))
         tmp = self._empty(deg, lv, count)
-        _lib.check(self._lib.vr_mul_plain(self._h, _lib.ptr_array([c.ptr() for c in cts]), _lib.row_ptrs(pts),
+        _lib.check(self._lib.vr_mul_plain(self.handle, _lib.ptr_array([c.ptr() for c in cts]), _lib.row_ptrs(pts),
                                           _lib.row_ptrs(tmp), count, deg, lv, 1 if shared else 0))
         out = self._empty(deg, lv - 1, count)
-        _lib.check(self._lib.vr_rescale(self._h, _lib.row_ptrs(tmp), _lib.row_ptrs(out), count, deg, lv))
+        _lib.check(self._lib.vr_rescale(self.handle, _lib.row_ptrs(tmp), _lib.row_ptrs(out), count, deg, lv))
         res = []
         for i, c in enumerate(cts):
             self._meter.cmul_count += 1
@@ -507,7 +527,7 @@ class CkksEngine:
             self._check(c)
         lv, deg, count = xs[0].level, xs[0].degree, len(xs)
         out = self._empty(deg, lv, count)
-        _lib.check(self._lib.vr_add(self._h, _lib.ptr_array([x.ptr() for x in xs]), _lib.ptr_array([y.ptr() for y in ys]),
+        _lib.check(self._lib.vr_add(self.handle, _lib.ptr_array([x.ptr() for x in xs]), _lib.ptr_array([y.ptr() for y in ys]),
                                     _lib.row_ptrs(out), count, deg, lv, 0))
         res = []
         for i, (x, y) in enumerate(zip(xs, ys)):
@@ -529,7 +549,7 @@ class CkksEngine:
         lv, count = cts[0].level, len(cts)
         out = torch.empty((count, len(steps), 2, lv + 1, self.N), dtype=torch.int64, device=self.device)
         st = (ctypes.c_int64 * len(steps))(*steps)
-        _lib.check(self._lib.vr_rotate(self._h, _lib.ptr_array([c.ptr() for c in cts]), _lib.row_ptrs(out.flatten(0, 1)),
+        _lib.check(self._lib.vr_rotate(self.handle, _lib.ptr_array([c.ptr() for c in cts]), _lib.row_ptrs(out.flatten(0, 1)),
                                        count, lv, len(steps), st))
         res = []
         for i, c in enumerate(cts):
@@ -572,14 +592,14 @@ class CkksEngine:
         vals = self._pad([values])
         d_vals = self._h2d(vals)
         pt = torch.empty((level + 1, self.N), dtype=torch.int64, device=self.device)
-        _lib.check(self._lib.vr_encode(self._h, d_vals.data_ptr(), 1, vals.shape[1], level, scale, pt.data_ptr()))
+        _lib.check(self._lib.vr_encode(self.handle, d_vals.data_ptr(), 1, vals.shape[1], level, scale, pt.data_ptr()))
         return pt
 
     def _binop(self, a: Ciphertext, b: Ciphertext, op: int) -> torch.Tensor:
         if a.degree != b.degree:
             raise EngineError("operand degrees differ")
         out = self._empty(a.degree, a.level)
-        _lib.check(self._lib.vr_add(self._h, _lib.ptr_array([a.ptr()]), _lib.ptr_array([b.ptr()]),
+        _lib.check(self._lib.vr_add(self.handle, _lib.ptr_array([a.ptr()]), _lib.ptr_array([b.ptr()]),
                                     _lib.ptr_array([out.data_ptr()]), 1, a.degree, a.level, op))
         return out
 
@@ -588,7 +608,7 @@ class CkksEngine:
         steps = [int(s) for s in steps]
         outs = [self._empty(1, ct.level) for _ in steps]
         st = (ctypes.c_int64 * len(steps))(*steps)
-        _lib.check(self._lib.vr_rotate(self._h, _lib.ptr_array([ct.ptr()]), _lib.ptr_array([o.data_ptr() for o in outs]),
+        _lib.check(self._lib.vr_rotate(self.handle, _lib.ptr_array([ct.ptr()]), _lib.ptr_array([o.data_ptr() for o in outs]),
                                        1, ct.level, len(steps), st))
         return outs
 
@@ -604,15 +624,15 @@ class CkksEngine:
         cur, lv = ct, ct.level
         if lv > level + 1:
             dropped = self._empty(cur.degree, level + 1)
-            _lib.check(self._lib.vr_drop_level(self._h, _lib.ptr_array([cur.ptr()]), _lib.ptr_array([dropped.data_ptr()]),
+            _lib.check(self._lib.vr_drop_level(self.handle, _lib.ptr_array([cur.ptr()]), _lib.ptr_array([dropped.data_ptr()]),
                                                1, cur.degree, lv, level + 1))
             cur = Ciphertext(dropped, level + 1, ct.scale, ct.depth, ct.layout, self._id)
-        k = int(round(self.scales[level] * float(self.q[level + 1]) / cur.scale))
+        k = scalar_i64(self.scales[level] * float(self.q[level + 1]) / cur.scale)
         tmp = self._empty(cur.degree, level + 1)
-        _lib.check(self._lib.vr_mul_scalar(self._h, _lib.ptr_array([cur.ptr()]), k, _lib.ptr_array([tmp.data_ptr()]),
+        _lib.check(self._lib.vr_mul_scalar(self.handle, _lib.ptr_array([cur.ptr()]), k, _lib.ptr_array([tmp.data_ptr()]),
                                            1, cur.degree, level + 1))
         out = self._empty(cur.degree, level)
-        _lib.check(self._lib.vr_rescale(self._h, _lib.ptr_array([tmp.data_ptr()]), _lib.ptr_array([out.data_ptr()]),
+        _lib.check(self._lib.vr_rescale(self.handle, _lib.ptr_array([tmp.data_ptr()]), _lib.ptr_array([out.data_ptr()]),
                                         1, cur.degree, level + 1))
         return Ciphertext(out, level, self.scales[level], ct.depth, ct.layout, self._id)
 
@@ -625,7 +645,7 @@ class CkksEngine:
         return self.adjust(a, lv), self.adjust(b, lv)
 
     def sync(self) -> None:
-        _lib.check(self._lib.vr_sync(self._h))
+        _lib.check(self._lib.vr_sync(self.handle))
 
 
 # The reference name: algorithm modules construct ``SlotEngine(EngineParams(...))``.
