@@ -120,6 +120,18 @@ int vr_mod_reduce(vr_ctx *ctx, uint64_t *data, long long polys, int level);
  * blocks share R (nb in {1,2,4}) */
 int vr_matmul_outer(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
                     uint64_t *const *out);
+/* matmul_outer without waiting for the result: the product is computed on one of the context's
+ * slot streams, which first waits for all work already queued on the context stream.  *slot_stream
+ * receives that stream (the result is complete once it reaches the current point of that stream),
+ * or NULL if the call ran synchronously on the context stream.  Consecutive independent calls
+ * overlap on the device.  The caller must order every later use of `out` (and every reuse of the
+ * operand buffers) after *slot_stream, e.g. with vr_join. */
+int vr_matmul_outer_async(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
+                          uint64_t *const *out, void **slot_stream);
+/* the slot stream the next vr_matmul_outer_async call will run on (allocate its output there) */
+int vr_async_slot(vr_ctx *ctx, void **slot_stream);
+/* make the context stream wait for everything queued on the slot streams */
+int vr_join(vr_ctx *ctx);
 /* the degree-2 partial sum only (multi-GPU: all-reduce, vr_mod_reduce, then vr_relin + vr_rescale) */
 int vr_tensor_sum(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
                   uint64_t *const *out);

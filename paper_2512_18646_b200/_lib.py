@@ -60,6 +60,9 @@ _SIGS = {
     "vr_bench_butterflies_f64": [c_vp, ctypes.c_int, ctypes.c_int, c_vp],
     "vr_matmul_outer": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp],
     "vr_tensor_sum": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp],
+    "vr_matmul_outer_async": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp, ctypes.POINTER(c_vp)],
+    "vr_join": [c_vp],
+    "vr_async_slot": [c_vp, ctypes.POINTER(c_vp)],
     "vr_tensor_sum_mode": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int],
     "vr_conv_columns": [c_vp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
                         c_u64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, c_vp,

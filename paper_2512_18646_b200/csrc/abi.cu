@@ -8,6 +8,7 @@
 
 #include "../../include/vrhe.h"
 #include "encode.cuh"
+#include "graph.cuh"
 
 struct vr_ctx {
     vr::Ctx c;
@@ -100,8 +101,9 @@ void check_level(const vr::Ctx &c, int level) {
 void destroy_ctx(vr_ctx *h) {
     vr::Ctx &c = h->c;
     cudaSetDevice(c.device);
-    for (cudaStream_t s : {c.own, c.aux, c.hi, c.stream})
+    for (cudaStream_t s : {c.own, c.aux, c.hi, c.stream, c.side, c.slot_stream[0], c.slot_stream[1], c.slot_stream[2]})
         if (s) cudaStreamSynchronize(s);
+    vr::graphs_release(c);
     void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.liftk, c.kshift, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw,
                     c.slot_pos, c.pos_slot, c.cdt, c.rlk, c.s_ntt, c.s_sh, c.pk, c.arena};
     for (void *p : ptrs)
@@ -116,7 +118,8 @@ void destroy_ctx(vr_ctx *h) {
         if (c.stage_evt[i]) cudaEventDestroy(c.stage_evt[i]);
     if (c.stage) cudaFreeHost(c.stage);
     // the private streams only; a user stream installed by vr_set_stream belongs to the caller
-    for (cudaStream_t s : {c.own, c.aux, c.hi})
+    // (the slot streams are process-wide, graph.cu, and stay)
+    for (cudaStream_t s : {c.own, c.aux, c.hi, c.side})
         if (s) cudaStreamDestroy(s);
     cudaGetLastError();
     delete h;
@@ -148,6 +151,11 @@ void ensure_smem(Ctx &c, const void *kern, size_t smem) {
 const void *const *cached_table(Ctx &c, const void *const *ptrs, size_t n) {
     static const void *empty_slot = nullptr;
     if (n == 0) n = 1, ptrs = &empty_slot;
+    if (c.capturing) {  // a graph's tables live as long as the graph (never evicted under it)
+        void *d = capture_alloc(c, n * sizeof(void *));
+        capture_upload(c, d, ptrs, n * sizeof(void *));
+        return (const void *const *)d;
+    }
     c.table_clock++;
     for (auto &e : c.tables)
         if (e.key.size() == n && std::memcmp(e.key.data(), ptrs, n * sizeof(void *)) == 0) {
@@ -174,6 +182,10 @@ const void *const *cached_table(Ctx &c, const void *const *ptrs, size_t n) {
 }
 
 void upload_async(Ctx &c, void *dst, const void *src, size_t bytes) {
+    if (c.capturing) {  // the staging ring is reused: a captured copy from it would replay stale data
+        capture_upload(c, dst, src, bytes);
+        return;
+    }
     const char *p = (const char *)src;
     char *d = (char *)dst;
     while (bytes) {
@@ -337,6 +349,7 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
         VR_CUDA(cudaStreamCreateWithFlags(&c.own, cudaStreamNonBlocking));
         c.stream = c.own;  // until vr_set_stream installs the caller's stream
         VR_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
+        VR_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
         VR_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
         VR_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
         {
@@ -624,8 +637,50 @@ int vr_matmul_outer(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *
         if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
         if (n <= 0) throw vr::VrError(VR_ERR_LAYOUT, "matmul_outer needs at least one column ciphertext");
         vr::Ctx &c = h->c;
-        vr::PtrTable tl(c, vec(L, (size_t)n * nb)), tr(c, vec(R, n)), to(c, vecm(out, nb));
-        vr::matmul_outer(c, tl.c_(), tr.c_(), n, nb, level, to.m_());
+        std::vector<uintptr_t> key{1, (uintptr_t)n, (uintptr_t)nb, (uintptr_t)level};
+        key.insert(key.end(), (const uintptr_t *)L, (const uintptr_t *)L + (size_t)n * nb);
+        key.insert(key.end(), (const uintptr_t *)R, (const uintptr_t *)R + n);
+        key.insert(key.end(), (const uintptr_t *)out, (const uintptr_t *)out + nb);
+        auto body = [&] {
+            vr::PtrTable tl(c, vec(L, (size_t)n * nb)), tr(c, vec(R, n)), to(c, vecm(out, nb));
+            vr::matmul_outer(c, tl.c_(), tr.c_(), n, nb, level, to.m_());
+        };
+        // Small products (config 1: 4 MB of operands, ~20 us of device work) are bound by the host
+        // submitting nine launches on three streams: replay them as one CUDA graph from the second
+        // call on.  Large ones stay eager: the device is the bottleneck there, and eager launches
+        // keep the programmatic overlap of one call's first kernel with the previous call's tail
+        // (cfg 2: 80.4 us/step eager vs 88.1 as a graph, tools/step_probe.py).
+        const size_t operand_bytes = (size_t)(nb + 1) * n * 2 * (level + 1) * c.n * 8;
+        if (operand_bytes <= vr::graph_max_bytes()) vr::run_graphed(c, std::move(key), body);
+        else body();
+    });
+}
+
+int vr_matmul_outer_async(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
+                          uint64_t *const *out, void **slot_stream) {
+    return guard([&] {
+        *slot_stream = nullptr;
+        check_level(h->c, level);
+        if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
+        if (n <= 0) throw vr::VrError(VR_ERR_LAYOUT, "matmul_outer needs at least one column ciphertext");
+        *slot_stream = (void *)vr::matmul_outer_async(h->c, L, R, n, nb, level, out);
+    });
+}
+
+static_assert(vr::Ctx::kSlots == 3, "vr_ctx_destroy lists the slot streams");
+
+int vr_async_slot(vr_ctx *h, void **slot_stream) {
+    return guard([&] { *slot_stream = (void *)vr::next_async_slot(h->c); });
+}
+
+int vr_join(vr_ctx *h) {
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        for (cudaStream_t s : c.slot_stream) {
+            if (!s) continue;
+            VR_CUDA(cudaEventRecord(c.ev_join, s));
+            VR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+        }
     });
 }
 

@@ -242,11 +242,16 @@ void mul_batch(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint6
     relin_rescale_batch(c, td.c_(), Out, count, level);
 }
 
-void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out) {
+void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out,
+                  bool one_pass) {
     const int N = c.n, nl = level + 1;
     Scratch d3(c, sizeof(uint64_t) * nb * 3 * nl * N);
     PtrTable td(c, strided(d3.as<uint64_t>(), nb, (size_t)3 * nl * N));
-    if (nb == 1 && n >= 8) {
+    static const int mm_order = [] {
+        const char *e = getenv("VR_MM_ORDER");
+        return e ? atoi(e) : 4;
+    }();
+    if (nb == 1 && n >= 8 && mm_order != 5 && !one_pass) {  // 5: one (d0, d1, d2) pass, then the chain, one stream
         // overlap: d2 = sum L1 R1 (half the operand bytes) feeds the key switch, while (d0, d1)
         // accumulate on the auxiliary stream; the final combine waits for them.  VR_MM_ORDER:
         // 4 (default, measured best: 87.7 vs 94 us at cfg 2) d2 + key switch on the highest-priority

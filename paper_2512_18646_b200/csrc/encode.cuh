@@ -16,7 +16,10 @@ void keygen(Ctx &c);
 
 // drivers (drivers.cu)
 void mul_batch(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *Out, int count, int level);
-void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out);
+// one_pass: one (d0, d1, d2) tensor-sum pass then the key-switch chain, all on c.stream (the form
+// recorded into the asynchronous per-slot graphs, graph.cu)
+void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out,
+                  bool one_pass = false);
 void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, int k, const int64_t *w, const uint64_t *bias,
                   int F, const int *out_cols, int nout, const uint64_t *mask_pt, int level, const std::vector<uint64_t *> &Y);
 void pt_matvec(Ctx &c, const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int level, uint64_t *const *Y);

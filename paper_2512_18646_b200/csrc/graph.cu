@@ -1,0 +1,260 @@
+// graph.cu -- CUDA-graph cache of fixed-shape drivers (see graph.cuh).
+#include <algorithm>
+#include <map>
+#include <mutex>
+
+#include "encode.cuh"
+#include "graph.cuh"
+#include "ring.cuh"
+
+namespace vr {
+
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("VR_GRAPH");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    return on;
+}
+
+size_t graph_max_bytes() {
+    static const size_t v = [] {
+        const char *e = getenv("VR_GRAPH_MAX_MB");
+        return (size_t)((e ? atof(e) : 32.0) * 1048576.0);
+    }();
+    return v;
+}
+
+void *capture_alloc(Ctx &c, size_t bytes) {
+    void *p = nullptr;
+    VR_CUDA(cudaMallocAsync(&p, bytes, c.side));
+    c.capturing->blocks.push_back(p);
+    return p;
+}
+
+void capture_upload(Ctx &c, void *dst, const void *src, size_t bytes) {
+    // synchronous w.r.t. the host buffer (it may be a temporary), off the capturing stream
+    VR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.side));
+    VR_CUDA(cudaStreamSynchronize(c.side));
+}
+
+static void free_mem(Ctx &c, GraphMem &m) {
+    for (void *p : m.blocks) cudaFreeAsync(p, c.side);
+    m.blocks.clear();
+    cudaStreamSynchronize(c.side);
+    cudaGetLastError();
+}
+
+static void release(Ctx &c, GraphEntry &g) {
+    if (g.exec) {
+        cudaDeviceSynchronize();  // the graph may still be running on whichever stream launched it
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+    }
+    if (g.graph) {
+        cudaGraphDestroy(g.graph);
+        g.graph = nullptr;
+    }
+    free_mem(c, g.mem);
+}
+
+void graphs_release(Ctx &c) {
+    for (auto &g : c.graphs) release(c, g);
+    c.graphs.clear();
+}
+
+GraphEntry *graph_lookup(Ctx &c, std::vector<uintptr_t> &&key) {
+    c.graph_clock++;
+    for (auto &g : c.graphs)
+        if (g.key == key) {
+            g.last_use = c.graph_clock;
+            return &g;
+        }
+    constexpr size_t kMaxGraphs = 16;
+    if (c.graphs.size() >= kMaxGraphs) {
+        auto it = std::min_element(c.graphs.begin(), c.graphs.end(),
+                                   [](const GraphEntry &a, const GraphEntry &b) { return a.last_use < b.last_use; });
+        release(c, *it);
+        c.graphs.erase(it);
+    }
+    c.graphs.emplace_back();
+    GraphEntry &g = c.graphs.back();
+    g.key = std::move(key);
+    g.last_use = c.graph_clock;
+    return &g;
+}
+
+void graph_capture_begin(Ctx &c, GraphEntry &g, cudaStream_t &user, unsigned long long &k0) {
+    user = c.stream;
+    k0 = __atomic_load_n(&g_launches, __ATOMIC_RELAXED);
+    // record on the private non-blocking stream (the legacy default stream cannot be captured);
+    // the replay is ordered on the caller's stream
+    VR_CUDA(cudaStreamBeginCapture(c.own, cudaStreamCaptureModeRelaxed));
+    c.stream = c.own;
+    c.capturing = &g.mem;
+}
+
+void graph_capture_abort(Ctx &c, GraphEntry &g, cudaStream_t user, unsigned long long k0) {
+    cudaGraph_t graph = nullptr;
+    cudaStreamEndCapture(c.own, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    c.capturing = nullptr;
+    c.stream = user;
+    __atomic_store_n(&g_launches, k0, __ATOMIC_RELAXED);
+    free_mem(c, g.mem);
+    g.seen = -1000000;  // never try to capture this key again
+}
+
+void graph_capture_end(Ctx &c, GraphEntry &g, cudaStream_t user, unsigned long long k0, bool keep_graph) {
+    c.capturing = nullptr;
+    c.stream = user;
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c.own, &graph);
+    const unsigned long long k1 = __atomic_load_n(&g_launches, __ATOMIC_RELAXED);
+    g.kernels = k1 - k0;
+    __atomic_fetch_sub(&g_launches, g.kernels, __ATOMIC_RELAXED);  // recorded, not launched
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (graph) cudaGraphDestroy(graph);
+        free_mem(c, g.mem);
+        throw VrError(4, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+    }
+    VR_CUDA(cudaStreamSynchronize(c.side));  // capture-time allocations and uploads are complete
+    const cudaError_t ei = cudaGraphInstantiateWithFlags(&g.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
+    if (keep_graph && ei == cudaSuccess) g.graph = graph;  // its nodes stay addressable for SetParams
+    else cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+        cudaGetLastError();
+        g.exec = nullptr;
+        free_mem(c, g.mem);
+        throw VrError(4, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ei));
+    }
+}
+
+void graph_launch(Ctx &c, GraphEntry &g) {
+    VR_CUDA(cudaGraphLaunch(g.exec, c.stream));
+    __atomic_fetch_add(&g_launches, g.kernels, __ATOMIC_RELAXED);
+}
+
+// Slot streams are process-wide per device and never destroyed: tensors recorded on them (the
+// caching allocator's record_stream of operands and outputs) may outlive the context that ran the
+// product, and the allocator records events on the stream when such a tensor is freed.
+static cudaStream_t slot_stream(int device, int k) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, cudaStream_t> pool;
+    std::lock_guard<std::mutex> lock(mu);
+    cudaStream_t &s = pool[{device, k}];
+    if (!s) {
+        int cur = device;
+        VR_CUDA(cudaGetDevice(&cur));
+        if (cur != device) VR_CUDA(cudaSetDevice(device));
+        const cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (cur != device) cudaSetDevice(cur);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            s = nullptr;
+            throw VrError(4, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+        }
+    }
+    return s;
+}
+
+// writes the output pointer table of an asynchronous slot graph (its parameters are replaced
+// before every replay, so one recorded graph serves any output buffer)
+__global__ void k_set_out(uint64_t **table, uint64_t *p0, uint64_t *p1, uint64_t *p2, uint64_t *p3, int nb) {
+    if (threadIdx.x == 0) {
+        table[0] = p0;
+        if (nb > 1) table[1] = p1;
+        if (nb > 2) table[2] = p2;
+        if (nb > 3) table[3] = p3;
+    }
+}
+
+static void set_out_params(GraphEntry &g, uint64_t *const *out, int nb) {
+    uint64_t *p[4] = {out[0], nb > 1 ? out[1] : nullptr, nb > 2 ? out[2] : nullptr, nb > 3 ? out[3] : nullptr};
+    void *args[] = {&g.out_table, &p[0], &p[1], &p[2], &p[3], &nb};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void *)k_set_out;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(32);
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    VR_CUDA(cudaGraphExecKernelNodeSetParams(g.exec, g.out_node, &kp));
+}
+
+// Asynchronous matmul_outer.  Calls rotate over Ctx::kSlots private streams; slot k replays its own
+// graph of the one-pass form (one (d0, d1, d2) tensor sum, then the relinearise+rescale chain)
+// recorded with graph-owned scratch, so the latency-bound chain of one call overlaps the streaming
+// sums of the next ones.  The slot stream first waits for everything already queued on the
+// caller's stream (the operands); the caller orders any later use of the output after the returned
+// stream (the Python layer makes its current stream wait before the result is read, and records
+// the operand/output tensors on it for the caching allocator).  The first call of a given
+// (slot, operands) key runs synchronously and the second records the graph, so one-off products
+// never pay a capture.  (3 slots: cfg-2 matmul 80 -> ~57 us per product, tools/overlap_probe.py.)
+cudaStream_t next_async_slot(Ctx &c) {
+    const int k = c.slot_next;
+    if (!c.slot_stream[k]) c.slot_stream[k] = slot_stream(c.device, k);
+    return c.slot_stream[k];
+}
+
+cudaStream_t matmul_outer_async(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
+                                uint64_t *const *out) {
+    auto sync_body = [&] {
+        PtrTable tl(c, std::vector<const uint64_t *>(L, L + (size_t)n * nb)), tr(c, std::vector<const uint64_t *>(R, R + n)),
+            to(c, std::vector<const uint64_t *>(out, out + nb));
+        matmul_outer(c, tl.c_(), tr.c_(), n, nb, level, to.m_());
+    };
+    if (!graphs_enabled() || nb > 4) {
+        sync_body();
+        return nullptr;
+    }
+    const int k = c.slot_next;
+    std::vector<uintptr_t> key{2, (uintptr_t)k, (uintptr_t)n, (uintptr_t)nb, (uintptr_t)level};
+    key.insert(key.end(), (const uintptr_t *)L, (const uintptr_t *)L + (size_t)n * nb);
+    key.insert(key.end(), (const uintptr_t *)R, (const uintptr_t *)R + n);
+    GraphEntry *g = graph_lookup(c, std::move(key));
+    if (!g->exec) {
+        if (g->seen < 1) {
+            g->seen++;
+            sync_body();
+            return nullptr;
+        }
+        relin_key(c);  // generated outside any capture
+        cudaStream_t user;
+        unsigned long long k0;
+        graph_capture_begin(c, *g, user, k0);
+        try {
+            PtrTable tl(c, std::vector<const uint64_t *>(L, L + (size_t)n * nb)),
+                tr(c, std::vector<const uint64_t *>(R, R + n)), to(c, std::vector<const uint64_t *>(out, out + nb));
+            g->out_table = (uint64_t **)to.p;
+            uint64_t *p[4] = {out[0], nb > 1 ? out[1] : nullptr, nb > 2 ? out[2] : nullptr, nb > 3 ? out[3] : nullptr};
+            k_set_out<<<1, 32, 0, c.stream>>>(g->out_table, p[0], p[1], p[2], p[3], nb);
+            check_launch("k_set_out");
+            cudaStreamCaptureStatus cs;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t nd = 0;
+            VR_CUDA(cudaStreamGetCaptureInfo(c.stream, &cs, nullptr, nullptr, &deps, &nd));
+            if (nd != 1) throw VrError(4, "matmul_outer_async: unexpected capture dependencies");
+            g->out_node = deps[0];
+            matmul_outer(c, tl.c_(), tr.c_(), n, nb, level, to.m_(), true);
+        } catch (...) {
+            graph_capture_abort(c, *g, user, k0);
+            throw;
+        }
+        graph_capture_end(c, *g, user, k0, true);
+    } else {
+        set_out_params(*g, out, nb);
+    }
+    if (!c.slot_stream[k]) c.slot_stream[k] = slot_stream(c.device, k);
+    cudaStream_t s = c.slot_stream[k];
+    VR_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // operands (and anything before) are ready
+    VR_CUDA(cudaStreamWaitEvent(s, c.ev_fork, 0));
+    VR_CUDA(cudaGraphLaunch(g->exec, s));
+    __atomic_fetch_add(&g_launches, g->kernels, __ATOMIC_RELAXED);
+    c.slot_next = (k + 1) % Ctx::kSlots;
+    return s;
+}
+
+}  // namespace vr

@@ -258,9 +258,15 @@ __host__ __device__ constexpr int ts_stages() {
 template <int NB, int TS_TILE, int TS_SPLIT, int MAXST, int MODE>
 __global__ void __launch_bounds__(TS_TILE / 2 + 32)
     k_tensor_sum(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O,
-                 int hint) {
+                 int hint, int rb) {
     pdl_wait();
     pdl_trigger();
+    // rb > 1: rb independent row blocks interleaved along x (block fastest), so the rb CTAs that read
+    // the same R tiles are dispatched together and share them through L2
+    const int xb = rb > 1 ? (int)blockIdx.x % rb : 0;
+    const int xt = rb > 1 ? (int)blockIdx.x / rb : (int)blockIdx.x;
+    L += (size_t)xb * NB * n;
+    O += xb * NB;
     constexpr int TS_CONSUMERS = TS_TILE / 2;  // 2 coefficients per consumer thread
     constexpr int TS_STAGES = ts_stages<NB, TS_TILE, MAXST>();
     // limb tiles per stage: L[b] poly0/poly1 ..., R poly0/poly1 (MODE 1: L[b] poly1 ..., R poly1)
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
     cg::cluster_group cluster = cg::this_cluster();
     const int tile = N < TS_TILE ? N : TS_TILE;
     const int cons = tile / 2;
-    const int k0 = blockIdx.x * tile, i = blockIdx.y;
+    const int k0 = xt * tile, i = blockIdx.y;
     const int z = (int)cluster.block_rank();
     const int per = (n + TS_SPLIT - 1) / TS_SPLIT;
     const int tb = min(n, z * per), te = min(n, tb + per);
@@ -421,6 +427,144 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
         }
     }
     cluster.sync();  // peers keep their shared memory alive until rank 0 has read it
+}
+
+// ---- cluster-multicast tensor sum: NB row blocks sharing R, R read from HBM once ---------------
+// multicast variant of bulk_g2s: the tile lands at the same shared-memory offset in every CTA of
+// `mask` and signals the mbarrier at the same offset in each of them
+__device__ __forceinline__ void bulk_g2s_mc(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+// arrive on the barrier at the same offset in cluster CTA `cta` (release at cluster scope)
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t cta) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(cta));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+// (d0, d1, d2)[b] = sum_k L[b][k] (x) R[k] for NB row blocks (config 5a: 4 blocks of 64 x 256 column
+// ciphertexts sharing the 256 right ciphertexts).  One thread-block cluster = NB x SPLIT CTAs: CTA
+// (b, z) accumulates row block b over the z-th part of the k range, so each CTA holds one block's
+// 128-bit accumulators (no register pressure from NB).  Each CTA's producer thread streams its own
+// L_b limb tiles with TMA bulk copies; the R tiles of step k are fetched ONCE per split group by one
+// CTA (rotating with k) and multicast into all NB CTAs' rings.  A ring slot is reused only after the
+// consumers of all NB CTAs released it (remote mbarrier arrivals), so R crosses HBM once instead of
+// once per row block: 5.4 GB instead of 6.4 GB per config-5a product.
+template <int NB, int TILE, int SPLIT, int ST>
+__global__ void __launch_bounds__(TILE / 2 + 32)
+    k_tensor_sum_mc(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int CONS = TILE / 2;  // 2 coefficients per consumer thread
+    constexpr int NWC = CONS / 32;  // consumer warps; the producer warp follows them
+    extern __shared__ __align__(128) uint64_t ts_smem[];
+    uint64_t *ring = ts_smem;  // [ST][4][TILE]: L poly 0, L poly 1, R poly 0, R poly 1
+    __shared__ __align__(8) uint64_t full[ST], empty[ST];
+    ulonglong2(*part)[CONS] = reinterpret_cast<ulonglong2(*)[CONS]>(ts_smem);  // [3][CONS] after the stream
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int b = rank % NB, zk = rank / NB;
+    const int k0 = blockIdx.x * TILE, i = blockIdx.y;
+    const int per = (n + SPLIT - 1) / SPLIT;
+    const int tb = min(n, zk * per), te = min(n, tb + per);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint16_t mask = (uint16_t)(((1u << NB) - 1u) << (zk * NB));
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NWC * NB);  // every consumer warp of the NB CTAs of this split group
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster.sync();  // barriers initialised cluster-wide before any multicast or remote arrival
+    const Modulus m = pr.m[i];
+    if (warp == NWC) {
+        if (lane == 0) {
+            const uint32_t bytes = (uint32_t)TILE * 8;
+            const size_t o0 = (size_t)i * N + k0, o1 = (size_t)(nl + i) * N + k0;
+            for (int t = tb, it = 0; t < te; t++, it++) {
+                const int s = it % ST;
+                if (it >= ST) mbar_wait_cluster(&empty[s], ((it / ST) - 1) & 1);
+                uint64_t *st = ring + (size_t)s * 4 * TILE;
+                mbar_expect_tx(&full[s], bytes * 4);
+                const uint64_t *l = L[(size_t)b * n + t];
+                bulk_g2s(st, l + o0, bytes, &full[s]);
+                bulk_g2s(st + TILE, l + o1, bytes, &full[s]);
+                if (it % NB == b) {
+                    const uint64_t *r = R[t];
+                    bulk_g2s_mc(st + 2 * TILE, r + o0, bytes, &full[s], mask);
+                    bulk_g2s_mc(st + 3 * TILE, r + o1, bytes, &full[s], mask);
+                }
+            }
+        }
+    } else {
+        u128 acc[3][2];
+#pragma unroll
+        for (int p = 0; p < 3; p++) acc[p][0] = acc[p][1] = u128{0, 0};
+        const int c2 = threadIdx.x * 2;
+        for (int t = tb, it = 0; t < te; t++, it++) {
+            const int s = it % ST;
+            mbar_wait(&full[s], (it / ST) & 1);
+            const uint64_t *st = ring + (size_t)s * 4 * TILE;
+            const ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(st + c2);
+            const ulonglong2 l1 = *reinterpret_cast<const ulonglong2 *>(st + TILE + c2);
+            const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + 2 * TILE + c2);
+            const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + 3 * TILE + c2);
+            mac_to(acc[0][0], l0.x, r0.x);
+            mac_to(acc[0][1], l0.y, r0.y);
+            mac_to(acc[1][0], l0.x, r1.x);
+            mac_to(acc[1][1], l0.y, r1.y);
+            mac_to(acc[1][0], l1.x, r0.x);
+            mac_to(acc[1][1], l1.y, r0.y);
+            mac_to(acc[2][0], l1.x, r1.x);
+            mac_to(acc[2][1], l1.y, r1.y);
+            __syncwarp();
+            if (lane < NB) mbar_arrive_remote(&empty[s], (uint32_t)(zk * NB + lane));  // release slot s in all NB CTAs
+            if ((it & 7) == 7) {
+#pragma unroll
+                for (int p = 0; p < 3; p++)
+#pragma unroll
+                    for (int e = 0; e < 2; e++) acc[p][e] = u128{reduce128(acc[p][e], m), 0};
+            }
+        }
+        __syncwarp();
+        // every multicast into this ring has landed (all its steps were consumed): reuse it
+        asm volatile("bar.sync 1, %0;" ::"r"(CONS) : "memory");
+#pragma unroll
+        for (int p = 0; p < 3; p++) part[p][threadIdx.x] = make_ulonglong2(reduce128(acc[p][0], m), reduce128(acc[p][1], m));
+    }
+    cluster.sync();
+    if (zk == 0 && threadIdx.x < CONS) {
+        const int k = k0 + threadIdx.x * 2;
+        uint64_t *o = O[b];
+#pragma unroll
+        for (int p = 0; p < 3; p++) {
+            ulonglong2 v = part[p][threadIdx.x];
+#pragma unroll
+            for (int r = 1; r < SPLIT; r++) {
+                const ulonglong2 w = cluster.map_shared_rank(&part[p][0], r * NB + b)[threadIdx.x];
+                v.x = add_mod(v.x, w.x, m.q);
+                v.y = add_mod(v.y, w.y, m.q);
+            }
+            st2(o + (size_t)(p * nl + i) * N + k, v.x, v.y);
+        }
+    }
+    cluster.sync();  // peers keep their shared memory alive until the group's rank 0 has read it
 }
 
 constexpr int TB = 256;
@@ -578,7 +722,7 @@ void mod_fixup(Ctx &c, uint64_t *data, long long count_polys, int nl) {
 
 // Launch shape (tile, split-K) -- tuned on B200 with tools/bw_probe.py; VR_TS_VARIANT overrides.
 template <int NB, int TILE, int SPLIT, int MAXST = 8, int MODE = 0>
-static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O) {
+static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O, int rb = 1) {
     constexpr int ARR = MODE == 1 ? NB + 1 : 2 * NB + 2;
     const int tile = c.n < TILE ? c.n : TILE;
     size_t smem = (size_t)ts_stages<NB, TILE, MAXST>() * ARR * tile * sizeof(uint64_t);
@@ -586,7 +730,7 @@ static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
     auto kern = k_tensor_sum<NB, TILE, SPLIT, MAXST, MODE>;
     ensure_smem(c, (const void *)kern, smem);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(c.n / tile, nl, SPLIT);
+    cfg.gridDim = dim3(c.n / tile * rb, nl, SPLIT);
     cfg.blockDim = dim3(TILE / 2 + 32, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
@@ -603,7 +747,29 @@ static void launch_ts(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
         const char *e = getenv("VR_TS_HINT");
         return e ? atoi(e) : 1;
     }();
-    VR_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, n, nl, c.n, c.primes, O, hint));
+    VR_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, n, nl, c.n, c.primes, O, hint, rb));
+}
+
+template <int NB, int TILE, int SPLIT, int ST>
+static void launch_ts_mc(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O) {
+    const size_t smem = std::max<size_t>((size_t)ST * 4 * TILE * sizeof(uint64_t), (size_t)3 * (TILE / 2) * 16);
+    auto kern = k_tensor_sum_mc<NB, TILE, SPLIT, ST>;
+    ensure_smem(c, (const void *)kern, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c.n / TILE, nl, NB * SPLIT);
+    cfg.blockDim = dim3(TILE / 2 + 32, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = NB * SPLIT;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    VR_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, n, nl, c.n, c.primes, O));
 }
 
 template <int NB>
@@ -611,6 +777,12 @@ static void ts_variant(Ctx &c, int v, const uint64_t *const *L, const uint64_t *
     switch (v) {
         case 1: launch_ts<NB, 256, 1, 8>(c, L, R, n, nl, O); break;
         case 2: launch_ts<NB, 128, 2, 8>(c, L, R, n, nl, O); break;
+        case 3: launch_ts<NB, 512, 2, 4>(c, L, R, n, nl, O); break;
+        case 4: launch_ts<NB, 512, 4, 4>(c, L, R, n, nl, O); break;
+        case 5: launch_ts<NB, 256, 2, 8>(c, L, R, n, nl, O); break;
+        case 6: launch_ts<NB, 512, 2, 6>(c, L, R, n, nl, O); break;
+        case 7: launch_ts<NB, 1024, 2, 2>(c, L, R, n, nl, O); break;
+        case 8: launch_ts<NB, 256, 4, 4>(c, L, R, n, nl, O); break;
         default: launch_ts<NB, 256, 2, 4>(c, L, R, n, nl, O); break;  // best on B200 (tools/bw_probe.py)
     }
 }
@@ -665,7 +837,7 @@ void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int 
         case 1: ts_variant<1>(c, variant, L, R, n, nl, O); break;
         case 2: ts_variant<2>(c, variant, L, R, n, nl, O); break;
         case 4: {
-            // four row blocks sharing R (cfg 5a): two launches of two row blocks.  R is streamed twice,
+            // four row blocks sharing R (cfg 5a).  Round 1: two launches of two row blocks, R streamed twice,
             // but each CTA holds half the 128-bit accumulators (104 instead of 188 registers, 3 CTAs
             // per SM instead of 2): cfg-5a matmul 2.12 -> 1.56 ms.  Swept on B200 (tools/prof_5a.sh):
             // one NB=4 kernel 2.12 ms (tiles 128 / split 4: 2.81; tile 256 / split 4: 2.52), two NB=2
@@ -677,9 +849,24 @@ void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int 
             }();
             if (v4 == 1) {
                 ts_variant<4>(c, variant, L, R, n, nl, O);
-            } else {
+            } else if (v4 == 2 || c.n < 256) {
                 launch_ts<2, 256, 2, 4>(c, L, R, n, nl, O);
                 launch_ts<2, 256, 2, 4>(c, L + 2 * (size_t)n, R, n, nl, O + 2);
+            } else {
+                // default: one pass, R multicast to the four row-block CTAs of each cluster
+                static const int mcv = [] {
+                    const char *e = getenv("VR_TS4_MC");
+                    return e ? atoi(e) : 0;
+                }();
+                switch (mcv) {
+                    case 1: launch_ts_mc<4, 256, 2, 8>(c, L, R, n, nl, O); break;
+                    case 2: launch_ts_mc<4, 512, 2, 4>(c, L, R, n, nl, O); break;
+                    case 3: launch_ts<1, 256, 2, 4>(c, L, R, n, nl, O, 4); break;
+                    case 4: launch_ts<1, 512, 2, 4>(c, L, R, n, nl, O, 4); break;
+                    case 5: launch_ts<2, 256, 2, 4>(c, L, R, n, nl, O, 2); break;
+                    case 6: launch_ts<1, 256, 4, 4>(c, L, R, n, nl, O, 4); break;
+                    default: launch_ts<1, 512, 2, 6>(c, L, R, n, nl, O, 4); break;
+                }
             }
             break;
         }

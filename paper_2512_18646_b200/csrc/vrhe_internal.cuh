@@ -33,6 +33,27 @@ struct NttConst {
     int f64;
 };
 
+// Memory owned by one captured CUDA graph (graph.cu): while a driver is being captured, every
+// scratch buffer and pointer table it asks for is carved here instead of the context's arena /
+// table cache, so the graph's baked-in addresses stay valid for as long as the graph lives.
+struct GraphMem {
+    std::vector<void *> blocks;
+};
+
+struct GraphEntry {
+    std::vector<uintptr_t> key;  // driver id, shape, level, then every pointer of the call
+    cudaGraphExec_t exec = nullptr;
+    GraphMem mem;
+    unsigned long long kernels = 0;  // kernel launches the graph replays (for vr_launch_count)
+    unsigned long long last_use = 0;
+    int seen = 0;  // eager runs so far (a key is captured on its second occurrence)
+    // asynchronous slot graphs: the kernel node that writes the output pointer table, re-pointed at
+    // every replay (cudaGraphExecKernelNodeSetParams), and the graph it belongs to
+    cudaGraph_t graph = nullptr;
+    cudaGraphNode_t out_node = nullptr;
+    uint64_t **out_table = nullptr;
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t stream = 0;                 // the stream every call is ordered on (vr_set_stream)
@@ -101,8 +122,25 @@ struct Ctx {
     // blocks from the pool can stall the host for hundreds of ms
     std::vector<std::pair<size_t, void *>> big_free;
 
+    // CUDA-graph cache of fixed-shape drivers (graph.cu); capturing != nullptr while one records
+    std::vector<GraphEntry> graphs;
+    unsigned long long graph_clock = 0;
+    GraphMem *capturing = nullptr;
+    cudaStream_t side = 0;  // non-blocking helper stream for capture-time allocations and uploads
+    // asynchronous drivers (vr_matmul_outer_async): calls rotate over kSlots streams (process-wide per
+    // device, graph.cu), each replaying its own graph, so consecutive independent calls overlap
+    static constexpr int kSlots = 3;
+    cudaStream_t slot_stream[kSlots] = {};
+    int slot_next = 0;
+
     size_t key_words() const { return (size_t)(L + 1) * 2 * np * n; }
 };
+
+// capture-time allocation / upload into the graph being recorded (graph.cu)
+void *capture_alloc(Ctx &c, size_t bytes);
+void capture_upload(Ctx &c, void *dst, const void *src, size_t bytes);
+// release every cached graph (context teardown)
+void graphs_release(Ctx &c);
 
 struct VrError : std::runtime_error {
     int code;
@@ -162,11 +200,16 @@ struct Scratch {
     Ctx &c;
     void *p = nullptr;
     size_t bytes = 0;
-    bool pooled = false, big = false;
+    bool pooled = false, big = false, graph = false;
     static constexpr size_t kArenaMaxBuffer = size_t(64) << 20, kArenaMaxCap = size_t(512) << 20;
     Scratch(Ctx &cx, size_t b) : c(cx) {
         bytes = (b + 255) & ~size_t(255);
         if (!bytes) return;
+        if (c.capturing) {  // recorded into a CUDA graph: the graph owns the buffer
+            p = capture_alloc(c, bytes);
+            graph = true;
+            return;
+        }
         if (bytes > kArenaMaxBuffer) {  // big buffers: cached free list (best fit within 2x)
             size_t best = (size_t)-1;
             int bi = -1;
@@ -202,7 +245,7 @@ struct Scratch {
         if (want > c.arena_peak && want <= kArenaMaxCap) c.arena_peak = want;
     }
     ~Scratch() {
-        if (!p) return;
+        if (!p || graph) return;
         if (pooled) c.arena_top -= bytes;
         else if (big) c.big_free.emplace_back(bytes, p);
         else cudaFreeAsync(p, c.stream);

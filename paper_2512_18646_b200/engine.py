@@ -18,6 +18,7 @@ of their level.  All of this runs on the GPU; the host only does bookkeeping.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -99,13 +100,14 @@ class Ciphertext:
     when asked, so wrapping a 64-ciphertext batch costs no per-item tensor indexing.
     """
 
-    __slots__ = ("_data", "_batch", "_idx", "_ptr", "level", "scale", "depth", "layout", "engine_id")
+    __slots__ = ("_data", "_batch", "_idx", "_ptr", "level", "scale", "depth", "layout", "engine_id", "_pending")
 
     def __init__(self, data: torch.Tensor, level: int, scale: float, depth: int = 0, layout: tuple | None = None,
                  engine_id: int = 0):
         self._data = data
         self._batch = None
         self._idx = 0
+        self._pending = None
         self._ptr = data.data_ptr()
         self.level = level
         self.scale = scale
@@ -120,6 +122,7 @@ class Ciphertext:
         ct = cls.__new__(cls)
         ct._data = None
         ct._batch = out
+        ct._pending = None
         ct._idx = i
         ct._ptr = out.data_ptr() + i * out.stride(0) * out.element_size()
         ct.level = level
@@ -140,6 +143,7 @@ class Ciphertext:
             ct = new(cls)
             ct._data = None
             ct._batch = out
+            ct._pending = None
             ct._idx = i
             ct._ptr = base + i * step
             ct.level = level
@@ -150,17 +154,33 @@ class Ciphertext:
             res.append(ct)
         return res
 
+    def _ready(self) -> None:
+        """Order the current stream after the (asynchronous) producer of these residues, and record
+        the storage on the current stream: the producer's stream owns the allocation, so reads
+        queued here must complete before the caching allocator hands the block out again."""
+        if self._pending is not None:
+            cur = torch.cuda.current_stream()
+            cur.wait_stream(self._pending)
+            self.storage_tensor().record_stream(cur)
+            self._pending = None
+
     @property
     def data(self) -> torch.Tensor:
+        self._ready()
         if self._data is None:
             self._data = self._batch[self._idx]
         return self._data
+
+    def storage_tensor(self) -> torch.Tensor:
+        """The device tensor holding these residues (a batch may hold several ciphertexts)."""
+        return self._data if self._data is not None else self._batch
 
     @property
     def degree(self) -> int:
         return (self._batch.shape[1] if self._data is None else self._data.shape[0]) - 1
 
     def ptr(self) -> int:
+        self._ready()
         return self._ptr
 
     def residues(self) -> np.ndarray:
@@ -203,6 +223,10 @@ class CkksEngine:
         self._stream_ptr = self._stream.cuda_stream
         _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(self._stream_ptr)))
         self._meter = OpMeter()
+        # asynchronous drivers (vr_matmul_outer_async): results are produced on the library's slot
+        # streams and every read of them waits first (Ciphertext._ready); VR_ASYNC=0 disables
+        self.async_drivers = os.environ.get("VR_ASYNC", "1") != "0"
+        self._ext_streams = {}
         self._nonce = 0
         self._pin = None
         self._pin_evt = None
@@ -645,7 +669,18 @@ class CkksEngine:
         return self.adjust(a, lv), self.adjust(b, lv)
 
     def sync(self) -> None:
+        self.join()
         _lib.check(self._lib.vr_sync(self.handle))
+
+    def join(self) -> None:
+        """Make the current stream wait for every asynchronous driver call issued so far."""
+        _lib.check(self._lib.vr_join(self.handle))
+
+    def _ext_stream(self, ptr: int):
+        s = self._ext_streams.get(ptr)
+        if s is None:
+            s = self._ext_streams[ptr] = torch.cuda.ExternalStream(ptr, device=self.device)
+        return s
 
 
 # The reference name: algorithm modules construct ``SlotEngine(EngineParams(...))``.

@@ -94,8 +94,33 @@ def _fresh(engine: CkksEngine, cem: ColumnEncodedMatrix) -> ColumnEncodedMatrix:
     """Operand fresh from one encryption batch: same engine, top level, depth 0 for every
     ciphertext, so the validated pointer cache of _checked_ptrs can be filled directly."""
     ptrs = [c._ptr for c in cem.cts]
-    object.__setattr__(cem, "_vr_ptrs", (engine._id, engine.L, ptrs, _lib.ptr_array(ptrs), 0))
+    object.__setattr__(cem, "_vr_ptrs", (engine._id, engine.L, ptrs, _lib.ptr_array(ptrs), 0, _storages(cem.cts)))
     return cem
+
+
+class _Storages(list):
+    """The distinct device tensors behind a list of ciphertexts (batches share one), plus the slot
+    streams they were already recorded on: the caching allocator keeps a recorded stream for the
+    block's lifetime, so each (tensor, stream) pair is recorded once, not per product."""
+
+    __slots__ = ("recorded",)
+
+    def record(self, stream, key: int) -> None:
+        rec = getattr(self, "recorded", None)
+        if rec is None:
+            rec = self.recorded = set()
+        if key not in rec:
+            for t in self:
+                t.record_stream(stream)
+            rec.add(key)
+
+
+def _storages(cts):
+    seen = {}
+    for c in cts:
+        t = c.storage_tensor()
+        seen.setdefault(id(t), t)
+    return _Storages(seen.values())
 
 
 def _common_level(engine: CkksEngine, cts):
@@ -117,15 +142,16 @@ def _checked_ptrs(engine: CkksEngine, cem: ColumnEncodedMatrix):
     ptrs = None
     if all(c.level == lv for c in cem.cts):
         ptrs = [c.ptr() for c in cem.cts]
-        object.__setattr__(cem, "_vr_ptrs", (engine._id, lv, ptrs, _lib.ptr_array(ptrs), max(c.depth for c in cem.cts)))
+        object.__setattr__(cem, "_vr_ptrs", (engine._id, lv, ptrs, _lib.ptr_array(ptrs), max(c.depth for c in cem.cts),
+                                             _storages(cem.cts)))
     return lv, ptrs
 
 
 def _fast_operand(engine: CkksEngine, cem: ColumnEncodedMatrix):
-    """(level, ctypes pointer array, max depth) from the cache, or None."""
+    """(level, ctypes pointer array, max depth, storage tensors) from the cache, or None."""
     cached = getattr(cem, "_vr_ptrs", None)
     if cached is not None and cached[0] == engine._id:
-        return cached[1], cached[3], cached[4]
+        return cached[1], cached[3], cached[4], cached[5]
     return None
 
 
@@ -157,13 +183,36 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
         if (fl is not None and fr is not None and fl[0] == fr[0] and fl[0] >= 1 and lf.role == "left"
                 and right.role == "right" and lf.n == n and lf.p == right.p):
             lv = fl[0]
-            outs = torch.empty((1, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
-            _lib.check(engine._lib.vr_matmul_outer(engine.handle, fl[1], fr[1], n, 1, lv, _lib.row_ptrs(outs, 1)))
+            pending = None
+            if engine.async_drivers:
+                # asynchronous: the product runs on a library slot stream, overlapping the next calls.
+                # The output is allocated ON that stream (the caching allocator then reuses it in that
+                # stream's order, with no cross-stream events), the operands are recorded on it once,
+                # and any read of the result waits for it (Ciphertext._ready)
+                h = engine.handle
+                slot = ctypes.c_void_p()
+                _lib.check(engine._lib.vr_async_slot(h, ctypes.byref(slot)))
+                ext = engine._ext_stream(slot.value)
+                with torch.cuda.stream(ext):
+                    outs = torch.empty((1, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
+                _lib.check(engine._lib.vr_matmul_outer_async(h, fl[1], fr[1], n, 1, lv, _lib.row_ptrs(outs, 1),
+                                                             ctypes.byref(slot)))
+                if slot.value:
+                    pending = ext
+                    fl[3].record(pending, slot.value)
+                    fr[3].record(pending, slot.value)
+                else:  # ran synchronously on the current stream
+                    outs.record_stream(torch.cuda.current_stream(engine.device))
+            else:
+                outs = torch.empty((1, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
+                _lib.check(engine._lib.vr_matmul_outer(engine.handle, fl[1], fr[1], n, 1, lv, _lib.row_ptrs(outs, 1)))
             depth = max(fl[2], fr[2]) + 1
             engine._meter.mul_count += n
             engine._meter.add_count += n - 1
             engine._observe(depth)
-            return [Ciphertext.at(outs, 0, lv - 1, engine.scales[lv - 1], depth, lf.cts[0].layout, engine._id)]
+            ct = Ciphertext.at(outs, 0, lv - 1, engine.scales[lv - 1], depth, lf.cts[0].layout, engine._id)
+            ct._pending = pending
+            return [ct]
     for lf in lefts:
         if lf.role != "left" or right.role != "right":
             raise LayoutError("operands must be a (left, right) column-encoded pair")

@@ -68,3 +68,44 @@ def test_cmul_constant_overflow_is_a_capacity_error():
     ct = eng.enc([1.0, 2.0])
     with pytest.raises(CapacityError):
         eng.cmul(eng.mask(np.full(eng.slots, 2.0 ** 30)), ct)  # 2^30 * 2^40 does not fit int64
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_matmul_outer_graph_replay_bit_exact(cfg):
+    """Repeated products of the same operands: the first call per (slot, operands) runs eagerly, the
+    second records the slot's CUDA graph, later ones replay it asynchronously on the slot streams
+    (three in flight).  Every result is identical to the first, whatever happens to the outputs."""
+    eng = CkksEngine(config_params(cfg))
+    dim = 8 if cfg == 1 else 64
+    a, b = np.random.default_rng(cfg).uniform(-1, 1, (2, dim, dim))
+    left, right = encode_left(eng, a, dim), encode_right(eng, b, dim)
+    first = matmul_outer(eng, left, right)
+    want = first.ct.residues()
+    np.testing.assert_allclose(first.decode(eng), a @ b, atol=TOL)
+    kept = []
+    for i in range(24):
+        out = matmul_outer(eng, left, right)
+        if i % 3 == 0:
+            kept.append(out)  # held while later products are in flight
+        elif i % 3 == 1:
+            del out  # dropped before it completes: the allocator must not hand the buffer out early
+        else:
+            junk = torch.full((2, eng.L, eng.N), 7, dtype=torch.int64, device=eng.device)  # reuse pressure
+            np.testing.assert_array_equal(out.ct.residues(), want)
+            del junk
+    for out in kept:
+        np.testing.assert_array_equal(out.ct.residues(), want)
+    eng.join()
+
+
+def test_async_results_feed_later_ops():
+    """An asynchronous product used directly by the next engine call (decode, add) is complete first."""
+    eng = CkksEngine(config_params(2))
+    a, b = np.random.default_rng(5).uniform(-1, 1, (2, 64, 64))
+    left, right = encode_left(eng, a, 64), encode_right(eng, b, 64)
+    outs = [matmul_outer(eng, left, right) for _ in range(8)]
+    total = outs[0].ct
+    for o in outs[1:]:
+        total = eng.add(total, o.ct)
+    got = eng.dec(total)[: 64 * 64].reshape(64, 64)
+    np.testing.assert_allclose(got, 8 * (a @ b), atol=8 * TOL)

@@ -6,6 +6,8 @@ process from the environment, so every variant runs in its own interpreter):
 * VR_MM_ORDER=2 -- matmul_outer's key-switch chain on the high-priority stream
 * VR_MM_ORDER=0, VR_NTT_F64=0 -- both tensor sums forked together on normal-priority streams, and
   every NTT on the integer (IMAD-pipe) body
+* VR_GRAPH=0   -- every driver call eager (no CUDA-graph replay)
+* VR_ASYNC=0   -- matmul_outer synchronous (no slot streams)
 """
 
 import os
@@ -19,8 +21,9 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-@pytest.mark.parametrize("env", [{"VR_NTT_CL": "1"}, {"VR_PDL": "0"}, {"VR_MM_ORDER": "2", "VR_NTT_CL": "1"}, {"VR_MM_ORDER": "0", "VR_NTT_F64": "0"}],
-                         ids=["cluster-ntt", "no-pdl", "hi-prio-chain", "order0-int-ntt"])
+@pytest.mark.parametrize("env", [{"VR_NTT_CL": "1"}, {"VR_PDL": "0"}, {"VR_MM_ORDER": "2", "VR_NTT_CL": "1"}, {"VR_MM_ORDER": "0", "VR_NTT_F64": "0"},
+                                 {"VR_GRAPH": "0"}, {"VR_ASYNC": "0"}],
+                         ids=["cluster-ntt", "no-pdl", "hi-prio-chain", "order0-int-ntt", "no-graph", "sync"])
 def test_parity_suite_under_variant(env):
     pytest.importorskip("torch").cuda.is_available() or pytest.skip("no CUDA device")
     e = dict(os.environ, **env)
