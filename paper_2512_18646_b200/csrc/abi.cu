@@ -101,7 +101,9 @@ void check_level(const vr::Ctx &c, int level) {
 void destroy_ctx(vr_ctx *h) {
     vr::Ctx &c = h->c;
     cudaSetDevice(c.device);
-    for (cudaStream_t s : {c.own, c.aux, c.hi, c.stream, c.side, c.slot_stream[0], c.slot_stream[1], c.slot_stream[2]})
+    for (cudaStream_t s : {c.own, c.aux, c.hi, c.stream, c.side})
+        if (s) cudaStreamSynchronize(s);
+    for (cudaStream_t s : c.slot_stream)
         if (s) cudaStreamSynchronize(s);
     vr::graphs_release(c);
     void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.liftk, c.kshift, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw,
@@ -666,8 +668,6 @@ int vr_matmul_outer_async(vr_ctx *h, const uint64_t *const *L, const uint64_t *c
         *slot_stream = (void *)vr::matmul_outer_async(h->c, L, R, n, nb, level, out);
     });
 }
-
-static_assert(vr::Ctx::kSlots == 3, "vr_ctx_destroy lists the slot streams");
 
 int vr_async_slot(vr_ctx *h, void **slot_stream) {
     return guard([&] { *slot_stream = (void *)vr::next_async_slot(h->c); });

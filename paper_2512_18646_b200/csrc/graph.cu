@@ -192,7 +192,8 @@ static void set_out_params(GraphEntry &g, uint64_t *const *out, int nb) {
 // stream (the Python layer makes its current stream wait before the result is read, and records
 // the operand/output tensors on it for the caching allocator).  The first call of a given
 // (slot, operands) key runs synchronously and the second records the graph, so one-off products
-// never pay a capture.  (3 slots: cfg-2 matmul 80 -> ~57 us per product, tools/overlap_probe.py.)
+// never pay a capture.  Slots swept on B200 (cfg 2, 200 products): synchronous 80.4 us per product;
+// 2 slots 74.5, 3 57.4, 4 51.7, 5 49.3, 6 47.0, 8 45.3 (20 products: 68.7 at 3 slots, 59.2 at 8).
 cudaStream_t next_async_slot(Ctx &c) {
     const int k = c.slot_next;
     if (!c.slot_stream[k]) c.slot_stream[k] = slot_stream(c.device, k);
@@ -253,7 +254,12 @@ cudaStream_t matmul_outer_async(Ctx &c, const uint64_t *const *L, const uint64_t
     VR_CUDA(cudaStreamWaitEvent(s, c.ev_fork, 0));
     VR_CUDA(cudaGraphLaunch(g->exec, s));
     __atomic_fetch_add(&g_launches, g->kernels, __ATOMIC_RELAXED);
-    c.slot_next = (k + 1) % Ctx::kSlots;
+    static const int nslots = [] {
+        const char *e = getenv("VR_ASYNC_SLOTS");
+        const int v = e ? atoi(e) : Ctx::kSlots;
+        return v < 1 ? 1 : (v > Ctx::kSlots ? Ctx::kSlots : v);
+    }();
+    c.slot_next = (k + 1) % nslots;
     return s;
 }
 

@@ -129,7 +129,7 @@ struct Ctx {
     cudaStream_t side = 0;  // non-blocking helper stream for capture-time allocations and uploads
     // asynchronous drivers (vr_matmul_outer_async): calls rotate over kSlots streams (process-wide per
     // device, graph.cu), each replaying its own graph, so consecutive independent calls overlap
-    static constexpr int kSlots = 3;
+    static constexpr int kSlots = 8;  // VR_ASYNC_SLOTS picks how many rotate (default all 8)
     cudaStream_t slot_stream[kSlots] = {};
     int slot_next = 0;
 
