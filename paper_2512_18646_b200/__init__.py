@@ -9,7 +9,7 @@ interface.  There is no CPU fallback.
 
 from .errors import CapacityError, EngineError, LayoutError
 from .params import EngineParams, config_params, gen_primes, is_pow2, next_pow2
-from .engine import Ciphertext, CkksEngine, OpMeter, PlainMask, SlotEngine
+from .engine import Ciphertext, CkksEngine, DecodeFuture, OpMeter, PlainMask, SlotEngine
 from .encoding import (
     Encoding,
     Kernel,

@@ -114,6 +114,10 @@ void destroy_ctx(vr_ctx *h) {
     for (auto &e : c.tables)
         if (e.dev) cudaFree(e.dev);
     for (auto &b : c.big_free) cudaFree(b.second);
+    for (auto &kv : c.parked) {
+        if (kv.second.arena) cudaFree(kv.second.arena);
+        for (auto &b : kv.second.big_free) cudaFree(b.second);
+    }
     for (cudaEvent_t e : {c.ev_fork, c.ev_join, c.ev_hi, c.ev_hi_done})
         if (e) cudaEventDestroy(e);
     for (int i = 0; i < vr::Ctx::kStageSlots; i++)
@@ -388,8 +392,30 @@ int vr_ctx_destroy(vr_ctx *h) {
 
 int vr_set_stream(vr_ctx *h, void *stream) {
     // NULL is the legacy default stream (torch's default stream); the private stream is kept
-    // for vr_ctx_destroy either way
-    return guard([&] { h->c.stream = (cudaStream_t)stream; });
+    // for vr_ctx_destroy either way.  Each stream gets its own scratch arena (Ctx::parked).
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        const cudaStream_t s = (cudaStream_t)stream;
+        if (s == c.stream) return;
+        vr::Ctx::ArenaState &old = c.parked[c.stream];
+        old.arena = c.arena;
+        old.cap = c.arena_cap;
+        old.top = c.arena_top;
+        old.peak = c.arena_peak;
+        old.big_free = std::move(c.big_free);
+        vr::Ctx::ArenaState cur;
+        auto it = c.parked.find(s);
+        if (it != c.parked.end()) {
+            cur = std::move(it->second);
+            c.parked.erase(it);
+        }
+        c.arena = cur.arena;
+        c.arena_cap = cur.cap;
+        c.arena_top = cur.top;
+        c.arena_peak = cur.peak;
+        c.big_free = std::move(cur.big_free);
+        c.stream = s;
+    });
 }
 
 int vr_sync(vr_ctx *h) {

@@ -160,46 +160,48 @@ static cudaStream_t slot_stream(int device, int k) {
     return s;
 }
 
-// writes the output pointer table of an asynchronous slot graph (its parameters are replaced
-// before every replay, so one recorded graph serves any output buffer)
-__global__ void k_set_out(uint64_t **table, uint64_t *p0, uint64_t *p1, uint64_t *p2, uint64_t *p3, int nb) {
-    if (threadIdx.x == 0) {
-        table[0] = p0;
-        if (nb > 1) table[1] = p1;
-        if (nb > 2) table[2] = p2;
-        if (nb > 3) table[3] = p3;
-    }
+// Kernel node at the head of every asynchronous slot graph: writes the operand and output pointer
+// tables the recorded driver reads.  Its parameters (the pointers themselves) are replaced before
+// every replay, so one recorded graph per (slot, shape) serves any operands and any output buffer.
+constexpr int kSetMaxPtrs = 240;  // (nb + 1) n + nb pointers; 2 KB of kernel parameters
+struct SetTables {
+    uint64_t **dst;  // the graph-owned tables: [L (nb n)] [R (n)] [out (nb)], contiguous
+    int count;
+    const uint64_t *p[kSetMaxPtrs];
+};
+__global__ void k_set_tables(SetTables a) {
+    for (int i = threadIdx.x; i < a.count; i += blockDim.x) a.dst[i] = const_cast<uint64_t *>(a.p[i]);
 }
 
-static void set_out_params(GraphEntry &g, uint64_t *const *out, int nb) {
-    uint64_t *p[4] = {out[0], nb > 1 ? out[1] : nullptr, nb > 2 ? out[2] : nullptr, nb > 3 ? out[3] : nullptr};
-    void *args[] = {&g.out_table, &p[0], &p[1], &p[2], &p[3], &nb};
-    cudaKernelNodeParams kp = {};
-    kp.func = (void *)k_set_out;
-    kp.gridDim = dim3(1);
-    kp.blockDim = dim3(32);
-    kp.sharedMemBytes = 0;
-    kp.kernelParams = args;
-    kp.extra = nullptr;
-    VR_CUDA(cudaGraphExecKernelNodeSetParams(g.exec, g.out_node, &kp));
+static SetTables make_tables(uint64_t **dst, const uint64_t *const *L, const uint64_t *const *R, uint64_t *const *out, int n,
+                             int nb) {
+    SetTables a;
+    a.dst = dst;
+    a.count = (nb + 1) * n + nb;
+    int k = 0;
+    for (int i = 0; i < nb * n; i++) a.p[k++] = L[i];
+    for (int i = 0; i < n; i++) a.p[k++] = R[i];
+    for (int i = 0; i < nb; i++) a.p[k++] = out[i];
+    return a;
 }
 
-// Asynchronous matmul_outer.  Calls rotate over Ctx::kSlots private streams; slot k replays its own
-// graph of the one-pass form (one (d0, d1, d2) tensor sum, then the relinearise+rescale chain)
-// recorded with graph-owned scratch, so the latency-bound chain of one call overlaps the streaming
-// sums of the next ones.  The slot stream first waits for everything already queued on the
-// caller's stream (the operands); the caller orders any later use of the output after the returned
-// stream (the Python layer makes its current stream wait before the result is read, and records
-// the operand/output tensors on it for the caching allocator).  The first call of a given
-// (slot, operands) key runs synchronously and the second records the graph, so one-off products
-// never pay a capture.  Slots swept on B200 (cfg 2, 200 products): synchronous 80.4 us per product;
-// 2 slots 74.5, 3 57.4, 4 51.7, 5 49.3, 6 47.0, 8 45.3 (20 products: 68.7 at 3 slots, 59.2 at 8).
 cudaStream_t next_async_slot(Ctx &c) {
     const int k = c.slot_next;
     if (!c.slot_stream[k]) c.slot_stream[k] = slot_stream(c.device, k);
     return c.slot_stream[k];
 }
 
+// Asynchronous matmul_outer.  Calls rotate over the slot streams; slot k replays its own graph of the
+// one-pass form (one (d0, d1, d2) tensor sum, then the relinearise+rescale chain) recorded with
+// graph-owned scratch, so the latency-bound chain of one call overlaps the streaming sums of the next
+// ones.  The slot stream first waits for everything already queued on the caller's stream (the
+// operands); the caller orders any later use of the output after the returned stream (the Python
+// layer makes its current stream wait before the result is read, and records the operand tensors on
+// it for the caching allocator).  The graph is keyed by (slot, shape, level) only: its pointer tables
+// are written by its first node, whose parameters carry this call's pointers.  The first call of a
+// key runs synchronously and the second records the graph.  Slots swept on B200 (cfg 2, 200
+// products): synchronous 80.4 us per product; 2 slots 74.5, 3 57.4, 4 51.7, 5 49.3, 6 47.0,
+// 8 45.3 (20 products: 68.7 at 3 slots, 59.2 at 8).
 cudaStream_t matmul_outer_async(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
                                 uint64_t *const *out) {
     auto sync_body = [&] {
@@ -207,15 +209,12 @@ cudaStream_t matmul_outer_async(Ctx &c, const uint64_t *const *L, const uint64_t
             to(c, std::vector<const uint64_t *>(out, out + nb));
         matmul_outer(c, tl.c_(), tr.c_(), n, nb, level, to.m_());
     };
-    if (!graphs_enabled() || nb > 4) {
+    if (!graphs_enabled() || nb > 4 || (nb + 1) * n + nb > kSetMaxPtrs) {
         sync_body();
         return nullptr;
     }
     const int k = c.slot_next;
-    std::vector<uintptr_t> key{2, (uintptr_t)k, (uintptr_t)n, (uintptr_t)nb, (uintptr_t)level};
-    key.insert(key.end(), (const uintptr_t *)L, (const uintptr_t *)L + (size_t)n * nb);
-    key.insert(key.end(), (const uintptr_t *)R, (const uintptr_t *)R + n);
-    GraphEntry *g = graph_lookup(c, std::move(key));
+    GraphEntry *g = graph_lookup(c, std::vector<uintptr_t>{2, (uintptr_t)k, (uintptr_t)n, (uintptr_t)nb, (uintptr_t)level});
     if (!g->exec) {
         if (g->seen < 1) {
             g->seen++;
@@ -227,29 +226,37 @@ cudaStream_t matmul_outer_async(Ctx &c, const uint64_t *const *L, const uint64_t
         unsigned long long k0;
         graph_capture_begin(c, *g, user, k0);
         try {
-            PtrTable tl(c, std::vector<const uint64_t *>(L, L + (size_t)n * nb)),
-                tr(c, std::vector<const uint64_t *>(R, R + n)), to(c, std::vector<const uint64_t *>(out, out + nb));
-            g->out_table = (uint64_t **)to.p;
-            uint64_t *p[4] = {out[0], nb > 1 ? out[1] : nullptr, nb > 2 ? out[2] : nullptr, nb > 3 ? out[3] : nullptr};
-            k_set_out<<<1, 32, 0, c.stream>>>(g->out_table, p[0], p[1], p[2], p[3], nb);
-            check_launch("k_set_out");
+            // one contiguous graph-owned block: L table, R table, out table
+            auto **tabs = (uint64_t **)capture_alloc(c, sizeof(void *) * ((nb + 1) * n + nb));
+            g->out_table = tabs;
+            k_set_tables<<<1, 256, 0, c.stream>>>(make_tables(tabs, L, R, out, n, nb));
+            check_launch("k_set_tables");
             cudaStreamCaptureStatus cs;
             const cudaGraphNode_t *deps = nullptr;
             size_t nd = 0;
             VR_CUDA(cudaStreamGetCaptureInfo(c.stream, &cs, nullptr, nullptr, &deps, &nd));
             if (nd != 1) throw VrError(4, "matmul_outer_async: unexpected capture dependencies");
             g->out_node = deps[0];
-            matmul_outer(c, tl.c_(), tr.c_(), n, nb, level, to.m_(), true);
+            matmul_outer(c, (const uint64_t *const *)tabs, (const uint64_t *const *)(tabs + (size_t)nb * n), n, nb, level,
+                         tabs + (size_t)(nb + 1) * n, true);
         } catch (...) {
             graph_capture_abort(c, *g, user, k0);
             throw;
         }
         graph_capture_end(c, *g, user, k0, true);
     } else {
-        set_out_params(*g, out, nb);
+        SetTables a = make_tables(g->out_table, L, R, out, n, nb);
+        void *args[] = {&a};
+        cudaKernelNodeParams kp = {};
+        kp.func = (void *)k_set_tables;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(256);
+        kp.sharedMemBytes = 0;
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        VR_CUDA(cudaGraphExecKernelNodeSetParams(g->exec, g->out_node, &kp));
     }
-    if (!c.slot_stream[k]) c.slot_stream[k] = slot_stream(c.device, k);
-    cudaStream_t s = c.slot_stream[k];
+    cudaStream_t s = next_async_slot(c);
     VR_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // operands (and anything before) are ready
     VR_CUDA(cudaStreamWaitEvent(s, c.ev_fork, 0));
     VR_CUDA(cudaGraphLaunch(g->exec, s));

@@ -121,6 +121,15 @@ struct Ctx {
     // free list of big scratch blocks (> 64 MB), reused in stream order; mapping fresh multi-GB
     // blocks from the pool can stall the host for hundreds of ms
     std::vector<std::pair<size_t, void *>> big_free;
+    // The arena and the big-block list are reused in the order of ONE stream.  When the caller moves
+    // the context to another stream (vr_set_stream), the current arena is parked under its stream and
+    // the new stream gets its own, so a call on stream B never reuses bytes stream A may still touch.
+    struct ArenaState {
+        char *arena = nullptr;
+        size_t cap = 0, top = 0, peak = 0;
+        std::vector<std::pair<size_t, void *>> big_free;
+    };
+    std::map<cudaStream_t, ArenaState> parked;
 
     // CUDA-graph cache of fixed-shape drivers (graph.cu); capturing != nullptr while one records
     std::vector<GraphEntry> graphs;

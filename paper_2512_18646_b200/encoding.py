@@ -39,6 +39,11 @@ class PackedMatrix:
         m, n = self.shape.m, self.shape.n
         return engine.dec(self.ct)[: m * n].reshape(m, n)
 
+    def decode_async(self, engine):
+        """``decode`` as a future (CkksEngine.dec_batch_async): ``.result()`` returns the matrix."""
+        m, n = self.shape.m, self.shape.n
+        return engine.dec_batch_async([self.ct], post=lambda v: v[0][: m * n].reshape(m, n).copy())
+
     def with_ct(self, ct) -> "PackedMatrix":
         return PackedMatrix(ct, self.shape, self.encoding, self.revolve_p)
 

@@ -37,6 +37,7 @@ __all__ = [
     "Ciphertext",
     "PlainMask",
     "CkksEngine",
+    "DecodeFuture",
     "SlotEngine",
     "is_pow2",
     "next_pow2",
@@ -202,6 +203,21 @@ class PlainMask:
                 raise EngineError("filter masks may contain only 0.0 and 1.0")
 
 
+class DecodeFuture:
+    """Result of ``CkksEngine.dec_batch_async``: ``result()`` waits for the copy and returns the
+    decoded slots as numpy (``post`` applied)."""
+
+    __slots__ = ("_done", "_host", "_post")
+
+    def __init__(self, done, host, post=None):
+        self._done, self._host, self._post = done, host, post
+
+    def result(self) -> np.ndarray:
+        self._done.synchronize()
+        out = self._host.numpy()
+        return self._post(out) if self._post is not None else out
+
+
 class CkksEngine:
     """Metered RNS-CKKS engine over ``params.slots`` slots on one CUDA device."""
 
@@ -287,21 +303,32 @@ class CkksEngine:
         self._check(a)
         self._check(b)
 
+    _PIN_RING = 8
+
     def _h2d(self, vals: np.ndarray) -> torch.Tensor:
-        """Host float64 array -> device, staged through a reusable pinned buffer."""
+        """Host float64 array -> device, staged through a ring of reusable pinned buffers: a buffer is
+        refilled only after its previous copy has executed, so the host may run up to eight uploads
+        ahead of the device (pipelined encrypt -> product -> decode steps)."""
         self.handle  # noqa: B018 -- adopt the caller's current stream before copying
         nbytes = vals.nbytes
-        if self._pin is None or self._pin.numel() < vals.size:
-            self._pin = torch.empty(max(vals.size, 1 << 16), dtype=torch.float64, pin_memory=True)
-            self._pin_evt = None
-        if self._pin_evt is not None:
-            self._pin_evt.synchronize()
-        stage = self._pin[: vals.size].view(vals.shape)
+        if self._pin is None:
+            self._pin = [None] * self._PIN_RING
+            self._pin_evt = [None] * self._PIN_RING
+            self._pin_next = 0
+        i = self._pin_next
+        self._pin_next = (i + 1) % self._PIN_RING
+        if self._pin_evt[i] is not None:
+            self._pin_evt[i].synchronize()
+        if self._pin[i] is None or self._pin[i].numel() < vals.size:
+            self._pin[i] = torch.empty(max(vals.size, 1 << 16), dtype=torch.float64, pin_memory=True)
+        stage = self._pin[i][: vals.size].view(vals.shape)
         stage.numpy()[...] = vals
         out = torch.empty(vals.shape, dtype=torch.float64, device=self.device)
         out.copy_(stage, non_blocking=True)
-        self._pin_evt = torch.cuda.Event()
-        self._pin_evt.record(self._stream)
+        evt = self._pin_evt[i]
+        if evt is None:
+            evt = self._pin_evt[i] = torch.cuda.Event()
+        evt.record(self._stream)
         self.h2d_bytes += nbytes
         return out
 
@@ -370,6 +397,9 @@ class CkksEngine:
     def dec_batch(self, cts, select=None) -> np.ndarray:
         """Decrypt + decode many ciphertexts -> [count][slots] (real parts).  ``select`` (slot
         indices) keeps only those slots, gathered on the device before the copy to the host."""
+        return self._dec_device(cts, select).cpu().numpy()
+
+    def _dec_device(self, cts, select=None) -> torch.Tensor:
         cts = list(cts)
         for ct in cts:
             self._check(ct)
@@ -378,12 +408,28 @@ class CkksEngine:
         degs = (ctypes.c_int * count)(*[ct.degree for ct in cts])
         lvls = (ctypes.c_int * count)(*[ct.level for ct in cts])
         scl = (ctypes.c_double * count)(*[ct.scale for ct in cts])
-        _lib.check(self._lib.vr_decrypt_decode(self.handle, _lib.ptr_array([ct.ptr() for ct in cts]), degs, lvls, scl,
-                                               count, out.data_ptr(), None))
+        ptrs = _lib.ptr_array([ct.ptr() for ct in cts])
+        _lib.check(self._lib.vr_decrypt_decode(self.handle, ptrs, degs, lvls, scl, count, out.data_ptr(), None))
         if select is not None:
             idx = torch.as_tensor(np.asarray(select, dtype=np.int64), device=self.device)
             out = out.index_select(1, idx)
-        return out.cpu().numpy()
+        return out
+
+    def dec_batch_async(self, cts, select=None, post=None) -> "DecodeFuture":
+        """``dec_batch`` without blocking the host: decrypt + decode + the copy into pinned host
+        memory are queued (on the producer's slot stream when every ciphertext comes from the same
+        asynchronous driver call, else on the current stream) and ``DecodeFuture.result()`` waits.
+        Lets a caller keep several encrypt -> product -> decode steps in flight."""
+        cts = list(cts)
+        pend = cts[0]._pending if cts else None
+        stream = pend if pend is not None and all(c._pending is pend for c in cts) else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(stream):
+            out = self._dec_device(cts, select)
+            host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+            host.copy_(out, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(stream)
+        return DecodeFuture(done, host, post)
 
     def add(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
         self._check_pair(a, b)

@@ -109,3 +109,14 @@ def test_async_results_feed_later_ops():
         total = eng.add(total, o.ct)
     got = eng.dec(total)[: 64 * 64].reshape(64, 64)
     np.testing.assert_allclose(got, 8 * (a @ b), atol=8 * TOL)
+
+
+def test_decode_async_pipeline_matches_decode():
+    """Several encrypt -> matmul_outer -> decode_async steps in flight (fresh operands every step, so
+    the slot graphs are re-pointed at new operands each time): every result equals A B."""
+    eng = CkksEngine(config_params(2))
+    rng = np.random.default_rng(9)
+    mats = [rng.uniform(-1, 1, (2, 64, 64)) for _ in range(20)]
+    futs = [matmul_outer(eng, encode_left(eng, a, 64), encode_right(eng, b, 64)).decode_async(eng) for a, b in mats]
+    for (a, b), f in zip(mats, futs):
+        np.testing.assert_allclose(f.result(), a @ b, atol=TOL)
