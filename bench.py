@@ -857,7 +857,7 @@ def bench_cfg5a(ws, rank, local, max_over_ranks, barrier, peaks, steps=5):
     import torch
 
     from paper_2512_18646_b200 import CkksEngine, config_params
-    from paper_2512_18646_b200.dist import encode_operands_sharded, matmul_outer_sharded_owned, shard_range
+    from paper_2512_18646_b200.dist import NativeComm, encode_operands_sharded, matmul_outer_sharded_owned, shard_range
     from tools.workloads import cfg_matmul
 
     a, b = cfg_matmul(5)
@@ -865,18 +865,20 @@ def bench_cfg5a(ws, rank, local, max_over_ranks, barrier, peaks, steps=5):
     eng = CkksEngine(config_params(5), device=local)
     lo, hi = shard_range(256, rank, ws)
     lefts, right = encode_operands_sharded(eng, blocks, b, lo, hi)
-    outs = matmul_outer_sharded_owned(eng, lefts, right)
+    # N > 1: the partial sums travel over libvrhe's own NCCL communicator (vr_sum_partials)
+    comm = NativeComm.from_group(eng) if ws > 1 else None
+    outs = matmul_outer_sharded_owned(eng, lefts, right, comm=comm)
     errs = [float(np.max(np.abs(eng.dec(o)[: 64 * 256].reshape(64, 256) - blocks[bi] @ b))) for bi, o in outs.items()]
     err = max_over_ranks(max(errs) if errs else 0.0)
     for _ in range(2):
-        matmul_outer_sharded_owned(eng, lefts, right)
+        matmul_outer_sharded_owned(eng, lefts, right, comm=comm)
     barrier()
-    t = Timer(max_over_ranks)(lambda: matmul_outer_sharded_owned(eng, lefts, right), steps)
+    t = Timer(max_over_ranks)(lambda: matmul_outer_sharded_owned(eng, lefts, right, comm=comm), steps)
 
     # e2e: host A row blocks + B -> encrypt this rank's shard -> sharded matmul -> decode owned blocks to host
     def e2e():
         ls, r = encode_operands_sharded(eng, blocks, b, lo, hi)
-        o = matmul_outer_sharded_owned(eng, ls, r)
+        o = matmul_outer_sharded_owned(eng, ls, r, comm=comm)
         return {bi: eng.dec_batch([c], select=np.arange(64 * 256))[0] for bi, c in o.items()}
 
     e2e()
@@ -888,7 +890,8 @@ def bench_cfg5a(ws, rank, local, max_over_ranks, barrier, peaks, steps=5):
     torch.cuda.synchronize()
     te = max_over_ranks((time.perf_counter() - t0) / 2)
     del lefts, right, outs
-    res = {"metric": "HE matmul/s (cfg5a 256x256, 4 row blocks x 256 column cts, k sharded, NCCL int64 reduce per block)",
+    res = {"metric": "HE matmul/s (cfg5a 256x256, 4 row blocks x 256 column cts, k sharded, NCCL uint64 reduce per block)",
+           "collective": "libvrhe vr_sum_partials (native NCCL communicator)" if comm else "none (1 rank)",
            "value": 1.0 / t, "ms_per_matmul": t * 1e3, "n_gpus": ws, "scaling": "strong", "max_abs_err": err,
            "k_per_rank": hi - lo, "roofline": roofline_for("5a", t * ws, eng.q, peaks),
            "e2e": {"value": 1.0 / te, "unit": UNIT, "h2d_bytes_per_step": (4 * 64 * 256 + 256 * 256) * 8,

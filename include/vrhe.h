@@ -35,6 +35,8 @@ extern "C" {
 #define VR_ERR_CUDA 4
 
 typedef struct vr_ctx vr_ctx;
+/* a ciphertext owned through the C-ABI (engine.py:140-150): device residues + level/degree/scale */
+typedef struct vr_ct vr_ct;
 
 /* ---- context ------------------------------------------------------------- */
 /* EngineParams + SlotEngine.__init__ (engine.py:54-90, 175-178).  primes holds
@@ -49,6 +51,37 @@ unsigned long long vr_launch_count(void);
  * private stream (the default after vr_ctx_create) stays alive until vr_ctx_destroy */
 int vr_set_stream(vr_ctx *ctx, void *cuda_stream);
 int vr_sync(vr_ctx *ctx);
+
+/* ---- ciphertexts owned through the C-ABI (host-buffer I/O, no PyTorch) -------- */
+/* Ciphertext objects for bindings that own no device memory (cgo / JNI / plain ctypes): the
+ * SlotEngine.enc -> ops -> dec round trip of engine.py:193-206 from host buffers.  vr_ct_data is a
+ * device pointer accepted by every raw entry point below. */
+int vr_ct_alloc(vr_ctx *ctx, int level, int degree, double scale, vr_ct **out);
+int vr_ct_free(vr_ctx *ctx, vr_ct *ct);
+uint64_t *vr_ct_data(const vr_ct *ct);
+int vr_ct_level(const vr_ct *ct);
+int vr_ct_degree(const vr_ct *ct);
+double vr_ct_scale(const vr_ct *ct);
+/* residues [degree+1][level+1][N] (uint64, limb-major, NTT form) to / from host memory */
+int vr_ct_upload(vr_ctx *ctx, vr_ct *ct, const uint64_t *host);
+int vr_ct_download(vr_ctx *ctx, const vr_ct *ct, uint64_t *host);
+/* SlotEngine.enc (engine.py:193-202) from host doubles [count][nvals] into fresh top-level cts */
+int vr_encrypt_host(vr_ctx *ctx, const double *host_vals, int count, int nvals, double scale, uint64_t nonce0,
+                    vr_ct *const *cts);
+/* SlotEngine.dec (engine.py:204-206) of count cts into host doubles [count][S] */
+int vr_decrypt_host(vr_ctx *ctx, const vr_ct *const *cts, int count, double *host_out);
+/* matmul_outer (multicipher.py:88-103) on vr_ct operands: out[b] (degree 1, level - 1) receives
+ * rescale(relin(sum_k L[b*n+k] (x) R[k])) and the scale L.scale * R.scale / q_level */
+int vr_matmul_outer_ct(vr_ctx *ctx, const vr_ct *const *L, const vr_ct *const *R, int n, int nb, vr_ct *const *out);
+
+/* ---- multi-GPU: native NCCL communicator per context ------ */
+/* 128-byte NCCL unique id, generated on one rank and shared with the others (any channel) */
+int vr_comm_unique_id(void *id_out);
+int vr_comm_init(vr_ctx *ctx, const void *id, int rank, int nranks);
+int vr_comm_destroy(vr_ctx *ctx);
+/* sum degree-2 partials [polys][level+1][N] over the ranks (uint64 NCCL sum, <= 8 ranks) and reduce
+ * mod q_i: root < 0 = all-reduce (every rank gets the sum), else only rank `root` (multicipher.py:100-102) */
+int vr_sum_partials(vr_ctx *ctx, uint64_t *data, long long polys, int level, int root);
 
 /* ---- keys ---------------------------------------------------------------- */
 int vr_gen_relin_key(vr_ctx *ctx);

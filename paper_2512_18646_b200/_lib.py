@@ -63,6 +63,17 @@ _SIGS = {
     "vr_matmul_outer_async": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp, ctypes.POINTER(c_vp)],
     "vr_join": [c_vp],
     "vr_async_slot": [c_vp, ctypes.POINTER(c_vp)],
+    "vr_ct_alloc": [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.POINTER(c_vp)],
+    "vr_ct_free": [c_vp, c_vp],
+    "vr_ct_upload": [c_vp, c_vp, c_vp],
+    "vr_ct_download": [c_vp, c_vp, c_vp],
+    "vr_encrypt_host": [c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_uint64, c_vpp],
+    "vr_decrypt_host": [c_vp, c_vpp, ctypes.c_int, c_vp],
+    "vr_matmul_outer_ct": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, c_vpp],
+    "vr_comm_unique_id": [c_vp],
+    "vr_comm_init": [c_vp, c_vp, ctypes.c_int, ctypes.c_int],
+    "vr_comm_destroy": [c_vp],
+    "vr_sum_partials": [c_vp, c_vp, ctypes.c_longlong, ctypes.c_int, ctypes.c_int],
     "vr_tensor_sum_mode": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int],
     "vr_conv_columns": [c_vp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
                         c_u64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, c_vp,
@@ -71,7 +82,10 @@ _SIGS = {
     "vr_poly_activation": [c_vp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, c_vpp],
 }
 
-EXPORTED = tuple(_SIGS) + ("vr_last_error", "vr_launch_count")
+_ACCESSORS = {"vr_ct_data": (c_vp, [c_vp]), "vr_ct_level": (ctypes.c_int, [c_vp]), "vr_ct_degree": (ctypes.c_int, [c_vp]),
+              "vr_ct_scale": (ctypes.c_double, [c_vp])}
+
+EXPORTED = tuple(_SIGS) + tuple(_ACCESSORS) + ("vr_last_error", "vr_launch_count")
 
 
 def build(force: bool = False) -> Path:
@@ -99,6 +113,10 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = ctypes.c_int
+    for name, (res, argtypes) in _ACCESSORS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = res
     lib.vr_last_error.restype = ctypes.c_char_p
     lib.vr_last_error.argtypes = []
     lib.vr_launch_count.restype = ctypes.c_ulonglong

@@ -14,6 +14,14 @@ struct vr_ctx {
     vr::Ctx c;
 };
 
+// A ciphertext owned through the C-ABI (engine.py:140-150 Ciphertext): device residues
+// [degree+1][level+1][N] in NTT form plus the level / scale bookkeeping the engine keeps.
+struct vr_ct {
+    uint64_t *data = nullptr;
+    int level = 0, degree = 1;
+    double scale = 1.0;
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -106,6 +114,10 @@ void destroy_ctx(vr_ctx *h) {
     for (cudaStream_t s : c.slot_stream)
         if (s) cudaStreamSynchronize(s);
     vr::graphs_release(c);
+    try {
+        vr::comm_destroy(c);
+    } catch (...) {
+    }
     void *ptrs[] = {c.tw2, c.itw2, c.twd, c.itwd, c.liftk, c.kshift, c.ntt_const, c.inv_tab, c.rr_tab, c.zr, c.zi, c.ftw,
                     c.slot_pos, c.pos_slot, c.cdt, c.rlk, c.s_ntt, c.s_sh, c.pk, c.arena};
     for (void *p : ptrs)
@@ -707,6 +719,146 @@ int vr_join(vr_ctx *h) {
             VR_CUDA(cudaEventRecord(c.ev_join, s));
             VR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
         }
+    });
+}
+
+// ---- ciphertexts owned through the C-ABI ------------------------------------------------------
+int vr_ct_alloc(vr_ctx *h, int level, int degree, double scale, vr_ct **out) {
+    return guard([&] {
+        *out = nullptr;
+        check_level(h->c, level);
+        if (degree < 1 || degree > 2) throw vr::VrError(VR_ERR_ENGINE, "degree must be 1 or 2");
+        auto *ct = new vr_ct();
+        ct->level = level;
+        ct->degree = degree;
+        ct->scale = scale;
+        const cudaError_t e = cudaMalloc((void **)&ct->data, sizeof(uint64_t) * (degree + 1) * (level + 1) * h->c.n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            delete ct;
+            throw vr::VrError(VR_ERR_CUDA, std::string("vr_ct_alloc: ") + cudaGetErrorString(e));
+        }
+        *out = ct;
+    });
+}
+
+int vr_ct_free(vr_ctx *h, vr_ct *ct) {
+    if (!ct) return VR_OK;
+    return guard([&] {
+        VR_CUDA(cudaStreamSynchronize(h->c.stream));  // no queued work may still touch it
+        cudaFree(ct->data);
+        delete ct;
+    });
+}
+
+uint64_t *vr_ct_data(const vr_ct *ct) { return ct ? ct->data : nullptr; }
+int vr_ct_level(const vr_ct *ct) { return ct ? ct->level : -1; }
+int vr_ct_degree(const vr_ct *ct) { return ct ? ct->degree : -1; }
+double vr_ct_scale(const vr_ct *ct) { return ct ? ct->scale : 0.0; }
+
+static size_t ct_words(const vr::Ctx &c, const vr_ct *ct) { return (size_t)(ct->degree + 1) * (ct->level + 1) * c.n; }
+
+int vr_ct_upload(vr_ctx *h, vr_ct *ct, const uint64_t *host) {
+    return guard([&] {
+        VR_CUDA(cudaMemcpyAsync(ct->data, host, ct_words(h->c, ct) * 8, cudaMemcpyHostToDevice, h->c.stream));
+        VR_CUDA(cudaStreamSynchronize(h->c.stream));
+    });
+}
+
+int vr_ct_download(vr_ctx *h, const vr_ct *ct, uint64_t *host) {
+    return guard([&] {
+        VR_CUDA(cudaMemcpyAsync(host, ct->data, ct_words(h->c, ct) * 8, cudaMemcpyDeviceToHost, h->c.stream));
+        VR_CUDA(cudaStreamSynchronize(h->c.stream));
+    });
+}
+
+int vr_encrypt_host(vr_ctx *h, const double *host_vals, int count, int nvals, double scale, uint64_t nonce0,
+                    vr_ct *const *cts) {
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        if (nvals > c.slots) throw vr::VrError(VR_ERR_CAPACITY, "payload exceeds slot count");
+        if (count <= 0) return;
+        for (int i = 0; i < count; i++)
+            if (cts[i]->level != c.L || cts[i]->degree != 1) throw vr::VrError(VR_ERR_ENGINE, "fresh ciphertexts are degree 1 at the top level");
+        const int w = nvals > 0 ? nvals : 1;
+        vr::Scratch vals(c, sizeof(double) * count * w), outs(c, sizeof(uint64_t) * count * 2 * (c.L + 1) * c.n);
+        if (nvals > 0) VR_CUDA(cudaMemcpyAsync(vals.p, host_vals, sizeof(double) * count * nvals, cudaMemcpyHostToDevice, c.stream));
+        vr::encrypt(c, vals.as<double>(), count, nvals, c.L, scale, nonce0, outs.as<uint64_t>());
+        const size_t words = (size_t)2 * (c.L + 1) * c.n;
+        for (int i = 0; i < count; i++) {
+            VR_CUDA(cudaMemcpyAsync(cts[i]->data, outs.as<uint64_t>() + i * words, words * 8, cudaMemcpyDeviceToDevice, c.stream));
+            cts[i]->scale = scale;
+        }
+        VR_CUDA(cudaStreamSynchronize(c.stream));  // the host buffer may be released on return
+    });
+}
+
+int vr_decrypt_host(vr_ctx *h, const vr_ct *const *cts, int count, double *host_out) {
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        if (count <= 0) return;
+        std::vector<const uint64_t *> ptrs(count);
+        std::vector<int> degs(count), lvls(count);
+        std::vector<double> scl(count);
+        for (int i = 0; i < count; i++) {
+            ptrs[i] = cts[i]->data;
+            degs[i] = cts[i]->degree;
+            lvls[i] = cts[i]->level;
+            scl[i] = cts[i]->scale;
+        }
+        vr::Scratch out(c, sizeof(double) * count * c.slots);
+        {
+            vr::PtrTable t(c, ptrs);
+            vr::DevArray<int> dd(c, degs.data(), count), dl(c, lvls.data(), count);
+            vr::DevArray<double> ds(c, scl.data(), count);
+            vr::decrypt_decode(c, t.c_(), dd.get(), dl.get(), ds.get(), count, out.as<double>(), nullptr);
+        }
+        VR_CUDA(cudaMemcpyAsync(host_out, out.p, sizeof(double) * count * c.slots, cudaMemcpyDeviceToHost, c.stream));
+        VR_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int vr_matmul_outer_ct(vr_ctx *h, const vr_ct *const *L, const vr_ct *const *R, int n, int nb, vr_ct *const *out) {
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        if (n <= 0 || nb < 1 || nb > 4 || nb == 3) throw vr::VrError(VR_ERR_LAYOUT, "matmul_outer needs n >= 1 and 1, 2 or 4 row blocks");
+        const int level = R[0]->level;
+        const double ls = L[0]->scale, rs = R[0]->scale;
+        for (int i = 0; i < nb * n; i++)
+            if (L[i]->level != level || L[i]->degree != 1 || L[i]->scale != ls) throw vr::VrError(VR_ERR_LAYOUT, "left operands differ in level/scale/degree");
+        for (int i = 0; i < n; i++)
+            if (R[i]->level != level || R[i]->degree != 1 || R[i]->scale != rs) throw vr::VrError(VR_ERR_LAYOUT, "right operands differ in level/scale/degree");
+        if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
+        for (int b = 0; b < nb; b++)
+            if (out[b]->level != level - 1 || out[b]->degree != 1) throw vr::VrError(VR_ERR_LAYOUT, "outputs must be degree 1 at level - 1");
+        std::vector<const uint64_t *> lp(nb * n), rp(n), op(nb);
+        for (int i = 0; i < nb * n; i++) lp[i] = L[i]->data;
+        for (int i = 0; i < n; i++) rp[i] = R[i]->data;
+        for (int b = 0; b < nb; b++) op[b] = out[b]->data;
+        vr::PtrTable tl(c, lp), tr(c, rp), to(c, op);
+        vr::matmul_outer(c, tl.c_(), tr.c_(), n, nb, level, to.m_());
+        for (int b = 0; b < nb; b++) out[b]->scale = ls * rs / (double)c.q[level];
+    });
+}
+
+// ---- multi-GPU: native NCCL communicator --------------------------------------------------------
+int vr_comm_unique_id(void *id_out) {
+    return guard([&] { vr::comm_unique_id(id_out); });
+}
+
+int vr_comm_init(vr_ctx *h, const void *id, int rank, int nranks) {
+    return guard([&] { vr::comm_init(h->c, id, rank, nranks); });
+}
+
+int vr_comm_destroy(vr_ctx *h) {
+    return guard([&] { vr::comm_destroy(h->c); });
+}
+
+int vr_sum_partials(vr_ctx *h, uint64_t *data, long long polys, int level, int root) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (root >= h->c.nranks) throw vr::VrError(VR_ERR_ENGINE, "root rank out of range");
+        vr::sum_partials(h->c, data, polys, level, root);
     });
 }
 

@@ -16,6 +16,11 @@ void keygen(Ctx &c);
 
 // drivers (drivers.cu)
 void mul_batch(Ctx &c, const uint64_t *const *A, const uint64_t *const *B, uint64_t *const *Out, int count, int level);
+// comm.cu: NCCL communicator of the context and the partial-product sum of config 5a
+void comm_unique_id(void *out128);
+void comm_init(Ctx &c, const void *id, int rank, int nranks);
+void comm_destroy(Ctx &c);
+void sum_partials(Ctx &c, uint64_t *data, long long polys, int level, int root);
 // one_pass: one (d0, d1, d2) tensor-sum pass then the key-switch chain, all on c.stream (the form
 // recorded into the asynchronous per-slot graphs, graph.cu)
 void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out,

@@ -142,6 +142,10 @@ struct Ctx {
     cudaStream_t slot_stream[kSlots] = {};
     int slot_next = 0;
 
+    // multi-GPU (comm.cu): NCCL communicator of this context's rank, or null
+    void *comm = nullptr;
+    int rank = 0, nranks = 1;
+
     size_t key_words() const { return (size_t)(L + 1) * 2 * np * n; }
 };
 

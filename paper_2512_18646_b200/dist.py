@@ -28,7 +28,51 @@ from .multicipher import ColumnEncodedMatrix
 
 __all__ = ["shard_range", "matmul_nonce_plan", "encode_operands_sharded", "allreduce_partials", "block_owner",
            "reduce_partials_to_owners", "matmul_partials", "matmul_finish", "matmul_outer_sharded",
-           "matmul_outer_sharded_owned", "image_groups"]
+           "matmul_outer_sharded_owned", "image_groups", "NativeComm"]
+
+
+class NativeComm:
+    """NCCL communicator owned by the engine's C context (vr_comm_*): the partial-product sum of
+    config 5a runs inside libvrhe (uint64 NCCL sum + mod-q reduction on the device) instead of
+    through torch.distributed.  torch.distributed (any backend) is only used, in ``from_group``, to
+    hand the 128-byte NCCL unique id from rank 0 to the other ranks."""
+
+    def __init__(self, engine: CkksEngine, uid: bytes, rank: int, world: int):
+        import ctypes
+
+        if len(uid) != 128:
+            raise EngineError("an NCCL unique id has 128 bytes")
+        self.engine, self.rank, self.world = engine, rank, world
+        buf = ctypes.create_string_buffer(uid, 128)
+        _lib.check(engine._lib.vr_comm_init(engine.handle, buf, rank, world))
+
+    @staticmethod
+    def unique_id(engine: CkksEngine) -> bytes:
+        import ctypes
+
+        buf = ctypes.create_string_buffer(128)
+        _lib.check(engine._lib.vr_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_group(cls, engine: CkksEngine, group=None) -> "NativeComm":
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        obj = [cls.unique_id(engine) if rank == 0 else None]
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(obj, src=src, group=group)
+        return cls(engine, obj[0], rank, world)
+
+    def sum_partials(self, part: torch.Tensor, level: int, root: int = -1) -> None:
+        """In-place sum of [polys][level+1][N] residues over ranks, reduced mod q (root < 0: every rank)."""
+        if part.dtype != torch.int64 or not part.is_contiguous():
+            raise EngineError("partials must be contiguous int64 residues")
+        polys = part.numel() // ((level + 1) * self.engine.N)
+        _lib.check(self.engine._lib.vr_sum_partials(self.engine.handle, part.data_ptr(), polys, level, root))
+
+    def close(self) -> None:
+        _lib.check(self.engine._lib.vr_comm_destroy(self.engine.handle))
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -130,11 +174,12 @@ def matmul_partials(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -> tu
     return part, lv
 
 
-def matmul_finish(engine: CkksEngine, part: torch.Tensor, level: int, m: int, p: int) -> list[Ciphertext]:
-    """Summed partials -> mod q -> one fused relinearisation + rescale per row block."""
+def matmul_finish(engine: CkksEngine, part: torch.Tensor, level: int, m: int, p: int, reduced: bool = False) -> list[Ciphertext]:
+    """Summed partials -> mod q (unless already ``reduced``) -> one fused relinearisation + rescale per row block."""
     nb = part.shape[0]
     lib = engine._lib
-    _lib.check(lib.vr_mod_reduce(engine.handle, part.data_ptr(), nb * 3, level))
+    if not reduced:
+        _lib.check(lib.vr_mod_reduce(engine.handle, part.data_ptr(), nb * 3, level))
     out = torch.empty((nb, 2, level, engine.N), dtype=torch.int64, device=engine.device)
     _lib.check(lib.vr_relin_rescale(engine.handle, _lib.row_ptrs(part, nb),
                                     _lib.row_ptrs(out, nb), nb, level))
@@ -150,11 +195,22 @@ def matmul_outer_sharded(engine: CkksEngine, lefts, right: ColumnEncodedMatrix, 
     return matmul_finish(engine, part, lv, right.m, right.p)
 
 
-def matmul_outer_sharded_owned(engine: CkksEngine, lefts, right: ColumnEncodedMatrix, group=None) -> dict[int, Ciphertext]:
+def matmul_outer_sharded_owned(engine: CkksEngine, lefts, right: ColumnEncodedMatrix, group=None,
+                               comm: NativeComm | None = None) -> dict[int, Ciphertext]:
     """Distributed matmul_outer with the finish sharded as well: local tensor-sum, per-block reduce to the
     block's owner, then each rank relinearises + rescales only the blocks it owns ({block: ciphertext};
-    empty on ranks that own none).  Residues are identical to matmul_outer_sharded's."""
+    empty on ranks that own none).  Residues are identical to matmul_outer_sharded's.  With ``comm`` the
+    reduce runs on the library's own NCCL communicator (vr_sum_partials), else on torch.distributed."""
     part, lv = matmul_partials(engine, lefts, right)
+    if comm is not None:
+        nb = part.shape[0]
+        for b in range(nb):
+            comm.sum_partials(part[b], lv, root=block_owner(b, comm.world) if comm.world > 1 else -1)
+        mine = [b for b in range(nb) if block_owner(b, comm.world) == comm.rank]
+        if not mine:
+            return {}
+        sub = part if len(mine) == nb else part[mine].contiguous()
+        return dict(zip(mine, matmul_finish(engine, sub, lv, right.m, right.p, reduced=True)))
     mine = reduce_partials_to_owners(part, group)
     if not mine:
         return {}
