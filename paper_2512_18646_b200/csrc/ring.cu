@@ -377,13 +377,18 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
                     const ulonglong2 l1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * b + 1) * tile + c2);
                     mac_to(acc[b][0][0], l0.x, r0.x);
                     mac_to(acc[b][0][1], l0.y, r0.y);
-                    mac_to(acc[b][1][0], l0.x, r1.x);
-                    mac_to(acc[b][1][1], l0.y, r1.y);
-                    mac_to(acc[b][1][0], l1.x, r0.x);
-                    mac_to(acc[b][1][1], l1.y, r0.y);
                     if constexpr (MODE == 0) {
+                        // Karatsuba: three 64x64 products instead of four.  acc[1] collects
+                        // (l0 + l1)(r0 + r1) (< 2^124: residues < 2^61); d1 = that - d0 - d2 at the end.
                         mac_to(acc[b][2][0], l1.x, r1.x);
                         mac_to(acc[b][2][1], l1.y, r1.y);
+                        mac_to(acc[b][1][0], l0.x + l1.x, r0.x + r1.x);
+                        mac_to(acc[b][1][1], l0.y + l1.y, r0.y + r1.y);
+                    } else {
+                        mac_to(acc[b][1][0], l0.x, r1.x);
+                        mac_to(acc[b][1][1], l0.y, r1.y);
+                        mac_to(acc[b][1][0], l1.x, r0.x);
+                        mac_to(acc[b][1][1], l1.y, r0.y);
                     }
                 }
             }
@@ -402,10 +407,19 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
     __syncthreads();  // ring drained: reuse it for the partials
     if (warp != producer_warp && threadIdx.x < cons) {
 #pragma unroll
-        for (int b = 0; b < NB; b++)
+        for (int b = 0; b < NB; b++) {
+            uint64_t v[3][2];
 #pragma unroll
             for (int p = P0; p < P1; p++)
-                part[b * 3 + p][threadIdx.x] = make_ulonglong2(reduce128(acc[b][p][0], m), reduce128(acc[b][p][1], m));
+#pragma unroll
+                for (int e = 0; e < 2; e++) v[p][e] = reduce128(acc[b][p][e], m);
+            if constexpr (MODE == 0) {  // undo Karatsuba: d1 = (l0 + l1)(r0 + r1) - d0 - d2
+#pragma unroll
+                for (int e = 0; e < 2; e++) v[1][e] = sub_mod(sub_mod(v[1][e], v[0][e], m.q), v[2][e], m.q);
+            }
+#pragma unroll
+            for (int p = P0; p < P1; p++) part[b * 3 + p][threadIdx.x] = make_ulonglong2(v[p][0], v[p][1]);
+        }
     }
     cluster.sync();
     if (z == 0 && threadIdx.x < cons) {

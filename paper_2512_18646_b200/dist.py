@@ -24,7 +24,7 @@ import torch
 
 from . import _lib
 from .engine import Ciphertext, CkksEngine, EngineError, LayoutError
-from .multicipher import ColumnEncodedMatrix
+from .multicipher import ColumnEncodedMatrix, _checked_ptrs
 
 __all__ = ["shard_range", "matmul_nonce_plan", "encode_operands_sharded", "allreduce_partials", "block_owner",
            "reduce_partials_to_owners", "matmul_partials", "matmul_finish", "matmul_outer_sharded",
@@ -156,17 +156,30 @@ def matmul_partials(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -> tu
             raise LayoutError("operands must be (left, right) column-encoded shards")
         if lf.n != n or lf.p != right.p or lf.m != right.m:
             raise LayoutError("row blocks must match the right operand's local shard")
-    allc = [c for lf in lefts for c in lf.cts] + list(right.cts)
-    lv = min(c.level for c in allc) if allc else engine.L
+    # validated pointer arrays cached on the operands (multicipher._checked_ptrs): a steady-state
+    # call does no per-ciphertext Python work (1280 ciphertexts at config 5a)
+    infos = [_checked_ptrs(engine, lf) for lf in lefts] + [_checked_ptrs(engine, right)] if n > 0 else []
+    lvs = {lv for lv, _ in infos}
+    if len(lvs) == 1 and all(p is not None for _, p in infos):
+        lv = lvs.pop()
+        key = tuple(id(lf) for lf in lefts)
+        cat = getattr(right, "_vr_cat", None)
+        if cat is None or cat[0] != key:  # the concatenated left table, cached with these row blocks
+            cat = (key, _lib.ptr_array([p for _, ps in infos[:-1] for p in ps]), list(lefts))
+            object.__setattr__(right, "_vr_cat", cat)
+        lptrs = cat[1]
+        rptrs = getattr(right, "_vr_ptrs")[3]
+    else:
+        allc = [c for lf in lefts for c in lf.cts] + list(right.cts)
+        lv = min(c.level for c in allc) if allc else engine.L
+        allc = [engine.adjust(c, lv) for c in allc]
+        lptrs = _lib.ptr_array([c.ptr() for c in allc[: nb * n]])
+        rptrs = _lib.ptr_array([c.ptr() for c in allc[nb * n:]])
     if lv < 1:
         raise EngineError("multiplicative depth exhausted")
-    allc = [engine.adjust(c, lv) for c in allc]
-    Ls, Rs = allc[: nb * n], allc[nb * n:]
     part = torch.empty((nb, 3, lv + 1, engine.N), dtype=torch.int64, device=engine.device)
     if n > 0:
-        _lib.check(engine._lib.vr_tensor_sum(engine.handle, _lib.ptr_array([c.ptr() for c in Ls]),
-                                             _lib.ptr_array([c.ptr() for c in Rs]), n, nb, lv,
-                                             _lib.row_ptrs(part, nb)))
+        _lib.check(engine._lib.vr_tensor_sum(engine.handle, lptrs, rptrs, n, nb, lv, _lib.row_ptrs(part, nb)))
     else:
         part.zero_()
     engine._meter.mul_count += nb * n
