@@ -873,7 +873,7 @@ def bench_cfg5a(ws, rank, local, max_over_ranks, barrier, peaks, steps=5):
     for _ in range(2):
         matmul_outer_sharded_owned(eng, lefts, right, comm=comm)
     barrier()
-    t = Timer(max_over_ranks)(lambda: matmul_outer_sharded_owned(eng, lefts, right, comm=comm), steps)
+    t = Timer(max_over_ranks, eng.join)(lambda: matmul_outer_sharded_owned(eng, lefts, right, comm=comm), steps)
 
     # e2e: host A row blocks + B -> encrypt this rank's shard -> sharded matmul -> decode owned blocks to host
     def e2e():

@@ -151,13 +151,13 @@ def rotate_batch(engine: CkksEngine, cts, steps):
     cts = list(cts)
     lv = cts[0].level
     steps = [int(s) for s in steps]
-    out = torch.empty((len(cts), len(steps), 2, lv + 1, engine.N), dtype=torch.int64, device=engine.device)
-    st = (ctypes.c_int64 * len(steps))(*steps)
-    _lib.check(engine._lib.vr_rotate(engine.handle, _lib.ptr_array([c.ptr() for c in cts]),
-                                     _lib.row_ptrs(out.flatten(0, 1)),
-                                     len(cts), lv, len(steps), st))
-    engine._meter.rot_count += len(cts) * len(steps)
-    return [[Ciphertext.at(out[i], r, lv, c.scale, c.depth, c.layout, engine._id) for r in range(len(steps))]
+    nr = len(steps)
+    flat = torch.empty((len(cts) * nr, 2, lv + 1, engine.N), dtype=torch.int64, device=engine.device)
+    st = (ctypes.c_int64 * nr)(*steps)
+    _lib.check(engine._lib.vr_rotate(engine.handle, _lib.ptr_array([c.ptr() for c in cts]), _lib.row_ptrs(flat),
+                                     len(cts), lv, nr, st))
+    engine._meter.rot_count += len(cts) * nr
+    return [[Ciphertext.at(flat, i * nr + r, lv, c.scale, c.depth, c.layout, engine._id) for r in range(nr)]
             for i, c in enumerate(cts)]
 
 

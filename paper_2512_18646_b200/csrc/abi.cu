@@ -441,9 +441,14 @@ int vr_gen_relin_key(vr_ctx *h) {
 int vr_galois_elt(vr_ctx *h, int64_t steps, uint32_t *g_out) {
     return guard([&] {
         const int64_t S = h->c.slots;
-        const int64_t r = ((steps % S) + S) % S;
-        uint64_t g = 1;
-        for (int64_t i = 0; i < r; i++) g = (g * 5) % (2ull * h->c.n);
+        uint64_t e = (uint64_t)(((steps % S) + S) % S);
+        const uint64_t m = 2ull * h->c.n;
+        uint64_t g = 1, b = 5 % m;  // 5^e mod 2N by squaring (the rotation hot path asks for many)
+        while (e) {
+            if (e & 1) g = g * b % m;
+            b = b * b % m;
+            e >>= 1;
+        }
         *g_out = (uint32_t)g;
     });
 }

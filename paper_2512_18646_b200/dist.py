@@ -220,15 +220,31 @@ def matmul_outer_sharded_owned(engine: CkksEngine, lefts, right: ColumnEncodedMa
         for b in range(nb):
             comm.sum_partials(part[b], lv, root=block_owner(b, comm.world) if comm.world > 1 else -1)
         mine = [b for b in range(nb) if block_owner(b, comm.world) == comm.rank]
-        if not mine:
-            return {}
-        sub = part if len(mine) == nb else part[mine].contiguous()
-        return dict(zip(mine, matmul_finish(engine, sub, lv, right.m, right.p, reduced=True)))
-    mine = reduce_partials_to_owners(part, group)
+        reduced = True
+    else:
+        mine = reduce_partials_to_owners(part, group)
+        reduced = False
     if not mine:
         return {}
     sub = part if len(mine) == part.shape[0] else part[mine].contiguous()
-    return dict(zip(mine, matmul_finish(engine, sub, lv, right.m, right.p)))
+    return dict(zip(mine, _finish_async(engine, sub, lv, right.m, right.p, reduced)))
+
+
+def _finish_async(engine: CkksEngine, part: torch.Tensor, level: int, m: int, p: int, reduced: bool) -> list[Ciphertext]:
+    """matmul_finish on the engine's side stream: the latency-bound relinearisation of this product
+    overlaps the next product's streaming tensor sum (config 5a issues them back to back).  The
+    results are pending on the side stream; any read waits for it (Ciphertext._ready)."""
+    if not engine.async_drivers:
+        return matmul_finish(engine, part, level, m, p, reduced)
+    side = engine._side_stream()
+    cur = torch.cuda.current_stream(engine.device)
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        outs = matmul_finish(engine, part, level, m, p, reduced)
+    part.record_stream(side)
+    for ct in outs:
+        ct._pending = side
+    return outs
 
 
 def image_groups(n_images: int, group: int, rank: int, world: int) -> list[tuple[int, int]]:

@@ -79,6 +79,10 @@ class OpMeter:
         )
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None) or (
+    lambda dev: torch.cuda.current_stream(dev).cuda_stream)  # the current stream's cudaStream_t, cheaply
+
+
 def scalar_i64(x: float) -> int:
     """round(x) as a signed 64-bit scalar for the C-ABI; ctypes would wrap larger values silently."""
     k = int(round(x))
@@ -237,6 +241,7 @@ class CkksEngine:
             self._stream = torch.cuda.current_stream(self.device)
         self._h = h
         self._stream_ptr = self._stream.cuda_stream
+        self._dev_index = self.device.index
         _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(self._stream_ptr)))
         self._meter = OpMeter()
         # asynchronous drivers (vr_matmul_outer_async): results are produced on the library's slot
@@ -275,8 +280,8 @@ class CkksEngine:
         kernels, the output allocations, the pinned H2D staging copies and the decode's D2H all
         share that one stream, so no cross-stream hazard exists inside a call.
         """
-        cur = torch.cuda.current_stream(self.device)
-        if cur.cuda_stream != self._stream_ptr:
+        if _raw_stream(self._dev_index) != self._stream_ptr:
+            cur = torch.cuda.current_stream(self.device)
             _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(cur.cuda_stream)))
             self._stream, self._stream_ptr = cur, cur.cuda_stream
         return self._h
@@ -617,15 +622,16 @@ class CkksEngine:
         for c in cts:
             self._check(c)
         lv, count = cts[0].level, len(cts)
-        out = torch.empty((count, len(steps), 2, lv + 1, self.N), dtype=torch.int64, device=self.device)
-        st = (ctypes.c_int64 * len(steps))(*steps)
-        _lib.check(self._lib.vr_rotate(self.handle, _lib.ptr_array([c.ptr() for c in cts]), _lib.row_ptrs(out.flatten(0, 1)),
-                                       count, lv, len(steps), st))
+        nr = len(steps)
+        flat = torch.empty((count * nr, 2, lv + 1, self.N), dtype=torch.int64, device=self.device)
+        st = (ctypes.c_int64 * nr)(*steps)
+        _lib.check(self._lib.vr_rotate(self.handle, _lib.ptr_array([c.ptr() for c in cts]), _lib.row_ptrs(flat),
+                                       count, lv, nr, st))
         res = []
         for i, c in enumerate(cts):
             self._meter.rot_count += len(steps)
             self._observe(c.depth)
-            res.append([Ciphertext.at(out[i], r, lv, c.scale, c.depth, c.layout, self._id) for r in range(len(steps))])
+            res.append([Ciphertext.at(flat, i * nr + r, lv, c.scale, c.depth, c.layout, self._id) for r in range(nr)])
         return res
 
     def sum_batch(self, acc: Ciphertext, cts) -> Ciphertext:
@@ -721,6 +727,16 @@ class CkksEngine:
     def join(self) -> None:
         """Make the current stream wait for every asynchronous driver call issued so far."""
         _lib.check(self._lib.vr_join(self.handle))
+        side = self._ext_streams.get("side")
+        if side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(side)
+
+    def _side_stream(self):
+        """A second stream of this engine for asynchronous finishing work (dist._finish_async)."""
+        s = self._ext_streams.get("side")
+        if s is None:
+            s = self._ext_streams["side"] = torch.cuda.Stream(device=self.device)
+        return s
 
     def _ext_stream(self, ptr: int):
         s = self._ext_streams.get(ptr)

@@ -20,6 +20,7 @@ def timed(fn, reps):
     st.record()
     for _ in range(reps):
         fn()
+    eng.join()
     en.record()
     torch.cuda.synchronize()
     return st.elapsed_time(en) / reps * 1e3
