@@ -113,6 +113,12 @@ int vr_encrypt(vr_ctx *ctx, const double *vals, int count, int nvals, int level,
  * (zeros beyond), src = the raw device matrix/images */
 int vr_encrypt_strided(vr_ctx *ctx, const double *src, long long sc, long long s1, long long s2, int p, int nvals, int count,
                        int level, double scale, uint64_t nonce0, uint64_t *ct_out);
+/* encode_left + encode_right of one product (multicipher.py:62-85) as one launch: ciphertexts
+ * 0..count0-1 from (src0, strides 0) into ct0, then count1 from (src1, strides 1) into ct1, nonces
+ * nonce0 + c consecutive over both (secret-key encryption only) */
+int vr_encrypt_strided2(vr_ctx *ctx, const double *src0, long long sc0, long long s1_0, long long s2_0, int p0, int nvals0,
+                        int count0, uint64_t *ct0, const double *src1, long long sc1, long long s1_1, long long s2_1, int p1,
+                        int nvals1, int count1, uint64_t *ct1, int level, double scale, uint64_t nonce0);
 /* SlotEngine.dec (engine.py:204-206): decrypt on q0 and decode to real slots.
  * out: device [count][S] doubles (may be NULL); coeffs_out: device [count][N] int64 (may be NULL). */
 int vr_decrypt_decode(vr_ctx *ctx, const uint64_t *const *cts, const int *degs, const int *levels, const double *scales,

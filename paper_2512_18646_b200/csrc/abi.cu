@@ -517,6 +517,18 @@ int vr_encrypt_strided(vr_ctx *h, const double *src, long long sc, long long s1,
     });
 }
 
+int vr_encrypt_strided2(vr_ctx *h, const double *src0, long long sc0, long long s1_0, long long s2_0, int p0, int nvals0,
+                        int count0, uint64_t *ct0, const double *src1, long long sc1, long long s1_1, long long s2_1, int p1,
+                        int nvals1, int count1, uint64_t *ct1, int level, double scale, uint64_t nonce0) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (nvals0 > h->c.slots || nvals1 > h->c.slots) throw vr::VrError(VR_ERR_CAPACITY, "payload exceeds slot count");
+        if (count0 <= 0 || count1 <= 0) throw vr::VrError(VR_ERR_ENGINE, "both batches must be non-empty");
+        vr::encrypt_src2(h->c, src0, sc0, s1_0, s2_0, p0, nvals0, count0, ct0, src1, sc1, s1_1, s2_1, p1, nvals1, count1, ct1,
+                         level, scale, nonce0);
+    });
+}
+
 int vr_decrypt_decode(vr_ctx *h, const uint64_t *const *cts, const int *degs, const int *levels, const double *scales,
                       int count, double *out, int64_t *coeffs_out) {
     return guard([&] {

@@ -125,7 +125,16 @@ struct SlotSrc {
     const double *src;
     long long sc, s1, s2;
     int p, nvals;
+    // optional second source for ciphertexts c >= split (two strided operands encrypted in one launch)
+    const double *src_b = nullptr;
+    long long sc_b = 0, s1_b = 0, s2_b = 0;
+    int p_b = 1, nvals_b = 0, split = 0x7fffffff;
     __device__ __forceinline__ double at(int c, int j) const {
+        if (c >= split) {
+            if (j >= nvals_b) return 0.0;
+            const int a = j / p_b, b = j - a * p_b;
+            return src_b[(long long)(c - split) * sc_b + (long long)a * s1_b + (long long)b * s2_b];
+        }
         if (j >= nvals) return 0.0;
         const int a = j / p, b = j - a * p;
         return src[(long long)c * sc + (long long)a * s1 + (long long)b * s2];
@@ -545,6 +554,31 @@ void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long lon
 
 void encrypt(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t nonce0, uint64_t *d_ct) {
     encrypt_src(c, d_vals, nvals, 0, 1, nvals > 0 ? nvals : 1, nvals, count, level, scale, nonce0, d_ct);
+}
+
+// Two strided operands (encode_left + encode_right of one product) as ONE secret-key encryption: one
+// slot-FFT launch and one fused NTT over both batches (ciphertexts count0.. go to d_ct2, nonces stay
+// consecutive), so the latency-bound encode and the NTT's tail are paid once.
+void encrypt_src2(Ctx &c, const double *src0, long long sc0, long long s1_0, long long s2_0, int p0, int nvals0, int count0,
+                  uint64_t *d_ct0, const double *src1, long long sc1, long long s1_1, long long s2_1, int p1, int nvals1,
+                  int count1, uint64_t *d_ct1, int level, double scale, uint64_t nonce0) {
+    if (!c.sym_enc) throw VrError(3, "combined encryption needs secret-key encryption");
+    const int N = c.n, nl = level + 1, count = count0 + count1;
+    Scratch m(c, sizeof(int64_t) * count * N), keys(c, sizeof(uint64_t) * count * nl);
+    SlotSrc vs{src0, sc0, s1_0, s2_0, p0 > 0 ? p0 : 1, nvals0};
+    vs.src_b = src1;
+    vs.sc_b = sc1;
+    vs.s1_b = s1_1;
+    vs.s2_b = s2_1;
+    vs.p_b = p1 > 0 ? p1 : 1;
+    vs.nvals_b = nvals1;
+    vs.split = count0;
+    encode_src(c, vs, count, scale, m.as<int64_t>(), EncNoise{c.cdt, c.seed, nonce0, nl, keys.as<uint64_t>()});
+    NttBatch b{d_ct0, count * nl, nl, (long long)2 * nl * N, nl, 0, 0, 0};
+    b.data2 = d_ct1;
+    b.split = count0 * nl;
+    ntt_forward_fused(c, b, LdSymEnc{m.as<int64_t>(), nl, N, c.f64mask, c.kshift},
+                      StSymEnc{c.s_ntt, c.s_sh, keys.as<uint64_t>(), nl, N});
 }
 
 void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long long s2, int p, int nvals, int count, int level,

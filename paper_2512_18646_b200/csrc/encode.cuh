@@ -8,6 +8,9 @@ void encode_coeffs(Ctx &c, const double *d_vals, int count, int nvals, double sc
 void encode_plain(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t *d_pt);
 void encrypt(Ctx &c, const double *d_vals, int count, int nvals, int level, double scale, uint64_t nonce0, uint64_t *d_ct);
 // ciphertext c encrypts slot values src[c*sc + (j/p)*s1 + (j%p)*s2], j < nvals (zeros beyond)
+void encrypt_src2(Ctx &c, const double *src0, long long sc0, long long s1_0, long long s2_0, int p0, int nvals0, int count0,
+                  uint64_t *d_ct0, const double *src1, long long sc1, long long s1_1, long long s2_1, int p1, int nvals1,
+                  int count1, uint64_t *d_ct1, int level, double scale, uint64_t nonce0);
 void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long long s2, int p, int nvals, int count, int level,
                  double scale, uint64_t nonce0, uint64_t *d_ct);
 void decrypt_decode(Ctx &c, const uint64_t *const *d_cts, const int *d_degs, const int *d_levels, const double *d_scales,

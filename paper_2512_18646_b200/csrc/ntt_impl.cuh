@@ -35,7 +35,8 @@ namespace nttk {
 __device__ __forceinline__ bool locate(const NttBatch &b, int t, int N, uint64_t *&ptr, int &pidx) {
     const int g = t / b.group, r = t - g * b.group;
     if (b.skip_diag > 0 && r == g % b.skip_diag) return false;
-    ptr = b.data + (long long)g * b.gstride + (long long)r * N;
+    ptr = (t < b.split ? b.data + (long long)g * b.gstride : b.data2 + (long long)(g - b.split / b.group) * b.gstride) +
+          (long long)r * N;
     pidx = r < b.nq ? b.poff + r : b.pspecial;
     return true;
 }

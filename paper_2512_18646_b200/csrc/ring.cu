@@ -360,40 +360,55 @@ __global__ void __launch_bounds__(TS_TILE / 2 + 32)
             const int s = it % TS_STAGES;
             mbar_wait(&full[s], (it / TS_STAGES) & 1);
             const uint64_t *st = ring + (size_t)s * ARR * tile;
+            if (hint & 8) {  // diagnostic (VR_TS_HINT bit 3): stream only, no arithmetic
+                __syncwarp(wmask);
+                if (lane == 0) mbar_arrive(&empty[s]);
+                continue;
+            }
+            // copy this thread's operands out of the slot and release it BEFORE the arithmetic, so
+            // the producer refills it while the products run (one more stage of effective buffering)
+            ulonglong2 r0, r1, l0[NB], l1[NB];
             if constexpr (MODE == 1) {
-                const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + NB * tile + c2);
+                r1 = *reinterpret_cast<const ulonglong2 *>(st + NB * tile + c2);
 #pragma unroll
-                for (int b = 0; b < NB; b++) {
-                    const ulonglong2 l1 = *reinterpret_cast<const ulonglong2 *>(st + b * tile + c2);
-                    mac_to(acc[b][2][0], l1.x, r1.x);
-                    mac_to(acc[b][2][1], l1.y, r1.y);
-                }
+                for (int b = 0; b < NB; b++) l1[b] = *reinterpret_cast<const ulonglong2 *>(st + b * tile + c2);
             } else {
-                const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB) * tile + c2);
-                const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB + 1) * tile + c2);
+                r0 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB) * tile + c2);
+                r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * NB + 1) * tile + c2);
 #pragma unroll
                 for (int b = 0; b < NB; b++) {
-                    const ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(st + (2 * b) * tile + c2);
-                    const ulonglong2 l1 = *reinterpret_cast<const ulonglong2 *>(st + (2 * b + 1) * tile + c2);
-                    mac_to(acc[b][0][0], l0.x, r0.x);
-                    mac_to(acc[b][0][1], l0.y, r0.y);
-                    if constexpr (MODE == 0) {
-                        // Karatsuba: three 64x64 products instead of four.  acc[1] collects
-                        // (l0 + l1)(r0 + r1) (< 2^124: residues < 2^61); d1 = that - d0 - d2 at the end.
-                        mac_to(acc[b][2][0], l1.x, r1.x);
-                        mac_to(acc[b][2][1], l1.y, r1.y);
-                        mac_to(acc[b][1][0], l0.x + l1.x, r0.x + r1.x);
-                        mac_to(acc[b][1][1], l0.y + l1.y, r0.y + r1.y);
-                    } else {
-                        mac_to(acc[b][1][0], l0.x, r1.x);
-                        mac_to(acc[b][1][1], l0.y, r1.y);
-                        mac_to(acc[b][1][0], l1.x, r0.x);
-                        mac_to(acc[b][1][1], l1.y, r0.y);
-                    }
+                    l0[b] = *reinterpret_cast<const ulonglong2 *>(st + (2 * b) * tile + c2);
+                    l1[b] = *reinterpret_cast<const ulonglong2 *>(st + (2 * b + 1) * tile + c2);
                 }
             }
             __syncwarp(wmask);
             if (lane == 0) mbar_arrive(&empty[s]);
+            if constexpr (MODE == 1) {
+#pragma unroll
+                for (int b = 0; b < NB; b++) {
+                    mac_to(acc[b][2][0], l1[b].x, r1.x);
+                    mac_to(acc[b][2][1], l1[b].y, r1.y);
+                }
+            } else {
+#pragma unroll
+                for (int b = 0; b < NB; b++) {
+                    mac_to(acc[b][0][0], l0[b].x, r0.x);
+                    mac_to(acc[b][0][1], l0[b].y, r0.y);
+                    if constexpr (MODE == 0) {
+                        // Karatsuba: three 64x64 products instead of four.  acc[1] collects
+                        // (l0 + l1)(r0 + r1) (< 2^124: residues < 2^61); d1 = that - d0 - d2 at the end.
+                        mac_to(acc[b][2][0], l1[b].x, r1.x);
+                        mac_to(acc[b][2][1], l1[b].y, r1.y);
+                        mac_to(acc[b][1][0], l0[b].x + l1[b].x, r0.x + r1.x);
+                        mac_to(acc[b][1][1], l0[b].y + l1[b].y, r0.y + r1.y);
+                    } else {
+                        mac_to(acc[b][1][0], l0[b].x, r1.x);
+                        mac_to(acc[b][1][1], l0[b].y, r1.y);
+                        mac_to(acc[b][1][0], l1[b].x, r0.x);
+                        mac_to(acc[b][1][1], l1[b].y, r0.y);
+                    }
+                }
+            }
             if ((it & 7) == 7) {
 #pragma unroll
                 for (int b = 0; b < NB; b++)
@@ -842,13 +857,171 @@ void tensor_sum_mode(Ctx &c, const uint64_t *const *L, const uint64_t *const *R,
     check_launch("k_tensor_sum");
 }
 
+// ---- register-pipelined tensor sum (no shared-memory ring) ------------------------------------
+// (d0, d1, d2) = sum_k L[k] (x) R[k] (Karatsuba d1) with plain 16-byte global loads: thread (k-group
+// g, coefficient pair e) of a CTA walks its k range with the next step's four operand loads issued
+// before the current step's products, and the KG k-groups of a CTA combine through shared memory;
+// cluster ranks (split-K across CTAs) combine through DSMEM.  rb > 1: rb row blocks interleaved along
+// x sharing R through L2 (config 5a).  Compared with the TMA ring it trades the producer warp and the
+// per-stage mbarrier handshake for occupancy (every thread has loads in flight).
+template <int KG, int SPLIT>
+__global__ void __launch_bounds__(64 * KG)
+    k_tensor_sum_ld(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O,
+                    int rb) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int TP = 64;  // coefficient pairs per CTA
+    const int xb = rb > 1 ? (int)blockIdx.x % rb : 0;
+    const int xt = rb > 1 ? (int)blockIdx.x / rb : (int)blockIdx.x;
+    L += (size_t)xb * n;
+    O += xb;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int z = (int)cluster.block_rank();
+    const int tp = threadIdx.x % TP, g = threadIdx.x / TP;
+    const int i = blockIdx.y;
+    const long long e2 = (long long)xt * TP + tp;  // coefficient pair index
+    const bool live = 2 * e2 < N;
+    const Modulus m = pr.m[i];
+    // k range of this (cluster rank, k-group)
+    const int parts = SPLIT * KG, part = z * KG + g;
+    const int per = (n + parts - 1) / parts;
+    const int kb = min(n, part * per), ke = min(n, kb + per);
+    const size_t o0 = (size_t)i * N + 2 * e2, o1 = (size_t)(nl + i) * N + 2 * e2;
+    u128 acc[3][2];
+#pragma unroll
+    for (int p = 0; p < 3; p++) acc[p][0] = acc[p][1] = u128{0, 0};
+    if (live && kb < ke) {
+        ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(L[kb] + o0), l1 = *reinterpret_cast<const ulonglong2 *>(L[kb] + o1);
+        ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R[kb] + o0), r1 = *reinterpret_cast<const ulonglong2 *>(R[kb] + o1);
+        for (int k = kb, it = 0; k < ke; k++, it++) {
+            ulonglong2 nl0 = l0, nl1 = l1, nr0 = r0, nr1 = r1;
+            if (k + 1 < ke) {  // next step's operands in flight while this step multiplies
+                const uint64_t *lp = L[k + 1], *rp = R[k + 1];
+                nl0 = __ldcs(reinterpret_cast<const ulonglong2 *>(lp + o0));
+                nl1 = __ldcs(reinterpret_cast<const ulonglong2 *>(lp + o1));
+                nr0 = __ldcs(reinterpret_cast<const ulonglong2 *>(rp + o0));
+                nr1 = __ldcs(reinterpret_cast<const ulonglong2 *>(rp + o1));
+            }
+            mac_to(acc[0][0], l0.x, r0.x);
+            mac_to(acc[0][1], l0.y, r0.y);
+            mac_to(acc[2][0], l1.x, r1.x);
+            mac_to(acc[2][1], l1.y, r1.y);
+            mac_to(acc[1][0], l0.x + l1.x, r0.x + r1.x);
+            mac_to(acc[1][1], l0.y + l1.y, r0.y + r1.y);
+            if ((it & 7) == 7) {
+#pragma unroll
+                for (int p = 0; p < 3; p++)
+#pragma unroll
+                    for (int e = 0; e < 2; e++) acc[p][e] = u128{reduce128(acc[p][e], m), 0};
+            }
+            l0 = nl0;
+            l1 = nl1;
+            r0 = nr0;
+            r1 = nr1;
+        }
+    }
+    __shared__ ulonglong2 part_s[KG][3][TP];
+    {
+        uint64_t v[3][2];
+#pragma unroll
+        for (int p = 0; p < 3; p++)
+#pragma unroll
+            for (int e = 0; e < 2; e++) v[p][e] = reduce128(acc[p][e], m);
+#pragma unroll
+        for (int e = 0; e < 2; e++) v[1][e] = sub_mod(sub_mod(v[1][e], v[0][e], m.q), v[2][e], m.q);  // undo Karatsuba
+#pragma unroll
+        for (int p = 0; p < 3; p++) part_s[g][p][tp] = make_ulonglong2(v[p][0], v[p][1]);
+    }
+    __syncthreads();
+    if (g == 0) {  // k-groups of this CTA
+#pragma unroll
+        for (int p = 0; p < 3; p++) {
+            ulonglong2 v = part_s[0][p][tp];
+#pragma unroll
+            for (int gg = 1; gg < KG; gg++) {
+                const ulonglong2 w = part_s[gg][p][tp];
+                v.x = add_mod(v.x, w.x, m.q);
+                v.y = add_mod(v.y, w.y, m.q);
+            }
+            part_s[0][p][tp] = v;
+        }
+    }
+    cluster.sync();
+    if (z == 0 && g == 0 && live) {
+        uint64_t *o = O[0];
+#pragma unroll
+        for (int p = 0; p < 3; p++) {
+            ulonglong2 v = part_s[0][p][tp];
+#pragma unroll
+            for (int r = 1; r < SPLIT; r++) {
+                const ulonglong2 w = cluster.map_shared_rank(&part_s[0][p][0], r)[tp];
+                v.x = add_mod(v.x, w.x, m.q);
+                v.y = add_mod(v.y, w.y, m.q);
+            }
+            st2(o + (size_t)(p * nl + i) * N + 2 * e2, v.x, v.y);
+        }
+    }
+    cluster.sync();
+}
+
+template <int KG, int SPLIT>
+static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O, int rb) {
+    cudaLaunchConfig_t cfg = {};
+    const int tiles = (c.n / 2 + 63) / 64;
+    cfg.gridDim = dim3(tiles * rb, nl, SPLIT);
+    cfg.blockDim = dim3(64 * KG, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = SPLIT;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    VR_CUDA(cudaLaunchKernelEx(&cfg, k_tensor_sum_ld<KG, SPLIT>, L, R, n, nl, c.n, c.primes, O, rb));
+}
+
+// VR_TS_LD selects the register-pipelined kernel for one-pass sums (0 = the TMA ring).  Swept on
+// B200 (config 2, tools/ts_probe.py): TMA ring 38.1 us; KG x SPLIT = 4x1 37.8, 4x2 41.1, 8x1 55.7,
+// 2x2 36.3 (default, 4.66 TB/s), 8x2 63.0, 2x4 54.3, 2x1 39.6, 1x4 47.7, 1x2 57.2, 1x8 53.9.  Config 5a
+// (4 interleaved row blocks): 2x2 1.19 ms vs 1.24 ms for the ring.
+static int ts_ld_variant() {
+    static const int v = [] {
+        const char *e = getenv("VR_TS_LD");
+        return e ? atoi(e) : 4;
+    }();
+    return v;
+}
+
+static bool try_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O, int rb) {
+    switch (ts_ld_variant()) {
+        case 1: launch_ts_ld<4, 1>(c, L, R, n, nl, O, rb); return true;
+        case 2: launch_ts_ld<4, 2>(c, L, R, n, nl, O, rb); return true;
+        case 3: launch_ts_ld<8, 1>(c, L, R, n, nl, O, rb); return true;
+        case 4: launch_ts_ld<2, 2>(c, L, R, n, nl, O, rb); return true;
+        case 5: launch_ts_ld<8, 2>(c, L, R, n, nl, O, rb); return true;
+        case 6: launch_ts_ld<2, 4>(c, L, R, n, nl, O, rb); return true;
+        case 7: launch_ts_ld<2, 1>(c, L, R, n, nl, O, rb); return true;
+        case 8: launch_ts_ld<1, 4>(c, L, R, n, nl, O, rb); return true;
+        case 9: launch_ts_ld<1, 2>(c, L, R, n, nl, O, rb); return true;
+        case 10: launch_ts_ld<1, 8>(c, L, R, n, nl, O, rb); return true;
+        default: return false;
+    }
+}
+
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O) {
     static int variant = [] {
         const char *e = getenv("VR_TS_VARIANT");
         return e ? atoi(e) : 0;  // 0 = tuned default
     }();
     switch (nb) {
-        case 1: ts_variant<1>(c, variant, L, R, n, nl, O); break;
+        case 1:
+            if (!try_ts_ld(c, L, R, n, nl, O, 1)) ts_variant<1>(c, variant, L, R, n, nl, O);
+            break;
         case 2: ts_variant<2>(c, variant, L, R, n, nl, O); break;
         case 4: {
             // four row blocks sharing R (cfg 5a).  Round 1: two launches of two row blocks, R streamed twice,
@@ -872,10 +1045,11 @@ void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int 
                     const char *e = getenv("VR_TS4_MC");
                     return e ? atoi(e) : 0;
                 }();
-                switch (mcv) {
+                switch (mcv ? mcv : (ts_ld_variant() ? 7 : 0)) {
                     case 1: launch_ts_mc<4, 256, 2, 8>(c, L, R, n, nl, O); break;
                     case 2: launch_ts_mc<4, 512, 2, 4>(c, L, R, n, nl, O); break;
                     case 3: launch_ts<1, 256, 2, 4>(c, L, R, n, nl, O, 4); break;
+                    case 7: if (!try_ts_ld(c, L, R, n, nl, O, 4)) launch_ts<1, 512, 2, 6>(c, L, R, n, nl, O, 4); break;
                     case 4: launch_ts<1, 512, 2, 4>(c, L, R, n, nl, O, 4); break;
                     case 5: launch_ts<2, 256, 2, 4>(c, L, R, n, nl, O, 2); break;
                     case 6: launch_ts<1, 256, 4, 4>(c, L, R, n, nl, O, 4); break;

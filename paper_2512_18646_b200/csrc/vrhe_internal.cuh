@@ -297,6 +297,10 @@ struct NttBatch {
     int poff;
     int pspecial;
     int skip_diag;
+    // optional second segment: transforms t >= split (a multiple of group) live at data2 instead
+    // (two separately allocated ciphertext batches encrypted by one launch)
+    uint64_t *data2 = nullptr;
+    int split = 0x7fffffff;
 };
 
 inline NttBatch batch_limbs(uint64_t *data, int polys, int limbs, int n) {

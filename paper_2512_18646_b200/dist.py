@@ -145,8 +145,9 @@ def reduce_partials_to_owners(partial: torch.Tensor, group=None) -> list[int]:
     return [b for b in range(nb) if block_owner(b, world) == rank]
 
 
-def matmul_partials(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -> tuple[torch.Tensor, int]:
-    """Local degree-2 partial sum [nb][3][l+1][N] (int64 residues) over this rank's k shard."""
+def matmul_partials(engine: CkksEngine, lefts, right: ColumnEncodedMatrix, out: torch.Tensor | None = None) -> tuple[torch.Tensor, int]:
+    """Local degree-2 partial sum [nb][3][l+1][N] (int64 residues) over this rank's k shard (into ``out``
+    when given and of the right shape)."""
     nb = len(lefts)
     if nb not in (1, 2, 4):
         raise EngineError("sharded matmul supports 1, 2 or 4 row blocks")
@@ -177,7 +178,8 @@ def matmul_partials(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -> tu
         rptrs = _lib.ptr_array([c.ptr() for c in allc[nb * n:]])
     if lv < 1:
         raise EngineError("multiplicative depth exhausted")
-    part = torch.empty((nb, 3, lv + 1, engine.N), dtype=torch.int64, device=engine.device)
+    shape = (nb, 3, lv + 1, engine.N)
+    part = out if out is not None and tuple(out.shape) == shape else torch.empty(shape, dtype=torch.int64, device=engine.device)
     if n > 0:
         _lib.check(engine._lib.vr_tensor_sum(engine.handle, lptrs, rptrs, n, nb, lv, _lib.row_ptrs(part, nb)))
     else:
@@ -214,7 +216,8 @@ def matmul_outer_sharded_owned(engine: CkksEngine, lefts, right: ColumnEncodedMa
     block's owner, then each rank relinearises + rescales only the blocks it owns ({block: ciphertext};
     empty on ranks that own none).  Residues are identical to matmul_outer_sharded's.  With ``comm`` the
     reduce runs on the library's own NCCL communicator (vr_sum_partials), else on torch.distributed."""
-    part, lv = matmul_partials(engine, lefts, right)
+    ring = _partials_buffer(engine, len(lefts), right) if engine.async_drivers else None
+    part, lv = matmul_partials(engine, lefts, right, out=ring[0] if ring else None)
     if comm is not None:
         nb = part.shape[0]
         for b in range(nb):
@@ -227,10 +230,30 @@ def matmul_outer_sharded_owned(engine: CkksEngine, lefts, right: ColumnEncodedMa
     if not mine:
         return {}
     sub = part if len(mine) == part.shape[0] else part[mine].contiguous()
-    return dict(zip(mine, _finish_async(engine, sub, lv, right.m, right.p, reduced)))
+    return dict(zip(mine, _finish_async(engine, sub, lv, right.m, right.p, reduced, ring if sub is part else None)))
 
 
-def _finish_async(engine: CkksEngine, part: torch.Tensor, level: int, m: int, p: int, reduced: bool) -> list[Ciphertext]:
+def _partials_buffer(engine: CkksEngine, nb: int, right: ColumnEncodedMatrix):
+    """Two alternating partial-sum buffers per engine and shape: the tensor sum of product i+1 writes one
+    while the side stream still relinearises product i from the other (it first waits for the side
+    stream's use of its buffer two products ago).  Fresh allocations per product would be recorded on
+    the side stream, and the caching allocator would then fall back to synchronous cudaMalloc calls."""
+    lv = min((c.level for c in right.cts), default=engine.L)
+    key = ("partials", nb, lv)
+    ring = engine._ext_streams.get(key)
+    if ring is None:
+        ring = engine._ext_streams[key] = {"i": 0, "bufs": [torch.empty((nb, 3, lv + 1, engine.N), dtype=torch.int64,
+                                                                        device=engine.device) for _ in range(2)],
+                                           "done": [None, None]}
+    i = ring["i"]
+    ring["i"] = 1 - i
+    done = ring["done"][i]
+    if done is not None:
+        torch.cuda.current_stream(engine.device).wait_event(done)
+    return ring["bufs"][i], ring, i
+
+
+def _finish_async(engine: CkksEngine, part: torch.Tensor, level: int, m: int, p: int, reduced: bool, ring=None) -> list[Ciphertext]:
     """matmul_finish on the engine's side stream: the latency-bound relinearisation of this product
     overlaps the next product's streaming tensor sum (config 5a issues them back to back).  The
     results are pending on the side stream; any read waits for it (Ciphertext._ready)."""
@@ -241,7 +264,13 @@ def _finish_async(engine: CkksEngine, part: torch.Tensor, level: int, m: int, p:
     side.wait_stream(cur)
     with torch.cuda.stream(side):
         outs = matmul_finish(engine, part, level, m, p, reduced)
-    part.record_stream(side)
+    if ring is not None:  # the persistent buffer is free again once the side stream passes this point
+        _, state, i = ring
+        ev = state["done"][i] or torch.cuda.Event()
+        ev.record(side)
+        state["done"][i] = ev
+    else:
+        part.record_stream(side)
     for ct in outs:
         ct._pending = side
     return outs

@@ -163,9 +163,13 @@ class Ciphertext:
         """Order the current stream after the (asynchronous) producer of these residues, and record
         the storage on the current stream: the producer's stream owns the allocation, so reads
         queued here must complete before the caching allocator hands the block out again."""
-        if self._pending is not None:
+        p = self._pending
+        if p is not None:
+            if isinstance(p, CkksEngine):  # a deferred encryption: launch it (and its queue) now
+                p._flush_enc()
+                return
             cur = torch.cuda.current_stream()
-            cur.wait_stream(self._pending)
+            cur.wait_stream(p)
             self.storage_tensor().record_stream(cur)
             self._pending = None
 
@@ -247,6 +251,9 @@ class CkksEngine:
         # asynchronous drivers (vr_matmul_outer_async): results are produced on the library's slot
         # streams and every read of them waits first (Ciphertext._ready); VR_ASYNC=0 disables
         self.async_drivers = os.environ.get("VR_ASYNC", "1") != "0"
+        # deferred strided encryptions (secret-key engines): VR_DEFER_ENC=0 launches each at once
+        self._defer_enc = p.encryption == "secret" and os.environ.get("VR_DEFER_ENC", "1") != "0"
+        self._enc_queue = []
         self._ext_streams = {}
         self._nonce = 0
         self._pin = None
@@ -280,11 +287,16 @@ class CkksEngine:
         kernels, the output allocations, the pinned H2D staging copies and the decode's D2H all
         share that one stream, so no cross-stream hazard exists inside a call.
         """
+        self._adopt_stream()
+        if self._enc_queue:
+            self._flush_enc()
+        return self._h
+
+    def _adopt_stream(self) -> None:
         if _raw_stream(self._dev_index) != self._stream_ptr:
             cur = torch.cuda.current_stream(self.device)
             _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(cur.cuda_stream)))
             self._stream, self._stream_ptr = cur, cur.cuda_stream
-        return self._h
 
     def _observe(self, depth: int) -> None:
         if depth > self._meter.max_depth:
@@ -314,7 +326,7 @@ class CkksEngine:
         """Host float64 array -> device, staged through a ring of reusable pinned buffers: a buffer is
         refilled only after its previous copy has executed, so the host may run up to eight uploads
         ahead of the device (pipelined encrypt -> product -> decode steps)."""
-        self.handle  # noqa: B018 -- adopt the caller's current stream before copying
+        self._adopt_stream()  # the caller's current stream (no flush: an upload is not an engine call)
         nbytes = vals.nbytes
         if self._pin is None:
             self._pin = [None] * self._PIN_RING
@@ -387,13 +399,60 @@ class CkksEngine:
         d_src = self._h2d(arr) if arr.size else torch.zeros(1, dtype=torch.float64, device=self.device)
         out = self._empty(1, self.L, count)
         n0 = self._nonce if nonce0 is None else int(nonce0)
-        _lib.check(self._lib.vr_encrypt_strided(self.handle, d_src.data_ptr() + 8 * int(offset), sc, s1, s2, max(1, p), nvals,
-                                                count, self.L, self.scales[self.L], n0, out.data_ptr()))
+        job = (d_src, d_src.data_ptr() + 8 * int(offset), sc, s1, s2, max(1, p), nvals, count, n0, out, self._stream)
         if nonce0 is None:
             self._nonce += count
         self._meter.enc_count += count
         self._observe(0)
-        return Ciphertext.batch(out, self.L, self.scales[self.L], 0, layout, self._id)
+        cts = Ciphertext.batch(out, self.L, self.scales[self.L], 0, layout, self._id)
+        if self._defer_enc and count > 0:
+            # deferred: launched at the next engine call or read of these ciphertexts (_flush_enc), so
+            # the two operands of one product (encode_left + encode_right) become ONE encryption launch
+            for ct in cts:
+                ct._pending = self
+            self._enc_queue.append((job, cts))
+        else:
+            self._launch_enc([job])
+        return cts
+
+    def _launch_enc(self, jobs) -> None:
+        h = self._h
+        if len(jobs) == 1:
+            _, src, sc, s1, s2, p, nvals, count, n0, out, _ = jobs[0]
+            _lib.check(self._lib.vr_encrypt_strided(h, src, sc, s1, s2, p, nvals, count, self.L, self.scales[self.L], n0,
+                                                    out.data_ptr()))
+            return
+        (_, a_src, a_sc, a_s1, a_s2, a_p, a_nv, a_cnt, a_n0, a_out, _), (_, b_src, b_sc, b_s1, b_s2, b_p, b_nv, b_cnt, _, b_out, _) = jobs
+        _lib.check(self._lib.vr_encrypt_strided2(h, a_src, a_sc, a_s1, a_s2, a_p, a_nv, a_cnt, a_out.data_ptr(), b_src, b_sc,
+                                                 b_s1, b_s2, b_p, b_nv, b_cnt, b_out.data_ptr(), self.L, self.scales[self.L],
+                                                 a_n0))
+
+    def _flush_enc(self) -> None:
+        """Launch the deferred encryptions (consecutive-nonce pairs as one combined launch), ordered on
+        the current stream after the streams their host copies were queued on."""
+        queue, self._enc_queue = self._enc_queue, []
+        if not queue:
+            return
+        self._adopt_stream()
+        cur = self._stream
+        for (job, _) in queue:
+            if job[10].cuda_stream != cur.cuda_stream:
+                cur.wait_stream(job[10])
+        i = 0
+        while i < len(queue):
+            job, cts = queue[i]
+            if i + 1 < len(queue) and queue[i + 1][0][8] == job[8] + job[7]:  # nonces continue: one launch
+                self._launch_enc([job, queue[i + 1][0]])
+                group = [cts, queue[i + 1][1]]
+                i += 2
+            else:
+                self._launch_enc([job])
+                group = [cts]
+                i += 1
+            for g in group:
+                for ct in g:
+                    if ct._pending is self:
+                        ct._pending = None
 
     def dec(self, ct: Ciphertext) -> np.ndarray:
         """Full slot vector (real parts), like engine.py:204-206."""
@@ -427,7 +486,11 @@ class CkksEngine:
         Lets a caller keep several encrypt -> product -> decode steps in flight."""
         cts = list(cts)
         pend = cts[0]._pending if cts else None
-        stream = pend if pend is not None and all(c._pending is pend for c in cts) else torch.cuda.current_stream(self.device)
+        if isinstance(pend, torch.cuda.Stream) and all(c._pending is pend for c in cts):
+            stream = pend
+        else:
+            self.handle  # noqa: B018 -- deferred encryptions first
+            stream = torch.cuda.current_stream(self.device)
         with torch.cuda.stream(stream):
             out = self._dec_device(cts, select)
             host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
