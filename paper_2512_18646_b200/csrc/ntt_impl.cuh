@@ -566,10 +566,41 @@ inline int pick_tpc(int count, int tiles_per_tf, int T, int max_tpc, int min_tpc
 // trip per transform instead of two.
 __device__ __forceinline__ int sidx_row(int L) { return L ^ ((L >> 4) & 15); }
 
+// DSMEM exchange with asynchronous stores (sm_90+): st.async writes a 64-bit value into a peer CTA's
+// shared memory and completes transaction bytes on the peer's mbarrier, so a receiver waits only for
+// the bytes addressed to it -- no release fence and no cluster-wide barrier after the scatter.
+__device__ __forceinline__ uint32_t cl_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cl_mapa(uint32_t a, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void st_async_b64(uint32_t raddr, uint64_t v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(v), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void cl_mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(cl_smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+inline bool cl_st_async() {
+    static const bool on = [] {
+        const char *e = getenv("VR_NTT_ST_ASYNC");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    return on;
+}
+
 template <bool INV, int LOGC, bool F64, class LD, class ST>
 __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, const ulonglong2 *__restrict__ tw,
                                              const double *__restrict__ twd, const NttConst &nc, uint64_t *ptr, int t,
-                                             int pidx, const LD &ld, const ST &st, uint64_t *sm) {
+                                             int pidx, const LD &ld, const ST &st, uint64_t *sm, uint64_t *xbar, bool async_x) {
     namespace cg = cooperative_groups;
     using V = typename std::conditional<F64, double, uint64_t>::type;
     constexpr int LE = 3, EPT = 8, C = 1 << LOGC, NG = (LOGC + LE - 1) / LE;
@@ -635,10 +666,25 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
 #pragma unroll
         for (int u = 0; u < 8; u++) x[u] = in(ld(ptr, t, (long long)col + ((long long)u << LOGC), pr, pidx));
         compute(std::integral_constant<int, 3>{}, 1, 0, 3, 0, 0, zero_base);
-        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer is resident
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer is resident (and its barrier set up)
+        if (async_x) {
+            if (threadIdx.x == 0)  // this CTA receives its whole chunk: C words from the 8 ranks
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cl_smem_u32(xbar)), "r"((uint32_t)C * 8)
+                             : "memory");
+            const uint32_t dst = cl_smem_u32(&smv[sidx_row(col)]), bar = cl_smem_u32(xbar);
 #pragma unroll
-        for (int u = 0; u < 8; u++) cluster.map_shared_rank(smv, u)[sidx_row(col)] = x[u];
-        cluster.sync();
+            for (int u = 0; u < 8; u++) {
+                uint64_t bits;
+                if constexpr (F64) bits = (uint64_t)__double_as_longlong(x[u]);
+                else bits = x[u];
+                st_async_b64(cl_mapa(dst, u), bits, cl_mapa(bar, u));
+            }
+            cl_mbar_wait(xbar, 0);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; u++) cluster.map_shared_rank(smv, u)[sidx_row(col)] = x[u];
+            cluster.sync();
+        }
         local_stages(false);
         // coalesced store of the chunk through the Store functor (prefetch its loads first)
         typename ST::Pre pre[EPT];
@@ -651,10 +697,32 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
         }
     } else {
         local_stages(true);
-        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-        cluster.sync();
+        if (async_x) {
+            // push instead of gather: CTA u's thread `sub` needs element sidx_row(u C/8 + sub) of every
+            // rank; it lands in u's receive buffer (behind its chunk) at [rank][sub]
+            V *rx = smv + C;
+            asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // peers resident, barriers set up
+            if (threadIdx.x == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cl_smem_u32(xbar)), "r"((uint32_t)C * 8)
+                             : "memory");
+            const uint32_t dst = cl_smem_u32(&rx[r * (C / 8) + sub]), bar = cl_smem_u32(xbar);
 #pragma unroll
-        for (int u = 0; u < 8; u++) x[u] = cluster.map_shared_rank(smv, u)[sidx_row(col)];
+            for (int u = 0; u < 8; u++) {
+                const V v = smv[sidx_row(u * (C / 8) + sub)];
+                uint64_t bits;
+                if constexpr (F64) bits = (uint64_t)__double_as_longlong(v);
+                else bits = v;
+                st_async_b64(cl_mapa(dst, u), bits, cl_mapa(bar, u));
+            }
+            cl_mbar_wait(xbar, 0);
+#pragma unroll
+            for (int u = 0; u < 8; u++) x[u] = rx[u * (C / 8) + sub];
+        } else {
+            asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+            cluster.sync();
+#pragma unroll
+            for (int u = 0; u < 8; u++) x[u] = cluster.map_shared_rank(smv, u)[sidx_row(col)];
+        }
         compute(std::integral_constant<int, 3>{}, 1, 0, 3, 0, 0, zero_base);
         typename ST::Pre pre[EPT];
 #pragma unroll
@@ -662,31 +730,36 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
 #pragma unroll
         for (int u = 0; u < 8; u++)
             st.finish(ptr, t, (long long)col + ((long long)u << LOGC), final_value(x[u]), pre[u], pr, pidx);
-        cluster.sync();  // peers keep their shared memory until every gather has finished
+        if (!async_x) cluster.sync();  // peers keep their shared memory until every gather has finished
     }
 }
 
 template <bool INV, int LOGC, class LD, class ST>
 __global__ void __launch_bounds__((1 << LOGC) / 8, 65536 / (((1 << LOGC) / 8) * kCapRegs)) ntt_cl8(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *__restrict__ tw,
                                                            const double *__restrict__ twd,
-                                                           const NttConst *__restrict__ ncs, LD ld, ST st) {
+                                                           const NttConst *__restrict__ ncs, LD ld, ST st, bool async_x) {
     extern __shared__ uint64_t sm[];
+    __shared__ __align__(8) uint64_t xbar;
     const int t = blockIdx.x >> 3;
     pdl_wait();
     pdl_trigger();
     uint64_t *ptr;
     int pidx;
     if (!locate(b, t, 1 << logN, ptr, pidx)) return;  // uniform over the cluster (same transform)
+    if (async_x && threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cl_smem_u32(&xbar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     const NttConst nc = ncs[pidx];
-    if (nc.f64) ntt_cl8_body<INV, LOGC, true>(logN, pr, tw, twd, nc, ptr, t, pidx, ld, st, sm);
-    else ntt_cl8_body<INV, LOGC, false>(logN, pr, tw, twd, nc, ptr, t, pidx, ld, st, sm);
+    if (nc.f64) ntt_cl8_body<INV, LOGC, true>(logN, pr, tw, twd, nc, ptr, t, pidx, ld, st, sm, &xbar, async_x);
+    else ntt_cl8_body<INV, LOGC, false>(logN, pr, tw, twd, nc, ptr, t, pidx, ld, st, sm, &xbar, async_x);
 }
 
 template <bool INV, int LOGC, class LD, class ST>
 void launch_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
     constexpr int C = 1 << LOGC;
-    const size_t smem = (size_t)C * sizeof(uint64_t);
+    const size_t smem = (size_t)C * sizeof(uint64_t) * (INV && cl_st_async() ? 2 : 1);  // inverse: + receive buffer
     auto kern = ntt_cl8<INV, LOGC, LD, ST>;
     ensure_smem(c, (const void *)kern, smem);
     cudaLaunchConfig_t cfg = {};
@@ -704,7 +777,7 @@ void launch_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     VR_CUDA(cudaLaunchKernelEx(&cfg, kern, b, c.log_n, c.primes, (const ulonglong2 *)(INV ? c.itw2 : c.tw2),
-                               (const double *)(INV ? c.itwd : c.twd), (const NttConst *)c.ntt_const, ld, st));
+                               (const double *)(INV ? c.itwd : c.twd), (const NttConst *)c.ntt_const, ld, st, cl_st_async()));
     check_launch("ntt_cl8");
 }
 
