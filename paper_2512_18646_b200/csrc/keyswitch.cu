@@ -48,7 +48,15 @@ struct LdStrided {
 template <int KS_MAXD, int KS_CG>
 __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint64_t *const *P, long long poly_off, int count,
                                                   int level, int N, int logN, int np, const uint64_t *key, uint32_t g,
-                                                  DevPrimes pr, uint64_t *A, const NttConst *__restrict__ ncs) {
+                                                  DevPrimes pr, uint64_t *A, const NttConst *__restrict__ ncs,
+                                                  const uint64_t *const *keys_r, const uint32_t *gs_r) {
+    // keys_r: one launch for every rotation amount of a hoisted batch (grid z = amount r): key and
+    // Galois element of amount r, output ciphertext c*nrot + r
+    const int nrot = gridDim.z, rz = blockIdx.z;
+    if (keys_r) {
+        key = keys_r[rz];
+        g = gs_r[rz];
+    }
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int nl = level + 1, nt = level + 2;
     if (e >= (long long)nt * N) {
@@ -104,8 +112,9 @@ __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint6
                     a0 = __dadd_rn(a0, nttk::mulmod_f(dd, kd0[j], nc.qd, nc.qinv));
                     a1 = __dadd_rn(a1, nttk::mulmod_f(dd, kd1[j], nc.qd, nc.qinv));
                 }
-            A[(((long long)c * 2 + 0) * nt + t) * N + k] = nttk::canon_f(a0, nc.qd, nc.qinv);
-            A[(((long long)c * 2 + 1) * nt + t) * N + k] = nttk::canon_f(a1, nc.qd, nc.qinv);
+            const long long co = (long long)c * nrot + rz;
+            A[((co * 2 + 0) * nt + t) * N + k] = nttk::canon_f(a0, nc.qd, nc.qinv);
+            A[((co * 2 + 1) * nt + t) * N + k] = nttk::canon_f(a1, nc.qd, nc.qinv);
         }
         return;
     }
@@ -122,8 +131,9 @@ __global__ void __launch_bounds__(128) k_ks_inner(const uint64_t *D, const uint6
                 if ((j & 7) == 7) { a0 = u128{reduce128(a0, m), 0}; a1 = u128{reduce128(a1, m), 0}; }
             }
         }
-        A[(((long long)c * 2 + 0) * nt + t) * N + k] = reduce128(a0, m);
-        A[(((long long)c * 2 + 1) * nt + t) * N + k] = reduce128(a1, m);
+        const long long co = (long long)c * nrot + rz;
+        A[((co * 2 + 0) * nt + t) * N + k] = reduce128(a0, m);
+        A[((co * 2 + 1) * nt + t) * N + k] = reduce128(a1, m);
     }
 }
 
@@ -236,23 +246,25 @@ void modup(Ctx &c, const uint64_t *const *Polys, int count, int level, uint64_t 
 
 template <int CG>
 static void launch_ks_inner_cg(Ctx &c, const uint64_t *D, const uint64_t *const *Polys, long long poly_off, int count, int level,
-                               const uint64_t *key, uint32_t g, uint64_t *A) {
+                               const uint64_t *key, uint32_t g, uint64_t *A, const uint64_t *const *keys_r,
+                               const uint32_t *gs_r, int nrot) {
     const int N = c.n, nl = level + 1, nt = level + 2;
-    const dim3 blocks(nblocks((long long)nt * N, 128), (count + CG - 1) / CG);
+    const dim3 blocks(nblocks((long long)nt * N, 128), (count + CG - 1) / CG, nrot);
     if (nl <= 8)
         launch_pdl(k_ks_inner<8, CG>, blocks, dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N, c.log_n, c.np, key, g,
-                   c.primes, A, (const NttConst *)c.ntt_const);
+                   c.primes, A, (const NttConst *)c.ntt_const, keys_r, gs_r);
     else if (nl <= 16)
         launch_pdl(k_ks_inner<16, CG>, blocks, dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N, c.log_n, c.np, key,
-                   g, c.primes, A, (const NttConst *)c.ntt_const);
+                   g, c.primes, A, (const NttConst *)c.ntt_const, keys_r, gs_r);
     else
-        launch_pdl(k_ks_inner<40, 1>, dim3(blocks.x, count), dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N,
-                   c.log_n, c.np, key, g, c.primes, A, (const NttConst *)c.ntt_const);
+        launch_pdl(k_ks_inner<40, 1>, dim3(blocks.x, count, nrot), dim3(128), 0, c.stream, D, Polys, poly_off, count, level, N,
+                   c.log_n, c.np, key, g, c.primes, A, (const NttConst *)c.ntt_const, keys_r, gs_r);
     check_launch("k_ks_inner");
 }
 
 static void launch_ks_inner(Ctx &c, const uint64_t *D, const uint64_t *const *Polys, long long poly_off, int count, int level,
-                            const uint64_t *key, uint32_t g, uint64_t *A) {
+                            const uint64_t *key, uint32_t g, uint64_t *A, const uint64_t *const *keys_r = nullptr,
+                            const uint32_t *gs_r = nullptr, int nrot = 1) {
     static int cg_env = [] {
         const char *e = getenv("VR_KS_CG");
         return e ? atoi(e) : 0;
@@ -261,10 +273,10 @@ static void launch_ks_inner(Ctx &c, const uint64_t *D, const uint64_t *const *Po
     // ciphertext per thread (146 instead of 175 registers) is ~1.5% faster
     const int cg = cg_env ? cg_env : (level + 1 > 8 ? 1 : 2);
     switch (cg) {
-        case 1: launch_ks_inner_cg<1>(c, D, Polys, poly_off, count, level, key, g, A); break;
-        case 2: launch_ks_inner_cg<2>(c, D, Polys, poly_off, count, level, key, g, A); break;
-        case 8: launch_ks_inner_cg<8>(c, D, Polys, poly_off, count, level, key, g, A); break;
-        default: launch_ks_inner_cg<4>(c, D, Polys, poly_off, count, level, key, g, A); break;
+        case 1: launch_ks_inner_cg<1>(c, D, Polys, poly_off, count, level, key, g, A, keys_r, gs_r, nrot); break;
+        case 2: launch_ks_inner_cg<2>(c, D, Polys, poly_off, count, level, key, g, A, keys_r, gs_r, nrot); break;
+        case 8: launch_ks_inner_cg<8>(c, D, Polys, poly_off, count, level, key, g, A, keys_r, gs_r, nrot); break;
+        default: launch_ks_inner_cg<4>(c, D, Polys, poly_off, count, level, key, g, A, keys_r, gs_r, nrot); break;
     }
 }
 
@@ -280,6 +292,26 @@ static void inner_moddown(Ctx &c, const uint64_t *D, const uint64_t *const *Poly
                       LdStrided{a.as<uint64_t>(), (long long)nt * N, (long long)nl * N}, nttk::StPlain{});
     PtrTable ta(c, strided_ptrs(a.as<uint64_t>(), count, (size_t)2 * nt * N));
     nttk::StCombine st{ta.c_(), Out, Add, c.inv_tab + (size_t)P * c.np * 2, nl, 2, nt, add_polys, c.log_n, g};
+    ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), rows, nl, N), nttk::LdLift{y.as<uint64_t>(), nl, 1, P, N, c.f64mask, c.liftk}, st);
+}
+
+// inner_moddown for every rotation amount of a hoisted batch at once: one inner-product launch (grid z
+// = amount), one INTT and one NTT + combine over count * nrot ciphertexts; Out [count * nrot] ordered
+// [ct][amount], Add[ct] permuted by amount r's Galois element.  Replaces 4 launches per amount.
+static void inner_moddown_multi(Ctx &c, const uint64_t *D, const uint64_t *const *Polys, long long poly_off, int count,
+                                int level, const uint64_t *const *keys_r, const uint32_t *gs_r, int nrot,
+                                uint64_t *const *Out, const uint64_t *const *Add, int add_polys) {
+    const int N = c.n, nl = level + 1, nt = level + 2, P = c.np - 1, total = count * nrot;
+    Scratch a(c, sizeof(uint64_t) * total * 2 * nt * N);
+    launch_ks_inner(c, D, Polys, poly_off, count, level, nullptr, 1, a.as<uint64_t>(), keys_r, gs_r, nrot);
+    const int rows = total * 2;
+    Scratch y(c, sizeof(uint64_t) * rows * N), z(c, sizeof(uint64_t) * rows * nl * N);
+    ntt_inverse_fused(c, NttBatch{y.as<uint64_t>(), rows, 1, (long long)N, 1, P, 0, 0},
+                      LdStrided{a.as<uint64_t>(), (long long)nt * N, (long long)nl * N}, nttk::StPlain{});
+    PtrTable ta(c, strided_ptrs(a.as<uint64_t>(), total, (size_t)2 * nt * N));
+    nttk::StCombine st{ta.c_(), Out, Add, c.inv_tab + (size_t)P * c.np * 2, nl, 2, nt, add_polys, c.log_n, 1u};
+    st.gs_rows = gs_r;
+    st.add_div = nrot;
     ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), rows, nl, N), nttk::LdLift{y.as<uint64_t>(), nl, 1, P, N, c.f64mask, c.liftk}, st);
 }
 
@@ -330,6 +362,21 @@ void rotate_batch(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int c
     Scratch d(c, any ? sizeof(uint64_t) * count * nl * nt * N : 0);
     const long long off = (long long)nl * N;
     if (any) modup_impl(c, In, off, count, level, d.as<uint64_t>());
+    // VR_ROT_BATCH=1: one launch sequence for all amounts (parity-tested; measured on B200 Alg 3 90.8
+    // vs 94.0 HE matmul/s, cfg 3/4/5b and Table 1 unchanged -- the rotations are device-bound)
+    static const bool batched = [] {
+        const char *e = getenv("VR_ROT_BATCH");
+        return e != nullptr && atoi(e) != 0;
+    }();
+    bool all_rot = nrot > 1;
+    for (int r = 0; r < nrot; r++) all_rot &= gs[r] != 1;
+    if (batched && all_rot) {  // every amount a real rotation: one launch sequence for all of them
+        std::vector<const uint64_t *> kv(keys.begin(), keys.end());
+        PtrTable tk(c, kv);
+        DevArray<uint32_t> dg(c, gs, nrot);
+        inner_moddown_multi(c, d.as<uint64_t>(), In, off, count, level, tk.c_(), dg.get(), nrot, Out, In, 1);
+        return;
+    }
     for (int r = 0; r < nrot; r++) {
         Scratch tbl(c, sizeof(void *) * count);
         VR_CUDA(cudaMemcpy2DAsync(tbl.p, sizeof(void *), (const void *)(Out + r), sizeof(void *) * nrot, sizeof(void *), count,

@@ -133,6 +133,9 @@ struct StCombine {
     const uint64_t *inv;  // inv_tab row: (inv, shoup) pairs per target prime
     int nout, rdiv, a_limbs, add_polys, logN;
     uint32_t g;
+    // hoisted rotations batched over amounts: output r0 = c * add_div + r adds add[c] permuted by gs_rows[r]
+    const uint32_t *gs_rows = nullptr;
+    int add_div = 1;
     struct Pre {
         uint64_t a, b;
     };
@@ -145,12 +148,14 @@ struct StCombine {
         p.b = 0;
         if (add && r1 < add_polys) {
             long long src = E;
+            const int ra = r0 / add_div;
+            const uint32_t g = gs_rows ? gs_rows[r0 - ra * add_div] : this->g;
             if (g != 1) {
                 const uint32_t brk = __brev((uint32_t)E) >> (32 - logN);
                 const uint32_t e = ((2u * brk + 1u) * g) & ((2u << logN) - 1u);
                 src = (long long)(__brev((e - 1u) >> 1) >> (32 - logN));
             }
-            p.b = add[r0][((long long)r1 * nout + i) * N + src];
+            p.b = add[ra][((long long)r1 * nout + i) * N + src];
         }
         return p;
     }

@@ -8,6 +8,8 @@ process from the environment, so every variant runs in its own interpreter):
   every NTT on the integer (IMAD-pipe) body
 * VR_GRAPH=0   -- every driver call eager (no CUDA-graph replay)
 * VR_ASYNC=0   -- matmul_outer synchronous (no slot streams)
+* VR_ROT_BATCH=1, VR_NTT_ST_ASYNC=0, VR_TS_LD=0 -- hoisted rotations in one launch sequence, the
+  cluster NTT exchanging through scatter + cluster barriers, the TMA-ring tensor sum
 """
 
 import os
@@ -22,8 +24,9 @@ ROOT = Path(__file__).resolve().parent.parent
 
 
 @pytest.mark.parametrize("env", [{"VR_NTT_CL": "1"}, {"VR_PDL": "0"}, {"VR_MM_ORDER": "2", "VR_NTT_CL": "1"}, {"VR_MM_ORDER": "0", "VR_NTT_F64": "0"},
-                                 {"VR_GRAPH": "0"}, {"VR_ASYNC": "0"}],
-                         ids=["cluster-ntt", "no-pdl", "hi-prio-chain", "order0-int-ntt", "no-graph", "sync"])
+                                 {"VR_GRAPH": "0"}, {"VR_ASYNC": "0"},
+                                 {"VR_ROT_BATCH": "1", "VR_NTT_ST_ASYNC": "0", "VR_TS_LD": "0"}],
+                         ids=["cluster-ntt", "no-pdl", "hi-prio-chain", "order0-int-ntt", "no-graph", "sync", "alt-kernels"])
 def test_parity_suite_under_variant(env):
     pytest.importorskip("torch").cuda.is_available() or pytest.skip("no CUDA device")
     e = dict(os.environ, **env)
