@@ -286,8 +286,13 @@ __device__ __forceinline__ void group_compute_f(double (&x)[EPT], const int (&ba
                     X = mulmod_f(__dadd_rn(a, b), nc.ninv_d, q, qinv);
                     Y = mulmod_f(__dsub_rn(a, b), nc.w0n_d, q, qinv);
                 } else if (INV) {
+                    // Lazy sums: a group starts with |x| <= q (folded sums and products of the previous
+                    // group, or canonical input), each stage at most doubles a sum, so after R <= 3
+                    // stages |x| <= 8q < 2^49 -- inside mulmod_f's |y| < 2^51 domain (its input a - b
+                    // is bounded by the same sums).  Only the sums leaving the group are folded back
+                    // to |x| <= q/2: 4 folds per 12 butterflies of a radix-8 group instead of 12.
                     const double a = X, b = Y;
-                    X = fold_f(__dadd_rn(a, b), q, qinv);
+                    X = rr == R - 1 ? fold_f(__dadd_rn(a, b), q, qinv) : __dadd_rn(a, b);
                     Y = mulmod_f(__dsub_rn(a, b), tw[n0 + w / (2 * half)], q, qinv);
                 } else {
                     const double t = mulmod_f(Y, tw[n0 + w / (2 * half)], q, qinv);
@@ -350,6 +355,29 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
 
     V x[EPT];
     int base[EPT];
+    const int wl = blockDim.x < 32 ? (int)blockDim.x : 32;
+    const int own0 = ((int)threadIdx.x / wl) * (wl * EPT) + ((int)threadIdx.x % wl);  // warp-owned block, lane-contiguous
+    // The inverse rows pass starts with its shortest-distance round, where a thread owns runs of
+    // consecutive elements: loaded directly, every warp-wide load touches 32 sectors.  Stage the tile
+    // through shared memory instead (lane-contiguous loads of the warp's own block, which is exactly
+    // what that round reads, so __syncwarp orders it).
+    constexpr bool STAGE_IN = INV && !COLS;
+    if constexpr (STAGE_IN) {
+        V y[EPT];
+#pragma unroll
+        for (int r = 0; r < EPT; r++) {
+            const int idx = own0 + r * wl;
+            const int jj = idx >> LOGT, mid = idx & (T - 1);
+            const int tl = tile0 + jj, h2 = tl >> lo_bits, lo2 = tl & lomask;
+            y[r] = in(ld(ptr, t, ((long long)h2 << (logN - s0)) | ((long long)mid << lo_bits) | lo2, pr, pidx));
+        }
+#pragma unroll
+        for (int r = 0; r < EPT; r++) {
+            const int idx = own0 + r * wl;
+            smv[sidx<COLS>(idx >> LOGT, idx & (T - 1), T, TPC)] = y[r];
+        }
+        __syncwarp();
+    }
 #pragma unroll
     for (int step = 0; step < NG; step++) {
         const int gi = INV ? NG - 1 - step : step;
@@ -366,7 +394,7 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
 #pragma unroll
         for (int e = 0; e < EPT; e++) {
             const int L = base[e >> R] | ((e & (E2 - 1)) << logd);
-            if (step == 0) x[e] = in(ld(ptr, t, ebase | ((long long)L << lo_bits), pr, pidx));
+            if (step == 0 && !STAGE_IN) x[e] = in(ld(ptr, t, ebase | ((long long)L << lo_bits), pr, pidx));
             else x[e] = smv[sidx_off<COLS>(sb[e >> R], (e & (E2 - 1)) << logd, TPC)];
         }
         if constexpr (F64) {
@@ -397,14 +425,24 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
         }
 #pragma unroll
         for (int e = 0; e < EPT; e++) smv[sidx_off<COLS>(sb[e >> R], (e & (E2 - 1)) << logd, TPC)] = x[e];
-        __syncthreads();  // one owner per element within a group: a single barrier per group boundary
+        // One owner per element within a group: a single barrier per group boundary.  Rows passes: a
+        // warp's 32 * EPT elements are one contiguous block of the flat tile array, and a round whose
+        // span (2^(LOGT - s)) fits that block reads and writes only that block, so the exchange with the
+        // next round (and with the warp-owned store below) never leaves the warp: __syncwarp, and the
+        // warps of a CTA drift apart instead of meeting at every radix group.
+        {
+            constexpr int W = 32 * EPT;
+            const int need = INV ? (gi > 0 ? (1 << (LOGT - LE * (gi - 1))) : T) : (1 << (LOGT - s));
+            if (!COLS && need <= W) __syncwarp();
+            else __syncthreads();
+        }
     }
-    // rows: coalesced cooperative store out of shared memory (prefetch the epilogue's loads first)
+    // rows: coalesced store out of shared memory, each warp its own block (prefetch the epilogue's loads first)
     long long Es[EPT];
     typename ST::Pre pre[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; r++) {  // blockDim.x * EPT == TPC * T
-        const int idx = threadIdx.x + r * blockDim.x;
+        const int idx = own0 + r * wl;
         const int jj = idx >> LOGT, mid = idx & (T - 1);
         const int tl = tile0 + jj, h2 = tl >> lo_bits, lo2 = tl & lomask;
         Es[r] = ((long long)h2 << (logN - s0)) | ((long long)mid << lo_bits) | lo2;
@@ -412,7 +450,7 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
     }
 #pragma unroll
     for (int r = 0; r < EPT; r++) {
-        const int idx = threadIdx.x + r * blockDim.x;
+        const int idx = own0 + r * wl;
         const int jj = idx >> LOGT, mid = idx & (T - 1);
         const V v = smv[sidx<COLS>(jj, mid, T, TPC)];
         st.finish(ptr, t, Es[r], a.last ? out_final(v) : (a.raw_out ? out_raw(v) : out_final(v)), pre[r], pr, pidx);
@@ -639,6 +677,15 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
         else group_compute<INV, RR, EPT>(x, bs, d, s, logT, s0, hi, q, W, nc);
     };
     auto local_stages = [&](bool from_global) {
+        if (from_global) {  // inverse: coalesced loads of the warp-owned block, staged through shared memory
+            const int own0 = (sub >> 5) * (32 * EPT) + (sub & 31);
+            V y[EPT];
+#pragma unroll
+            for (int k = 0; k < EPT; k++) y[k] = in(ld(ptr, t, (long long)r * C + own0 + 32 * k, pr, pidx));
+#pragma unroll
+            for (int k = 0; k < EPT; k++) smv[sidx_row(own0 + 32 * k)] = y[k];
+            __syncwarp();
+        }
 #pragma unroll
         for (int step = 0; step < NG; step++) {
             const int gi = INV ? NG - 1 - step : step;
@@ -653,17 +700,20 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
 #pragma unroll
             for (int v = 0; v < EPT; v++) sb[v] = swz(base[v]);
 #pragma unroll
-            for (int e = 0; e < EPT; e++) {
-                const int L = base[e >> R] | ((e & (E2 - 1)) << logd);
-                x[e] = (from_global && step == 0) ? in(ld(ptr, t, (long long)r * C + L, pr, pidx))
-                                                  : smv[sb[e >> R] ^ swz((e & (E2 - 1)) << logd)];
-            }
+            for (int e = 0; e < EPT; e++) x[e] = smv[sb[e >> R] ^ swz((e & (E2 - 1)) << logd)];
             if (R == 3) compute(std::integral_constant<int, 3>{}, d, s, LOGC, 3, r, base);
             else if (R == 2) compute(std::integral_constant<int, 2>{}, d, s, LOGC, 3, r, base);
             else compute(std::integral_constant<int, 1>{}, d, s, LOGC, 3, r, base);
 #pragma unroll
             for (int e = 0; e < EPT; e++) smv[sb[e >> R] ^ swz((e & (E2 - 1)) << logd)] = x[e];
-            __syncthreads();
+            // warp-owned 256-element blocks once a round's span fits them (see ntt_pass_body): only the
+            // chunk-wide first round (forward) / last round and the peer exchange (inverse) meet CTA-wide
+            {
+                constexpr int W = 32 * EPT;
+                const int need = INV ? (gi > 0 ? (1 << (LOGC - LE * (gi - 1))) : C) : (1 << (LOGC - s));
+                if (need <= W) __syncwarp();
+                else __syncthreads();
+            }
         }
     };
 
@@ -693,11 +743,12 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
         local_stages(false);
         // coalesced store of the chunk through the Store functor (prefetch its loads first)
         typename ST::Pre pre[EPT];
+        const int own0 = (sub >> 5) * (32 * EPT) + (sub & 31);  // each warp stores the block it owns
 #pragma unroll
-        for (int k = 0; k < EPT; k++) pre[k] = st.prefetch(t, (long long)r * C + sub + k * (C / 8), pr, pidx);
+        for (int k = 0; k < EPT; k++) pre[k] = st.prefetch(t, (long long)r * C + own0 + 32 * k, pr, pidx);
 #pragma unroll
         for (int k = 0; k < EPT; k++) {
-            const int mid = sub + k * (C / 8);
+            const int mid = own0 + 32 * k;
             st.finish(ptr, t, (long long)r * C + mid, final_value(smv[sidx_row(mid)]), pre[k], pr, pidx);
         }
     } else {
