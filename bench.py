@@ -588,7 +588,7 @@ def run_ours(args, ws, rank, local):
     pin_a = torch.from_numpy(a).pin_memory()
     pin_b = torch.from_numpy(b).pin_memory()
     e2e_steps = max(8, min(100, args.steps // 2))
-    E2E_DEPTH = int(os.environ.get("VR_E2E_DEPTH", "2"))  # encrypt -> product -> decode steps in flight (decode_async futures)
+    E2E_DEPTH = int(os.environ.get("VR_E2E_DEPTH", "3"))  # encrypt -> product -> decode steps in flight (decode_async futures)
 
     def e2e_run(k):
         """k steps through the public API; every step's decoded result is read on the host."""
@@ -657,7 +657,7 @@ def run_ours(args, ws, rank, local):
             "e2e": {"value": ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps, "pipeline_depth": E2E_DEPTH,
                     "path": "per step: pinned host A,B -> encode_left+encode_right (encrypt 128 cts) -> matmul_outer -> "
-                            "decode_async; at most E2E_DEPTH (2) steps in flight, every step's result read on the host"},
+                            f"decode_async; at most {E2E_DEPTH} steps in flight, every step's result read on the host"},
             "gpu_launches": int(launches),
             "gpu_launches_per_step": launches / args.steps,
             "clocks": clk.summary(),

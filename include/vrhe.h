@@ -119,6 +119,25 @@ int vr_encrypt_strided(vr_ctx *ctx, const double *src, long long sc, long long s
 int vr_encrypt_strided2(vr_ctx *ctx, const double *src0, long long sc0, long long s1_0, long long s2_0, int p0, int nvals0,
                         int count0, uint64_t *ct0, const double *src1, long long sc1, long long s1_1, long long s2_1, int p1,
                         int nvals1, int count1, uint64_t *ct1, int level, double scale, uint64_t nonce0);
+/* The same strided encryptions from HOST arrays (the raw matrices encode_left / encode_right /
+ * encode_image_columns receive, multicipher.py:62-85,106-120): host[0..len) is staged through the
+ * context's pinned ring into stream-ordered device scratch; the source of ciphertext c starts at
+ * element off + c*sc.  The host array may be reused as soon as the call returns. */
+int vr_encrypt_strided_host(vr_ctx *ctx, const double *host, long long len, long long off, long long sc, long long s1,
+                            long long s2, int p, int nvals, int count, int level, double scale, uint64_t nonce0,
+                            uint64_t *ct_out);
+int vr_encrypt_strided2_host(vr_ctx *ctx, const double *host0, long long len0, long long off0, long long sc0, long long s1_0,
+                             long long s2_0, int p0, int nvals0, int count0, uint64_t *ct0, const double *host1,
+                             long long len1, long long off1, long long sc1, long long s1_1, long long s2_1, int p1, int nvals1,
+                             int count1, uint64_t *ct1, int level, double scale, uint64_t nonce0);
+/* SlotEngine.dec (engine.py:204-206) to host memory without blocking the caller: decrypt + decode
+ * on `stream` (NULL: the context stream; e.g. the slot stream that produced the ciphertexts), copy
+ * the [count][S] real slots into a pinned buffer owned by the context and record an event.
+ * vr_decode_wait(ticket) blocks until that event, copies the slots to host_out ([count][S] doubles,
+ * may be NULL) and releases the ticket.  Lets a caller keep encrypt -> product -> decode steps in flight. */
+int vr_decode_submit(vr_ctx *ctx, const uint64_t *const *cts, const int *degs, const int *levels, const double *scales,
+                     int count, void *stream, int *ticket);
+int vr_decode_wait(vr_ctx *ctx, int ticket, double *host_out);
 /* SlotEngine.dec (engine.py:204-206): decrypt on q0 and decode to real slots.
  * out: device [count][S] doubles (may be NULL); coeffs_out: device [count][N] int64 (may be NULL). */
 int vr_decrypt_decode(vr_ctx *ctx, const uint64_t *const *cts, const int *degs, const int *levels, const double *scales,

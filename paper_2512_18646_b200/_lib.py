@@ -44,6 +44,16 @@ _SIGS = {
     "vr_encrypt_strided2": [c_vp, c_vp, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_int, ctypes.c_int,
                             ctypes.c_int, c_vp, c_vp, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_int,
                             ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64],
+    "vr_encrypt_strided_host": [c_vp, c_vp, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong,
+                                ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                ctypes.c_uint64, c_vp],
+    "vr_encrypt_strided2_host": [c_vp, c_vp, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong,
+                                 ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp, ctypes.c_longlong,
+                                 ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_int,
+                                 ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64],
+    "vr_decode_submit": [c_vp, c_vpp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                         ctypes.POINTER(ctypes.c_double), ctypes.c_int, c_vp, ctypes.POINTER(ctypes.c_int)],
+    "vr_decode_wait": [c_vp, ctypes.c_int, c_vp],
     "vr_decrypt_decode": [c_vp, c_vpp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                           ctypes.POINTER(ctypes.c_double), ctypes.c_int, c_vp, c_vp],
     "vr_add": [c_vp, c_vpp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int],

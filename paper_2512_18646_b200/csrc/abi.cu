@@ -125,6 +125,11 @@ void destroy_ctx(vr_ctx *h) {
     for (auto &kv : c.gkeys) cudaFree(kv.second);
     for (auto &e : c.tables)
         if (e.dev) cudaFree(e.dev);
+    for (auto &tk : c.tickets) {
+        if (tk.host) cudaFreeHost(tk.host);
+        if (tk.done) cudaEventDestroy(tk.done);
+    }
+    c.tickets.clear();
     for (auto &b : c.big_free) cudaFree(b.second);
     for (auto &kv : c.parked) {
         if (kv.second.arena) cudaFree(kv.second.arena);
@@ -402,32 +407,34 @@ int vr_ctx_destroy(vr_ctx *h) {
     return guard([&] { destroy_ctx(h); });
 }
 
+// Move the context to stream s: the current scratch arena is parked under its stream and s gets
+// its own (Ctx::parked), so a call on one stream never reuses bytes another may still touch.
+static void set_stream(vr::Ctx &c, cudaStream_t s) {
+    if (s == c.stream) return;
+    vr::Ctx::ArenaState &old = c.parked[c.stream];
+    old.arena = c.arena;
+    old.cap = c.arena_cap;
+    old.top = c.arena_top;
+    old.peak = c.arena_peak;
+    old.big_free = std::move(c.big_free);
+    vr::Ctx::ArenaState cur;
+    auto it = c.parked.find(s);
+    if (it != c.parked.end()) {
+        cur = std::move(it->second);
+        c.parked.erase(it);
+    }
+    c.arena = cur.arena;
+    c.arena_cap = cur.cap;
+    c.arena_top = cur.top;
+    c.arena_peak = cur.peak;
+    c.big_free = std::move(cur.big_free);
+    c.stream = s;
+}
+
 int vr_set_stream(vr_ctx *h, void *stream) {
     // NULL is the legacy default stream (torch's default stream); the private stream is kept
-    // for vr_ctx_destroy either way.  Each stream gets its own scratch arena (Ctx::parked).
-    return guard([&] {
-        vr::Ctx &c = h->c;
-        const cudaStream_t s = (cudaStream_t)stream;
-        if (s == c.stream) return;
-        vr::Ctx::ArenaState &old = c.parked[c.stream];
-        old.arena = c.arena;
-        old.cap = c.arena_cap;
-        old.top = c.arena_top;
-        old.peak = c.arena_peak;
-        old.big_free = std::move(c.big_free);
-        vr::Ctx::ArenaState cur;
-        auto it = c.parked.find(s);
-        if (it != c.parked.end()) {
-            cur = std::move(it->second);
-            c.parked.erase(it);
-        }
-        c.arena = cur.arena;
-        c.arena_cap = cur.cap;
-        c.arena_top = cur.top;
-        c.arena_peak = cur.peak;
-        c.big_free = std::move(cur.big_free);
-        c.stream = s;
-    });
+    // for vr_ctx_destroy either way.
+    return guard([&] { set_stream(h->c, (cudaStream_t)stream); });
 }
 
 int vr_sync(vr_ctx *h) {
@@ -526,6 +533,111 @@ int vr_encrypt_strided2(vr_ctx *h, const double *src0, long long sc0, long long 
         if (count0 <= 0 || count1 <= 0) throw vr::VrError(VR_ERR_ENGINE, "both batches must be non-empty");
         vr::encrypt_src2(h->c, src0, sc0, s1_0, s2_0, p0, nvals0, count0, ct0, src1, sc1, s1_1, s2_1, p1, nvals1, count1, ct1,
                          level, scale, nonce0);
+    });
+}
+
+// Host-array forms of the strided encryptions: the raw matrix is staged through the context's
+// pinned ring into stream-ordered scratch (one cudaMemcpyAsync per 64 KB) and encrypted by the
+// same launches, so a caller holding plain host arrays needs no device buffers of its own.
+int vr_encrypt_strided_host(vr_ctx *h, const double *host, long long len, long long off, long long sc, long long s1,
+                            long long s2, int p, int nvals, int count, int level, double scale, uint64_t nonce0,
+                            uint64_t *ct_out) {
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        check_level(c, level);
+        if (nvals > c.slots) throw vr::VrError(VR_ERR_CAPACITY, "payload exceeds slot count");
+        if (len <= 0 || off < 0 || off >= len) throw vr::VrError(VR_ERR_ENGINE, "empty host source");
+        if (count <= 0) return;
+        vr::Scratch d(c, sizeof(double) * (size_t)len);
+        vr::upload_async(c, d.p, host, sizeof(double) * (size_t)len);
+        vr::encrypt_src(c, d.as<double>() + off, sc, s1, s2, p, nvals, count, level, scale, nonce0, ct_out);
+    });
+}
+
+int vr_encrypt_strided2_host(vr_ctx *h, const double *host0, long long len0, long long off0, long long sc0, long long s1_0,
+                             long long s2_0, int p0, int nvals0, int count0, uint64_t *ct0, const double *host1,
+                             long long len1, long long off1, long long sc1, long long s1_1, long long s2_1, int p1, int nvals1,
+                             int count1, uint64_t *ct1, int level, double scale, uint64_t nonce0) {
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        check_level(c, level);
+        if (nvals0 > c.slots || nvals1 > c.slots) throw vr::VrError(VR_ERR_CAPACITY, "payload exceeds slot count");
+        if (count0 <= 0 || count1 <= 0) throw vr::VrError(VR_ERR_ENGINE, "both batches must be non-empty");
+        if (len0 <= 0 || len1 <= 0 || off0 < 0 || off1 < 0 || off0 >= len0 || off1 >= len1)
+            throw vr::VrError(VR_ERR_ENGINE, "empty host source");
+        vr::Scratch d0(c, sizeof(double) * (size_t)len0), d1(c, sizeof(double) * (size_t)len1);
+        vr::upload_async(c, d0.p, host0, sizeof(double) * (size_t)len0);
+        vr::upload_async(c, d1.p, host1, sizeof(double) * (size_t)len1);
+        vr::encrypt_src2(c, d0.as<double>() + off0, sc0, s1_0, s2_0, p0, nvals0, count0, ct0, d1.as<double>() + off1, sc1, s1_1,
+                         s2_1, p1, nvals1, count1, ct1, level, scale, nonce0);
+    });
+}
+
+// Decode without blocking the host: decrypt + decode on `stream` (NULL: the context stream), copy
+// the [count][S] doubles into the ticket's pinned buffer and record its completion event.  The
+// ciphertext metadata travels as one staged upload (pointers | scales | degrees | levels).
+int vr_decode_submit(vr_ctx *h, const uint64_t *const *cts, const int *degs, const int *levels, const double *scales,
+                     int count, void *stream, int *ticket) {
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        *ticket = -1;
+        if (count <= 0) throw vr::VrError(VR_ERR_ENGINE, "nothing to decode");
+        int id = -1;
+        for (int i = 0; i < (int)c.tickets.size() && id < 0; i++)
+            if (!c.tickets[i].busy) id = i;
+        if (id < 0) {
+            if (c.tickets.size() >= 256) throw vr::VrError(VR_ERR_ENGINE, "too many decodes in flight (vr_decode_wait releases one)");
+            c.tickets.emplace_back();
+            id = (int)c.tickets.size() - 1;
+        }
+        const size_t bytes = sizeof(double) * (size_t)count * c.slots;
+        {
+            vr::Ctx::DecodeTicket &tk = c.tickets[id];
+            if (tk.cap < bytes) {
+                if (tk.host) cudaFreeHost(tk.host);
+                tk.host = nullptr;
+                tk.cap = 0;
+                VR_CUDA(cudaHostAlloc((void **)&tk.host, bytes, cudaHostAllocDefault));
+                tk.cap = bytes;
+            }
+            if (!tk.done) VR_CUDA(cudaEventCreateWithFlags(&tk.done, cudaEventDisableTiming));
+        }
+        struct Restore {
+            vr::Ctx &c;
+            cudaStream_t caller;
+            ~Restore() { set_stream(c, caller); }
+        } restore{c, c.stream};
+        const cudaStream_t s = stream ? (cudaStream_t)stream : c.stream;
+        set_stream(c, s);
+        const size_t n = (size_t)count, off_s = 8 * n, off_d = 16 * n, off_l = 20 * n, total = 24 * n;
+        std::vector<char> blob(total);
+        std::memcpy(blob.data(), cts, 8 * n);
+        std::memcpy(blob.data() + off_s, scales, 8 * n);
+        std::memcpy(blob.data() + off_d, degs, 4 * n);
+        std::memcpy(blob.data() + off_l, levels, 4 * n);
+        vr::Scratch meta(c, total), out(c, bytes);
+        vr::upload_async(c, meta.p, blob.data(), total);
+        const char *m = (const char *)meta.p;
+        vr::decrypt_decode(c, (const uint64_t *const *)m, (const int *)(m + off_d), (const int *)(m + off_l),
+                           (const double *)(m + off_s), count, out.as<double>(), nullptr);
+        vr::Ctx::DecodeTicket &tk = c.tickets[id];
+        VR_CUDA(cudaMemcpyAsync(tk.host, out.p, bytes, cudaMemcpyDeviceToHost, s));
+        VR_CUDA(cudaEventRecord(tk.done, s));
+        tk.bytes = bytes;
+        tk.busy = true;
+        *ticket = id;
+    });
+}
+
+int vr_decode_wait(vr_ctx *h, int ticket, double *host_out) {
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        if (ticket < 0 || ticket >= (int)c.tickets.size() || !c.tickets[ticket].busy)
+            throw vr::VrError(VR_ERR_ENGINE, "unknown decode ticket");
+        vr::Ctx::DecodeTicket &tk = c.tickets[ticket];
+        VR_CUDA(cudaEventSynchronize(tk.done));
+        if (host_out) std::memcpy(host_out, tk.host, tk.bytes);
+        tk.busy = false;
     });
 }
 

@@ -101,18 +101,22 @@ __device__ __forceinline__ void fft_round(double *re, double *im, int S, int h, 
 // all stages of length 2 .. S (S = 2^logS), one barrier per round of up to three stages
 // RBMAX = 2: radix-4 rounds (twice the threads per round, half the dependent chain per thread) for
 // the latency-bound single-ciphertext decode; the butterflies and their order are unchanged.
+// tws: shared-memory copy of the table's first `staged` entries (a round with half-length h and RB
+// stages reads indices < h 2^RB); rounds reaching beyond it read the global table tw (L1-resident:
+// every CTA of the launch reads the same entries).
 template <int RBMAX = 3>
-__device__ __forceinline__ void fft_stages(double *re, double *im, int S, int logS, const double2 *tw, bool inverse) {
+__device__ __forceinline__ void fft_stages(double *re, double *im, int S, int logS, const double2 *tw, const double2 *tws,
+                                           int staged, bool inverse) {
     int h = 1, rem = logS;
     for (; rem >= RBMAX; rem -= RBMAX, h <<= RBMAX) {
-        fft_round<RBMAX>(re, im, S, h, tw, inverse);
+        fft_round<RBMAX>(re, im, S, h, (h << RBMAX) <= staged ? tws : tw, inverse);
         __syncthreads();
     }
     if (rem == 2) {
-        fft_round<2>(re, im, S, h, tw, inverse);
+        fft_round<2>(re, im, S, h, (h << 2) <= staged ? tws : tw, inverse);
         __syncthreads();
     } else if (rem == 1) {
-        fft_round<1>(re, im, S, h, tw, inverse);
+        fft_round<1>(re, im, S, h, (h << 1) <= staged ? tws : tw, inverse);
         __syncthreads();
     }
 }
@@ -150,15 +154,23 @@ constexpr int FFT_CL = 8;
 // The local stages read their twiddles (indices < C) from a shared-memory copy of the table's
 // first C entries (tws, filled by stage_twiddles before the PDL wait: the table is constant, so
 // its load overlaps the previous kernel); only the cross-cluster round reads the global table.
-__device__ __forceinline__ void stage_twiddles(double2 *tws, const double2 *tw, int C) {
-    for (int i = threadIdx.x; i < C; i += blockDim.x) tws[i] = __ldg(tw + i);
+__device__ __forceinline__ void stage_twiddles(double2 *tws, const double2 *tw, int staged) {
+    for (int i = threadIdx.x; i < staged; i += blockDim.x) tws[i] = __ldg(tw + i);
+}
+// Twiddles staged per CTA: the entries the full-radix local rounds read, 2^(RBMAX floor(log2 C / RBMAX)).
+// A trailing partial round reads the global table, which keeps a 1024-point CTA at 26.6 KB of shared
+// memory: eight CTAs per SM, so the 1024 CTAs of a 128-ciphertext cfg-2 encryption are one wave.
+__host__ __device__ inline int fft_staged(int C, int rbmax) {
+    int logc = 0;
+    while ((1 << (logc + 1)) <= C) logc++;
+    return 1 << (rbmax * (logc / rbmax));
 }
 
 template <int CL, int RBMAX = 3>
 __device__ __forceinline__ void fft_cluster(double *re, double *im, int S, int logS, const double2 *tw, const double2 *tws,
                                             bool inverse) {
     const int C = S / CL;
-    fft_stages<RBMAX>(re, im, C, logS - (CL == 8 ? 3 : 0), tws, inverse);
+    fft_stages<RBMAX>(re, im, C, logS - (CL == 8 ? 3 : 0), tw, tws, fft_staged(C, 3), inverse);
     if constexpr (CL == 8) {
         namespace cg = cooperative_groups;
         cg::cluster_group cluster = cg::this_cluster();
@@ -195,7 +207,7 @@ struct EncNoise {
 
 // cluster of CL CTAs per ciphertext: slot values -> m [count][N] (int64)
 template <int CL, int RBMAX = 3>
-__global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr, const double *zi, const double2 *tw,
+__global__ void __launch_bounds__(512, 2) k_encode(SlotSrc vs, int S, int logS, double f, const double *zr, const double *zi, const double2 *tw,
                          const int *pos_slot, EncNoise nz, int64_t *m) {
     extern __shared__ double fft_sm[];
     __shared__ uint64_t cdt_s[CDT_LEN];
@@ -203,7 +215,7 @@ __global__ void k_encode(SlotSrc vs, int S, int logS, double f, const double *zr
     const int c = blockIdx.x / CL;
     double *re = fft_sm, *im = fft_sm + C + C / 8;
     double2 *tws = reinterpret_cast<double2 *>(im + C + C / 8);
-    stage_twiddles(tws, tw, C);
+    stage_twiddles(tws, tw, fft_staged(C, 3));
     pdl_wait();
     pdl_trigger();
     if (nz.keys) {
@@ -245,7 +257,7 @@ __global__ void k_decode(const int64_t *m, const double *scales, int S, int logS
     const int c = blockIdx.x / CL;
     double *re = fft_sm, *im = fft_sm + C + C / 8;
     double2 *tws = reinterpret_cast<double2 *>(im + C + C / 8);
-    stage_twiddles(tws, tw, C);
+    stage_twiddles(tws, tw, fft_staged(C, 3));
     if constexpr (RBMAX == 2) {
         // latency-bound single-ciphertext decode: the constant twist tables zr/zi (read at bit-reversed
         // positions spread over every line) and this CTA's slot map go to L2 before the PDL wait
@@ -479,7 +491,7 @@ int fft_threads(int S) {
 }
 size_t fft_smem(int S) {
     const int C = S / fft_cl(S);
-    return (size_t)2 * (C + C / 8) * sizeof(double) + (size_t)C * sizeof(double2);  // re, im (padded) + twiddles
+    return (size_t)2 * (C + C / 8) * sizeof(double) + (size_t)fft_staged(C, 3) * sizeof(double2);  // re, im (padded) + twiddles
 }
 
 template <typename K, typename... Args>

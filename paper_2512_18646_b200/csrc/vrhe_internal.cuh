@@ -142,6 +142,16 @@ struct Ctx {
     cudaStream_t slot_stream[kSlots] = {};
     int slot_next = 0;
 
+    // asynchronous decodes (vr_decode_submit / vr_decode_wait): a pinned result buffer and a
+    // completion event per ticket, reused once the ticket has been waited for
+    struct DecodeTicket {
+        double *host = nullptr;
+        size_t cap = 0, bytes = 0;
+        cudaEvent_t done = nullptr;
+        bool busy = false;
+    };
+    std::vector<DecodeTicket> tickets;
+
     // multi-GPU (comm.cu): NCCL communicator of this context's rank, or null
     void *comm = nullptr;
     int rank = 0, nranks = 1;

@@ -169,7 +169,7 @@ def matmul_partials(engine: CkksEngine, lefts, right: ColumnEncodedMatrix, out: 
             cat = (key, _lib.ptr_array([p for _, ps in infos[:-1] for p in ps]), list(lefts))
             object.__setattr__(right, "_vr_cat", cat)
         lptrs = cat[1]
-        rptrs = getattr(right, "_vr_ptrs")[3]
+        rptrs = getattr(right, "_vr_ptrs").arr
     else:
         allc = [c for lf in lefts for c in lf.cts] + list(right.cts)
         lv = min(c.level for c in allc) if allc else engine.L

@@ -226,6 +226,93 @@ class DecodeFuture:
         return self._post(out) if self._post is not None else out
 
 
+class TicketFuture:
+    """Result of ``dec_batch_async`` on the library's own decode tickets (``vr_decode_submit``): the
+    decrypt + decode + copy into a pinned buffer owned by the context are queued by ONE C call;
+    ``result()`` waits for the ticket's event and returns the slots as a fresh numpy array."""
+
+    __slots__ = ("_engine", "_ticket", "_shape", "_post", "_out")
+
+    def __init__(self, engine, ticket, shape, post=None):
+        self._engine, self._ticket, self._shape, self._post, self._out = engine, ticket, shape, post, None
+
+    def result(self) -> np.ndarray:
+        if self._out is None:
+            out = np.empty(self._shape, dtype=np.float64)
+            eng = self._engine
+            if not eng._h:
+                raise EngineError("the engine of this decode future has been destroyed")
+            _lib.check(eng._lib.vr_decode_wait(eng._h, self._ticket, out.ctypes.data))
+            self._ticket = -1
+            self._out = self._post(out) if self._post is not None else out
+        return self._out
+
+    def __del__(self):
+        t = getattr(self, "_ticket", -1)
+        if t is not None and t >= 0 and getattr(self._engine, "_h", None):
+            try:  # an abandoned future still has to hand its ticket back
+                self._engine._lib.vr_decode_wait(self._engine._h, t, None)
+            except Exception:
+                pass
+
+
+class CtBatch:
+    """The ciphertexts of one batched kernel output ([count][deg+1][l+1][N]) as a list-like
+    sequence whose ``Ciphertext`` objects are created on first access: an operand that only feeds
+    ``matmul_outer`` never materialises them (its pointer table is base + i * stride)."""
+
+    __slots__ = ("out", "level", "scale", "depth", "layout", "engine_id", "count", "_items", "_pending")
+
+    def __init__(self, out, level, scale, depth, layout, engine_id, count=None, pending=None):
+        self.out, self.level, self.scale, self.depth = out, level, scale, depth
+        self.layout, self.engine_id = layout, engine_id
+        self.count = out.shape[0] if count is None else count
+        self._items = None
+        self._pending = pending
+
+    def _all(self) -> list:
+        items = self._items
+        if items is None:
+            items = self._items = Ciphertext.batch(self.out, self.level, self.scale, self.depth, self.layout,
+                                                   self.engine_id, self.count)
+            if self._pending is not None:
+                for ct in items:
+                    ct._pending = self._pending
+        return items
+
+    def clear_pending(self, owner) -> None:
+        """The deferred encryption behind this batch has been launched."""
+        if self._pending is owner:
+            self._pending = None
+            if self._items is not None:
+                for ct in self._items:
+                    if ct._pending is owner:
+                        ct._pending = None
+
+    def pointers(self) -> np.ndarray:
+        """Device addresses of the ciphertexts (uint64), without creating them."""
+        step = self.out.stride(0) * self.out.element_size()
+        return self.out.data_ptr() + step * np.arange(self.count, dtype=np.uint64)
+
+    def __len__(self) -> int:
+        return self.count
+
+    def __getitem__(self, i):
+        return self._all()[i]
+
+    def __iter__(self):
+        return iter(self._all())
+
+    def __add__(self, other):
+        return self._all() + list(other)
+
+    def __radd__(self, other):
+        return list(other) + self._all()
+
+    def __repr__(self) -> str:
+        return f"CtBatch(count={self.count}, level={self.level})"
+
+
 class CkksEngine:
     """Metered RNS-CKKS engine over ``params.slots`` slots on one CUDA device."""
 
@@ -254,6 +341,9 @@ class CkksEngine:
         # deferred strided encryptions (secret-key engines): VR_DEFER_ENC=0 launches each at once
         self._defer_enc = p.encryption == "secret" and os.environ.get("VR_DEFER_ENC", "1") != "0"
         self._enc_queue = []
+        # dec_batch_async through the library's decode tickets (one C call); VR_DECODE_TICKETS=0 keeps
+        # the torch path (device tensor + pinned tensor + copy + event)
+        self._decode_tickets = os.environ.get("VR_DECODE_TICKETS", "1") != "0"
         self._ext_streams = {}
         self._nonce = 0
         self._pin = None
@@ -396,36 +486,55 @@ class CkksEngine:
         if nvals > self.slots:
             raise CapacityError(f"{nvals} values exceed {self.slots} slots")
         arr = np.ascontiguousarray(np.asarray(src, dtype=np.float64)).reshape(-1)
-        d_src = self._h2d(arr) if arr.size else torch.zeros(1, dtype=torch.float64, device=self.device)
+        defer = self._defer_enc and count > 0
         out = self._empty(1, self.L, count)
         n0 = self._nonce if nonce0 is None else int(nonce0)
-        job = (d_src, d_src.data_ptr() + 8 * int(offset), sc, s1, s2, max(1, p), nvals, count, n0, out, self._stream)
+        if defer and 0 < arr.nbytes <= self._HOST_STAGE_MAX:
+            # small raw arrays stay on the host until the launch: the library stages them through its
+            # pinned ring itself (vr_encrypt_strided*_host), one C call for copy + encode + encrypt.
+            # The snapshot lets the caller reuse its array before the deferred launch.
+            snap = arr.copy()
+            job = (None, snap.ctypes.data, sc, s1, s2, max(1, p), nvals, count, n0, out, None, snap, int(offset))
+            self.h2d_bytes += arr.nbytes
+        else:
+            d_src = self._h2d(arr) if arr.size else torch.zeros(1, dtype=torch.float64, device=self.device)
+            job = (d_src, d_src.data_ptr() + 8 * int(offset), sc, s1, s2, max(1, p), nvals, count, n0, out, self._stream,
+                   None, 0)
         if nonce0 is None:
             self._nonce += count
         self._meter.enc_count += count
         self._observe(0)
-        cts = Ciphertext.batch(out, self.L, self.scales[self.L], 0, layout, self._id)
-        if self._defer_enc and count > 0:
+        cts = CtBatch(out, self.L, self.scales[self.L], 0, layout, self._id, count, self if defer else None)
+        if defer:
             # deferred: launched at the next engine call or read of these ciphertexts (_flush_enc), so
             # the two operands of one product (encode_left + encode_right) become ONE encryption launch
-            for ct in cts:
-                ct._pending = self
             self._enc_queue.append((job, cts))
         else:
             self._launch_enc([job])
         return cts
 
+    _HOST_STAGE_MAX = 1 << 20  # raw arrays up to 1 MB ride the library's pinned ring
+
     def _launch_enc(self, jobs) -> None:
         h = self._h
+        L, scale = self.L, self.scales[self.L]
         if len(jobs) == 1:
-            _, src, sc, s1, s2, p, nvals, count, n0, out, _ = jobs[0]
-            _lib.check(self._lib.vr_encrypt_strided(h, src, sc, s1, s2, p, nvals, count, self.L, self.scales[self.L], n0,
-                                                    out.data_ptr()))
+            _, src, sc, s1, s2, p, nvals, count, n0, out, _, snap, off = jobs[0]
+            if snap is not None:
+                _lib.check(self._lib.vr_encrypt_strided_host(h, src, snap.size, off, sc, s1, s2, p, nvals, count, L, scale, n0,
+                                                             out.data_ptr()))
+            else:
+                _lib.check(self._lib.vr_encrypt_strided(h, src, sc, s1, s2, p, nvals, count, L, scale, n0, out.data_ptr()))
             return
-        (_, a_src, a_sc, a_s1, a_s2, a_p, a_nv, a_cnt, a_n0, a_out, _), (_, b_src, b_sc, b_s1, b_s2, b_p, b_nv, b_cnt, _, b_out, _) = jobs
-        _lib.check(self._lib.vr_encrypt_strided2(h, a_src, a_sc, a_s1, a_s2, a_p, a_nv, a_cnt, a_out.data_ptr(), b_src, b_sc,
-                                                 b_s1, b_s2, b_p, b_nv, b_cnt, b_out.data_ptr(), self.L, self.scales[self.L],
-                                                 a_n0))
+        ((_, a_src, a_sc, a_s1, a_s2, a_p, a_nv, a_cnt, a_n0, a_out, _, a_snap, a_off),
+         (_, b_src, b_sc, b_s1, b_s2, b_p, b_nv, b_cnt, _, b_out, _, b_snap, b_off)) = jobs
+        if a_snap is not None:
+            _lib.check(self._lib.vr_encrypt_strided2_host(h, a_src, a_snap.size, a_off, a_sc, a_s1, a_s2, a_p, a_nv, a_cnt,
+                                                          a_out.data_ptr(), b_src, b_snap.size, b_off, b_sc, b_s1, b_s2, b_p,
+                                                          b_nv, b_cnt, b_out.data_ptr(), L, scale, a_n0))
+        else:
+            _lib.check(self._lib.vr_encrypt_strided2(h, a_src, a_sc, a_s1, a_s2, a_p, a_nv, a_cnt, a_out.data_ptr(), b_src, b_sc,
+                                                     b_s1, b_s2, b_p, b_nv, b_cnt, b_out.data_ptr(), L, scale, a_n0))
 
     def _flush_enc(self) -> None:
         """Launch the deferred encryptions (consecutive-nonce pairs as one combined launch), ordered on
@@ -436,13 +545,15 @@ class CkksEngine:
         self._adopt_stream()
         cur = self._stream
         for (job, _) in queue:
-            if job[10].cuda_stream != cur.cuda_stream:
+            if job[10] is not None and job[10].cuda_stream != cur.cuda_stream:
                 cur.wait_stream(job[10])
         i = 0
         while i < len(queue):
             job, cts = queue[i]
-            if i + 1 < len(queue) and queue[i + 1][0][8] == job[8] + job[7]:  # nonces continue: one launch
-                self._launch_enc([job, queue[i + 1][0]])
+            nxt = queue[i + 1][0] if i + 1 < len(queue) else None
+            # nonces continue and both sources live on the same side (host / device): one launch
+            if nxt is not None and nxt[8] == job[8] + job[7] and (nxt[11] is None) == (job[11] is None):
+                self._launch_enc([job, nxt])
                 group = [cts, queue[i + 1][1]]
                 i += 2
             else:
@@ -450,9 +561,7 @@ class CkksEngine:
                 group = [cts]
                 i += 1
             for g in group:
-                for ct in g:
-                    if ct._pending is self:
-                        ct._pending = None
+                g.clear_pending(self)
 
     def dec(self, ct: Ciphertext) -> np.ndarray:
         """Full slot vector (real parts), like engine.py:204-206."""
@@ -486,7 +595,25 @@ class CkksEngine:
         Lets a caller keep several encrypt -> product -> decode steps in flight."""
         cts = list(cts)
         pend = cts[0]._pending if cts else None
-        if isinstance(pend, torch.cuda.Stream) and all(c._pending is pend for c in cts):
+        on_slot = isinstance(pend, torch.cuda.Stream) and all(c._pending is pend for c in cts)
+        if select is None and cts and self._decode_tickets:
+            # one C call: the library decodes on the producer's stream (the ciphertexts were allocated
+            # and written there) or on the current one, into its own pinned ticket buffer
+            h = self.handle  # adopts the current stream, launches deferred encryptions
+            for ct in cts:
+                self._check(ct)
+            count = len(cts)
+            stream_ptr = pend.cuda_stream if on_slot else None
+            ptrs = _lib.ptr_array([ct._ptr if on_slot else ct.ptr() for ct in cts])
+            degs = (ctypes.c_int * count)(*[ct.degree for ct in cts])
+            lvls = (ctypes.c_int * count)(*[ct.level for ct in cts])
+            scl = (ctypes.c_double * count)(*[ct.scale for ct in cts])
+            ticket = ctypes.c_int(-1)
+            _lib.check(self._lib.vr_decode_submit(h, ptrs, degs, lvls, scl, count, stream_ptr, ctypes.byref(ticket)))
+            # (the storages need no keep-alive: they are read on the stream that owns their allocation,
+            # or were recorded on the current stream by ct.ptr())
+            return TicketFuture(self, ticket.value, (count, self.slots), post)
+        if on_slot:
             stream = pend
         else:
             self.handle  # noqa: B018 -- deferred encryptions first

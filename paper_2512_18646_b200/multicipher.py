@@ -28,7 +28,7 @@ import torch
 
 from . import _lib
 from .encoding import Encoding, Kernel, MatrixShape, PackedMatrix
-from .engine import CapacityError, Ciphertext, CkksEngine, EngineError, LayoutError
+from .engine import CapacityError, Ciphertext, CkksEngine, CtBatch, EngineError, LayoutError
 
 __all__ = [
     "ColumnEncodedMatrix",
@@ -90,11 +90,43 @@ def encode_right(engine: CkksEngine, b, m: int) -> ColumnEncodedMatrix:
     return _fresh(engine, ColumnEncodedMatrix(cts, "right", m, n, p))
 
 
+class _OperandCache:
+    """Validated view of a column-encoded operand for one engine: level, max depth, the storage
+    tensors, and the device pointer table -- kept as a uint64 numpy array; the ctypes array the
+    C-ABI takes and the Python list are made from it on first use."""
+
+    __slots__ = ("eid", "level", "depth", "storages", "_np", "_arr", "_list")
+
+    def __init__(self, eid, level, depth, storages, np_ptrs=None, ptrs=None):
+        self.eid, self.level, self.depth, self.storages = eid, level, depth, storages
+        self._np = np_ptrs if np_ptrs is not None else np.array(ptrs, dtype=np.uint64)
+        self._arr = None
+        self._list = ptrs
+
+    @property
+    def arr(self):
+        a = self._arr
+        if a is None:
+            a = self._arr = (ctypes.c_void_p * max(1, self._np.size)).from_buffer(self._np) if self._np.size else _lib.ptr_array([])
+        return a
+
+    @property
+    def ptrs(self) -> list:
+        if self._list is None:
+            self._list = [int(v) for v in self._np]
+        return self._list
+
+
 def _fresh(engine: CkksEngine, cem: ColumnEncodedMatrix) -> ColumnEncodedMatrix:
     """Operand fresh from one encryption batch: same engine, top level, depth 0 for every
-    ciphertext, so the validated pointer cache of _checked_ptrs can be filled directly."""
-    ptrs = [c._ptr for c in cem.cts]
-    object.__setattr__(cem, "_vr_ptrs", (engine._id, engine.L, ptrs, _lib.ptr_array(ptrs), 0, _storages(cem.cts)))
+    ciphertext, so the validated pointer cache of _checked_ptrs can be filled directly -- from the
+    batch's base address and stride, without creating the Ciphertext objects."""
+    cts = cem.cts
+    if isinstance(cts, CtBatch):
+        cache = _OperandCache(engine._id, engine.L, 0, _Storages([cts.out]), np_ptrs=cts.pointers())
+    else:
+        cache = _OperandCache(engine._id, engine.L, 0, _storages(cts), ptrs=[c._ptr for c in cts])
+    object.__setattr__(cem, "_vr_ptrs", cache)
     return cem
 
 
@@ -116,11 +148,18 @@ class _Storages(list):
 
 
 def _storages(cts):
+    if isinstance(cts, CtBatch):
+        return _Storages([cts.out])
     seen = {}
     for c in cts:
         t = c.storage_tensor()
         seen.setdefault(id(t), t)
     return _Storages(seen.values())
+
+
+def _layout0(cts):
+    """Layout tag of the first ciphertext (without materialising a lazy batch)."""
+    return cts.layout if isinstance(cts, CtBatch) else cts[0].layout
 
 
 def _common_level(engine: CkksEngine, cts):
@@ -134,24 +173,24 @@ def _checked_ptrs(engine: CkksEngine, cem: ColumnEncodedMatrix):
     """(level, [device pointers]) of a column-encoded operand, validated and cached on the object
     (operands are immutable; the cache also holds the ctypes pointer array and the max depth)."""
     cached = getattr(cem, "_vr_ptrs", None)
-    if cached is not None and cached[0] == engine._id:
-        return cached[1], cached[2]
+    if cached is not None and cached.eid == engine._id:
+        return cached.level, cached.ptrs
     for c in cem.cts:
         engine._check(c)
     lv = min(c.level for c in cem.cts)
     ptrs = None
     if all(c.level == lv for c in cem.cts):
         ptrs = [c.ptr() for c in cem.cts]
-        object.__setattr__(cem, "_vr_ptrs", (engine._id, lv, ptrs, _lib.ptr_array(ptrs), max(c.depth for c in cem.cts),
-                                             _storages(cem.cts)))
+        object.__setattr__(cem, "_vr_ptrs", _OperandCache(engine._id, lv, max(c.depth for c in cem.cts), _storages(cem.cts),
+                                                          ptrs=ptrs))
     return lv, ptrs
 
 
 def _fast_operand(engine: CkksEngine, cem: ColumnEncodedMatrix):
-    """(level, ctypes pointer array, max depth, storage tensors) from the cache, or None."""
+    """The operand's validated cache (level, arr, depth, storages) for this engine, or None."""
     cached = getattr(cem, "_vr_ptrs", None)
-    if cached is not None and cached[0] == engine._id:
-        return cached[1], cached[3], cached[4], cached[5]
+    if cached is not None and cached.eid == engine._id:
+        return cached
     return None
 
 
@@ -180,9 +219,9 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
         # steady state (operands already validated once): cached pointer arrays, no per-call scans
         fl, fr = _fast_operand(engine, lefts[0]), _fast_operand(engine, right)
         lf = lefts[0]
-        if (fl is not None and fr is not None and fl[0] == fr[0] and fl[0] >= 1 and lf.role == "left"
+        if (fl is not None and fr is not None and fl.level == fr.level and fl.level >= 1 and lf.role == "left"
                 and right.role == "right" and lf.n == n and lf.p == right.p):
-            lv = fl[0]
+            lv = fl.level
             pending = None
             if engine.async_drivers:
                 # asynchronous: the product runs on a library slot stream, overlapping the next calls.
@@ -195,22 +234,22 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
                 ext = engine._ext_stream(slot.value)
                 with torch.cuda.stream(ext):
                     outs = torch.empty((1, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
-                _lib.check(engine._lib.vr_matmul_outer_async(h, fl[1], fr[1], n, 1, lv, _lib.row_ptrs(outs, 1),
+                _lib.check(engine._lib.vr_matmul_outer_async(h, fl.arr, fr.arr, n, 1, lv, _lib.row_ptrs(outs, 1),
                                                              ctypes.byref(slot)))
                 if slot.value:
                     pending = ext
-                    fl[3].record(pending, slot.value)
-                    fr[3].record(pending, slot.value)
+                    fl.storages.record(pending, slot.value)
+                    fr.storages.record(pending, slot.value)
                 else:  # ran synchronously on the current stream
                     outs.record_stream(torch.cuda.current_stream(engine.device))
             else:
                 outs = torch.empty((1, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
-                _lib.check(engine._lib.vr_matmul_outer(engine.handle, fl[1], fr[1], n, 1, lv, _lib.row_ptrs(outs, 1)))
-            depth = max(fl[2], fr[2]) + 1
+                _lib.check(engine._lib.vr_matmul_outer(engine.handle, fl.arr, fr.arr, n, 1, lv, _lib.row_ptrs(outs, 1)))
+            depth = max(fl.depth, fr.depth) + 1
             engine._meter.mul_count += n
             engine._meter.add_count += n - 1
             engine._observe(depth)
-            ct = Ciphertext.at(outs, 0, lv - 1, engine.scales[lv - 1], depth, lf.cts[0].layout, engine._id)
+            ct = Ciphertext.at(outs, 0, lv - 1, engine.scales[lv - 1], depth, _layout0(lf.cts), engine._id)
             ct._pending = pending
             return [ct]
     for lf in lefts:
@@ -241,7 +280,7 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
         engine._meter.mul_count += n
         engine._meter.add_count += n - 1
         engine._observe(depth)
-        res.append(Ciphertext.at(outs, b, lv - 1, engine.scales[lv - 1], depth, lf.cts[0].layout, engine._id))
+        res.append(Ciphertext.at(outs, b, lv - 1, engine.scales[lv - 1], depth, _layout0(lf.cts), engine._id))
     return res
 
 

@@ -7,7 +7,7 @@ a, b = cfg_matmul(2)
 eng = CkksEngine(config_params(2))
 pa, pb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
 pc = time.perf_counter
-for depth in (1, 2, 3, 4, 8):
+for depth in (2, 3, 4):
     acc = {k: 0.0 for k in ("encL", "encR", "matmul", "decode_async", "result")}
     def run(k, rec):
         futs = []

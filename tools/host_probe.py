@@ -35,7 +35,7 @@ outs = torch.empty((1, 2, eng.L, eng.N), dtype=torch.int64, device="cuda")
 op = _lib.row_ptrs(outs, 1)
 slot = ctypes.c_void_p()
 h = eng.handle
-print(f"vr_matmul_outer_async alone: {burst(lambda: eng._lib.vr_matmul_outer_async(h, fl[1], fr[1], 64, 1, eng.L, op, ctypes.byref(slot))):.1f} us/call")
+print(f"vr_matmul_outer_async alone: {burst(lambda: eng._lib.vr_matmul_outer_async(h, fl.arr, fr.arr, 64, 1, eng.L, op, ctypes.byref(slot))):.1f} us/call")
 print(f"torch.empty: {burst(lambda: torch.empty((1, 2, eng.L, eng.N), dtype=torch.int64, device='cuda')):.1f} us/call")
 print(f"engine.handle: {burst(lambda: eng.handle):.1f} us/call")
 pr = cProfile.Profile()
