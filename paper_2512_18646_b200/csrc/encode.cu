@@ -453,28 +453,45 @@ struct LdSymEnc {
     int nl, N;
     uint64_t f64mask;
     const uint64_t *kshift;
-    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int pidx) const {
-        const int64_t v = m[(long long)(t / nl) * N + E];
-        if (((f64mask >> pidx) & 1ull) && v > -(1ll << 47) && v < (1ll << 47)) return (uint64_t)(v + (int64_t)kshift[pidx]);
-        return from_i64(v, pr.m[pidx]);
+    struct Prep {
+        const int64_t *m;
+        int64_t ks;  // < 0: the integer body (always reduce)
+        Modulus mod;
+    };
+    __device__ __forceinline__ Prep prep(int t, const DevPrimes &pr, int pidx) const {
+        Prep p;
+        p.m = m + (long long)(t / nl) * N;
+        p.ks = ((f64mask >> pidx) & 1ull) ? (int64_t)kshift[pidx] : -1;
+        p.mod = pr.m[pidx];
+        return p;
+    }
+    __device__ __forceinline__ uint64_t load(const Prep &p, long long E) const {
+        const int64_t v = p.m[E];
+        if (p.ks >= 0 && v > -(1ll << 47) && v < (1ll << 47)) return (uint64_t)(v + p.ks);
+        return from_i64(v, p.mod);
     }
 };
 struct StSymEnc {
     const uint64_t *s_ntt, *s_sh, *keys;
     int nl, N;
     struct Pre {
-        uint64_t s, s_sh, key;
+        uint64_t s, s_sh;
     };
-    __device__ __forceinline__ Pre prefetch(int t, long long E, const DevPrimes &, int) const {
-        const long long o = (long long)(t % nl) * N + E;
-        return Pre{s_ntt[o], s_sh[o], keys[t]};
+    struct Ctx {
+        const uint64_t *s, *s_sh;
+        uint64_t *c0;
+        uint64_t key, q;
+        long long c1_off;
+    };
+    __device__ __forceinline__ Ctx ctx(uint64_t *ptr, int t, const DevPrimes &pr, int pidx) const {
+        const long long o = (long long)(t % nl) * N;
+        return Ctx{s_ntt + o, s_sh + o, ptr, keys[t], pr.m[pidx].q, (long long)nl * N};
     }
-    __device__ __forceinline__ void finish(uint64_t *ptr, int, long long E, uint64_t v, const Pre &p, const DevPrimes &pr,
-                                           int pidx) const {
-        const uint64_t q = pr.m[pidx].q;
-        const uint64_t a = sample_uniform(rnd(p.key, (uint64_t)E), q);
-        ptr[E] = sub_mod(v, mul_shoup(a, p.s, p.s_sh, q), q);
-        ptr[(long long)nl * N + E] = a;
+    __device__ __forceinline__ Pre prefetch(const Ctx &c, long long E) const { return Pre{c.s[E], c.s_sh[E]}; }
+    __device__ __forceinline__ void finish(const Ctx &c, long long E, uint64_t v, const Pre &p) const {
+        const uint64_t a = sample_uniform(rnd(c.key, (uint64_t)E), c.q);
+        c.c0[E] = sub_mod(v, mul_shoup(a, p.s, p.s_sh, c.q), c.q);
+        c.c0[c.c1_off + E] = a;
     }
 };
 

@@ -158,18 +158,35 @@ struct LdCrt {
     const uint64_t *Y;
     const uint64_t *rr;
     int level, N;
-    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int pidx) const {
+    struct Prep {
+        const uint64_t *yq, *yp;
+        Modulus mq, m;
+        uint64_t c2, c3, r0, r1, r2, phalf, half_q;
+    };
+    __device__ __forceinline__ Prep prep(int t, const DevPrimes &pr, int pidx) const {
         const int cb = t / level, i = t - cb * level;
-        const Modulus &mq = pr.m[level];
-        const uint64_t yq = Y[((long long)cb * 2) * N + E], yp = Y[((long long)cb * 2 + 1) * N + E];
-        const uint64_t ql = mq.q;
-        const uint64_t tq = mul_shoup(sub_mod(yq, reduce64(yp, mq), ql), rr[MAXP * 8 + 2], rr[MAXP * 8 + 3], ql);
-        const Modulus &m = pr.m[pidx];
-        uint64_t v = add_mod(reduce64(yp, m), mul_shoup(reduce64(tq, m), rr[i * 8 + 0], rr[i * 8 + 1], m.q), m.q);
-        const uint64_t half_q = (ql - 1) >> 1;
-        const bool neg = tq > half_q || (tq == half_q && yp > (rr[MAXP * 8 + 4] >> 1));
-        if (neg) v = sub_mod(v, rr[i * 8 + 2], m.q);
-        return v;
+        Prep p;
+        p.yq = Y + ((long long)cb * 2) * N;
+        p.yp = p.yq + N;
+        p.mq = pr.m[level];
+        p.m = pr.m[pidx];
+        p.c2 = rr[MAXP * 8 + 2];
+        p.c3 = rr[MAXP * 8 + 3];
+        p.r0 = rr[i * 8 + 0];
+        p.r1 = rr[i * 8 + 1];
+        p.r2 = rr[i * 8 + 2];
+        p.phalf = rr[MAXP * 8 + 4] >> 1;
+        p.half_q = (p.mq.q - 1) >> 1;
+        return p;
+    }
+    __device__ __forceinline__ uint64_t load(const Prep &p, long long E) const {
+        const uint64_t yq = p.yq[E], yp = p.yp[E];
+        const uint64_t ql = p.mq.q;
+        const uint64_t tq = mul_shoup(sub_mod(yq, reduce64(yp, p.mq), ql), p.c2, p.c3, ql);
+        uint64_t v = add_mod(reduce64(yp, p.m), mul_shoup(reduce64(tq, p.m), p.r0, p.r1, p.m.q), p.m.q);
+        const bool neg = tq > p.half_q || (tq == p.half_q && yp > p.phalf);
+        const uint64_t w = sub_mod(v, p.r2, p.m.q);
+        return neg ? w : v;
     }
 };
 // out[c][b][i] = (P d_b[i] + acc_b[i] - z) * (P q_l)^-1 mod q_i   (t = (c*2+b) * level + i)
@@ -182,19 +199,28 @@ struct StRelinRescale {
     struct Pre {
         uint64_t a, d;
     };
-    __device__ __forceinline__ Pre prefetch(int t, long long E, const DevPrimes &, int) const {
+    struct Ctx {
+        const uint64_t *a, *d;
+        uint64_t *o;
+        uint64_t r0, r1, r3, r4, q;
+    };
+    __device__ __forceinline__ Ctx ctx(uint64_t *, int t, const DevPrimes &pr, int pidx) const {
         const int cb = t / level, i = t - cb * level, c = cb >> 1, b = cb & 1;
-        Pre p;
-        p.a = A[((long long)cb * nt + i) * N + E];
-        p.d = D3[c][((long long)b * (level + 1) + i) * N + E];
-        return p;
+        Ctx x;
+        x.a = A + ((long long)cb * nt + i) * N;
+        x.d = D3[c] + ((long long)b * (level + 1) + i) * N;
+        x.o = O[c] + ((long long)b * level + i) * N;
+        x.r0 = rr[i * 8 + 0];
+        x.r1 = rr[i * 8 + 1];
+        x.r3 = rr[i * 8 + 3];
+        x.r4 = rr[i * 8 + 4];
+        x.q = pr.m[pidx].q;
+        return x;
     }
-    __device__ __forceinline__ void finish(uint64_t *, int t, long long E, uint64_t z, const Pre &p, const DevPrimes &pr,
-                                           int pidx) const {
-        const int cb = t / level, i = t - cb * level, c = cb >> 1, b = cb & 1;
-        const uint64_t q = pr.m[pidx].q;
-        const uint64_t x = add_mod(mul_shoup(p.d, rr[i * 8 + 0], rr[i * 8 + 1], q), p.a, q);
-        O[c][((long long)b * level + i) * N + E] = mul_shoup(sub_mod(x, z, q), rr[i * 8 + 3], rr[i * 8 + 4], q);
+    __device__ __forceinline__ Pre prefetch(const Ctx &x, long long E) const { return Pre{x.a[E], x.d[E]}; }
+    __device__ __forceinline__ void finish(const Ctx &x, long long E, uint64_t z, const Pre &p) const {
+        const uint64_t v = add_mod(mul_shoup(p.d, x.r0, x.r1, x.q), p.a, x.q);
+        x.o[E] = mul_shoup(sub_mod(v, z, x.q), x.r3, x.r4, x.q);
     }
 };
 

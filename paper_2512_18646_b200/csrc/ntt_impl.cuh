@@ -76,6 +76,51 @@ __device__ __forceinline__ void bf_inv(uint64_t &X, uint64_t &Y, ulonglong2 w, u
     X = t;
 }
 
+// ---- functor plumbing ---------------------------------------------------------
+// A Load functor is `uint64_t operator()(ptr, t, E, primes, pidx)`.  A functor whose per-element
+// work depends on the transform (row pointers, the source prime, constants behind integer divisions
+// of t) may instead expose `Prep prep(t, primes, pidx)` -- evaluated once per thread -- and
+// `uint64_t load(const Prep &, E)`: the element loads are then straight-line and issue together.
+// Store functors likewise: either prefetch(t, E, ..) / finish(ptr, t, E, v, pre, ..), or
+// `Ctx ctx(ptr, t, primes, pidx)` with prefetch(ctx, E) / finish(ctx, E, v, pre).
+struct NoPrep {};
+template <class F, class = void>
+struct has_prep : std::false_type {};
+template <class F>
+struct has_prep<F, std::void_t<typename F::Prep>> : std::true_type {};
+template <class F, class = void>
+struct has_ctx : std::false_type {};
+template <class F>
+struct has_ctx<F, std::void_t<typename F::Ctx>> : std::true_type {};
+
+template <class LD>
+__device__ __forceinline__ auto ld_prep(const LD &ld, int t, const DevPrimes &pr, int pidx) {
+    if constexpr (has_prep<LD>::value) return ld.prep(t, pr, pidx);
+    else return NoPrep{};
+}
+template <class LD, class P>
+__device__ __forceinline__ uint64_t ld_at(const LD &ld, const P &p, const uint64_t *ptr, int t, long long E,
+                                          const DevPrimes &pr, int pidx) {
+    if constexpr (has_prep<LD>::value) return ld.load(p, E);
+    else return ld(ptr, t, E, pr, pidx);
+}
+template <class ST>
+__device__ __forceinline__ auto st_ctx(const ST &st, uint64_t *ptr, int t, const DevPrimes &pr, int pidx) {
+    if constexpr (has_ctx<ST>::value) return st.ctx(ptr, t, pr, pidx);
+    else return NoPrep{};
+}
+template <class ST, class C>
+__device__ __forceinline__ typename ST::Pre st_pre(const ST &st, const C &c, int t, long long E, const DevPrimes &pr, int pidx) {
+    if constexpr (has_ctx<ST>::value) return st.prefetch(c, E);
+    else return st.prefetch(t, E, pr, pidx);
+}
+template <class ST, class C>
+__device__ __forceinline__ void st_fin(const ST &st, const C &c, uint64_t *ptr, int t, long long E, uint64_t v,
+                                       const typename ST::Pre &pre, const DevPrimes &pr, int pidx) {
+    if constexpr (has_ctx<ST>::value) st.finish(c, E, v, pre);
+    else st.finish(ptr, t, E, v, pre, pr, pidx);
+}
+
 // ---- load functors (first pass of a transform) -----------------------------
 struct LdPlain {
     __device__ __forceinline__ uint64_t operator()(const uint64_t *ptr, int, long long E, const DevPrimes &, int) const {
@@ -92,12 +137,34 @@ struct LdLift {
     int div, mod, from_fixed, N;
     uint64_t f64mask;
     const uint64_t *liftk;  // [MAXP][MAXP]
-    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &pr, int pidx) const {
+    struct Prep {
+        const uint64_t *row;
+        uint64_t from, half, k, q, r_hi;
+        bool fast;
+    };
+    __device__ __forceinline__ Prep prep(int t, const DevPrimes &pr, int pidx) const {
         const int row = t / div;
         const int fp = from_fixed >= 0 ? from_fixed : row % mod;
-        const uint64_t x = src[(long long)row * N + E], from = pr.m[fp].q;
-        if ((f64mask >> fp) & (f64mask >> pidx) & 1ull) return x > (from >> 1) ? x + liftk[fp * MAXP + pidx] : x;
-        return lift_centered(x, from, pr.m[pidx]);
+        Prep p;
+        p.row = src + (long long)row * N;
+        p.from = pr.m[fp].q;
+        p.half = p.from >> 1;
+        p.fast = ((f64mask >> fp) & (f64mask >> pidx) & 1ull) != 0;  // uniform over the CTA
+        p.k = liftk[fp * MAXP + pidx];
+        p.q = pr.m[pidx].q;
+        p.r_hi = pr.m[pidx].r_hi;
+        return p;
+    }
+    // branch-free lift_centered: reduce x or from - x once, negate afterwards
+    __device__ __forceinline__ uint64_t load(const Prep &p, long long E) const {
+        const uint64_t x = p.row[E];
+        const bool neg = x > p.half;
+        if (p.fast) return neg ? x + p.k : x;
+        const uint64_t y = neg ? p.from - x : x;
+        uint64_t r = y - mulhi64(y, p.r_hi) * p.q;
+        r = r >= p.q ? r - p.q : r;
+        r = r >= p.q ? r - p.q : r;
+        return neg ? (r ? p.q - r : 0) : r;
     }
 };
 // ptrs[t / div] + (t % div) * stride + off + E
@@ -105,10 +172,14 @@ struct LdGather {
     const uint64_t *const *ptrs;
     int div;
     long long stride, off;
-    __device__ __forceinline__ uint64_t operator()(const uint64_t *, int t, long long E, const DevPrimes &, int) const {
+    struct Prep {
+        const uint64_t *p;
+    };
+    __device__ __forceinline__ Prep prep(int t, const DevPrimes &, int) const {
         const int a = t / div;
-        return ptrs[a][(long long)(t - a * div) * stride + off + E];
+        return Prep{ptrs[a] + (long long)(t - a * div) * stride + off};
     }
+    __device__ __forceinline__ uint64_t load(const Prep &p, long long E) const { return p.p[E]; }
 };
 
 // ---- store functors (last pass) ------------------------------------------------
@@ -139,35 +210,50 @@ struct StCombine {
     struct Pre {
         uint64_t a, b;
     };
-    __device__ __forceinline__ Pre prefetch(int t, long long E, const DevPrimes &, int) const {
-        const int N = 1 << logN;
+    struct Ctx {
+        const uint64_t *a, *add;  // add == nullptr: nothing to add
+        uint64_t *o;
+        uint64_t inv, inv_sh, q;
+        uint32_t g;
+    };
+    __device__ __forceinline__ Ctx ctx(uint64_t *, int t, const DevPrimes &pr, int pidx) const {
+        const long long N = 1ll << logN;
         const int row = t / nout, i = t - row * nout;
         const int r0 = row / rdiv, r1 = row - r0 * rdiv;
-        Pre p;
-        p.a = A[r0][((long long)r1 * a_limbs + i) * N + E];
-        p.b = 0;
+        Ctx c;
+        c.a = A[r0] + ((long long)r1 * a_limbs + i) * N;
+        c.o = O[r0] + ((long long)r1 * nout + i) * N;
+        c.add = nullptr;
+        c.g = 1;
         if (add && r1 < add_polys) {
-            long long src = E;
             const int ra = r0 / add_div;
-            const uint32_t g = gs_rows ? gs_rows[r0 - ra * add_div] : this->g;
-            if (g != 1) {
+            c.g = gs_rows ? gs_rows[r0 - ra * add_div] : g;
+            c.add = add[ra] + ((long long)r1 * nout + i) * N;
+        }
+        c.inv = inv[2 * i];
+        c.inv_sh = inv[2 * i + 1];
+        c.q = pr.m[pidx].q;
+        return c;
+    }
+    __device__ __forceinline__ Pre prefetch(const Ctx &c, long long E) const {
+        Pre p;
+        p.a = c.a[E];
+        p.b = 0;
+        if (c.add) {
+            long long src = E;
+            if (c.g != 1) {
                 const uint32_t brk = __brev((uint32_t)E) >> (32 - logN);
-                const uint32_t e = ((2u * brk + 1u) * g) & ((2u << logN) - 1u);
+                const uint32_t e = ((2u * brk + 1u) * c.g) & ((2u << logN) - 1u);
                 src = (long long)(__brev((e - 1u) >> 1) >> (32 - logN));
             }
-            p.b = add[ra][((long long)r1 * nout + i) * N + src];
+            p.b = c.add[src];
         }
         return p;
     }
-    __device__ __forceinline__ void finish(uint64_t *, int t, long long E, uint64_t v, const Pre &p, const DevPrimes &pr,
-                                           int pidx) const {
-        const int N = 1 << logN;
-        const int row = t / nout, i = t - row * nout;
-        const int r0 = row / rdiv, r1 = row - r0 * rdiv;
-        const uint64_t q = pr.m[pidx].q;
-        uint64_t r = mul_shoup(sub_mod(p.a, v, q), inv[2 * i], inv[2 * i + 1], q);
-        if (add && r1 < add_polys) r = add_mod(r, p.b, q);
-        O[r0][((long long)r1 * nout + i) * N + E] = r;
+    __device__ __forceinline__ void finish(const Ctx &c, long long E, uint64_t v, const Pre &p) const {
+        uint64_t r = mul_shoup(sub_mod(p.a, v, c.q), c.inv, c.inv_sh, c.q);
+        if (c.add) r = add_mod(r, p.b, c.q);
+        c.o[E] = r;
     }
 };
 
@@ -333,6 +419,7 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
     const int tile = tile0 + j, hi = tile >> lo_bits, lo = tile & lomask;
     const long long ebase = ((long long)hi << (logN - s0)) | lo;
     V *smv = reinterpret_cast<V *>(sm);
+    const auto lprep = ld_prep(ld, t, pr, pidx);  // per-thread state of the fused load (dead after the loads)
 
     // element conversion at the pass boundaries
     auto in = [&](uint64_t u) -> V {
@@ -369,7 +456,7 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
             const int idx = own0 + r * wl;
             const int jj = idx >> LOGT, mid = idx & (T - 1);
             const int tl = tile0 + jj, h2 = tl >> lo_bits, lo2 = tl & lomask;
-            y[r] = in(ld(ptr, t, ((long long)h2 << (logN - s0)) | ((long long)mid << lo_bits) | lo2, pr, pidx));
+            y[r] = in(ld_at(ld, lprep, ptr, t, ((long long)h2 << (logN - s0)) | ((long long)mid << lo_bits) | lo2, pr, pidx));
         }
 #pragma unroll
         for (int r = 0; r < EPT; r++) {
@@ -394,7 +481,7 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
 #pragma unroll
         for (int e = 0; e < EPT; e++) {
             const int L = base[e >> R] | ((e & (E2 - 1)) << logd);
-            if (step == 0 && !STAGE_IN) x[e] = in(ld(ptr, t, ebase | ((long long)L << lo_bits), pr, pidx));
+            if (step == 0 && !STAGE_IN) x[e] = in(ld_at(ld, lprep, ptr, t, ebase | ((long long)L << lo_bits), pr, pidx));
             else x[e] = smv[sidx_off<COLS>(sb[e >> R], (e & (E2 - 1)) << logd, TPC)];
         }
         if constexpr (F64) {
@@ -409,17 +496,18 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
         const bool last_group = step == NG - 1;
         if (last_group && COLS) {
             // consecutive threads own consecutive columns -> coalesced direct stores
+            const auto sctx = st_ctx(st, ptr, t, pr, pidx);  // built here: not live across the transform
             typename ST::Pre pre[EPT];
 #pragma unroll
             for (int e = 0; e < EPT; e++) {
                 const int L = base[e >> R] + (e & (E2 - 1)) * d;
-                pre[e] = st.prefetch(t, ebase | ((long long)L << lo_bits), pr, pidx);
+                pre[e] = st_pre(st, sctx, t, ebase | ((long long)L << lo_bits), pr, pidx);
             }
 #pragma unroll
             for (int e = 0; e < EPT; e++) {
                 const int L = base[e >> R] + (e & (E2 - 1)) * d;
                 const uint64_t v = a.last ? out_final(x[e]) : (a.raw_out ? out_raw(x[e]) : out_final(x[e]));
-                st.finish(ptr, t, ebase | ((long long)L << lo_bits), v, pre[e], pr, pidx);
+                st_fin(st, sctx, ptr, t, ebase | ((long long)L << lo_bits), v, pre[e], pr, pidx);
             }
             return;
         }
@@ -440,20 +528,21 @@ __device__ __forceinline__ void ntt_pass_body(const NttBatch &b, const PassArgs 
     // rows: coalesced store out of shared memory, each warp its own block (prefetch the epilogue's loads first)
     long long Es[EPT];
     typename ST::Pre pre[EPT];
+    const auto sctx = st_ctx(st, ptr, t, pr, pidx);
 #pragma unroll
     for (int r = 0; r < EPT; r++) {  // blockDim.x * EPT == TPC * T
         const int idx = own0 + r * wl;
         const int jj = idx >> LOGT, mid = idx & (T - 1);
         const int tl = tile0 + jj, h2 = tl >> lo_bits, lo2 = tl & lomask;
         Es[r] = ((long long)h2 << (logN - s0)) | ((long long)mid << lo_bits) | lo2;
-        pre[r] = st.prefetch(t, Es[r], pr, pidx);
+        pre[r] = st_pre(st, sctx, t, Es[r], pr, pidx);
     }
 #pragma unroll
     for (int r = 0; r < EPT; r++) {
         const int idx = own0 + r * wl;
         const int jj = idx >> LOGT, mid = idx & (T - 1);
         const V v = smv[sidx<COLS>(jj, mid, T, TPC)];
-        st.finish(ptr, t, Es[r], a.last ? out_final(v) : (a.raw_out ? out_raw(v) : out_final(v)), pre[r], pr, pidx);
+        st_fin(st, sctx, ptr, t, Es[r], a.last ? out_final(v) : (a.raw_out ? out_raw(v) : out_final(v)), pre[r], pr, pidx);
     }
 }
 
@@ -522,7 +611,9 @@ __global__ void ntt_tiny(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *_
     const uint64_t q = pr.m[pidx].q;
     const ulonglong2 *w = tw + (size_t)pidx * N;
     uint64_t a[4];
-    for (int k = 0; k < N; k++) a[k] = ld(ptr, t, k, pr, pidx);
+    const auto lprep = ld_prep(ld, t, pr, pidx);
+    const auto sctx = st_ctx(st, ptr, t, pr, pidx);
+    for (int k = 0; k < N; k++) a[k] = ld_at(ld, lprep, ptr, t, k, pr, pidx);
     if (!INV) {
         int tt = N;
         for (int m = 1; m < N; m <<= 1) {
@@ -549,7 +640,7 @@ __global__ void ntt_tiny(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *_
         const NttConst nc = ncs[pidx];
         for (int k = 0; k < N; k++) a[k] = mul_shoup(a[k], nc.ninv, nc.ninv_sh, q);
     }
-    for (int k = 0; k < N; k++) st.finish(ptr, t, k, a[k], st.prefetch(t, k, pr, pidx), pr, pidx);
+    for (int k = 0; k < N; k++) st_fin(st, sctx, ptr, t, k, a[k], st_pre(st, sctx, t, k, pr, pidx), pr, pidx);
 }
 
 template <bool INV, bool COLS, int LOGT, int LE, class LD, class ST>
@@ -658,6 +749,7 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
     V x[EPT];
     int base[EPT];
     const int zero_base[EPT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const auto lprep = ld_prep(ld, t, pr, pidx);  // per-thread state of the fused load (dead after the loads)
 
     auto in = [&](uint64_t u) -> V {
         if constexpr (F64) return u2d(u);
@@ -681,7 +773,7 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
             const int own0 = (sub >> 5) * (32 * EPT) + (sub & 31);
             V y[EPT];
 #pragma unroll
-            for (int k = 0; k < EPT; k++) y[k] = in(ld(ptr, t, (long long)r * C + own0 + 32 * k, pr, pidx));
+            for (int k = 0; k < EPT; k++) y[k] = in(ld_at(ld, lprep, ptr, t, (long long)r * C + own0 + 32 * k, pr, pidx));
 #pragma unroll
             for (int k = 0; k < EPT; k++) smv[sidx_row(own0 + 32 * k)] = y[k];
             __syncwarp();
@@ -719,7 +811,7 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
 
     if (!INV) {
 #pragma unroll
-        for (int u = 0; u < 8; u++) x[u] = in(ld(ptr, t, (long long)col + ((long long)u << LOGC), pr, pidx));
+        for (int u = 0; u < 8; u++) x[u] = in(ld_at(ld, lprep, ptr, t, (long long)col + ((long long)u << LOGC), pr, pidx));
         compute(std::integral_constant<int, 3>{}, 1, 0, 3, 0, 0, zero_base);
         asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer is resident (and its barrier set up)
         if (async_x) {
@@ -743,13 +835,14 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
         local_stages(false);
         // coalesced store of the chunk through the Store functor (prefetch its loads first)
         typename ST::Pre pre[EPT];
+        const auto sctx = st_ctx(st, ptr, t, pr, pidx);
         const int own0 = (sub >> 5) * (32 * EPT) + (sub & 31);  // each warp stores the block it owns
 #pragma unroll
-        for (int k = 0; k < EPT; k++) pre[k] = st.prefetch(t, (long long)r * C + own0 + 32 * k, pr, pidx);
+        for (int k = 0; k < EPT; k++) pre[k] = st_pre(st, sctx, t, (long long)r * C + own0 + 32 * k, pr, pidx);
 #pragma unroll
         for (int k = 0; k < EPT; k++) {
             const int mid = own0 + 32 * k;
-            st.finish(ptr, t, (long long)r * C + mid, final_value(smv[sidx_row(mid)]), pre[k], pr, pidx);
+            st_fin(st, sctx, ptr, t, (long long)r * C + mid, final_value(smv[sidx_row(mid)]), pre[k], pr, pidx);
         }
     } else {
         local_stages(true);
@@ -781,11 +874,12 @@ __device__ __forceinline__ void ntt_cl8_body(int logN, const DevPrimes &pr, cons
         }
         compute(std::integral_constant<int, 3>{}, 1, 0, 3, 0, 0, zero_base);
         typename ST::Pre pre[EPT];
+        const auto sctx = st_ctx(st, ptr, t, pr, pidx);
 #pragma unroll
-        for (int u = 0; u < 8; u++) pre[u] = st.prefetch(t, (long long)col + ((long long)u << LOGC), pr, pidx);
+        for (int u = 0; u < 8; u++) pre[u] = st_pre(st, sctx, t, (long long)col + ((long long)u << LOGC), pr, pidx);
 #pragma unroll
         for (int u = 0; u < 8; u++)
-            st.finish(ptr, t, (long long)col + ((long long)u << LOGC), final_value(x[u]), pre[u], pr, pidx);
+            st_fin(st, sctx, ptr, t, (long long)col + ((long long)u << LOGC), final_value(x[u]), pre[u], pr, pidx);
         if (!async_x) cluster.sync();  // peers keep their shared memory until every gather has finished
     }
 }
