@@ -891,6 +891,12 @@ __global__ void __launch_bounds__(64 * KG)
     u128 acc[3][2];
 #pragma unroll
     for (int p = 0; p < 3; p++) acc[p][0] = acc[p][1] = u128{0, 0};
+    // Lazy accumulation: with q < 2^b a d0/d2 term is < 2^(2b) and a Karatsuba term < 2^(2b+2), so
+    // 2^(128-2b) resp. 2^(126-2b) terms (plus a folded remainder < q) fit 128 bits.  A 60-bit limb
+    // folds d1 every 64 steps and d0, d2 every 256; limbs below 2^54 never fold inside a k range --
+    // the per-thread ranges of configs 2 and 5a (16 and 64 steps) run as pure multiply-accumulates.
+    const int qb = 64 - __clzll((long long)m.q);
+    const unsigned mask1 = (1u << max(0, min(20, 126 - 2 * qb))) - 1u, mask02 = (1u << max(0, min(20, 128 - 2 * qb))) - 1u;
     if (live && kb < ke) {
         ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(L[kb] + o0), l1 = *reinterpret_cast<const ulonglong2 *>(L[kb] + o1);
         ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R[kb] + o0), r1 = *reinterpret_cast<const ulonglong2 *>(R[kb] + o1);
@@ -909,11 +915,16 @@ __global__ void __launch_bounds__(64 * KG)
             mac_to(acc[2][1], l1.y, r1.y);
             mac_to(acc[1][0], l0.x + l1.x, r0.x + r1.x);
             mac_to(acc[1][1], l0.y + l1.y, r0.y + r1.y);
-            if ((it & 7) == 7) {
+            if (((unsigned)it & mask1) == mask1) {
 #pragma unroll
-                for (int p = 0; p < 3; p++)
+                for (int e = 0; e < 2; e++) acc[1][e] = u128{reduce128(acc[1][e], m), 0};
+                if (((unsigned)it & mask02) == mask02) {
 #pragma unroll
-                    for (int e = 0; e < 2; e++) acc[p][e] = u128{reduce128(acc[p][e], m), 0};
+                    for (int e = 0; e < 2; e++) {
+                        acc[0][e] = u128{reduce128(acc[0][e], m), 0};
+                        acc[2][e] = u128{reduce128(acc[2][e], m), 0};
+                    }
+                }
             }
             l0 = nl0;
             l1 = nl1;
