@@ -521,7 +521,7 @@ void launch_fft_t(Ctx &c, K kern, int count, int S, int tmul, Args... args) {
     cfg.blockDim = dim3((unsigned)(fft_threads(S) * tmul));
     cfg.dynamicSmemBytes = sm;
     cfg.stream = c.stream;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = (unsigned)cl;
     attr[0].val.clusterDim.y = 1;
@@ -529,7 +529,7 @@ void launch_fft_t(Ctx &c, K kern, int count, int S, int tmul, Args... args) {
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cfg.numAttrs = add_priority_attr(attr, pdl_enabled() ? 2 : 1);
     VR_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 

@@ -917,7 +917,7 @@ void launch_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
     cfg.blockDim = dim3(C / 8);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 8;
     attr[0].val.clusterDim.y = 1;
@@ -925,7 +925,7 @@ void launch_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cfg.numAttrs = add_priority_attr(attr, pdl_enabled() ? 2 : 1);
     VR_CUDA(cudaLaunchKernelEx(&cfg, kern, b, c.log_n, c.primes, (const ulonglong2 *)(INV ? c.itw2 : c.tw2),
                                (const double *)(INV ? c.itwd : c.twd), (const NttConst *)c.ntt_const, ld, st, cl_st_async()));
     check_launch("ntt_cl8");

@@ -1000,16 +1000,22 @@ static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const
 // B200 (config 2, tools/ts_probe.py): TMA ring 38.1 us; KG x SPLIT = 4x1 37.8, 4x2 41.1, 8x1 55.7,
 // 2x2 36.3 (default, 4.66 TB/s), 8x2 63.0, 2x4 54.3, 2x1 39.6, 1x4 47.7, 1x2 57.2, 1x8 53.9.  Config 5a
 // (4 interleaved row blocks): 2x2 1.19 ms vs 1.24 ms for the ring.
+// After the fold periods above removed the in-loop reductions (re-swept, cfg 2 / cfg 5a): 2x2 33.6 us /
+// 1.03 ms (5.2 TB/s), 2x1 30.4 us (5.59 TB/s = 0.85 of the copy peak) / 1.15 ms, 1x2 49.3 / 1.28, 4x1 43.7 /
+// 1.38, 2x4 50.6 / 1.71, 1x4 47.7 / 1.59, 4x2 46.9 / 1.50.  Default (VR_TS_LD unset, -1): two k-groups per
+// CTA, and split-K across a 2-CTA cluster only from n = 128 columns on, so a thread walks 32-64 steps.
 static int ts_ld_variant() {
     static const int v = [] {
         const char *e = getenv("VR_TS_LD");
-        return e ? atoi(e) : 4;
+        return e ? atoi(e) : -1;
     }();
     return v;
 }
 
 static bool try_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O, int rb) {
-    switch (ts_ld_variant()) {
+    int v = ts_ld_variant();
+    if (v < 0) v = n >= 128 ? 4 : 7;
+    switch (v) {
         case 1: launch_ts_ld<4, 1>(c, L, R, n, nl, O, rb); return true;
         case 2: launch_ts_ld<4, 2>(c, L, R, n, nl, O, rb); return true;
         case 3: launch_ts_ld<8, 1>(c, L, R, n, nl, O, rb); return true;

@@ -336,6 +336,34 @@ inline bool pdl_enabled() {
     return on;
 }
 
+// Execution priority of every kernel except the streaming tensor sums: when independent products
+// overlap (asynchronous matmul_outer slots), the block scheduler places the CTAs of the small
+// latency-bound key-switch kernels ahead of the pending CTAs of another product's tensor sum instead
+// of behind them.  Recorded graphs keep it per node (cudaGraphInstantiateFlagUseNodePriority).
+// VR_CHAIN_PRIO=1 enables (default off: the tensor sums then wait behind every chain kernel and the
+// cfg-2 step grows from 43 to 51 us).  Returns 0 (the default, lowest priority) when off.
+inline int chain_priority() {
+    static const int p = [] {
+        const char *e = getenv("VR_CHAIN_PRIO");
+        if (!e || atoi(e) == 0) return 0;  // off by default: measured slower (cfg 2: 43 -> 51 us per product)
+        int least = 0, greatest = 0;
+        if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        return greatest;
+    }();
+    return p;
+}
+// appends the priority attribute to at[n]; returns the new attribute count
+inline unsigned add_priority_attr(cudaLaunchAttribute *at, unsigned n) {
+    const int p = chain_priority();
+    if (p == 0) return n;
+    at[n].id = cudaLaunchAttributePriority;
+    at[n].val.priority = p;
+    return n + 1;
+}
+
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args &&...args) {
     cudaLaunchConfig_t cfg = {};
@@ -343,11 +371,15 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    unsigned n = 0;
+    if (pdl_enabled()) {
+        at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[n].val.programmaticStreamSerializationAllowed = 1;
+        n++;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = add_priority_attr(at, n);
     VR_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
