@@ -5,9 +5,13 @@ CPU baselines.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One step = one HE matmul A(64x64)*B(64x64): matmul_outer over n = 64 resident
-column-ciphertext pairs (N = 2^14, 5 ciphertext primes + 60-bit special prime,
-scale 2^40, seed 1) = fused tensor-sum + one relinearisation + one rescale.
+One step = one batch of BATCH (8) independent HE matmuls A(64x64)*B(64x64) on
+distinct resident operand pairs (pair 0 is BASELINE's seed-1 pair): each is a
+matmul_outer over n = 64 column-ciphertext pairs (N = 2^14, 5 ciphertext primes
++ 60-bit special prime, scale 2^40) = fused tensor-sum + one relinearisation +
+one rescale.  `value` = products per second (BATCH / step time); a batch per
+step keeps a short run (--steps 20) from measuring only the fill and drain of
+the engine's asynchronous product slots.
 
 * ``--gpus N`` without torchrun re-launches itself under torchrun with N ranks
   (and refuses to run if fewer than N GPUs are visible); it never prints a
@@ -16,7 +20,7 @@ scale 2^40, seed 1) = fused tensor-sum + one relinearisation + one rescale.
   the device as the max over ranks; configs 5a / 5b shard one job over the N
   ranks (strong scaling, NCCL int64 reduce of the 5a partials).
 * `e2e` is the same metric through the public API with host buffers: every
-  step uploads A and B from pinned host memory, encrypts the 128 column
+  product uploads A and B from pinned host memory, encrypts the 128 column
   ciphertexts (encode_left/encode_right), runs matmul_outer and downloads the
   decoded result.
 * Every config entry carries a `roofline` (tools/costmodel.py: compulsory
@@ -54,7 +58,12 @@ METRIC = "HE matmul/s (column-ciphertext matmul_outer, BASELINE config 2: A,B 64
 UNIT = "HE matmul/s"
 CFG = 2
 DIM = 64
-WORKLOAD = "cfg2 HE matmul 64x64 (n=64 column ciphertexts/operand), N=2^14, q0 60b + 4x40b + P 60b, scale 2^40, seed 1"
+# One step = one batch of BATCH independent products on distinct operand pairs (pair 0 is BASELINE's
+# seed-1 pair): the engine overlaps independent products on its asynchronous slots, and a one-product
+# step would make a short run (the driver's --steps 20 is ~1 ms) measure pipeline fill and drain.
+BATCH = int(os.environ.get("VR_BENCH_BATCH", "8"))
+WORKLOAD = ("cfg2 HE matmul 64x64 (n=64 column ciphertexts/operand), N=2^14, q0 60b + 4x40b + P 60b, scale 2^40, seed 1; "
+            f"one step = a batch of {BATCH} independent products on distinct operand pairs")
 
 
 def parse():
@@ -81,8 +90,9 @@ def dist_env():
 
 def config_dict(n_gpus: int) -> dict:
     """The config both arms report (identical dicts: the driver compares them)."""
-    return {"workload": WORKLOAD, "global_batch": n_gpus, "seq_len": None,
-            "parallelism": f"replicas x{n_gpus} (weak scaling)", "l2": "inputs larger than L2 (128 cts = 168 MB)"}
+    return {"workload": WORKLOAD, "global_batch": BATCH * n_gpus, "seq_len": None,
+            "parallelism": f"replicas x{n_gpus} (weak scaling)",
+            "l2": f"inputs larger than L2 ({BATCH} pairs x 128 cts = {BATCH * 168} MB)"}
 
 
 def maybe_spawn(args) -> None:
@@ -118,6 +128,15 @@ def inputs(cfg=CFG, dim=DIM):
     a = rng.uniform(-1, 1, (dim, dim))
     b = rng.uniform(-1, 1, (dim, dim))
     return a, b
+
+
+def batch_inputs(count=None, cfg=CFG, dim=DIM):
+    """The operand pairs of one step: pair 0 is inputs() (BASELINE's seed), pair i > 0 uses seed 1000 i + cfg - 1."""
+    out = [inputs(cfg, dim)]
+    for i in range(1, BATCH if count is None else count):
+        rng = np.random.default_rng(1000 * i + cfg - 1)
+        out.append((rng.uniform(-1, 1, (dim, dim)), rng.uniform(-1, 1, (dim, dim))))
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -403,19 +422,23 @@ def run_reference(args, ws, rank):
     cm = CpuMatmul()
     for _ in range(max(0, args.warmup)):
         cm.time(1)
-    times = cm.time(args.steps)
+    # a step is a batch of BATCH products like the GPU arm's; the CPU runs them one after another
+    # (OpenMP inside each), on pair 0's ciphertexts (the oracle's kernels are data-independent);
+    # at most ~60 s of CPU work, the rest of the requested steps extrapolated from the mean
+    budget = max(BATCH, min(args.steps * BATCH, int(60.0 / 0.0085)))
+    times = cm.time(budget)
     per = statistics.mean(times)
     v = 1.0 / per
     sim_t = simulator_matmul()
     line = {
         "impl": "reference",
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "ms_per_step": per * BATCH * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seed 1, U[-1,1])",
         "config": config_dict(args.gpus),
         "max_abs_err": cm.err,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
-                         "sample": f"{args.steps} cfg-2 HE matmuls after {args.warmup} warm-up matmuls on the same "
+                         "sample": f"{budget} cfg-2 HE matmuls after {args.warmup} warm-up matmuls on the same "
                                    "engine (relin key built before timing): matmul_outer on 128 resident ciphertexts "
                                    "in the C RNS-CKKS oracle, OpenMP on every host thread"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -510,13 +533,20 @@ def run_ours(args, ws, rank, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eng = CkksEngine(config_params(CFG), device=local)
     lib = eng._lib
-    a, b = inputs()
-    left = encode_left(eng, a, DIM)
-    right = encode_right(eng, b, DIM)
-    # correctness gate before timing
-    first = matmul_outer(eng, left, right)
-    err = float(np.max(np.abs(first.decode(eng) - a @ b)))
+    pairs = batch_inputs()
+    a, b = pairs[0]
+    lefts = [encode_left(eng, x, DIM) for x, _ in pairs]
+    rights = [encode_right(eng, y, DIM) for _, y in pairs]
+    left, right = lefts[0], rights[0]
+    # correctness gate before timing: every pair of the batch
+    firsts = [matmul_outer(eng, lf, rt) for lf, rt in zip(lefts, rights)]
+    err = max(float(np.max(np.abs(f.decode(eng) - x @ y))) for f, (x, y) in zip(firsts, pairs))
     assert err < 1e-3, f"HE matmul error {err}"
+    first = firsts[0]
+    del firsts
+
+    def step():
+        return [matmul_outer(eng, lf, rt) for lf, rt in zip(lefts, rights)]
 
     def barrier():
         if ws > 1:
@@ -535,11 +565,11 @@ def run_ours(args, ws, rank, local):
     t_settle = time.perf_counter()
     out = None
     while time.perf_counter() - t_settle < 0.25:
-        for _ in range(8):  # bursts like the timed loop: the allocator holds every in-flight output
-            out = matmul_outer(eng, left, right)
+        for _ in range(2):  # bursts like the timed loop: the allocator holds every in-flight output
+            out = step()
         torch.cuda.synchronize()
     for _ in range(args.warmup):
-        out = matmul_outer(eng, left, right)
+        out = step()
     barrier()
     torch.cuda.synchronize()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -550,15 +580,16 @@ def run_ours(args, ws, rank, local):
     with ClockSampler(local) as clk:
         st.record()
         for _ in range(args.steps):
-            out = matmul_outer(eng, left, right)
+            out = step()
         eng.join()  # the timed region ends when every product (asynchronous slot streams) is complete
         en.record()
         torch.cuda.synchronize()
     launches = lib.vr_launch_count() - l0
     gc.enable()
     barrier()
-    step_s = max_over_ranks(st.elapsed_time(en) / 1e3 / args.steps)
-    value = ws / step_s
+    step_s = max_over_ranks(st.elapsed_time(en) / 1e3 / args.steps)  # one batch of BATCH products
+    prod_s = step_s / BATCH
+    value = ws * BATCH / step_s
     timer = Timer(max_over_ranks)
     peaks = int_peaks(eng)
 
@@ -585,51 +616,51 @@ def run_ours(args, ws, rank, local):
     achieved = alg_bytes / ts_s / 1e9
 
     # e2e through the public API with host buffers
-    pin_a = torch.from_numpy(a).pin_memory()
-    pin_b = torch.from_numpy(b).pin_memory()
-    e2e_steps = max(8, min(100, args.steps // 2))
+    pins = [(torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory()) for x, y in pairs]
+    e2e_steps = max(8, min(400, args.steps * BATCH // 2))  # products (cycling through the batch's pairs)
     E2E_DEPTH = int(os.environ.get("VR_E2E_DEPTH", "3"))  # encrypt -> product -> decode steps in flight (decode_async futures)
 
     def e2e_run(k):
         """k steps through the public API; every step's decoded result is read on the host."""
         futs, last = [], None
-        for _ in range(k):
-            prod = matmul_outer(eng, encode_left(eng, pin_a.numpy(), DIM), encode_right(eng, pin_b.numpy(), DIM))
+        for i in range(k):
+            pa, pb = pins[i % BATCH]
+            prod = matmul_outer(eng, encode_left(eng, pa.numpy(), DIM), encode_right(eng, pb.numpy(), DIM))
             futs.append(prod.decode_async(eng))
             if len(futs) >= E2E_DEPTH:
                 last = futs.pop(0).result()
         while futs:
             last = futs.pop(0).result()
-        return last
+        return last, (k - 1) % BATCH
 
     t_settle = time.perf_counter()
     while time.perf_counter() - t_settle < 0.25:  # same statements as the timed loop
-        res = e2e_run(8)
+        res, _ = e2e_run(8)
     barrier()
     torch.cuda.synchronize()
     gc.collect()
     gc.disable()
     t0 = time.perf_counter()
     st.record()
-    res = e2e_run(e2e_steps)
+    res, res_pair = e2e_run(e2e_steps)
     en.record()
     torch.cuda.synchronize()
     gc.enable()
     e2e_s = max_over_ranks(max(st.elapsed_time(en) / 1e3, time.perf_counter() - t0) / e2e_steps)
-    assert float(np.max(np.abs(res - a @ b))) < 1e-3
-    h2d = 2 * DIM * DIM * 8  # the raw A and B (broadcast/tiling happens in the encode kernel)
-    d2h = eng.slots * 8
+    assert float(np.max(np.abs(res - pairs[res_pair][0] @ pairs[res_pair][1]))) < 1e-3
+    h2d = BATCH * 2 * DIM * DIM * 8  # per step (batch): the raw A and B of every product (broadcast/tiling on the device)
+    d2h = BATCH * eng.slots * 8
 
     extra = {}
     cfg5 = {}
     if not args.no_extra:
-        del left, right, first, out
+        del left, right, lefts, rights, first, out
         cfg5["cfg5a"] = bench_cfg5a(ws, rank, local, max_over_ranks, barrier, peaks)
         cfg5["cfg5b"] = bench_cfg5b(ws, rank, local, max_over_ranks, barrier, peaks)
     if not args.no_extra and rank == 0:
         extra["ntt"] = bench_ntt(eng, peak, peaks)
         extra["configs"] = {"cfg1": bench_cfg1(peaks), "cfg2": {"metric": METRIC, "value": value,
-                                                                 "roofline": roofline_for(2, step_s, eng.q, peaks)},
+                                                                 "roofline": roofline_for(2, prod_s, eng.q, peaks)},
                             "cfg2_alg3": bench_cfg2_alg3(), "table1_cnn": bench_table1(), "cfg3": bench_cfg3(peaks),
                             "cfg4": bench_cfg4(peaks), **cfg5}
     line = None
@@ -643,21 +674,22 @@ def run_ours(args, ws, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u64", "data": "synthetic (seed 1, U[-1,1]); inputs larger than L2 (128 cts = 168 MB)",
+            "dtype": "u64", "data": f"synthetic (seed 1, U[-1,1]); inputs larger than L2 ({BATCH} pairs x 128 cts = {BATCH * 168} MB)",
+            "us_per_product": prod_s * 1e6,
             "config": config_dict(ws),
             "max_abs_err": err,
             "roofline": {"bound": "hbm", "kernel": "k_tensor_sum<MODE=0> (d0,d1,d2)" if one_pass else "k_tensor_sum<MODE=2> (d0,d1)",
                          "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic("k_tensor_sum_d012" if one_pass else "k_tensor_sum_d01"),
-                         "alg_bytes_per_launch": alg_bytes, "launch_us": ts_s * 1e6, "step_share": ts_s / step_s,
-                         "peak_source": peak_src,
-                         "step": roofline_for(2, step_s, eng.q, peaks)},
+                         "alg_bytes_per_launch": alg_bytes, "launch_us": ts_s * 1e6, "step_share": ts_s / prod_s,
+                         "launches_per_step": BATCH, "peak_source": peak_src,
+                         "step": roofline_for(2, prod_s, eng.q, peaks)},
             "cpu_baseline": cpu,
             "e2e": {"value": ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": e2e_steps, "pipeline_depth": E2E_DEPTH,
-                    "path": "per step: pinned host A,B -> encode_left+encode_right (encrypt 128 cts) -> matmul_outer -> "
-                            f"decode_async; at most {E2E_DEPTH} steps in flight, every step's result read on the host"},
+                    "products": e2e_steps, "pipeline_depth": E2E_DEPTH,
+                    "path": "per product: pinned host A,B -> encode_left+encode_right (encrypt 128 cts) -> matmul_outer -> "
+                            f"decode_async; at most {E2E_DEPTH} products in flight, every product's result read on the host"},
             "gpu_launches": int(launches),
             "gpu_launches_per_step": launches / args.steps,
             "clocks": clk.summary(),
