@@ -283,7 +283,7 @@ int vr_ctx_create(int log_n, int num_q, const uint64_t *primes, uint64_t seed, i
             }();
             const int f64 = (f64_on && q < (1ull << 46)) ? 1 : 0;
             c.h_ntt_const[p] = vr::NttConst{ninv, h_shoup(ninv, q), w0n, h_shoup(w0n, q), (double)q, 1.0 / (double)q,
-                                            (double)ninv, (double)w0n, f64};
+                                            (double)ninv, (double)w0n, f64, (double)((1ull << 32) % q)};
         }
         std::vector<uint64_t> liftk((size_t)vr::MAXP * vr::MAXP, 0), kshift(vr::MAXP, 0);
         for (int a = 0; a < np; a++) kshift[a] = c.q[a] * (((1ull << 47) + c.q[a] - 1) / c.q[a]);

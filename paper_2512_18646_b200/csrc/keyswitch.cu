@@ -242,7 +242,7 @@ void rescale(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int count,
                       nttk::LdGather{In, polys, (long long)(level + 1) * N, (long long)level * N}, nttk::StPlain{});
     // out_i = (in_i - NTT_{q_i}(lift(y))) * q_l^-1
     nttk::StCombine st{In, Out, nullptr, c.inv_tab + (size_t)level * c.np * 2, level, polys, level + 1, 0, c.log_n, 1u};
-    ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), rows, level, N), nttk::LdLift{y.as<uint64_t>(), level, 1, level, N, c.f64mask, c.liftk}, st);
+    ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), rows, level, N), nttk::LdLift{y.as<uint64_t>(), level, 1, level, N, c.f64mask, c.liftk, c.ntt_const}, st);
 }
 
 // cl_intt: run the INTT of the digits as one cluster kernel whatever the batch size.  Measured on
@@ -265,7 +265,7 @@ static void modup_impl(Ctx &c, const uint64_t *const *Polys, long long poly_off,
         ntt_inverse_fused(c, batch_limbs(x.as<uint64_t>(), count, nl, N), nttk::LdGather{Polys, nl, (long long)N, poly_off},
                           nttk::StPlain{});
     ntt_forward_fused(c, NttBatch{D, count * nl * nt, nt, (long long)nt * N, nl, 0, c.np - 1, nl},
-                      nttk::LdLift{x.as<uint64_t>(), nt, nl, -1, N, c.f64mask, c.liftk}, nttk::StPlain{});
+                      nttk::LdLift{x.as<uint64_t>(), nt, nl, -1, N, c.f64mask, c.liftk, c.ntt_const}, nttk::StPlain{});
 }
 
 void modup(Ctx &c, const uint64_t *const *Polys, int count, int level, uint64_t *D) { modup_impl(c, Polys, 0, count, level, D); }
@@ -318,7 +318,7 @@ static void inner_moddown(Ctx &c, const uint64_t *D, const uint64_t *const *Poly
                       LdStrided{a.as<uint64_t>(), (long long)nt * N, (long long)nl * N}, nttk::StPlain{});
     PtrTable ta(c, strided_ptrs(a.as<uint64_t>(), count, (size_t)2 * nt * N));
     nttk::StCombine st{ta.c_(), Out, Add, c.inv_tab + (size_t)P * c.np * 2, nl, 2, nt, add_polys, c.log_n, g};
-    ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), rows, nl, N), nttk::LdLift{y.as<uint64_t>(), nl, 1, P, N, c.f64mask, c.liftk}, st);
+    ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), rows, nl, N), nttk::LdLift{y.as<uint64_t>(), nl, 1, P, N, c.f64mask, c.liftk, c.ntt_const}, st);
 }
 
 // inner_moddown for every rotation amount of a hoisted batch at once: one inner-product launch (grid z
@@ -338,7 +338,7 @@ static void inner_moddown_multi(Ctx &c, const uint64_t *D, const uint64_t *const
     nttk::StCombine st{ta.c_(), Out, Add, c.inv_tab + (size_t)P * c.np * 2, nl, 2, nt, add_polys, c.log_n, 1u};
     st.gs_rows = gs_r;
     st.add_div = nrot;
-    ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), rows, nl, N), nttk::LdLift{y.as<uint64_t>(), nl, 1, P, N, c.f64mask, c.liftk}, st);
+    ntt_forward_fused(c, batch_limbs(z.as<uint64_t>(), rows, nl, N), nttk::LdLift{y.as<uint64_t>(), nl, 1, P, N, c.f64mask, c.liftk, c.ntt_const}, st);
 }
 
 void keyswitch_poly(Ctx &c, const uint64_t *const *Polys, int count, int level, const uint64_t *key, uint64_t *const *Out) {

@@ -136,11 +136,18 @@ struct LdLift {
     const uint64_t *src;
     int div, mod, from_fixed, N;
     uint64_t f64mask;
-    const uint64_t *liftk;  // [MAXP][MAXP]
+    const uint64_t *liftk;  // [MAXP][MAXP]: q_dst ceil(q_src / q_dst) - q_src
+    const NttConst *ncs;
+    // mode 0: x + (neg ? k : 0) -- both primes on the FP64 body (any integer below 2^51 enters the
+    //         transform), or q_src <= q_dst (then k = q_dst - q_src and the result is canonical);
+    // mode 1: a 60-bit source into an FP64-body prime: x = xh 2^32 + xl == xh (2^32 mod q) + xl, the
+    //         product reduced on the FP64 pipe (|.| <= q), shifted by q to stay non-negative (< 2^51);
+    // mode 2: the integer centred lift (one Barrett reduction), branch-free.
     struct Prep {
         const uint64_t *row;
         uint64_t from, half, k, q, r_hi;
-        bool fast;
+        double qd, qinv, c32;
+        int mode;
     };
     __device__ __forceinline__ Prep prep(int t, const DevPrimes &pr, int pidx) const {
         const int row = t / div;
@@ -149,23 +156,22 @@ struct LdLift {
         p.row = src + (long long)row * N;
         p.from = pr.m[fp].q;
         p.half = p.from >> 1;
-        p.fast = ((f64mask >> fp) & (f64mask >> pidx) & 1ull) != 0;  // uniform over the CTA
         p.k = liftk[fp * MAXP + pidx];
         p.q = pr.m[pidx].q;
         p.r_hi = pr.m[pidx].r_hi;
+        const bool dst64 = (f64mask >> pidx) & 1ull;
+        p.mode = (((f64mask >> fp) & 1ull) && dst64) || p.from <= p.q ? 0 : (dst64 ? 1 : 2);  // uniform over the CTA
+        if (p.mode == 1) {
+            const NttConst nc = ncs[pidx];
+            p.qd = nc.qd;
+            p.qinv = nc.qinv;
+            p.c32 = nc.c32;
+        } else {
+            p.qd = p.qinv = p.c32 = 0.0;
+        }
         return p;
     }
-    // branch-free lift_centered: reduce x or from - x once, negate afterwards
-    __device__ __forceinline__ uint64_t load(const Prep &p, long long E) const {
-        const uint64_t x = p.row[E];
-        const bool neg = x > p.half;
-        if (p.fast) return neg ? x + p.k : x;
-        const uint64_t y = neg ? p.from - x : x;
-        uint64_t r = y - mulhi64(y, p.r_hi) * p.q;
-        r = r >= p.q ? r - p.q : r;
-        r = r >= p.q ? r - p.q : r;
-        return neg ? (r ? p.q - r : 0) : r;
-    }
+    __device__ __forceinline__ uint64_t load(const Prep &p, long long E) const;
 };
 // ptrs[t / div] + (t % div) * stride + off + E
 struct LdGather {
@@ -339,6 +345,22 @@ __device__ __forceinline__ uint64_t canon_f(double x, double q, double qinv) {
     double r = fold_f(x, q, qinv);
     r = r < 0.0 ? __dadd_rn(r, q) : r;
     return d2u(r);
+}
+
+__device__ __forceinline__ uint64_t LdLift::load(const Prep &p, long long E) const {
+    const uint64_t x = p.row[E];
+    const bool neg = x > p.half;
+    if (p.mode == 0) return neg ? x + p.k : x;
+    if (p.mode == 1) {
+        const double hi = mulmod_f(u2d(x >> 32), p.c32, p.qd, p.qinv);
+        const double lo = __dadd_rn(u2d(x & 0xffffffffull), neg ? u2d(p.k) : 0.0);
+        return d2u(__dadd_rn(__dadd_rn(hi, lo), p.qd));
+    }
+    const uint64_t y = neg ? p.from - x : x;
+    uint64_t r = y - mulhi64(y, p.r_hi) * p.q;
+    r = r >= p.q ? r - p.q : r;
+    r = r >= p.q ? r - p.q : r;
+    return neg ? (r ? p.q - r : 0) : r;
 }
 
 template <bool INV, int R, int EPT>
@@ -613,7 +635,8 @@ __global__ void ntt_tiny(NttBatch b, int logN, DevPrimes pr, const ulonglong2 *_
     uint64_t a[4];
     const auto lprep = ld_prep(ld, t, pr, pidx);
     const auto sctx = st_ctx(st, ptr, t, pr, pidx);
-    for (int k = 0; k < N; k++) a[k] = ld_at(ld, lprep, ptr, t, k, pr, pidx);
+    // fused loads may hand the FP64 body unreduced representatives; this integer loop wants [0, q)
+    for (int k = 0; k < N; k++) a[k] = reduce64(ld_at(ld, lprep, ptr, t, k, pr, pidx), pr.m[pidx]);
     if (!INV) {
         int tt = N;
         for (int m = 1; m < N; m <<= 1) {

@@ -31,6 +31,7 @@ struct NttConst {
     // FP64-pipe transform (primes below 2^46, see ntt_impl.cuh): q, 1/q, n^-1 and w0n as doubles
     double qd, qinv, ninv_d, w0n_d;
     int f64;
+    double c32;  // 2^32 mod q (centred lifts of 60-bit residues into an FP64-body prime, LdLift)
 };
 
 // Memory owned by one captured CUDA graph (graph.cu): while a driver is being captured, every
