@@ -83,6 +83,10 @@ _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None) or (
     lambda dev: torch.cuda.current_stream(dev).cuda_stream)  # the current stream's cudaStream_t, cheaply
 
 
+_cur_stream_raw = getattr(torch._C, "_cuda_getCurrentStream", None)  # (stream_id, device_index, device_type)
+_set_stream_raw = getattr(torch._C, "_cuda_setStream", None)
+
+
 def scalar_i64(x: float) -> int:
     """round(x) as a signed 64-bit scalar for the C-ABI; ctypes would wrap larger values silently."""
     k = int(round(x))
@@ -927,6 +931,22 @@ class CkksEngine:
         if s is None:
             s = self._ext_streams["side"] = torch.cuda.Stream(device=self.device)
         return s
+
+    def _empty_on(self, stream, shape) -> torch.Tensor:
+        """``torch.empty(shape, int64)`` allocated on ``stream`` (the caching allocator then reuses the
+        block in that stream's order).  Switches torch's current stream through the C bindings the
+        ``torch.cuda.stream`` context manager wraps: the manager's Python layers cost ~8 us per
+        product, more than the library call it brackets."""
+        get, put = _cur_stream_raw, _set_stream_raw
+        if get is None or put is None:
+            with torch.cuda.stream(stream):
+                return torch.empty(shape, dtype=torch.int64, device=self.device)
+        prev = get(self._dev_index)
+        put(stream_id=stream.stream_id, device_index=stream.device_index, device_type=stream.device_type)
+        try:
+            return torch.empty(shape, dtype=torch.int64, device=self.device)
+        finally:
+            put(stream_id=prev[0], device_index=prev[1], device_type=prev[2])
 
     def _ext_stream(self, ptr: int):
         s = self._ext_streams.get(ptr)

@@ -232,8 +232,7 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
                 slot = ctypes.c_void_p()
                 _lib.check(engine._lib.vr_async_slot(h, ctypes.byref(slot)))
                 ext = engine._ext_stream(slot.value)
-                with torch.cuda.stream(ext):
-                    outs = torch.empty((1, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
+                outs = engine._empty_on(ext, (1, 2, lv, engine.N))
                 _lib.check(engine._lib.vr_matmul_outer_async(h, fl.arr, fr.arr, n, 1, lv, _lib.row_ptrs(outs, 1),
                                                              ctypes.byref(slot)))
                 if slot.value:

@@ -11,7 +11,7 @@ cap() {  # tag regex skip cmd...   (ONLY="tag ..." restricts the run)
   echo "ncu $tag rc=$? $(ls -la gpurun_out/ncu_$tag.ncu-rep 2>/dev/null | awk '{print $5}')"
 }
 export VR_ASYNC=0 VR_MM_ORDER=5   # eager one-pass matmul_outer: the kernels the async slot graphs replay
-cap ts_onepass 'k_tensor_sum<.int.1,..int.256,..int.2,..int.4,..int.0>' 1 --import-source on python tools/step_profile.py --cfg 2 --steps 2
+cap ts_onepass 'k_tensor_sum_ld' 1 --import-source on python tools/step_profile.py --cfg 2 --steps 2
 cap modup_ntt 'ntt_cl8<.bool.0,..int.11,.*LdLift' 1 python tools/step_profile.py --cfg 2 --steps 2
 cap modup_intt 'ntt_cl8<.bool.1,..int.11,.*LdGather' 1 python tools/step_profile.py --cfg 2 --steps 2
 cap ks_inner_cfg2 'k_ks_inner' 1 python tools/step_profile.py --cfg 2 --steps 2
