@@ -864,7 +864,17 @@ void tensor_sum_mode(Ctx &c, const uint64_t *const *L, const uint64_t *const *R,
 // cluster ranks (split-K across CTAs) combine through DSMEM.  rb > 1: rb row blocks interleaved along
 // x sharing R through L2 (config 5a).  Compared with the TMA ring it trades the producer warp and the
 // per-stage mbarrier handshake for occupancy (every thread has loads in flight).
-template <int KG, int SPLIT>
+// ST > 0: the operand loads go through a per-thread shared-memory ring filled with 16-byte cp.async
+// copies ST steps deep (a thread reads back only what it copied itself: cp.async.wait_group orders it,
+// no barrier), so the bytes in flight no longer cost registers: ST - 1 steps x 64 B x 128 threads per CTA.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N_>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N_) : "memory"); }
+
+template <int KG, int SPLIT, int ST = 0>
 __global__ void __launch_bounds__(64 * KG)
     k_tensor_sum_ld(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O,
                     int rb) {
@@ -897,7 +907,48 @@ __global__ void __launch_bounds__(64 * KG)
     // the per-thread ranges of configs 2 and 5a (16 and 64 steps) run as pure multiply-accumulates.
     const int qb = 64 - __clzll((long long)m.q);
     const unsigned mask1 = (1u << max(0, min(20, 126 - 2 * qb))) - 1u, mask02 = (1u << max(0, min(20, 128 - 2 * qb))) - 1u;
-    if (live && kb < ke) {
+    if constexpr (ST > 0) {
+        __shared__ __align__(16) ulonglong2 ring[ST][4][64 * KG];
+        if (live && kb < ke) {
+            auto issue = [&](int k) {
+                if (k < ke) {
+                    const uint64_t *lp = L[k], *rp = R[k];
+                    const int sl = (k - kb) % ST;
+                    cp_async16(&ring[sl][0][threadIdx.x], lp + o0);
+                    cp_async16(&ring[sl][1][threadIdx.x], lp + o1);
+                    cp_async16(&ring[sl][2][threadIdx.x], rp + o0);
+                    cp_async16(&ring[sl][3][threadIdx.x], rp + o1);
+                }
+                cp_async_commit();  // one group per step, empty past the end: wait_group counts stay uniform
+            };
+#pragma unroll
+            for (int d = 0; d < ST - 1; d++) issue(kb + d);
+            for (int k = kb, it = 0; k < ke; k++, it++) {
+                issue(k + ST - 1);
+                cp_async_wait<ST - 1>();  // the group of step k has landed
+                const int sl = it % ST;
+                const ulonglong2 l0 = ring[sl][0][threadIdx.x], l1 = ring[sl][1][threadIdx.x];
+                const ulonglong2 r0 = ring[sl][2][threadIdx.x], r1 = ring[sl][3][threadIdx.x];
+                mac_to(acc[0][0], l0.x, r0.x);
+                mac_to(acc[0][1], l0.y, r0.y);
+                mac_to(acc[2][0], l1.x, r1.x);
+                mac_to(acc[2][1], l1.y, r1.y);
+                mac_to(acc[1][0], l0.x + l1.x, r0.x + r1.x);
+                mac_to(acc[1][1], l0.y + l1.y, r0.y + r1.y);
+                if (((unsigned)it & mask1) == mask1) {
+#pragma unroll
+                    for (int e = 0; e < 2; e++) acc[1][e] = u128{reduce128(acc[1][e], m), 0};
+                    if (((unsigned)it & mask02) == mask02) {
+#pragma unroll
+                        for (int e = 0; e < 2; e++) {
+                            acc[0][e] = u128{reduce128(acc[0][e], m), 0};
+                            acc[2][e] = u128{reduce128(acc[2][e], m), 0};
+                        }
+                    }
+                }
+            }
+        }
+    } else if (live && kb < ke) {
         ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(L[kb] + o0), l1 = *reinterpret_cast<const ulonglong2 *>(L[kb] + o1);
         ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R[kb] + o0), r1 = *reinterpret_cast<const ulonglong2 *>(R[kb] + o1);
         for (int k = kb, it = 0; k < ke; k++, it++) {
@@ -976,7 +1027,7 @@ __global__ void __launch_bounds__(64 * KG)
     cluster.sync();
 }
 
-template <int KG, int SPLIT>
+template <int KG, int SPLIT, int ST = 0>
 static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O, int rb) {
     cudaLaunchConfig_t cfg = {};
     const int tiles = (c.n / 2 + 63) / 64;
@@ -993,7 +1044,7 @@ static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    VR_CUDA(cudaLaunchKernelEx(&cfg, k_tensor_sum_ld<KG, SPLIT>, L, R, n, nl, c.n, c.primes, O, rb));
+    VR_CUDA(cudaLaunchKernelEx(&cfg, k_tensor_sum_ld<KG, SPLIT, ST>, L, R, n, nl, c.n, c.primes, O, rb));
 }
 
 // VR_TS_LD selects the register-pipelined kernel for one-pass sums (0 = the TMA ring).  Swept on
@@ -1003,7 +1054,7 @@ static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const
 // After the fold periods above removed the in-loop reductions (re-swept, cfg 2 / cfg 5a): 2x2 33.6 us /
 // 1.03 ms (5.2 TB/s), 2x1 30.4 us (5.59 TB/s = 0.85 of the copy peak) / 1.15 ms, 1x2 49.3 / 1.28, 4x1 43.7 /
 // 1.38, 2x4 50.6 / 1.71, 1x4 47.7 / 1.59, 4x2 46.9 / 1.50.  Default (VR_TS_LD unset, -1): two k-groups per
-// CTA, and split-K across a 2-CTA cluster only from n = 128 columns on, so a thread walks 32-64 steps.
+// CTA and no split-K; from n = 128 columns on the operands go through a per-thread cp.async ring.
 static int ts_ld_variant() {
     static const int v = [] {
         const char *e = getenv("VR_TS_LD");
@@ -1014,7 +1065,10 @@ static int ts_ld_variant() {
 
 static bool try_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O, int rb) {
     int v = ts_ld_variant();
-    if (v < 0) v = n >= 128 ? 4 : 7;
+    // long k ranges (cfg 5a, n = 256): the cp.async ring keeps four steps in flight per thread without
+    // split-K: 0.98 ms (5.5 TB/s) against 1.04 ms for the register-prefetch 2x2 form; at n = 64 the
+    // register form wins (30.2 vs 31.9 us)
+    if (v < 0) v = n >= 128 ? 12 : 7;
     switch (v) {
         case 1: launch_ts_ld<4, 1>(c, L, R, n, nl, O, rb); return true;
         case 2: launch_ts_ld<4, 2>(c, L, R, n, nl, O, rb); return true;
@@ -1026,6 +1080,12 @@ static bool try_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
         case 8: launch_ts_ld<1, 4>(c, L, R, n, nl, O, rb); return true;
         case 9: launch_ts_ld<1, 2>(c, L, R, n, nl, O, rb); return true;
         case 10: launch_ts_ld<1, 8>(c, L, R, n, nl, O, rb); return true;
+        case 11: launch_ts_ld<2, 1, 3>(c, L, R, n, nl, O, rb); return true;  // cp.async rings
+        case 12: launch_ts_ld<2, 1, 4>(c, L, R, n, nl, O, rb); return true;
+        case 13: launch_ts_ld<2, 2, 3>(c, L, R, n, nl, O, rb); return true;
+        case 14: launch_ts_ld<2, 2, 4>(c, L, R, n, nl, O, rb); return true;
+        case 15: launch_ts_ld<2, 1, 5>(c, L, R, n, nl, O, rb); return true;
+        case 16: launch_ts_ld<2, 2, 5>(c, L, R, n, nl, O, rb); return true;
         default: return false;
     }
 }
