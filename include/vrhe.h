@@ -50,6 +50,10 @@ unsigned long long vr_launch_count(void);
 /* order every later call on cuda_stream (NULL = the legacy default stream); the context's
  * private stream (the default after vr_ctx_create) stays alive until vr_ctx_destroy */
 int vr_set_stream(vr_ctx *ctx, void *cuda_stream);
+/* `stream` first waits for everything queued on the context's stream, then becomes the context's
+ * stream (vr_set_stream switches back): runs the following calls on a side stream, e.g. the deferred
+ * encryption of a product's operands (multicipher.py:62-85) on the slot stream of that product */
+int vr_fork_stream(vr_ctx *ctx, void *stream);
 int vr_sync(vr_ctx *ctx);
 
 /* ---- ciphertexts owned through the C-ABI (host-buffer I/O, no PyTorch) -------- */

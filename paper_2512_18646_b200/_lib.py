@@ -27,6 +27,7 @@ _SIGS = {
     "vr_ctx_create": [ctypes.c_int, ctypes.c_int, c_u64p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(c_vp)],
     "vr_ctx_destroy": [c_vp],
     "vr_set_stream": [c_vp, c_vp],
+    "vr_fork_stream": [c_vp, c_vp],
     "vr_sync": [c_vp],
     "vr_gen_relin_key": [c_vp],
     "vr_galois_elt": [c_vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_uint32)],

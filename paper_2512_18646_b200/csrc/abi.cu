@@ -437,6 +437,20 @@ int vr_set_stream(vr_ctx *h, void *stream) {
     return guard([&] { set_stream(h->c, (cudaStream_t)stream); });
 }
 
+int vr_fork_stream(vr_ctx *h, void *stream) {
+    // `stream` waits for everything queued on the context's stream, then becomes the context's stream
+    // (vr_set_stream switches back).  Lets a caller run a call on a side stream -- e.g. the deferred
+    // encryption of a product's operands on the slot stream that will run the product.
+    return guard([&] {
+        vr::Ctx &c = h->c;
+        const cudaStream_t s = (cudaStream_t)stream;
+        if (s == c.stream) return;
+        VR_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        VR_CUDA(cudaStreamWaitEvent(s, c.ev_fork, 0));
+        set_stream(c, s);
+    });
+}
+
 int vr_sync(vr_ctx *h) {
     return guard([&] { VR_CUDA(cudaStreamSynchronize(h->c.stream)); });
 }

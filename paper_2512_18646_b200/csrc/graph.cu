@@ -209,8 +209,17 @@ cudaStream_t matmul_outer_async(Ctx &c, const uint64_t *const *L, const uint64_t
             to(c, std::vector<const uint64_t *>(out, out + nb));
         matmul_outer(c, tl.c_(), tr.c_(), n, nb, level, to.m_());
     };
-    if (!graphs_enabled() || nb > 4 || (nb + 1) * n + nb > kSetMaxPtrs) {
+    // A caller may have produced the operands ON the slot stream this call was going to use (the
+    // deferred encryptions of encode_left / encode_right run there, vr_fork_stream): when the product
+    // runs synchronously on the context stream instead, that stream first waits for the slot.
+    auto sync_after_slot = [&] {
+        const cudaStream_t s = next_async_slot(c);
+        VR_CUDA(cudaEventRecord(c.ev_join, s));
+        VR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
         sync_body();
+    };
+    if (!graphs_enabled() || nb > 4 || (nb + 1) * n + nb > kSetMaxPtrs) {
+        sync_after_slot();
         return nullptr;
     }
     const int k = c.slot_next;
@@ -218,7 +227,7 @@ cudaStream_t matmul_outer_async(Ctx &c, const uint64_t *const *L, const uint64_t
     if (!g->exec) {
         if (g->seen < 1) {
             g->seen++;
-            sync_body();
+            sync_after_slot();
             return nullptr;
         }
         relin_key(c);  // generated outside any capture

@@ -265,14 +265,15 @@ class CtBatch:
     sequence whose ``Ciphertext`` objects are created on first access: an operand that only feeds
     ``matmul_outer`` never materialises them (its pointer table is base + i * stride)."""
 
-    __slots__ = ("out", "level", "scale", "depth", "layout", "engine_id", "count", "_items", "_pending")
+    __slots__ = ("out", "level", "scale", "depth", "layout", "engine_id", "count", "_items", "_pending", "_evt")
 
     def __init__(self, out, level, scale, depth, layout, engine_id, count=None, pending=None):
         self.out, self.level, self.scale, self.depth = out, level, scale, depth
         self.layout, self.engine_id = layout, engine_id
         self.count = out.shape[0] if count is None else count
         self._items = None
-        self._pending = pending
+        self._pending = pending  # the engine (encryption deferred) or the stream that produced the residues
+        self._evt = None         # completion event of that producer, when it ran on a side stream
 
     def _all(self) -> list:
         items = self._items
@@ -284,14 +285,29 @@ class CtBatch:
                     ct._pending = self._pending
         return items
 
-    def clear_pending(self, owner) -> None:
-        """The deferred encryption behind this batch has been launched."""
+    def set_pending(self, owner, new=None, evt=None) -> None:
+        """The producer ``owner`` of this batch is done or has been launched: ``new`` is None (ordered on
+        the current stream) or the side stream it runs on (readers on other streams wait for it)."""
         if self._pending is owner:
-            self._pending = None
+            self._pending = new
+            self._evt = evt
             if self._items is not None:
                 for ct in self._items:
                     if ct._pending is owner:
-                        ct._pending = None
+                        ct._pending = new
+
+    def order_on(self, stream) -> None:
+        """Make ``stream`` see these residues: nothing to do when it produced them or they are complete."""
+        pend = self._pending
+        if pend is None or pend is stream:
+            return
+        evt = self._evt
+        if evt is None:
+            stream.wait_stream(pend)
+        elif evt.query():  # the producer finished: settled for every stream
+            self.set_pending(pend, None)
+        else:
+            stream.wait_event(evt)
 
     def pointers(self) -> np.ndarray:
         """Device addresses of the ciphertexts (uint64), without creating them."""
@@ -348,6 +364,11 @@ class CkksEngine:
         # dec_batch_async through the library's decode tickets (one C call); VR_DECODE_TICKETS=0 keeps
         # the torch path (device tensor + pinned tensor + copy + event)
         self._decode_tickets = os.environ.get("VR_DECODE_TICKETS", "1") != "0"
+        # VR_ENC_ON_SLOT=1: deferred operand encryptions run on the slot stream of the product that
+        # consumes them, so the encryption of product i+1 overlaps the kernels of product i.  Measured
+        # slower (e2e 4.3k -> 3.8k HE matmul/s: the 1024-CTA slot FFT and the 5120-CTA encryption NTT of
+        # different products displace each other's CTAs), so off by default
+        self._enc_on_slot = os.environ.get("VR_ENC_ON_SLOT", "0") == "1"
         self._ext_streams = {}
         self._nonce = 0
         self._pin = None
@@ -540,9 +561,11 @@ class CkksEngine:
             _lib.check(self._lib.vr_encrypt_strided2(h, a_src, a_sc, a_s1, a_s2, a_p, a_nv, a_cnt, a_out.data_ptr(), b_src, b_sc,
                                                      b_s1, b_s2, b_p, b_nv, b_cnt, b_out.data_ptr(), L, scale, a_n0))
 
-    def _flush_enc(self) -> None:
+    def _flush_enc(self, on=None) -> None:
         """Launch the deferred encryptions (consecutive-nonce pairs as one combined launch), ordered on
-        the current stream after the streams their host copies were queued on."""
+        the current stream after the streams their host copies were queued on -- or, with ``on``, on that
+        side stream (the slot stream of the product that consumes them: the encryption of the next
+        product then overlaps this product's kernels instead of queueing behind them on one stream)."""
         queue, self._enc_queue = self._enc_queue, []
         if not queue:
             return
@@ -551,6 +574,24 @@ class CkksEngine:
         for (job, _) in queue:
             if job[10] is not None and job[10].cuda_stream != cur.cuda_stream:
                 cur.wait_stream(job[10])
+        if on is not None and on.cuda_stream == cur.cuda_stream:
+            on = None
+        if on is not None:  # `on` waits for the current stream, the context moves to it
+            _lib.check(self._lib.vr_fork_stream(self._h, ctypes.c_void_p(on.cuda_stream)))
+        try:
+            groups = self._launch_queue(queue)
+        finally:
+            if on is not None:
+                _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(self._stream_ptr)))
+        evt = None
+        if on is not None:
+            evt = torch.cuda.Event()
+            evt.record(on)
+        for g in groups:
+            g.set_pending(self, on, evt)
+
+    def _launch_queue(self, queue) -> list:
+        done = []
         i = 0
         while i < len(queue):
             job, cts = queue[i]
@@ -564,8 +605,8 @@ class CkksEngine:
                 self._launch_enc([job])
                 group = [cts]
                 i += 1
-            for g in group:
-                g.clear_pending(self)
+            done.extend(group)
+        return done
 
     def dec(self, ct: Ciphertext) -> np.ndarray:
         """Full slot vector (real parts), like engine.py:204-206."""

@@ -228,10 +228,16 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
                 # The output is allocated ON that stream (the caching allocator then reuses it in that
                 # stream's order, with no cross-stream events), the operands are recorded on it once,
                 # and any read of the result waits for it (Ciphertext._ready)
-                h = engine.handle
+                engine._adopt_stream()
+                h = engine._h
                 slot = ctypes.c_void_p()
                 _lib.check(engine._lib.vr_async_slot(h, ctypes.byref(slot)))
                 ext = engine._ext_stream(slot.value)
+                if engine._enc_queue:  # the operands' deferred encryption runs on the product's slot stream
+                    engine._flush_enc(on=ext if engine._enc_on_slot else None)
+                for op in (lf.cts, right.cts):  # operands produced on another side stream
+                    if type(op) is CtBatch and op._pending is not None:
+                        op.order_on(ext)
                 outs = engine._empty_on(ext, (1, 2, lv, engine.N))
                 _lib.check(engine._lib.vr_matmul_outer_async(h, fl.arr, fr.arr, n, 1, lv, _lib.row_ptrs(outs, 1),
                                                              ctypes.byref(slot)))
