@@ -148,3 +148,29 @@ def test_modarith_header_on_host(tmp_path):
             assert sh == (x * w) % q
             assert lift == (x - q if x > q // 2 else x) % q
             assert fi == ys % q
+
+
+def test_ct_batch_is_lazy_and_list_like():
+    """CtBatch (the `cts` of encode_left / encode_right): Ciphertext objects and the pointer table come
+    from base + i * stride, created on first access (no GPU needed for the bookkeeping)."""
+    import torch
+
+    from paper_2512_18646_b200.engine import CtBatch
+    from paper_2512_18646_b200.multicipher import _OperandCache, _layout0, _storages
+
+    out = torch.zeros((4, 2, 3, 8), dtype=torch.int64)
+    b = CtBatch(out, 2, 2.0 ** 40, 0, ("grid", 2, 2), 7, 4, None)
+    assert len(b) == 4 and b._items is None
+    step = out.stride(0) * out.element_size()
+    assert list(b.pointers()) == [out.data_ptr() + i * step for i in range(4)]
+    assert b._items is None  # the pointer table did not create the ciphertexts
+    assert [c._idx for c in b] == [0, 1, 2, 3] and b[1]._ptr == out.data_ptr() + step
+    assert len(b + [1]) == 5 and len([0] + b) == 5 and _layout0(b) == ("grid", 2, 2)
+    cache = _OperandCache(7, 2, 0, _storages(b), np_ptrs=b.pointers())
+    assert list(cache.arr) == cache.ptrs == [c._ptr for c in b]
+    # pending bookkeeping: a producer marks the batch, materialised items follow it
+    owner = object()
+    p = CtBatch(out, 2, 2.0 ** 40, 0, None, 7, 4, owner)
+    assert all(c._pending is owner for c in p)
+    p.set_pending(owner, None)
+    assert p._pending is None and all(c._pending is None for c in p)
