@@ -1005,7 +1005,9 @@ void run_fused(Ctx &c, const NttBatch &b, const LD &ld, const ST &st) {
         const char *e = getenv("VR_NTT_SMALL");
         return e ? atoi(e) : 64;
     }();
-    const int le = b.count <= small_batch ? 2 : 3;
+    // (the threshold is in elements: 64 transforms of 2^14; at N = 2^15 a 64-transform batch -- the
+    // fused relinearise+rescale of config 5a's four row blocks -- already fills the machine)
+    const int le = (long long)b.count * c.n <= (long long)small_batch << 14 ? 2 : 3;
     PassArgs p1{logN, 0, pick_tpc(b.count, 1 << lb, T1, 16, 4, le), 0, 0, 0, le == 2};
     PassArgs p2{logN, la, pick_tpc(b.count, 1 << la, T2, 2048 / T2, 1, le), 0, 0, 0, le == 2};
     // the first pass hands its intermediate to the second (raw doubles on the FP64 body)

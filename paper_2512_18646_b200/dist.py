@@ -226,7 +226,9 @@ def matmul_outer_sharded_owned(engine: CkksEngine, lefts, right: ColumnEncodedMa
         reduced = True
     else:
         mine = reduce_partials_to_owners(part, group)
-        reduced = False
+        # one rank: nothing was summed, the tensor sum's own output is already reduced mod q
+        import torch.distributed as dist
+        reduced = not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1
     if not mine:
         return {}
     sub = part if len(mine) == part.shape[0] else part[mine].contiguous()
