@@ -72,6 +72,11 @@ __global__ void __launch_bounds__(128) k_conv_mac(const uint64_t *const *T, cons
     }
 }
 
+__device__ __forceinline__ ulonglong2 ld2(const uint64_t *p) { return *reinterpret_cast<const ulonglong2 *>(p); }
+__device__ __forceinline__ void st2(uint64_t *p, uint64_t a, uint64_t b) {
+    *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(a, b);
+}
+
 // Small-weight conv MAC.  Quantised weights satisfy |w| < B = 2^bb, so w' = w + B
 // is a u32.  Splitting each residue v = vh * 2^32 + vl, every product w' * v is
 // accumulated as two 32x32+64 multiply-adds (IMAD.WIDE.U32) into 64-bit partial
@@ -86,12 +91,17 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(16) uint64_t smc[];
-    const int taps = C * k * k;
+    const int taps = C * k * k, tpad = (taps + 3) & ~3;  // the tap list padded to a multiple of four
     const uint64_t **sptr = (const uint64_t **)smc;
-    uint32_t *sw = (uint32_t *)(smc + ((taps + 1) & ~1));  // [taps][FG], 16-byte aligned rows for FG % 4 == 0
+    uint32_t *sw = (uint32_t *)(smc + tpad);  // [tpad][FG], 16-byte aligned rows for FG % 4 == 0
     const int nfg = F / FG;
     const int o = blockIdx.x / nfg, f0 = (blockIdx.x - o * nfg) * FG;
-    for (int t = threadIdx.x; t < taps; t += blockDim.x) {
+    for (int t = threadIdx.x; t < tpad; t += blockDim.x) {
+        if (t >= taps) {
+            sptr[t] = nullptr;
+            for (int f = 0; f < FG; f++) sw[t * FG + f] = 0;
+            continue;
+        }
         const int c = t / (k * k), r = t - c * k * k, q = r / k, p = r - q * k;  // tap order (c, q, p)
         sptr[t] = T[((size_t)c * W + cols[o] + q) * k + p];
         for (int f = 0; f < FG; f++) sw[t * FG + f] = wb[((size_t)(f0 + f) * C + c) * k * k + p * k + q];
@@ -105,18 +115,21 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
     uint64_t alo[2][FG], ahi[2][FG];
 #pragma unroll
     for (int f = 0; f < FG; f++) alo[0][f] = ahi[0][f] = alo[1][f] = ahi[1][f] = 0;
-    uint64_t svl[2] = {0, 0}, svh[2] = {0, 0};
-    for (int t0 = 0; t0 < taps; t0 += 4) {
+    // Four taps per iteration: their 16-byte loads are issued together, then 4 x 4 FG multiply-adds in
+    // the fused form (mad.wide.u32, 64-bit accumulator in place).  The tap list is padded to a multiple
+    // of four with null pointers (value 0: nothing is added to the accumulators or to sum(v)), so the
+    // loop has no guards; a null tap of the model (all-zero weights) reads as 0 the same way.
+    u128 sv[2] = {u128{0, 0}, u128{0, 0}};  // sum of the tap values (bias removal)
+    const int taps4 = (taps + 3) & ~3;
+    for (int t0 = 0; t0 < taps4; t0 += 4) {
         ulonglong2 vv[4];
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-            const uint64_t *src = (t0 + u < taps) ? sptr[t0 + u] : nullptr;
-            vv[u] = src ? *reinterpret_cast<const ulonglong2 *>(src + off) : make_ulonglong2(0, 0);  // null: all weights zero
+            const uint64_t *src = sptr[t0 + u];  // CTA-uniform
+            vv[u] = src ? ld2(src + off) : make_ulonglong2(0, 0);
         }
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-            if (t0 + u >= taps) break;
-            const uint64_t v2[2] = {vv[u].x, vv[u].y};
             uint32_t wv[FG];
 #pragma unroll
             for (int f = 0; f < FG; f += (FG >= 4 ? 4 : 1)) {
@@ -127,15 +140,15 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
                     wv[f] = sw[(t0 + u) * FG + f];
                 }
             }
+            const uint64_t v2[2] = {vv[u].x, vv[u].y};
 #pragma unroll
             for (int e = 0; e < 2; e++) {
                 const uint32_t vl = (uint32_t)v2[e], vh = (uint32_t)(v2[e] >> 32);
-                svl[e] += vl;
-                svh[e] += vh;
+                asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(sv[e].lo), "+l"(sv[e].hi) : "l"(v2[e]));
 #pragma unroll
                 for (int f = 0; f < FG; f++) {
-                    alo[e][f] += (uint64_t)vl * wv[f];
-                    ahi[e][f] += (uint64_t)vh * wv[f];
+                    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(alo[e][f]) : "r"(vl), "r"(wv[f]));
+                    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(ahi[e][f]) : "r"(vh), "r"(wv[f]));
                 }
             }
         }
@@ -146,9 +159,7 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
     uint64_t outv[FG][2];
 #pragma unroll
     for (int e = 0; e < 2; e++) {
-        // sum(v) = svh * 2^32 + svl
-        const u128 sv{svl[e] + (svh[e] << 32), (svh[e] >> 32) + ((svl[e] + (svh[e] << 32)) < svl[e] ? 1u : 0u)};
-        const uint64_t bias_sum = mul_mod(reduce128(sv, m), bq_pow, m);  // B * sum(v) mod q
+        const uint64_t bias_sum = mul_mod(reduce128(sv[e], m), bq_pow, m);  // B * sum(v) mod q
 #pragma unroll
         for (int f = 0; f < FG; f++) {
             u128 acc{alo[e][f], 0};
@@ -168,10 +179,6 @@ __global__ void __launch_bounds__(128) k_conv_mac_small(const uint64_t *const *T
 // adjacent coefficients (16-byte loads) of one limb for UG outputs; the CTA stages the pointers of
 // a chunk of JC inputs in shared memory (no dependent pointer load in the loop) and the j loop is
 // unrolled by two so the next input's loads are in flight during the current MACs.
-__device__ __forceinline__ ulonglong2 ld2(const uint64_t *p) { return *reinterpret_cast<const ulonglong2 *>(p); }
-__device__ __forceinline__ void st2(uint64_t *p, uint64_t a, uint64_t b) {
-    *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(a, b);
-}
 constexpr int PMV_JC = 128;
 template <int UG, int JU>
 __global__ void __launch_bounds__(128) k_pt_matvec(const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int nl,
@@ -395,7 +402,11 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
     }
     DevArray<uint32_t> dwb(c, small ? wbias.data() : nullptr, small ? wbias.size() : 0);
     const int taps = C * k * k;
-    const int FG = (F % 8 == 0) ? 8 : (F % 4 == 0 ? 4 : (F % 2 == 0 ? 2 : 1));
+    static const int fg_max = [] {
+        const char *e = getenv("VR_CONV_FG");
+        return e ? atoi(e) : 8;
+    }();
+    const int FG = (F % 8 == 0 && fg_max >= 8) ? 8 : (F % 4 == 0 && fg_max >= 4 ? 4 : (F % 2 == 0 && fg_max >= 2 ? 2 : 1));
     const int ocols = std::max(1, std::min(nout, (int)(((size_t)2 << 30) / (ctw * 8 * F))));
     Scratch yp(c, sizeof(uint64_t) * (size_t)F * ocols * ctw);
     for (int o0 = 0; o0 < nout; o0 += ocols) {
@@ -407,7 +418,8 @@ void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, 
         dim3 grid((unsigned)no * (F / FG), 2 * nl, nblocks(N, 128));
         const int *colp = dcols.get() + o0;
         if (small) {
-            const size_t sm = (size_t)((taps + 1) & ~1) * 8 + (size_t)taps * FG * 4 + 16;
+            const size_t tpad = (size_t)((taps + 3) & ~3);
+            const size_t sm = tpad * 8 + tpad * FG * 4 + 16;
             const uint64_t bpow = uint64_t(1) << bb;
             dim3 gs((unsigned)no * (F / FG), 2 * nl, nblocks(N / 2, 128));
             switch (FG) {
