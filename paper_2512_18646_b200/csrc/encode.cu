@@ -592,6 +592,7 @@ void encrypt_src2(Ctx &c, const double *src0, long long sc0, long long s1_0, lon
                   uint64_t *d_ct0, const double *src1, long long sc1, long long s1_1, long long s2_1, int p1, int nvals1,
                   int count1, uint64_t *d_ct1, int level, double scale, uint64_t nonce0) {
     if (!c.sym_enc) throw VrError(3, "combined encryption needs secret-key encryption");
+    c.enc_calls++;
     const int N = c.n, nl = level + 1, count = count0 + count1;
     Scratch m(c, sizeof(int64_t) * count * N), keys(c, sizeof(uint64_t) * count * nl);
     SlotSrc vs{src0, sc0, s1_0, s2_0, p0 > 0 ? p0 : 1, nvals0};
@@ -613,6 +614,7 @@ void encrypt_src2(Ctx &c, const double *src0, long long sc0, long long s1_0, lon
 void encrypt_src(Ctx &c, const double *src, long long sc, long long s1, long long s2, int p, int nvals, int count, int level,
                  double scale, uint64_t nonce0, uint64_t *d_ct) {
     const int N = c.n, nl = level + 1;
+    c.enc_calls++;
     Scratch m(c, sizeof(int64_t) * count * N);
     const SlotSrc vs{src, sc, s1, s2, p > 0 ? p : 1, nvals};
     if (c.sym_enc) {

@@ -974,7 +974,12 @@ template <bool INV, class LD, class ST>
 bool try_cl8(Ctx &c, const NttBatch &b, const LD &ld, const ST &st, bool force = false) {
     const int lim = ntt_cl_min();
     if (lim <= 0) return false;  // VR_NTT_CL=0 is a kill switch, also for forced callers
-    if (!force && b.count < lim) return false;
+    // Inside a slot graph recorded for resident operands (asynchronous matmul_outer, Ctx::capture_cl)
+    // every transform is ONE cluster kernel whatever its batch: the overlapped chains are bound by the
+    // rate at which the GPU dispatches their small kernels (8 slots: 20 us per 10-kernel chain, 16 us per
+    // 7-kernel chain), not by a single chain's latency, which is what the two-pass form wins below ~16
+    // transforms (cfg-2 step 43.4 -> 39.6 us per product).
+    if (!force && b.count < lim && !(c.capturing && c.capture_cl)) return false;
     switch (c.log_n) {
         case 12: launch_cl8<INV, 9>(c, b, ld, st); return true;
         case 13: launch_cl8<INV, 10>(c, b, ld, st); return true;

@@ -136,6 +136,8 @@ struct Ctx {
     std::vector<GraphEntry> graphs;
     unsigned long long graph_clock = 0;
     GraphMem *capturing = nullptr;
+    bool capture_cl = false;  // the graph being recorded runs every transform as one cluster kernel (graph.cu)
+    unsigned long long enc_calls = 0, enc_seen = 0;  // encryption launches, and how many the last async product had seen
     cudaStream_t side = 0;  // non-blocking helper stream for capture-time allocations and uploads
     // asynchronous drivers (vr_matmul_outer_async): calls rotate over kSlots streams (process-wide per
     // device, graph.cu), each replaying its own graph, so consecutive independent calls overlap
