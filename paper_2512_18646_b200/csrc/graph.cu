@@ -163,12 +163,6 @@ static cudaStream_t slot_stream(int device, int k) {
 // Kernel node at the head of every asynchronous slot graph: writes the operand and output pointer
 // tables the recorded driver reads.  Its parameters (the pointers themselves) are replaced before
 // every replay, so one recorded graph per (slot, shape) serves any operands and any output buffer.
-constexpr int kSetMaxPtrs = 240;  // (nb + 1) n + nb pointers; 2 KB of kernel parameters
-struct SetTables {
-    uint64_t **dst;  // the graph-owned tables: [L (nb n)] [R (n)] [out (nb)], contiguous
-    int count;
-    const uint64_t *p[kSetMaxPtrs];
-};
 __global__ void k_set_tables(SetTables a) {
     for (int i = threadIdx.x; i < a.count; i += blockDim.x) a.dst[i] = const_cast<uint64_t *>(a.p[i]);
 }
@@ -247,34 +241,60 @@ cudaStream_t matmul_outer_async(Ctx &c, const uint64_t *const *L, const uint64_t
             // one contiguous graph-owned block: L table, R table, out table
             auto **tabs = (uint64_t **)capture_alloc(c, sizeof(void *) * ((nb + 1) * n + nb));
             g->out_table = tabs;
-            k_set_tables<<<1, 256, 0, c.stream>>>(make_tables(tabs, L, R, out, n, nb));
-            check_launch("k_set_tables");
-            cudaStreamCaptureStatus cs;
-            const cudaGraphNode_t *deps = nullptr;
-            size_t nd = 0;
-            VR_CUDA(cudaStreamGetCaptureInfo(c.stream, &cs, nullptr, nullptr, &deps, &nd));
-            if (nd != 1) throw VrError(4, "matmul_outer_async: unexpected capture dependencies");
-            g->out_node = deps[0];
+            const SetTables first = make_tables(tabs, L, R, out, n, nb);
+            // the tensor sum carries the pointers in its own parameters when it can (one kernel less per
+            // product: the overlapped chains are dispatch-bound); else a one-block kernel writes the tables
+            g->ts_first = tensor_sum_takes_params(nb) && n >= 1;
+            if (g->ts_first) {
+                c.ts_params = &first;
+                c.ts_node = nullptr;
+            } else {
+                k_set_tables<<<1, 256, 0, c.stream>>>(first);
+                check_launch("k_set_tables");
+                cudaStreamCaptureStatus cs;
+                const cudaGraphNode_t *deps = nullptr;
+                size_t nd = 0;
+                VR_CUDA(cudaStreamGetCaptureInfo(c.stream, &cs, nullptr, nullptr, &deps, &nd));
+                if (nd != 1) throw VrError(4, "matmul_outer_async: unexpected capture dependencies");
+                g->out_node = deps[0];
+            }
             matmul_outer(c, (const uint64_t *const *)tabs, (const uint64_t *const *)(tabs + (size_t)nb * n), n, nb, level,
                          tabs + (size_t)(nb + 1) * n, true);
+            if (g->ts_first) {
+                if (c.ts_params || !c.ts_node) throw VrError(4, "matmul_outer_async: the tensor sum did not take its pointer parameters");
+                g->out_node = c.ts_node;
+            }
         } catch (...) {
             c.capture_cl = false;
+            c.ts_params = nullptr;
             graph_capture_abort(c, *g, user, k0);
             throw;
         }
         c.capture_cl = false;
         graph_capture_end(c, *g, user, k0, true);
+        if (g->ts_first) VR_CUDA(cudaGraphKernelNodeGetParams(g->out_node, &g->ts_kp));  // the graph is kept: its storage stays valid
     } else {
         SetTables a = make_tables(g->out_table, L, R, out, n, nb);
-        void *args[] = {&a};
-        cudaKernelNodeParams kp = {};
-        kp.func = (void *)k_set_tables;
-        kp.gridDim = dim3(1);
-        kp.blockDim = dim3(256);
-        kp.sharedMemBytes = 0;
-        kp.kernelParams = args;
-        kp.extra = nullptr;
-        VR_CUDA(cudaGraphExecKernelNodeSetParams(g->exec, g->out_node, &kp));
+        if (g->ts_first) {
+            // k_tensor_sum_ldp(SetTables, n, nl, N, primes, O, rb): replace the first parameter only
+            void *args[7];
+            for (int i = 0; i < 7; i++) args[i] = g->ts_kp.kernelParams[i];
+            args[0] = &a;
+            cudaKernelNodeParams kp = g->ts_kp;
+            kp.kernelParams = args;
+            kp.extra = nullptr;
+            VR_CUDA(cudaGraphExecKernelNodeSetParams(g->exec, g->out_node, &kp));
+        } else {
+            void *args[] = {&a};
+            cudaKernelNodeParams kp = {};
+            kp.func = (void *)k_set_tables;
+            kp.gridDim = dim3(1);
+            kp.blockDim = dim3(256);
+            kp.sharedMemBytes = 0;
+            kp.kernelParams = args;
+            kp.extra = nullptr;
+            VR_CUDA(cudaGraphExecKernelNodeSetParams(g->exec, g->out_node, &kp));
+        }
     }
     cudaStream_t s = next_async_slot(c);
     VR_CUDA(cudaEventRecord(c.ev_fork, c.stream));  // operands (and anything before) are ready

@@ -874,16 +874,28 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N_>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N_) : "memory"); }
 
-template <int KG, int SPLIT, int ST = 0>
-__global__ void __launch_bounds__(64 * KG)
-    k_tensor_sum_ld(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O,
-                    int rb) {
-    pdl_wait();
-    pdl_trigger();
+// Operand pointers of the tensor sum: device tables (PtrTab), or the kernel parameters of a slot
+// graph's first kernel (PtrPar, see SetTables), read from the constant bank.
+struct PtrTab {
+    const uint64_t *const *L, *const *R;
+    __device__ __forceinline__ const uint64_t *l(int k) const { return L[k]; }
+    __device__ __forceinline__ const uint64_t *r(int k) const { return R[k]; }
+    __device__ __forceinline__ void left_block(size_t ofs) { L += ofs; }
+};
+struct PtrPar {
+    const SetTables *a;
+    int lofs, rofs;
+    __device__ __forceinline__ const uint64_t *l(int k) const { return a->p[lofs + k]; }
+    __device__ __forceinline__ const uint64_t *r(int k) const { return a->p[rofs + k]; }
+    __device__ __forceinline__ void left_block(size_t ofs) { lofs += (int)ofs; }
+};
+
+template <int KG, int SPLIT, int ST, class PS>
+__device__ __forceinline__ void ts_ld_body(PS ps, int n, int nl, int N, const DevPrimes &pr, uint64_t *const *O, int rb) {
     constexpr int TP = 64;  // coefficient pairs per CTA
     const int xb = rb > 1 ? (int)blockIdx.x % rb : 0;
     const int xt = rb > 1 ? (int)blockIdx.x / rb : (int)blockIdx.x;
-    L += (size_t)xb * n;
+    ps.left_block((size_t)xb * n);
     O += xb;
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -912,7 +924,7 @@ __global__ void __launch_bounds__(64 * KG)
         if (live && kb < ke) {
             auto issue = [&](int k) {
                 if (k < ke) {
-                    const uint64_t *lp = L[k], *rp = R[k];
+                    const uint64_t *lp = ps.l(k), *rp = ps.r(k);
                     const int sl = (k - kb) % ST;
                     cp_async16(&ring[sl][0][threadIdx.x], lp + o0);
                     cp_async16(&ring[sl][1][threadIdx.x], lp + o1);
@@ -949,12 +961,12 @@ __global__ void __launch_bounds__(64 * KG)
             }
         }
     } else if (live && kb < ke) {
-        ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(L[kb] + o0), l1 = *reinterpret_cast<const ulonglong2 *>(L[kb] + o1);
-        ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R[kb] + o0), r1 = *reinterpret_cast<const ulonglong2 *>(R[kb] + o1);
+        ulonglong2 l0 = *reinterpret_cast<const ulonglong2 *>(ps.l(kb) + o0), l1 = *reinterpret_cast<const ulonglong2 *>(ps.l(kb) + o1);
+        ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(ps.r(kb) + o0), r1 = *reinterpret_cast<const ulonglong2 *>(ps.r(kb) + o1);
         for (int k = kb, it = 0; k < ke; k++, it++) {
             ulonglong2 nl0 = l0, nl1 = l1, nr0 = r0, nr1 = r1;
             if (k + 1 < ke) {  // next step's operands in flight while this step multiplies
-                const uint64_t *lp = L[k + 1], *rp = R[k + 1];
+                const uint64_t *lp = ps.l(k + 1), *rp = ps.r(k + 1);
                 nl0 = __ldcs(reinterpret_cast<const ulonglong2 *>(lp + o0));
                 nl1 = __ldcs(reinterpret_cast<const ulonglong2 *>(lp + o1));
                 nr0 = __ldcs(reinterpret_cast<const ulonglong2 *>(rp + o0));
@@ -1028,6 +1040,27 @@ __global__ void __launch_bounds__(64 * KG)
 }
 
 template <int KG, int SPLIT, int ST = 0>
+__global__ void __launch_bounds__(64 * KG)
+    k_tensor_sum_ld(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O,
+                    int rb) {
+    pdl_wait();
+    pdl_trigger();
+    ts_ld_body<KG, SPLIT, ST>(PtrTab{L, R}, n, nl, N, pr, O, rb);
+}
+
+// First kernel of a slot graph: the operand pointers arrive in the parameters (one row block), block
+// (0, 0, 0) publishes them -- the output pointer table above all -- for the later kernels of the graph.
+template <int KG, int SPLIT, int ST = 0>
+__global__ void __launch_bounds__(64 * KG)
+    k_tensor_sum_ldp(const __grid_constant__ SetTables a, int n, int nl, int N, DevPrimes pr, uint64_t *const *O, int rb) {
+    pdl_wait();
+    pdl_trigger();
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        for (int i = threadIdx.x; i < a.count; i += blockDim.x) a.dst[i] = const_cast<uint64_t *>(a.p[i]);
+    ts_ld_body<KG, SPLIT, ST>(PtrPar{&a, 0, rb * n}, n, nl, N, pr, O, rb);
+}
+
+template <int KG, int SPLIT, int ST = 0>
 static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O, int rb) {
     cudaLaunchConfig_t cfg = {};
     const int tiles = (c.n / 2 + 63) / 64;
@@ -1044,6 +1077,18 @@ static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    if (c.ts_params) {  // recording a slot graph: pointers in the parameters, no table-writing kernel
+        const SetTables *a = c.ts_params;
+        c.ts_params = nullptr;
+        VR_CUDA(cudaLaunchKernelEx(&cfg, k_tensor_sum_ldp<KG, SPLIT, ST>, *a, n, nl, c.n, c.primes, O, rb));
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        VR_CUDA(cudaStreamGetCaptureInfo(c.stream, &cs, nullptr, nullptr, &deps, &nd));
+        if (cs != cudaStreamCaptureStatusActive || nd != 1) throw VrError(4, "tensor sum: unexpected capture state");
+        c.ts_node = deps[0];
+        return;
+    }
     VR_CUDA(cudaLaunchKernelEx(&cfg, k_tensor_sum_ld<KG, SPLIT, ST>, L, R, n, nl, c.n, c.primes, O, rb));
 }
 
@@ -1089,6 +1134,10 @@ static bool try_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
         default: return false;
     }
 }
+
+// whether tensor_sum(n, nb) runs the register / cp.async kernel, which can take its operand pointers
+// from its parameters (slot graphs)
+bool tensor_sum_takes_params(int nb) { return ts_ld_variant() != 0 && (nb == 1 || nb == 4) && getenv("VR_TS_VARIANT") == nullptr && getenv("VR_TS4") == nullptr && getenv("VR_TS4_MC") == nullptr; }
 
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O) {
     static int variant = [] {

@@ -32,6 +32,7 @@ void bfly_peak_f64(Ctx &c, int blocks, int iters, uint64_t *sink);  // iters x 6
 void tensor_sum_mode(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O,
                      int mode);
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O);
+bool tensor_sum_takes_params(int nb);
 
 // rescale: in [polys][l+1][N] -> out [polys][l][N] for each ciphertext
 void rescale(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int count, int polys, int level);

@@ -41,6 +41,17 @@ struct GraphMem {
     std::vector<void *> blocks;
 };
 
+// Operand and output pointers of one asynchronous matmul_outer, carried in the kernel parameters of
+// the first kernel of its slot graph (replaced before every replay, so one recorded graph serves any
+// operands): p = [L (nb n)] [R (n)] [out (nb)]; the kernel copies them into the graph-owned table dst
+// that the later kernels of the graph read.
+constexpr int kSetMaxPtrs = 240;  // (nb + 1) n + nb pointers; 2 KB of kernel parameters
+struct SetTables {
+    uint64_t **dst;
+    int count;
+    const uint64_t *p[kSetMaxPtrs];
+};
+
 struct GraphEntry {
     std::vector<uintptr_t> key;  // driver id, shape, level, then every pointer of the call
     cudaGraphExec_t exec = nullptr;
@@ -53,6 +64,10 @@ struct GraphEntry {
     cudaGraph_t graph = nullptr;
     cudaGraphNode_t out_node = nullptr;
     uint64_t **out_table = nullptr;
+    // out_node is the tensor sum itself (pointers in its parameters) rather than a table-writing kernel:
+    // its recorded launch, whose first parameter is replaced before every replay
+    bool ts_first = false;
+    cudaKernelNodeParams ts_kp = {};
 };
 
 struct Ctx {
@@ -137,6 +152,11 @@ struct Ctx {
     unsigned long long graph_clock = 0;
     GraphMem *capturing = nullptr;
     bool capture_cl = false;  // the graph being recorded runs every transform as one cluster kernel (graph.cu)
+    // set while a slot graph is recorded: the one-pass tensor sum takes its operand pointers from these
+    // parameters (and publishes the table) instead of a separate table-writing kernel; it clears the
+    // pointer once it has consumed it
+    const SetTables *ts_params = nullptr;
+    cudaGraphNode_t ts_node = nullptr;  // the captured node of that tensor sum
     unsigned long long enc_calls = 0, enc_seen = 0;  // encryption launches, and how many the last async product had seen
     cudaStream_t side = 0;  // non-blocking helper stream for capture-time allocations and uploads
     // asynchronous drivers (vr_matmul_outer_async): calls rotate over kSlots streams (process-wide per
