@@ -101,6 +101,16 @@ def _frozen(values) -> np.ndarray:
     return out
 
 
+class _FailedProducer:
+    """Pending marker of ciphertexts whose deferred encryption raised: every later use raises too
+    instead of reading residues that were never written."""
+
+    __slots__ = ("why",)
+
+    def __init__(self, why: str):
+        self.why = why
+
+
 class Ciphertext:
     """RNS-CKKS ciphertext: residues [degree+1][level+1][N] on the GPU (treated as immutable).
 
@@ -169,9 +179,13 @@ class Ciphertext:
         queued here must complete before the caching allocator hands the block out again."""
         p = self._pending
         if p is not None:
+            if isinstance(p, _FailedProducer):
+                raise EngineError(f"the deferred encryption of this ciphertext failed: {p.why}")
             if isinstance(p, CkksEngine):  # a deferred encryption: launch it (and its queue) now
                 p._flush_enc()
-                return
+                if self._pending is None or self._pending is p:
+                    return
+                return self._ready()  # launched on a side stream, or failed
             cur = torch.cuda.current_stream()
             cur.wait_stream(p)
             self.storage_tensor().record_stream(cur)
@@ -301,6 +315,8 @@ class CtBatch:
         pend = self._pending
         if pend is None or pend is stream:
             return
+        if isinstance(pend, _FailedProducer):
+            raise EngineError(f"the deferred encryption of these ciphertexts failed: {pend.why}")
         evt = self._evt
         if evt is None:
             stream.wait_stream(pend)
@@ -580,6 +596,11 @@ class CkksEngine:
             _lib.check(self._lib.vr_fork_stream(self._h, ctypes.c_void_p(on.cuda_stream)))
         try:
             groups = self._launch_queue(queue)
+        except BaseException as exc:
+            failed = _FailedProducer(str(exc) or type(exc).__name__)
+            for (_, cts) in queue:  # nothing of this queue may be read as if it had been encrypted
+                cts.set_pending(self, failed)
+            raise
         finally:
             if on is not None:
                 _lib.check(self._lib.vr_set_stream(self._h, ctypes.c_void_p(self._stream_ptr)))

@@ -174,3 +174,21 @@ def test_ct_batch_is_lazy_and_list_like():
     assert all(c._pending is owner for c in p)
     p.set_pending(owner, None)
     assert p._pending is None and all(c._pending is None for c in p)
+
+
+def test_failed_deferred_encryption_poisons_its_ciphertexts():
+    """If the deferred launch raises, later uses of those ciphertexts raise as well (no garbage reads)."""
+    import torch
+
+    from paper_2512_18646_b200.engine import CtBatch, _FailedProducer
+    from paper_2512_18646_b200.errors import EngineError
+
+    out = torch.zeros((2, 2, 3, 8), dtype=torch.int64)
+    owner = object()
+    b = CtBatch(out, 2, 2.0 ** 40, 0, None, 7, 2, owner)
+    cts = list(b)
+    b.set_pending(owner, _FailedProducer("boom"))
+    with pytest.raises(EngineError, match="boom"):
+        cts[0].ptr()
+    with pytest.raises(EngineError, match="boom"):
+        b.order_on(object())
