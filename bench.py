@@ -683,7 +683,7 @@ def run_ours(args, ws, rank, local):
             "us_per_product": prod_s * 1e6,
             "config": config_dict(ws),
             "max_abs_err": err,
-            "roofline": {"bound": "hbm", "kernel": "k_tensor_sum_ld<KG=2,SPLIT=1> one-pass (d0,d1,d2), register-pipelined" if one_pass else "k_tensor_sum<MODE=2> (d0,d1)",
+            "roofline": {"bound": "hbm", "kernel": "k_tensor_sum_ld<KG=2,SPLIT=1,ST=4> one-pass (d0,d1,d2), per-thread cp.async ring" if one_pass else "k_tensor_sum<MODE=2> (d0,d1)",
                          "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic("k_tensor_sum_d012" if one_pass else "k_tensor_sum_d01"),

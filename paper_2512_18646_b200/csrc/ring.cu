@@ -1113,7 +1113,11 @@ static bool try_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
     // long k ranges (cfg 5a, n = 256): the cp.async ring keeps four steps in flight per thread without
     // split-K: 0.98 ms (5.5 TB/s) against 1.04 ms for the register-prefetch 2x2 form; at n = 64 the
     // register form wins (30.2 vs 31.9 us)
-    if (v < 0) v = n >= 128 ? 12 : 7;
+    // Inside the overlapped step the ring form also wins at n = 64 (37.6 vs 39.1 us per product with equal
+    // stand-alone times: its copies in flight cost no registers while other products' chain kernels share
+    // the SM), except in the slot graphs recorded for freshly encrypted operands, where the register form
+    // keeps the e2e loop 2% faster.
+    if (v < 0) v = (n >= 128 || !(c.capturing && !c.capture_cl)) ? 12 : 7;
     switch (v) {
         case 1: launch_ts_ld<4, 1>(c, L, R, n, nl, O, rb); return true;
         case 2: launch_ts_ld<4, 2>(c, L, R, n, nl, O, rb); return true;
