@@ -645,13 +645,18 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     gc.collect()
     gc.disable()
-    t0 = time.perf_counter()
-    st.record()
-    res, res_pair = e2e_run(e2e_steps)
-    en.record()
-    torch.cuda.synchronize()
+    # three timed blocks of e2e_steps products, the median reported: one caching-allocator or clock
+    # hiccup in a ~0.1 s region otherwise decides the number (observed: 3.7k in one run of 4.5k ones)
+    blocks = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        st.record()
+        res, res_pair = e2e_run(e2e_steps)
+        en.record()
+        torch.cuda.synchronize()
+        blocks.append(max(st.elapsed_time(en) / 1e3, time.perf_counter() - t0) / e2e_steps)
     gc.enable()
-    e2e_s = max_over_ranks(max(st.elapsed_time(en) / 1e3, time.perf_counter() - t0) / e2e_steps)
+    e2e_s = max_over_ranks(statistics.median(blocks))
     assert float(np.max(np.abs(res - pairs[res_pair][0] @ pairs[res_pair][1]))) < 1e-3
     h2d = BATCH * 2 * DIM * DIM * 8  # per step (batch): the raw A and B of every product (broadcast/tiling on the device)
     d2h = BATCH * eng.slots * 8
@@ -692,9 +697,11 @@ def run_ours(args, ws, rank, local):
                          "step": roofline_for(2, prod_s, eng.q, peaks)},
             "cpu_baseline": cpu,
             "e2e": {"value": ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "products": e2e_steps, "pipeline_depth": E2E_DEPTH,
+                    "products": e2e_steps, "blocks": 3, "block_products_per_s": [round(1.0 / b, 1) for b in blocks],
+                    "pipeline_depth": E2E_DEPTH,
                     "path": "per product: pinned host A,B -> encode_left+encode_right (encrypt 128 cts) -> matmul_outer -> "
-                            f"decode_async; at most {E2E_DEPTH} products in flight, every product's result read on the host"},
+                            f"decode_async; at most {E2E_DEPTH} products in flight, every product's result read on the host; "
+                            "median of three timed blocks"},
             "gpu_launches": int(launches),
             "gpu_launches_per_step": launches / args.steps,
             "clocks": clk.summary(),
