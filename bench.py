@@ -731,10 +731,25 @@ def bench_cfg1(peaks, steps=200):
     for _ in range(20):
         matmul_outer(eng, left, right)
     t = Timer(lambda x: x, eng.join)(lambda: matmul_outer(eng, left, right), steps)
+    # the same products through matmul_outer_many: MANY independent pairs per call share one tensor-sum
+    # launch and one relinearise + rescale chain (a product this small is bound by launches, not bytes)
+    from paper_2512_18646_b200 import matmul_outer_many
+    MANY = int(os.environ.get("VR_BENCH_MANY", "32"))
+    rng = np.random.default_rng(11)
+    mats = [(a, b)] + [tuple(rng.uniform(-1, 1, (2, 8, 8))) for _ in range(MANY - 1)]
+    pairs = [(encode_left(eng, x, 8), encode_right(eng, y, 8)) for x, y in mats]
+    outs = matmul_outer_many(eng, pairs)
+    err_many = max(float(np.max(np.abs(o.decode(eng) - x @ y))) for o, (x, y) in zip(outs, mats))
+    for _ in range(10):
+        matmul_outer_many(eng, pairs)
+    t_many = Timer(lambda x: x, eng.join)(lambda: matmul_outer_many(eng, pairs), max(20, steps // 4)) / MANY
     t_cpu = cpu_oracle_matmul_cfg(1, 8, 1, reps=20)
     t_sim = simulator_matmul(1, 8)
     return {"metric": "HE matmul/s (cfg1 8x8, N=2^13)", "value": 1.0 / t, "ms_per_matmul": t * 1e3, "max_abs_err": err,
             "roofline": roofline_for(1, t, eng.q, peaks),
+            "batched": {"value": 1.0 / t_many, "unit": UNIT, "products_per_call": MANY, "ms_per_matmul": t_many * 1e3,
+                        "max_abs_err": err_many, "roofline": roofline_for(1, t_many, eng.q, peaks),
+                        "path": "matmul_outer_many: one tensor-sum launch and one relinearise + rescale chain per call"},
             "cpu_baseline": _cpu_entry(1.0 / t_cpu, UNIT, "port", "best of 20 cfg-1 HE matmuls (matmul_outer, 16 cts, "
                                        "warmed engine) in the C RNS-CKKS oracle, OpenMP"),
             "reference_simulator": {"value": 1.0 / t_sim, "unit": UNIT, "cores": 1}}

@@ -182,6 +182,11 @@ int vr_mod_reduce(vr_ctx *ctx, uint64_t *data, long long polys, int level);
  * blocks share R (nb in {1,2,4}) */
 int vr_matmul_outer(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
                     uint64_t *const *out);
+/* `count` independent matmul_outer products (multicipher.py:88-103 once per operand pair) in one launch
+ * sequence: out[b] = rescale(relin(sum_k L[b*n+k] (x) R[b*n+k])), all operands at `level`.  Residues
+ * equal those of `count` separate vr_matmul_outer calls; small products share six kernel launches. */
+int vr_matmul_outer_many(vr_ctx *ctx, const uint64_t *const *L, const uint64_t *const *R, int n, int count, int level,
+                         uint64_t *const *out);
 /* matmul_outer without waiting for the result: the product is computed on one of the context's
  * slot streams, which first waits for all work already queued on the context stream.  *slot_stream
  * receives that stream (the result is complete once it reaches the current point of that stream),

@@ -35,6 +35,7 @@ from .multicipher import (
     encode_right,
     matmul_outer,
     matmul_outer_blocks,
+    matmul_outer_many,
     pad_images,
     reassemble_columns,
 )

@@ -73,6 +73,7 @@ _SIGS = {
     "vr_bench_butterflies": [c_vp, ctypes.c_int, ctypes.c_int, c_vp],
     "vr_bench_butterflies_f64": [c_vp, ctypes.c_int, ctypes.c_int, c_vp],
     "vr_matmul_outer": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp],
+    "vr_matmul_outer_many": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp],
     "vr_tensor_sum": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp],
     "vr_matmul_outer_async": [c_vp, c_vpp, c_vpp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vpp, ctypes.POINTER(c_vp)],
     "vr_join": [c_vp],

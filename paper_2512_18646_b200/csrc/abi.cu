@@ -839,6 +839,30 @@ int vr_matmul_outer(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *
     });
 }
 
+int vr_matmul_outer_many(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *R, int n, int count, int level,
+                         uint64_t *const *out) {
+    return guard([&] {
+        check_level(h->c, level);
+        if (level < 1) throw vr::VrError(VR_ERR_ENGINE, "multiplicative depth exhausted (level 0)");
+        if (n <= 0) throw vr::VrError(VR_ERR_LAYOUT, "matmul_outer needs at least one column ciphertext");
+        if (count <= 0) return;
+        if (count > 4096) throw vr::VrError(VR_ERR_LAYOUT, "matmul_outer_many: at most 4096 products per call");
+        vr::Ctx &c = h->c;
+        std::vector<uintptr_t> key{3, (uintptr_t)n, (uintptr_t)count, (uintptr_t)level};
+        key.insert(key.end(), (const uintptr_t *)L, (const uintptr_t *)L + (size_t)n * count);
+        key.insert(key.end(), (const uintptr_t *)R, (const uintptr_t *)R + (size_t)n * count);
+        key.insert(key.end(), (const uintptr_t *)out, (const uintptr_t *)out + count);
+        auto body = [&] {
+            vr::PtrTable tl(c, vec(L, (size_t)n * count)), tr(c, vec(R, (size_t)n * count)), to(c, vecm(out, count));
+            vr::matmul_outer_many(c, tl.c_(), tr.c_(), n, count, level, to.m_());
+        };
+        // launch-bound by construction (that is what the batch is for): replayed as one CUDA graph
+        const size_t pair_bytes = (size_t)2 * n * 2 * (level + 1) * c.n * 8;  // one product's operands
+        if (pair_bytes <= vr::graph_max_bytes()) vr::run_graphed(c, std::move(key), body);
+        else body();
+    });
+}
+
 int vr_matmul_outer_async(vr_ctx *h, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level,
                           uint64_t *const *out, void **slot_stream) {
     return guard([&] {

@@ -316,6 +316,18 @@ void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, in
     relin_rescale_batch(c, td.c_(), Out, nb, level);
 }
 
+// B independent matmul_outer products (multicipher.py:88-103 applied to B operand pairs of the same
+// n and level) as one launch sequence: one tensor-sum launch over all pairs, then one relinearise +
+// rescale chain over the B degree-2 sums.  Small products (config 1) are bound by kernel launches, not
+// by bytes: six launches then serve B products instead of one.  Residues are those of B separate calls.
+void matmul_outer_many(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int B, int level, uint64_t *const *Out) {
+    const int N = c.n, nl = level + 1;
+    Scratch d3(c, sizeof(uint64_t) * B * 3 * nl * N);
+    PtrTable td(c, strided(d3.as<uint64_t>(), B, (size_t)3 * nl * N));
+    tensor_sum_many(c, L, R, n, B, nl, td.m_());
+    relin_rescale_batch(c, td.c_(), Out, B, level);
+}
+
 void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, int k, const int64_t *w, const uint64_t *bias,
                   int F, const int *out_cols, int nout, const uint64_t *mask_pt, int level, const std::vector<uint64_t *> &Y) {
     const int N = c.n, nl = level + 1;

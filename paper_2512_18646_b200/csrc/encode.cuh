@@ -28,6 +28,7 @@ void sum_partials(Ctx &c, uint64_t *data, long long polys, int level, int root);
 // recorded into the asynchronous per-slot graphs, graph.cu)
 void matmul_outer(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int level, uint64_t *const *Out,
                   bool one_pass = false);
+void matmul_outer_many(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int B, int level, uint64_t *const *Out);
 void conv_columns(Ctx &c, const std::vector<const uint64_t *> &X, int C, int W, int k, const int64_t *w, const uint64_t *bias,
                   int F, const int *out_cols, int nout, const uint64_t *mask_pt, int level, const std::vector<uint64_t *> &Y);
 void pt_matvec(Ctx &c, const uint64_t *const *X, int nx, const uint64_t *const *PT, int ny, int level, uint64_t *const *Y);

@@ -881,6 +881,7 @@ struct PtrTab {
     __device__ __forceinline__ const uint64_t *l(int k) const { return L[k]; }
     __device__ __forceinline__ const uint64_t *r(int k) const { return R[k]; }
     __device__ __forceinline__ void left_block(size_t ofs) { L += ofs; }
+    __device__ __forceinline__ void right_block(size_t ofs) { R += ofs; }
 };
 struct PtrPar {
     const SetTables *a;
@@ -888,14 +889,19 @@ struct PtrPar {
     __device__ __forceinline__ const uint64_t *l(int k) const { return a->p[lofs + k]; }
     __device__ __forceinline__ const uint64_t *r(int k) const { return a->p[rofs + k]; }
     __device__ __forceinline__ void left_block(size_t ofs) { lofs += (int)ofs; }
+    __device__ __forceinline__ void right_block(size_t ofs) { rofs += (int)ofs; }
 };
 
 template <int KG, int SPLIT, int ST, class PS>
 __device__ __forceinline__ void ts_ld_body(PS ps, int n, int nl, int N, const DevPrimes &pr, uint64_t *const *O, int rb) {
     constexpr int TP = 64;  // coefficient pairs per CTA
-    const int xb = rb > 1 ? (int)blockIdx.x % rb : 0;
-    const int xt = rb > 1 ? (int)blockIdx.x / rb : (int)blockIdx.x;
+    // rb < 0: |rb| independent products interleaved along x, each with its own right operand
+    // (matmul_outer_many); rb > 1: row blocks sharing R
+    const int rbs = rb < 0 ? -rb : rb;
+    const int xb = rbs > 1 ? (int)blockIdx.x % rbs : 0;
+    const int xt = rbs > 1 ? (int)blockIdx.x / rbs : (int)blockIdx.x;
     ps.left_block((size_t)xb * n);
+    if (rb < 0) ps.right_block((size_t)xb * n);
     O += xb;
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -1057,14 +1063,14 @@ __global__ void __launch_bounds__(64 * KG)
     pdl_trigger();
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
         for (int i = threadIdx.x; i < a.count; i += blockDim.x) a.dst[i] = const_cast<uint64_t *>(a.p[i]);
-    ts_ld_body<KG, SPLIT, ST>(PtrPar{&a, 0, rb * n}, n, nl, N, pr, O, rb);
+    ts_ld_body<KG, SPLIT, ST>(PtrPar{&a, 0, (rb < 0 ? -rb : rb) * n}, n, nl, N, pr, O, rb);
 }
 
 template <int KG, int SPLIT, int ST = 0>
 static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O, int rb) {
     cudaLaunchConfig_t cfg = {};
     const int tiles = (c.n / 2 + 63) / 64;
-    cfg.gridDim = dim3(tiles * rb, nl, SPLIT);
+    cfg.gridDim = dim3(tiles * (rb < 0 ? -rb : rb), nl, SPLIT);
     cfg.blockDim = dim3(64 * KG, 1, 1);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = c.stream;
@@ -1142,6 +1148,14 @@ static bool try_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
 // whether tensor_sum(n, nb) runs the register / cp.async kernel, which can take its operand pointers
 // from its parameters (slot graphs)
 bool tensor_sum_takes_params(int nb) { return ts_ld_variant() != 0 && (nb == 1 || nb == 4) && getenv("VR_TS_VARIANT") == nullptr && getenv("VR_TS4") == nullptr && getenv("VR_TS4_MC") == nullptr; }
+
+// B independent products in one launch: O[b] = sum_k L[b*n + k] (x) R[b*n + k] (matmul_outer_many)
+void tensor_sum_many(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int B, int nl, uint64_t *const *O) {
+    if (c.ts_params) throw VrError(4, "tensor_sum_many inside a slot-graph capture");
+    if (n >= 32) launch_ts_ld<2, 1, 4>(c, L, R, n, nl, O, -B);
+    else launch_ts_ld<1, 1, 4>(c, L, R, n, nl, O, -B);  // short sums: one k-group per CTA
+    check_launch("k_tensor_sum (many)");
+}
 
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O) {
     static int variant = [] {

@@ -33,6 +33,8 @@ void tensor_sum_mode(Ctx &c, const uint64_t *const *L, const uint64_t *const *R,
                      int mode);
 void tensor_sum(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nb, int nl, uint64_t *const *O);
 bool tensor_sum_takes_params(int nb);
+// B independent products in one launch: O[b] = sum_k L[b*n + k] (x) R[b*n + k]
+void tensor_sum_many(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int B, int nl, uint64_t *const *O);
 
 // rescale: in [polys][l+1][N] -> out [polys][l][N] for each ciphertext
 void rescale(Ctx &c, const uint64_t *const *In, uint64_t *const *Out, int count, int polys, int level);

@@ -37,6 +37,7 @@ __all__ = [
     "encode_right",
     "matmul_outer",
     "matmul_outer_blocks",
+    "matmul_outer_many",
     "encode_image_columns",
     "conv_columns",
     "conv_columns_multi",
@@ -286,6 +287,62 @@ def matmul_outer_blocks(engine: CkksEngine, lefts, right: ColumnEncodedMatrix) -
         engine._meter.add_count += n - 1
         engine._observe(depth)
         res.append(Ciphertext.at(outs, b, lv - 1, engine.scales[lv - 1], depth, _layout0(lf.cts), engine._id))
+    return res
+
+
+def matmul_outer_many(engine: CkksEngine, pairs) -> list[PackedMatrix]:
+    """``[matmul_outer(engine, l, r) for l, r in pairs]`` as one launch sequence (vr_matmul_outer_many).
+
+    Every pair must have the same n (column ciphertexts per operand) and all operands the same level.
+    Small products are bound by kernel launches, not bytes: the batch shares one tensor-sum launch and
+    one relinearise + rescale chain.  Residues, meter counts and depths are those of separate calls
+    (multicipher.py:88-103 once per pair).
+    """
+    pairs = list(pairs)
+    if not pairs:
+        return []
+    n = pairs[0][1].n
+    for left, right in pairs:
+        if left.role != "left" or right.role != "right":
+            raise LayoutError("operands must be a (left, right) column-encoded pair")
+        if (left.n, left.m, left.p) != (right.n, right.m, right.p):
+            raise LayoutError(
+                f"operand dims differ: left {(left.m, left.n, left.p)}, right {(right.m, right.n, right.p)}"
+            )
+        if left.n != n:
+            raise LayoutError("matmul_outer_many needs the same n for every pair")
+    caches = []
+    for left, right in pairs:  # validated once per operand, then served from the operand's cache
+        for cem in (left, right):
+            c = _fast_operand(engine, cem)
+            if c is None:
+                _checked_ptrs(engine, cem)
+                c = _fast_operand(engine, cem)
+                if c is None:
+                    raise LayoutError("matmul_outer_many needs every operand ciphertext at one common level")
+            caches.append(c)
+    lv = caches[0].level
+    if any(c.level != lv for c in caches):
+        raise LayoutError("matmul_outer_many needs every operand ciphertext at one common level")
+    if lv < 1:
+        raise EngineError("multiplicative depth exhausted: operands are at level 0")
+    cnt = len(pairs)
+    lnp = np.concatenate([c._np for c in caches[0::2]])
+    rnp = np.concatenate([c._np for c in caches[1::2]])
+    h = engine.handle  # adopts the current stream and launches deferred encryptions
+    outs = torch.empty((cnt, 2, lv, engine.N), dtype=torch.int64, device=engine.device)
+    onp = outs.data_ptr() + np.arange(cnt, dtype=np.uint64) * np.uint64(outs.stride(0) * 8)
+    as_arr = lambda a: (ctypes.c_void_p * a.size).from_buffer(a)  # noqa: E731
+    _lib.check(engine._lib.vr_matmul_outer_many(h, as_arr(lnp), as_arr(rnp), n, cnt, lv, as_arr(onp)))
+    engine._meter.mul_count += n * cnt
+    engine._meter.add_count += (n - 1) * cnt
+    res = []
+    level, scale = lv - 1, engine.scales[lv - 1]
+    for b, (left, right) in enumerate(pairs):
+        depth = max(caches[2 * b].depth, caches[2 * b + 1].depth) + 1
+        engine._observe(depth)
+        ct = Ciphertext.at(outs, b, level, scale, depth, _layout0(left.cts), engine._id)
+        res.append(PackedMatrix(ct, MatrixShape(left.m, left.p), Encoding.ROW_MAJOR))
     return res
 
 

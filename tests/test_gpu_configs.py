@@ -10,7 +10,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from oracle.engine import OracleEngine  # noqa: E402
-from paper_2512_18646_b200 import CkksEngine, config_params, encode_left, encode_right, matmul_outer  # noqa: E402
+from paper_2512_18646_b200 import (CkksEngine, LayoutError, config_params, encode_left, encode_right, matmul_outer,  # noqa: E402
+                                   matmul_outer_many)
 from paper_2512_18646_b200.cnn import conv_layer, decode_layer, encode_images  # noqa: E402
 from tools.workloads import ACT4, cfg4, cfg_matmul, conv_plain, poly_plain  # noqa: E402
 
@@ -30,6 +31,52 @@ def test_matmul_configs_bit_exact(cfg):
     np.testing.assert_array_equal(out.ct.residues(), want.data)
     np.testing.assert_allclose(out.decode(g), a @ b, atol=TOL)
     assert out.ct.depth == 1
+
+
+@pytest.mark.parametrize("cfg,dim,count", [(1, 8, 8), (1, 8, 3), (2, 64, 2), (1, 5, 4)])
+def test_matmul_outer_many_equals_separate_products(cfg, dim, count):
+    """vr_matmul_outer_many: `count` independent products in one launch sequence -- residues equal the
+    separate matmul_outer calls and the CPU oracle (multicipher.py:88-103 once per pair); meter and
+    depth as for separate calls."""
+    p = config_params(cfg)
+    g, o = CkksEngine(p), OracleEngine.from_params(p)
+    rng = np.random.default_rng(100 + cfg)
+    mats = [rng.uniform(-1, 1, (2, dim, dim)) for _ in range(count)]
+    pairs = [(encode_left(g, a, dim), encode_right(g, b, dim)) for a, b in mats]
+    before = g.meter_snapshot()
+    outs = matmul_outer_many(g, pairs)
+    d = g.meter_snapshot().delta_since(before)
+    assert (d.mul_count, d.add_count) == (count * dim, count * (dim - 1))
+    assert len(outs) == count
+    for i, ((a, b), out) in enumerate(zip(mats, outs)):
+        single = matmul_outer(g, *pairs[i])
+        np.testing.assert_array_equal(out.ct.residues(), single.ct.residues())
+        np.testing.assert_allclose(out.decode(g), a @ b, atol=TOL)
+        assert out.ct.depth == 1 and out.ct.level == single.ct.level
+    # oracle: the encryptions consumed nonces pair by pair (left then right), as on the GPU
+    for i, (a, b) in enumerate(mats[:2]):
+        oL = [o.enc(np.repeat(a[:, k], dim)) for k in range(dim)]
+        oR = [o.enc(np.tile(b[k, :], dim)) for k in range(dim)]
+        want = o.matmul_outer_blocks([oL], oR)[0]
+        np.testing.assert_array_equal(outs[i].ct.residues(), want.data)
+    # twice with the same operands (the replayed graph) gives the same residues
+    again = matmul_outer_many(g, pairs)
+    for x, y in zip(outs, again):
+        np.testing.assert_array_equal(x.ct.residues(), y.ct.residues())
+
+
+def test_matmul_outer_many_validation():
+    g = CkksEngine(config_params(1))
+    a = np.random.default_rng(5).uniform(-1, 1, (8, 8))
+    l8, r8 = encode_left(g, a, 8), encode_right(g, a, 8)
+    l4, r4 = encode_left(g, a[:4, :4], 4), encode_right(g, a[:4, :4], 4)
+    assert matmul_outer_many(g, []) == []
+    with pytest.raises(LayoutError):
+        matmul_outer_many(g, [(r8, l8)])
+    with pytest.raises(LayoutError):
+        matmul_outer_many(g, [(l8, r8), (l4, r4)])
+    with pytest.raises(LayoutError):
+        matmul_outer_many(g, [(l8, r4)])
 
 
 def test_cfg4_reduced_bit_exact():
