@@ -371,14 +371,24 @@ __device__ __forceinline__ void group_compute_f(double (&x)[EPT], const int (&ba
 #pragma unroll
     for (int v = 0; v < U; v++) {
         double tw[E2 - 1];
-#pragma unroll
-        for (int r = 0, n = 0; r < R; r++) {
-            const int g = s0 + s + r, half = E2 >> (r + 1), shift = logT - (s + r);
-#pragma unroll
-            for (int w = 0; w < E2; w += 2 * half, n++) {
-                if (INV && g == 0) continue;
-                tw[n] = __ldg(W + ((1 << g) + (hi << (g - s0)) + (base[v] >> shift)) + (w >> (R - r)));
-            }
+        // Stage s + r of the group reads 2^r twiddles at consecutive table indices starting at a
+        // multiple of 2^r (base has no bits below the group's span and g - s0 >= r), so the two
+        // twiddles of the second stage and the four of the third arrive as 16-byte loads: 4 loads per
+        // radix-8 group instead of 7.
+        auto twp = [&](int r) { return W + ((1 << (s0 + s + r)) + (hi << (s + r)) + (base[v] >> (logT - (s + r)))); };
+        if (!(INV && s0 + s == 0)) tw[0] = __ldg(twp(0));
+        if constexpr (R >= 2) {
+            const double2 t = __ldg(reinterpret_cast<const double2 *>(twp(1)));
+            tw[1] = t.x;
+            tw[2] = t.y;
+        }
+        if constexpr (R >= 3) {
+            const double2 *p = reinterpret_cast<const double2 *>(twp(2));
+            const double2 t0 = __ldg(p), t1 = __ldg(p + 1);
+            tw[3] = t0.x;
+            tw[4] = t0.y;
+            tw[5] = t1.x;
+            tw[6] = t1.y;
         }
 #pragma unroll
         for (int rr = 0; rr < R; rr++) {
