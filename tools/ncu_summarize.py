@@ -25,6 +25,7 @@ ALG = {
     "ts_d2": 2 * 64 * 5 * N14 * 8 + 1 * 5 * N14 * 8,
     "ts_cfg5a": (4 * 256 + 256) * 2 * 8 * N15 * 8 + 4 * 3 * 8 * N15 * 8,
     "ntt_cl8_fwd": 2 * 256 * 5 * N14 * 8,  # in place: read + write every limb
+    "ts_many_cfg1": 32 * (4 * 8 * 2 * (1 << 13) * 8 + 3 * 2 * (1 << 13) * 8),  # 32 products of 16 cts + their (d0, d1, d2)
 }
 NOTES = {
     "ts_onepass": "config 2 one-pass (d0, d1, d2) tensor sum, the dominant kernel of the asynchronous step (multicipher.py:88-103)",
@@ -45,6 +46,7 @@ NOTES = {
     "enc_ntt": "fused secret-key encryption through the cluster NTT (sampler + NTT(m+e) - a s), config 2 encode_left (engine.py:193-202)",
     "encode": "slot FFT encode + Gaussian noise, 64 ciphertexts (config 2)",
     "decode": "slot FFT decode (engine.py:204-206)",
+    "ts_many_cfg1": "matmul_outer_many tensor sum: 32 independent config-1 products in one launch (a right operand per product)",
 }
 WANT = {
     "duration_ns": "gpu__time_duration.sum",
@@ -57,6 +59,9 @@ WANT = {
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "warp_instructions": "smsp__inst_executed.sum",
     "l2_hit_rate_pct": "lts__t_sector_hit_rate.pct",
+    "l1_hit_rate_pct": "l1tex__t_sector_hit_rate.pct",
+    "lsu_data_pipe_pct": "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "l2_throughput_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "grid_size": "launch__grid_size",
     "block_size": "launch__block_size",
     "cluster_size": "launch__cluster_dim_x",

@@ -31,6 +31,7 @@ cap encode 'k_encode' 1 python tools/e2e_profile.py
 cap decode 'k_decode' 1 python tools/e2e_profile.py
 unset VR_ASYNC
 cap ts_cfg5a 'k_tensor_sum' 1 python tools/cfg5a_prof.py
+cap ts_many_cfg1 'k_tensor_sum_ld<.int.1,' 1 python tools/many_probe.py 1 32
 
 python tools/ncu_summarize.py gpurun_out gpurun_out/ncu_summary.json > gpurun_out/ncu_summarize.log 2>&1; echo "summary rc=$?"
 for t in ts_onepass conv_mac; do
