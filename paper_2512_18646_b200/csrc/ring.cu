@@ -892,9 +892,9 @@ struct PtrPar {
     __device__ __forceinline__ void right_block(size_t ofs) { rofs += (int)ofs; }
 };
 
-template <int KG, int SPLIT, int ST, class PS>
+template <int KG, int SPLIT, int ST, class PS, int TP = 64>
 __device__ __forceinline__ void ts_ld_body(PS ps, int n, int nl, int N, const DevPrimes &pr, uint64_t *const *O, int rb) {
-    constexpr int TP = 64;  // coefficient pairs per CTA
+    // TP coefficient pairs per CTA
     // rb < 0: |rb| independent products interleaved along x, each with its own right operand
     // (matmul_outer_many); rb > 1: row blocks sharing R
     const int rbs = rb < 0 ? -rb : rb;
@@ -926,7 +926,7 @@ __device__ __forceinline__ void ts_ld_body(PS ps, int n, int nl, int N, const De
     const int qb = 64 - __clzll((long long)m.q);
     const unsigned mask1 = (1u << max(0, min(20, 126 - 2 * qb))) - 1u, mask02 = (1u << max(0, min(20, 128 - 2 * qb))) - 1u;
     if constexpr (ST > 0) {
-        __shared__ __align__(16) ulonglong2 ring[ST][4][64 * KG];
+        __shared__ __align__(16) ulonglong2 ring[ST][4][TP * KG];
         if (live && kb < ke) {
             auto issue = [&](int k) {
                 if (k < ke) {
@@ -1045,13 +1045,13 @@ __device__ __forceinline__ void ts_ld_body(PS ps, int n, int nl, int N, const De
     cluster.sync();
 }
 
-template <int KG, int SPLIT, int ST = 0>
-__global__ void __launch_bounds__(64 * KG)
+template <int KG, int SPLIT, int ST = 0, int TP = 64>
+__global__ void __launch_bounds__(TP * KG)
     k_tensor_sum_ld(const uint64_t *const *L, const uint64_t *const *R, int n, int nl, int N, DevPrimes pr, uint64_t *const *O,
                     int rb) {
     pdl_wait();
     pdl_trigger();
-    ts_ld_body<KG, SPLIT, ST>(PtrTab{L, R}, n, nl, N, pr, O, rb);
+    ts_ld_body<KG, SPLIT, ST, PtrTab, TP>(PtrTab{L, R}, n, nl, N, pr, O, rb);
 }
 
 // First kernel of a slot graph: the operand pointers arrive in the parameters (one row block), block
@@ -1066,12 +1066,12 @@ __global__ void __launch_bounds__(64 * KG)
     ts_ld_body<KG, SPLIT, ST>(PtrPar{&a, 0, (rb < 0 ? -rb : rb) * n}, n, nl, N, pr, O, rb);
 }
 
-template <int KG, int SPLIT, int ST = 0>
+template <int KG, int SPLIT, int ST = 0, int TP = 64>
 static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R, int n, int nl, uint64_t *const *O, int rb) {
     cudaLaunchConfig_t cfg = {};
-    const int tiles = (c.n / 2 + 63) / 64;
+    const int tiles = (c.n / 2 + TP - 1) / TP;
     cfg.gridDim = dim3(tiles * (rb < 0 ? -rb : rb), nl, SPLIT);
-    cfg.blockDim = dim3(64 * KG, 1, 1);
+    cfg.blockDim = dim3(TP * KG, 1, 1);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[2];
@@ -1083,7 +1083,8 @@ static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    if (c.ts_params) {  // recording a slot graph: pointers in the parameters, no table-writing kernel
+    if (c.ts_params && TP != 64) throw VrError(4, "tensor sum: tile variants are not slot-graph kernels");
+    if constexpr (TP == 64) if (c.ts_params) {  // recording a slot graph: pointers in the parameters, no table-writing kernel
         const SetTables *a = c.ts_params;
         c.ts_params = nullptr;
         VR_CUDA(cudaLaunchKernelEx(&cfg, k_tensor_sum_ldp<KG, SPLIT, ST>, *a, n, nl, c.n, c.primes, O, rb));
@@ -1095,7 +1096,7 @@ static void launch_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const
         c.ts_node = deps[0];
         return;
     }
-    VR_CUDA(cudaLaunchKernelEx(&cfg, k_tensor_sum_ld<KG, SPLIT, ST>, L, R, n, nl, c.n, c.primes, O, rb));
+    VR_CUDA(cudaLaunchKernelEx(&cfg, k_tensor_sum_ld<KG, SPLIT, ST, TP>, L, R, n, nl, c.n, c.primes, O, rb));
 }
 
 // VR_TS_LD selects the register-pipelined kernel for one-pass sums (0 = the TMA ring).  Swept on
@@ -1123,7 +1124,10 @@ static bool try_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
     // stand-alone times: its copies in flight cost no registers while other products' chain kernels share
     // the SM), except in the slot graphs recorded for freshly encrypted operands, where the register form
     // keeps the e2e loop 2% faster.
-    if (v < 0) v = (n >= 128 || !(c.capturing && !c.capture_cl)) ? 12 : 7;
+    // Long sums outside a slot-graph capture (cfg 5a, n = 256: vr_tensor_sum of the sharded product) take
+    // 128 coefficient pairs per CTA and one k-group -- 2 KB row segments, each thread walks the whole k
+    // range: 981 -> 958 us (5.63 TB/s); at n = 64 the same tile is slower (34.3 vs 32.0 us).
+    if (v < 0) v = (n >= 128 && !c.ts_params) ? 20 : (n >= 128 || !(c.capturing && !c.capture_cl)) ? 12 : 7;
     switch (v) {
         case 1: launch_ts_ld<4, 1>(c, L, R, n, nl, O, rb); return true;
         case 2: launch_ts_ld<4, 2>(c, L, R, n, nl, O, rb); return true;
@@ -1141,6 +1145,10 @@ static bool try_ts_ld(Ctx &c, const uint64_t *const *L, const uint64_t *const *R
         case 14: launch_ts_ld<2, 2, 4>(c, L, R, n, nl, O, rb); return true;
         case 15: launch_ts_ld<2, 1, 5>(c, L, R, n, nl, O, rb); return true;
         case 16: launch_ts_ld<2, 2, 5>(c, L, R, n, nl, O, rb); return true;
+        case 20: launch_ts_ld<1, 1, 4, 128>(c, L, R, n, nl, O, rb); return true;  // 2 KB row segments per CTA
+        case 21: launch_ts_ld<4, 1, 4, 32>(c, L, R, n, nl, O, rb); return true;   // 512 B segments, four k-groups
+        case 22: launch_ts_ld<1, 1, 2, 256>(c, L, R, n, nl, O, rb); return true;  // 4 KB segments, two steps in flight
+        case 23: launch_ts_ld<2, 1, 2, 128>(c, L, R, n, nl, O, rb); return true;
         default: return false;
     }
 }
